@@ -1,0 +1,198 @@
+/*
+ * mfreg_cuda.h — C ABI of the B200-native NGF + curvature derivative hot path
+ * (paper_1804_10541_b200/libmfreg_cuda.so).
+ *
+ * Drop-in boundary for the reference C++ library mfreg (/root/reference/proj).
+ * The reference has no FFI; its public surface is the C++ API in
+ * include/mfreg/*.hpp. Each entry point below names the reference declaration
+ * it replaces (file:line under /root/reference/proj/include/mfreg/). Plain
+ * pointers and sizes only; no C++ or torch types cross this boundary.
+ *
+ * Conventions (same as the reference):
+ *  - fields are fp64, x fastest (grid.hpp:63); 3-vectors are component-major
+ *    (all x, all y, all z; ngf.cpp:75-77);
+ *  - `where` = MFREG_CU_HOST: pointers are host memory, copied in/out per call;
+ *    `where` = MFREG_CU_DEVICE: pointers are CUDA device memory on the current
+ *    device, nothing crosses PCIe;
+ *  - errors are returned as status codes; MFREG_CU_EINVAL corresponds to the
+ *    reference's std::invalid_argument (same message text, retrievable with
+ *    mfreg_cu_last_error), MFREG_CU_ELOGIC to std::logic_error;
+ *  - mode MFREG_CU_PARITY reproduces the reference bit for bit (same operation
+ *    order, no FMA, 4096-chunk reductions, closed-form Gauss-Newton Hv);
+ *    MFREG_CU_FAST uses tree reductions and the factored Hv
+ *    2h dT^T dr^T dr dT (max-rel <= 1e-9 vs the reference, tests/test_gpu_parity.py).
+ */
+#ifndef MFREG_CUDA_H
+#define MFREG_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MFREG_CU_OK 0
+#define MFREG_CU_EINVAL 1 /* std::invalid_argument in the reference */
+#define MFREG_CU_ELOGIC 2 /* std::logic_error */
+#define MFREG_CU_ECUDA 3  /* CUDA runtime / launch failure */
+#define MFREG_CU_EOTHER 4
+
+#define MFREG_CU_HOST 0
+#define MFREG_CU_DEVICE 1
+
+#define MFREG_CU_PARITY 0
+#define MFREG_CU_FAST 1
+
+#define MFREG_CU_LBFGS 0       /* mfreg::Method::Lbfgs (multilevel.hpp:36) */
+#define MFREG_CU_GAUSS_NEWTON 1 /* mfreg::Method::GaussNewton */
+
+/* mfreg::GridDesc (grid.hpp:50-120) without the kind tag: each call states
+ * whether it expects a cell-centred image grid or a nodal deformation grid. */
+typedef struct {
+    int64_t m[3];
+    double h[3];
+} mfreg_cu_grid;
+
+/* mfreg::OptimizerConfig (optimizer.hpp:145-155), field for field. */
+typedef struct {
+    int max_iters;
+    double c1;
+    double beta;
+    int max_backtracks;
+    int cg_max_iters;
+    double cg_rel_tol;
+    int h0_max_iters;
+    double h0_rel_tol;
+    int lbfgs_history;
+    double gamma;
+    double tol_rel_j;
+    double tol_grad;
+    double tol_step;
+} mfreg_cu_opt_config;
+
+/* mfreg::IterationRecord (optimizer.hpp:22-30). */
+typedef struct {
+    int iter;
+    int cg_iters;
+    double j;
+    double distance;
+    double regularizer;
+    double grad_norm;
+    double step;
+} mfreg_cu_iter_record;
+
+/* mfreg::MultilevelConfig (multilevel.hpp:38-45) + execution mode. */
+typedef struct {
+    int levels;
+    int64_t deform_ratio;
+    double tau;
+    double rho;
+    double alpha;
+    int method;
+    int mode;
+    mfreg_cu_opt_config opt;
+} mfreg_cu_ml_config;
+
+typedef struct mfreg_cu_ngf mfreg_cu_ngf;             /* NgfPrecomp + NgfWorkspace (ngf.hpp:21-37) */
+typedef struct mfreg_cu_objective mfreg_cu_objective; /* mfreg::Objective (optimizer.hpp:53-106) */
+
+/* ---- runtime -------------------------------------------------------------- */
+const char* mfreg_cu_last_error(void);
+int mfreg_cu_version(void);
+int mfreg_cu_device_count(int* n);
+int mfreg_cu_set_device(int device);
+int mfreg_cu_synchronize(void);
+/* kernel launches issued by this library since load (for launch accounting) */
+int64_t mfreg_cu_launch_count(void);
+
+/* ---- grids (grid.hpp:131-146; multilevel.hpp:31-33) ------------------------ */
+int mfreg_cu_make_deform_grid(const mfreg_cu_grid* image, const int64_t points[3], mfreg_cu_grid* out);
+int mfreg_cu_deformation_grid_for(const mfreg_cu_grid* image, int64_t ratio, mfreg_cu_grid* out);
+
+/* ---- grid transfer (transfer.hpp:22-30) ------------------------------------ */
+int mfreg_cu_transfer_apply(const mfreg_cu_grid* nodal, const mfreg_cu_grid* image, const double* y, double* out,
+                            int where);
+int mfreg_cu_transfer_apply_transpose(const mfreg_cu_grid* nodal, const mfreg_cu_grid* image, const double* w,
+                                      double* out, int where);
+
+/* ---- image (volume.hpp:18-56) ---------------------------------------------- */
+int mfreg_cu_sample_deformed(const mfreg_cu_grid* image, const double* tpl, const double* points, int64_t n,
+                             double* values, double* partials, int where);
+int mfreg_cu_downsample(const mfreg_cu_grid* image, const double* v, double* out, mfreg_cu_grid* out_grid,
+                        int where);
+
+/* ---- curvature (curvature.hpp:13-31), nodal grid ---------------------------- */
+int mfreg_cu_laplacian_apply(const mfreg_cu_grid* nodal, const double* u_comp, double* out, int where);
+int mfreg_cu_curvature_value(const mfreg_cu_grid* nodal, const double* u, double* out, int mode, int where);
+int mfreg_cu_curvature_gradient(const mfreg_cu_grid* nodal, const double* u, double* out, int where);
+int mfreg_cu_curvature_hessian_vec(const mfreg_cu_grid* nodal, const double* p, double* out, int where);
+
+/* ---- NGF distance (ngf.hpp:26-85) ------------------------------------------- */
+/* make_ngf_precomp(reference, rho) + empty workspace */
+int mfreg_cu_ngf_create(const double* ref, const mfreg_cu_grid* image, double tau, double rho, int mode, int where,
+                        mfreg_cu_ngf** out);
+int mfreg_cu_ngf_destroy(mfreg_cu_ngf* ngf);
+/* populate_ngf_workspace(ws, tpl, points, pre, params, g) */
+int mfreg_cu_ngf_populate(mfreg_cu_ngf* ngf, const double* tpl, const double* points, int where);
+/* ngf_value(ws, g) */
+int mfreg_cu_ngf_value(mfreg_cu_ngf* ngf, double* out);
+/* ngf_gradient(ws, pre, g, out), out length 3m */
+int mfreg_cu_ngf_gradient(mfreg_cu_ngf* ngf, double* out, int where);
+/* ngf_hessian_vec(p, ws, pre, g, out), image-grid p and out, length 3m */
+int mfreg_cu_ngf_hessian_vec(mfreg_cu_ngf* ngf, const double* p, double* out, int where);
+/* workspace fields: values (m), partials (3m), residual, inv1, inv2 (m each),
+ * rho_hat (7m, direction-major in kAllDirs order = ngf_rho(i, k)); any may be NULL */
+int mfreg_cu_ngf_workspace(mfreg_cu_ngf* ngf, double* values, double* partials, double* residual, double* inv1,
+                           double* inv2, double* rho_hat, int where);
+
+/* ---- Objective (optimizer.hpp:53-106) --------------------------------------- */
+int mfreg_cu_objective_create(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                              const mfreg_cu_grid* deform, double tau, double rho, double alpha, int mode, int where,
+                              mfreg_cu_objective** out);
+int mfreg_cu_objective_destroy(mfreg_cu_objective* obj);
+int mfreg_cu_objective_dof(mfreg_cu_objective* obj, int64_t* dof);
+int mfreg_cu_objective_min_spacing(mfreg_cu_objective* obj, double* out);
+int mfreg_cu_objective_identity(mfreg_cu_objective* obj, double* out, int where);
+/* Objective::eval(y, grad): grad may be NULL (value only) */
+int mfreg_cu_objective_eval(mfreg_cu_objective* obj, const double* y, double* grad, int where, double* j);
+/* last_distance() / last_regularizer() */
+int mfreg_cu_objective_last(mfreg_cu_objective* obj, double* distance, double* regularizer);
+/* Objective::gn_hessian_vec(p, q) at the last evaluated iterate */
+int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, double* q, int where);
+/* Objective::seed_hessian_vec(p, gamma, q) */
+int mfreg_cu_objective_seed_hessian_vec(mfreg_cu_objective* obj, const double* p, double gamma, double* q,
+                                        int where);
+
+/* ---- solvers (optimizer.hpp:123-166) ---------------------------------------- */
+/* cg_solve on the objective's GN operator (op = 0) or seed operator (op = 1, gamma) */
+int mfreg_cu_cg_solve(mfreg_cu_objective* obj, int op, double gamma, const double* b, int max_iters, double rel_tol,
+                      double* x, int* iters, double* relres, int* breakdown, int where);
+/* lbfgs_minimize / gauss_newton_minimize; trace holds up to `cap` records */
+int mfreg_cu_minimize(mfreg_cu_objective* obj, int method, const double* y0, const mfreg_cu_opt_config* cfg,
+                      double* y_out, mfreg_cu_iter_record* trace, int cap, int* ntrace, int* line_search_failed,
+                      int where);
+
+/* ---- multilevel (multilevel.hpp:20-64) -------------------------------------- */
+int mfreg_cu_prolong(const mfreg_cu_grid* coarse, const mfreg_cu_grid* fine, const double* y_coarse, double* y_fine,
+                     int where);
+/* register_multilevel(reference, tpl, cfg): y_out sized from the finest
+ * deformation grid (deformation_grid_for(image, ratio)); traces packed coarsest
+ * level first, level_iters[levels] records per level, ls_failed[levels]. */
+int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                 const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
+                                 mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
+                                 int where);
+
+/* ---- synthetic inputs (synthetic.hpp:13-44) --------------------------------- */
+int mfreg_cu_make_phantom(const mfreg_cu_grid* image, double* out, int where);
+/* warp_with(vol, make_sinusoid_warp(extent(image), max_amp, seed)) */
+int mfreg_cu_warp_sinusoid(const mfreg_cu_grid* image, const double* vol, double max_amp, uint64_t seed, double* out,
+                           int where);
+int mfreg_cu_scale(int64_t n, double a, double* x, int where);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MFREG_CUDA_H */

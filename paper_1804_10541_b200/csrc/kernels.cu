@@ -1,0 +1,827 @@
+// sm_100a kernels for the NGF + curvature matrix-free derivative path.
+// Compiled with --fmad=false (see common.cuh): every expression below keeps the
+// reference's operation order and rounding so `parity` results are bitwise
+// identical to the CPU reference.
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <map>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mfreg_b200 {
+
+namespace {
+
+constexpr int BX = 64, BY = 4;
+
+inline dim3 grid3(const Grid& g) {
+    return dim3(static_cast<unsigned>((g.m[0] + BX - 1) / BX), static_cast<unsigned>((g.m[1] + BY - 1) / BY),
+                static_cast<unsigned>(g.m[2]));
+}
+inline dim3 block3() { return dim3(BX, BY, 1); }
+
+inline unsigned blocks1(idx_t n, int t = 256) { return static_cast<unsigned>(std::max<idx_t>(1, (n + t - 1) / t)); }
+
+__device__ __forceinline__ bool coords(const Grid& g, idx_t& x, idx_t& y, idx_t& z) {
+    x = static_cast<idx_t>(blockIdx.x) * BX + threadIdx.x;
+    y = static_cast<idx_t>(blockIdx.y) * BY + threadIdx.y;
+    z = blockIdx.z;
+    return x < g.m[0] && y < g.m[1];
+}
+
+__device__ __forceinline__ idx_t clampi(idx_t v, idx_t hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
+
+// volume.cpp:19-25
+__device__ __forceinline__ double sample_or_zero(const double* __restrict__ t, const Grid& g, idx_t i, idx_t j,
+                                                 idx_t k) {
+    if (i < 0 || j < 0 || k < 0 || i >= g.m[0] || j >= g.m[1] || k >= g.m[2]) return 0.0;
+    return __ldg(&t[g.lin(i, j, k)]);
+}
+
+// volume.cpp:29-74 — trilinear sample with Dirichlet zeros; ties go to the lower
+// cell (ceil(s)-1); IEEE division p/h (a reciprocal multiply flips ties).
+__device__ __forceinline__ void interpolate(const double* __restrict__ t, const Grid& g, double px, double py,
+                                            double pz, double& value, double& gx, double& gy, double& gz) {
+    const double p[3] = {px, py, pz};
+    idx_t base[3];
+    double f[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double s = __ddiv_rn(p[a], g.h[a]) - 0.5;
+        const double c = ceil(s);
+        base[a] = static_cast<idx_t>(c) - 1;
+        f[a] = s - static_cast<double>(base[a]);
+    }
+    double v[2][2][2];
+#pragma unroll
+    for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int a = 0; a < 2; ++a) v[gg][b][a] = sample_or_zero(t, g, base[0] + a, base[1] + b, base[2] + gg);
+    const double fx = f[0], fy = f[1], fz = f[2];
+    double cx[2][2], dx[2][2];
+#pragma unroll
+    for (int gg = 0; gg < 2; ++gg)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            cx[gg][b] = v[gg][b][0] * (1.0 - fx) + v[gg][b][1] * fx;
+            dx[gg][b] = v[gg][b][1] - v[gg][b][0];
+        }
+    double cy[2], dyv[2], dxv[2];
+#pragma unroll
+    for (int gg = 0; gg < 2; ++gg) {
+        cy[gg] = cx[gg][0] * (1.0 - fy) + cx[gg][1] * fy;
+        dyv[gg] = cx[gg][1] - cx[gg][0];
+        dxv[gg] = dx[gg][0] * (1.0 - fy) + dx[gg][1] * fy;
+    }
+    value = cy[0] * (1.0 - fz) + cy[1] * fz;
+    const double ggx = dxv[0] * (1.0 - fz) + dxv[1] * fz;
+    const double ggy = dyv[0] * (1.0 - fz) + dyv[1] * fz;
+    const double ggz = cy[1] - cy[0];
+    gx = __ddiv_rn(ggx, g.h[0]);
+    gy = __ddiv_rn(ggy, g.h[1]);
+    gz = __ddiv_rn(ggz, g.h[2]);
+}
+
+// transfer.cpp:56-83 — acc += ((wx*wy)*wz)*y over corners in (g,b,a) order from 0.0
+__device__ __forceinline__ void transfer_point(const DevPlan& P, const double* __restrict__ y, idx_t x, idx_t yy,
+                                               idx_t z, double out[3]) {
+    const idx_t bx = P.base[0][x], by = P.base[1][yy], bz = P.base[2][z];
+    const double rx = P.rem[0][x], ry = P.rem[1][yy], rz = P.rem[2][z];
+    const double wx[2] = {1.0 - rx, rx}, wy[2] = {1.0 - ry, ry}, wz[2] = {1.0 - rz, rz};
+    const idx_t ns = P.src.count();
+    const idx_t sm0 = P.src.m[0], sm01 = P.src.m[0] * P.src.m[1];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double* yd = y + d * ns;
+        double acc = 0.0;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const idx_t src = (bx + a) + (by + b) * sm0 + (bz + g) * sm01;
+                    acc += wx[a] * wy[b] * wz[g] * __ldg(&yd[src]);
+                }
+        out[d] = acc;
+    }
+}
+
+__global__ void k_transfer_apply(DevPlan P, const double* __restrict__ y, double* __restrict__ out) {
+    idx_t x, yy, z;
+    if (!coords(P.tgt, x, yy, z)) return;
+    double v[3];
+    transfer_point(P, y, x, yy, z, v);
+    const idx_t n = P.tgt.count(), i = P.tgt.lin(x, yy, z);
+    out[i] = v[0];
+    out[n + i] = v[1];
+    out[2 * n + i] = v[2];
+}
+
+__global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __restrict__ T, double* __restrict__ Tw,
+                       double* __restrict__ dT) {
+    idx_t x, yy, z;
+    if (!coords(P.tgt, x, yy, z)) return;
+    double v[3];
+    transfer_point(P, y, x, yy, z, v);
+    double val, gx, gy, gz;
+    interpolate(T, P.tgt, v[0], v[1], v[2], val, gx, gy, gz);
+    const idx_t n = P.tgt.count(), i = P.tgt.lin(x, yy, z);
+    Tw[i] = val;
+    dT[i] = gx;
+    dT[n + i] = gy;
+    dT[2 * n + i] = gz;
+}
+
+__global__ void k_sample(Grid g, const double* __restrict__ T, const double* __restrict__ pts, idx_t n,
+                         double* __restrict__ vals, double* __restrict__ dT) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double val, gx, gy, gz;
+    interpolate(T, g, pts[i], pts[n + i], pts[2 * n + i], val, gx, gy, gz);
+    vals[i] = val;
+    dT[i] = gx;
+    dT[n + i] = gy;
+    dT[2 * n + i] = gz;
+}
+
+// transfer.cpp:92-150 as a per-node gather in the reference's exact accumulation
+// order: odd deformation z-slab first, then even; inside a slab image planes,
+// rows, columns ascending; each term ((wx*wy)*wz)*v. Deterministic, no atomics.
+__global__ void k_transfer_T(DevPlan P, const double* __restrict__ w, double* __restrict__ out) {
+    idx_t nx, ny, nz;
+    if (!coords(P.src, nx, ny, nz)) return;
+    const idx_t nt = P.tgt.count(), ns = P.src.count();
+    const idx_t tm0 = P.tgt.m[0], tm01 = P.tgt.m[0] * P.tgt.m[1];
+    const idx_t ncx = P.src.m[0] - 1, ncy = P.src.m[1] - 1, ncz = P.src.m[2] - 1;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+    // slab order: the odd one of {nz-1, nz} first (phase 0), then the even one
+    idx_t slabs[2];
+    int ns_ = 0;
+    const idx_t s_lo = nz - 1, s_hi = nz;
+    if (s_lo >= 0 && (s_lo & 1)) slabs[ns_++] = s_lo;
+    if (s_hi < ncz && (s_hi & 1)) slabs[ns_++] = s_hi;
+    if (s_lo >= 0 && !(s_lo & 1)) slabs[ns_++] = s_lo;
+    if (s_hi < ncz && !(s_hi & 1)) slabs[ns_++] = s_hi;
+    for (int si = 0; si < ns_; ++si) {
+        const idx_t sl = slabs[si];
+        const bool gz1 = (sl == nz - 1);
+        for (idx_t kz = P.cell_lo[2][sl]; kz < P.cell_hi[2][sl]; ++kz) {
+            const double rz = P.rem[2][kz];
+            const double wz = gz1 ? rz : 1.0 - rz;
+            for (int cyi = 0; cyi < 2; ++cyi) {
+                const idx_t cy = ny - 1 + cyi;  // cell ny-1 (b=1) precedes cell ny (b=0)
+                if (cy < 0 || cy >= ncy) continue;
+                const bool b1 = (cyi == 0);
+                for (idx_t ky = P.cell_lo[1][cy]; ky < P.cell_hi[1][cy]; ++ky) {
+                    const double ry = P.rem[1][ky];
+                    const double wy = b1 ? ry : 1.0 - ry;
+                    for (int cxi = 0; cxi < 2; ++cxi) {
+                        const idx_t cx = nx - 1 + cxi;
+                        if (cx < 0 || cx >= ncx) continue;
+                        const bool ax1 = (cxi == 0);
+                        for (idx_t kx = P.cell_lo[0][cx]; kx < P.cell_hi[0][cx]; ++kx) {
+                            const double rx = P.rem[0][kx];
+                            const double wx = ax1 ? rx : 1.0 - rx;
+                            const double wgt = wx * wy * wz;
+                            const idx_t ti = kx + ky * tm0 + kz * tm01;
+                            a0 += wgt * __ldg(&w[ti]);
+                            a1 += wgt * __ldg(&w[nt + ti]);
+                            a2 += wgt * __ldg(&w[2 * nt + ti]);
+                        }
+                    }
+                }
+            }
+        }
+    }
+    const idx_t o = P.src.lin(nx, ny, nz);
+    out[o] = a0;
+    out[ns + o] = a1;
+    out[2 * ns + o] = a2;
+}
+
+// volume.cpp:115-121
+__device__ __forceinline__ double eps_norm6(const double g[6], double eps) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s += g[k] * g[k];
+    return sqrt(0.5 * s + eps * eps);
+}
+
+// volume.cpp:96-109 — backward x,y,z then forward x,y,z with clamped neighbours
+__device__ __forceinline__ void dgrad6(const double* __restrict__ v, const Grid& g, idx_t x, idx_t y, idx_t z,
+                                       double r[6]) {
+    const idx_t i = g.lin(x, y, z);
+    const double vi = __ldg(&v[i]);
+    const idx_t nb[6] = {g.lin(clampi(x - 1, g.m[0] - 1), y, z), g.lin(x, clampi(y - 1, g.m[1] - 1), z),
+                         g.lin(x, y, clampi(z - 1, g.m[2] - 1)), g.lin(clampi(x + 1, g.m[0] - 1), y, z),
+                         g.lin(x, clampi(y + 1, g.m[1] - 1), z), g.lin(x, y, clampi(z + 1, g.m[2] - 1))};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        r[a] = __ddiv_rn(vi - __ldg(&v[nb[a]]), g.h[a]);
+        r[a + 3] = __ddiv_rn(__ldg(&v[nb[a + 3]]) - vi, g.h[a]);
+    }
+}
+
+// ngf.cpp:185-214 (workspace) fused with ngf.cpp:39-64 (rho-hat for all 7
+// directions, stored direction-major rh[k*n+i]); rho-hat(0) summed over kAllDirs.
+__global__ void k_ngf_ws(Grid g, const double* __restrict__ R, const double* __restrict__ Tw, double tau, double rho,
+                         double* __restrict__ r, double* __restrict__ inv1o, double* __restrict__ inv2o,
+                         double* __restrict__ rh) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    double gt[6], gr[6];
+    dgrad6(Tw, g, x, y, z, gt);
+    dgrad6(R, g, x, y, z, gr);
+    const double tn = eps_norm6(gt, tau);
+    const double rn = eps_norm6(gr, rho);
+    double num = tau * rho;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) num += 0.5 * gt[c] * gr[c];
+    const double in1 = __ddiv_rn(1.0, tn * rn);
+    const double in2 = __ddiv_rn(num, tn * tn * tn * rn);
+    r[i] = num * in1;
+    if (inv1o) inv1o[i] = in1;
+    if (inv2o) inv2o[i] = in2;
+    double hh[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) hh[a] = __ddiv_rn(1.0, 2.0 * g.h[a] * g.h[a]);
+    double center = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        if (k == CENTER) continue;
+        const int a = dir_axis(k), sgn = dir_sign(k);
+        const int comp = sgn > 0 ? a + 3 : a;
+        const double h = g.h[a];
+        const double dR = static_cast<double>(sgn) * h * gr[comp];
+        const double dTv = static_cast<double>(sgn) * h * gt[comp];
+        const double v = hh[a] * (dR * in1 - dTv * in2);
+        rh[k * n + i] = v;
+        center -= v;
+    }
+    rh[CENTER * n + i] = center;
+}
+
+// ngf.cpp:66-103 (Alg. 4.1): acc = sum_k r_{i+k} rho-hat_{i+k}(-k), kAllDirs order;
+// out_d = (-2 h_bar * acc) * dT_d. 3-D neighbours: wrapped linear neighbours of the
+// reference contribute exact zeros (clamped rho-hat), so skipping them is bitwise neutral.
+__global__ void k_ngf_gradient(Grid g, double scale, const double* __restrict__ r, const double* __restrict__ rh,
+                               const double* __restrict__ dT, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const idx_t jx = x + dir_dx(k), jy = y + dir_dy(k), jz = z + dir_dz(k);
+        if (jx < 0 || jy < 0 || jz < 0 || jx >= g.m[0] || jy >= g.m[1] || jz >= g.m[2]) continue;
+        const idx_t j = g.lin(jx, jy, jz);
+        acc += __ldg(&r[j]) * __ldg(&rh[dir_opp(k) * n + j]);
+    }
+    const double s = scale * acc;
+    out[i] = s * dT[i];
+    out[n + i] = s * dT[n + i];
+    out[2 * n + i] = s * dT[2 * n + i];
+}
+
+__global__ void k_Pp_s(DevPlan P, const double* __restrict__ p, const double* __restrict__ dT,
+                       double* __restrict__ sv) {
+    idx_t x, yy, z;
+    if (!coords(P.tgt, x, yy, z)) return;
+    double v[3];
+    transfer_point(P, p, x, yy, z, v);
+    const idx_t n = P.tgt.count(), i = P.tgt.lin(x, yy, z);
+    sv[i] = dT[i] * v[0] + dT[n + i] * v[1] + dT[2 * n + i] * v[2];
+}
+
+// ngf.cpp:105-163 (Alg. 4.2) bit-identical: entries by ascending kappa, pairs in
+// (da, db) insertion order, drdr accumulated from 0.0, c = drdr * s, q += c * dT_i.
+__global__ void k_hv_closed(Grid g, HvTable tab, double scale, const double* __restrict__ rh,
+                            const double* __restrict__ sv, const double* __restrict__ dT, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    double qx = 0.0, qy = 0.0, qz = 0.0;
+    const double d0 = dT[i], d1 = dT[n + i], d2 = dT[2 * n + i];
+    for (int e = 0; e < tab.ngroups; ++e) {
+        const idx_t tx = x + tab.dx[e], ty = y + tab.dy[e], tz = z + tab.dz[e];
+        if (tx < 0 || ty < 0 || tz < 0 || tx >= g.m[0] || ty >= g.m[1] || tz >= g.m[2]) continue;
+        double drdr = 0.0;
+        for (int q = 0; q < tab.npairs[e]; ++q) {
+            const int da = tab.pa[e][q], db = tab.pb[e][q];
+            const idx_t ux = x + dir_dx(db), uy = y + dir_dy(db), uz = z + dir_dz(db);
+            if (ux < 0 || uy < 0 || uz < 0 || ux >= g.m[0] || uy >= g.m[1] || uz >= g.m[2]) continue;
+            const idx_t t = g.lin(ux, uy, uz);
+            drdr += __ldg(&rh[dir_opp(da) * n + t]) * __ldg(&rh[dir_opp(db) * n + t]);
+        }
+        const double c = drdr * __ldg(&sv[g.lin(tx, ty, tz)]);
+        qx += c * d0;
+        qy += c * d1;
+        qz += c * d2;
+    }
+    out[i] = scale * qx;
+    out[n + i] = scale * qy;
+    out[2 * n + i] = scale * qz;
+}
+
+// fast mode, pass 1: w_t = (dr s)_t = sum_k rho-hat_t(k) s_{t+k}
+__global__ void k_hv_w(Grid g, const double* __restrict__ rh, const double* __restrict__ sv, double* __restrict__ w) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const idx_t jx = x + dir_dx(k), jy = y + dir_dy(k), jz = z + dir_dz(k);
+        if (jx < 0 || jy < 0 || jz < 0 || jx >= g.m[0] || jy >= g.m[1] || jz >= g.m[2]) continue;
+        acc = fma(__ldg(&rh[k * n + i]), __ldg(&sv[g.lin(jx, jy, jz)]), acc);
+    }
+    w[i] = acc;
+}
+
+// fast mode, pass 2: z_i = (dr^T w)_i = sum_k rho-hat_{i+k}(-k) w_{i+k}; q_d = 2h z dT_d
+__global__ void k_hv_z(Grid g, double scale, const double* __restrict__ rh, const double* __restrict__ w,
+                       const double* __restrict__ dT, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+        const idx_t jx = x + dir_dx(k), jy = y + dir_dy(k), jz = z + dir_dz(k);
+        if (jx < 0 || jy < 0 || jz < 0 || jx >= g.m[0] || jy >= g.m[1] || jz >= g.m[2]) continue;
+        const idx_t j = g.lin(jx, jy, jz);
+        acc = fma(__ldg(&rh[dir_opp(k) * n + j]), __ldg(&w[j]), acc);
+    }
+    const double s = scale * acc;
+    out[i] = s * dT[i];
+    out[n + i] = s * dT[n + i];
+    out[2 * n + i] = s * dT[2 * n + i];
+}
+
+__device__ __forceinline__ double sum_term(int kind, const double* __restrict__ a, const double* __restrict__ b,
+                                           idx_t i) {
+    const double x = __ldg(&a[i]);
+    if (kind == SUM_ONE_MINUS_SQ) return 1.0 - x * x;
+    if (kind == SUM_DOT) return x * __ldg(&b[i]);
+    return x * x;
+}
+
+// parallel.cpp:51-73: one thread per 4096-element chunk, sequential partial sum
+__global__ void k_chunks(int kind, idx_t n, const double* __restrict__ a, const double* __restrict__ b,
+                         double* __restrict__ partials) {
+    const idx_t c = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    const idx_t nch = (n + kChunk - 1) / kChunk;
+    if (c >= nch) return;
+    const idx_t lo = c * kChunk, hi = min(n, lo + kChunk);
+    double s = 0.0;
+    for (idx_t i = lo; i < hi; ++i) s += sum_term(kind, a, b, i);
+    partials[c] = s;
+}
+
+// partials combined in chunk order (parallel.cpp:69-72), times `scale` (ngf.cpp:227)
+__global__ void k_serial(const double* __restrict__ partials, idx_t nch, double scale, double* __restrict__ out) {
+    if (threadIdx.x != 0) return;
+    double t = 0.0;
+    for (idx_t c = 0; c < nch; ++c) t += partials[c];
+    *out = scale * t;
+}
+
+constexpr int kTreeThreads = 256;
+constexpr int kTreePerThread = 16;
+constexpr idx_t kTreeSpan = static_cast<idx_t>(kTreeThreads) * kTreePerThread;
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double sh[32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) sh[wid] = v;
+    __syncthreads();
+    v = (threadIdx.x < (blockDim.x >> 5)) ? sh[threadIdx.x] : 0.0;
+    if (wid == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    }
+    return v;
+}
+
+__global__ void k_tree_partials(int kind, idx_t n, const double* __restrict__ a, const double* __restrict__ b,
+                                double* __restrict__ partials) {
+    const idx_t base = static_cast<idx_t>(blockIdx.x) * kTreeSpan;
+    double s = 0.0;
+#pragma unroll 4
+    for (int k = 0; k < kTreePerThread; ++k) {
+        const idx_t i = base + static_cast<idx_t>(k) * kTreeThreads + threadIdx.x;
+        if (i < n) s += sum_term(kind, a, b, i);
+    }
+    s = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void k_tree_final(const double* __restrict__ partials, idx_t nb, double scale, double* __restrict__ out) {
+    double s = 0.0;
+    for (idx_t k = threadIdx.x; k < nb; k += blockDim.x) s += partials[k];
+    s = block_sum(s);
+    if (threadIdx.x == 0) *out = scale * s;
+}
+
+__global__ void k_inf_norm_init(double* out) { *out = 0.0; }
+
+__global__ void k_inf_norm(idx_t n, const double* __restrict__ a, double scale, unsigned long long* out) {
+    double m = 0.0;
+    for (idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<idx_t>(gridDim.x) * blockDim.x) {
+        const double v = fabs(scale * a[i]);
+        m = (m < v) ? v : m;  // NaN never wins, as std::max(m, |x|)
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double v = __shfl_down_sync(0xffffffffu, m, o);
+        m = (m < v) ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
+}
+
+// curvature.cpp:9-21 — ((u- - 2u) + u+) / (h*h) summed over x, y, z from 0.0
+__device__ __forceinline__ double lap_at(const double* __restrict__ u, const Grid& g, idx_t x, idx_t y, idx_t z) {
+    const double ui = u[g.lin(x, y, z)];
+    double s = 0.0;
+    {
+        const double h = g.h[0];
+        s += (u[g.lin(clampi(x - 1, g.m[0] - 1), y, z)] - 2.0 * ui + u[g.lin(clampi(x + 1, g.m[0] - 1), y, z)]) /
+             (h * h);
+    }
+    {
+        const double h = g.h[1];
+        s += (u[g.lin(x, clampi(y - 1, g.m[1] - 1), z)] - 2.0 * ui + u[g.lin(x, clampi(y + 1, g.m[1] - 1), z)]) /
+             (h * h);
+    }
+    {
+        const double h = g.h[2];
+        s += (u[g.lin(x, y, clampi(z - 1, g.m[2] - 1))] - 2.0 * ui + u[g.lin(x, y, clampi(z + 1, g.m[2] - 1))]) /
+             (h * h);
+    }
+    return s;
+}
+
+__global__ void k_lap3(Grid g, const double* __restrict__ u, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) out[d * n + i] = lap_at(u + d * n, g, x, y, z);
+}
+
+// curvature.cpp:53-72 second pass (+ the alpha axpy of optimizer.cpp:84-89/98-103,
+// or the gamma shift of optimizer.cpp:106-111)
+__global__ void k_bilap(Grid g, const double* __restrict__ lu, double scale, int mode, double alpha, double gamma,
+                        const double* __restrict__ p, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double v = scale * lap_at(lu + d * n, g, x, y, z);
+        const idx_t o = d * n + i;
+        if (mode == 0) out[o] = v;
+        else if (mode == 1) out[o] += alpha * v;
+        else out[o] = v + gamma * p[o];
+    }
+}
+
+__global__ void k_curv_finalize(const double* __restrict__ S3, double cellvol, double alpha, double* out) {
+    double total = 0.0;
+    total += S3[0];
+    total += S3[1];
+    total += S3[2];
+    *out = alpha * (cellvol * total);
+}
+
+__global__ void k_add_scalars(const double* a, const double* b, double* out) { *out = *a + *b; }
+
+__global__ void k_sub(idx_t n, const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ o) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = a[i] - b[i];
+}
+__global__ void k_neg(idx_t n, const double* __restrict__ a, double* __restrict__ o) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = -a[i];
+}
+__global__ void k_axpy_to(idx_t n, const double* __restrict__ x, double a, const double* __restrict__ y,
+                          double* __restrict__ o) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = x[i] + a * y[i];
+}
+__global__ void k_cg_update(idx_t n, double alpha, const double* __restrict__ p, const double* __restrict__ ap,
+                            double* __restrict__ x, double* __restrict__ r) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) {
+        x[i] += alpha * p[i];
+        r[i] -= alpha * ap[i];
+    }
+}
+__global__ void k_scale_to(idx_t n, double a, const double* __restrict__ x, double* __restrict__ o) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) o[i] = a * x[i];
+}
+__global__ void k_scale_inplace(idx_t n, double a, double* __restrict__ x) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) x[i] *= a;
+}
+
+// grid.hpp:91-101 nodal coordinates, component-major (optimizer.cpp:52-62)
+__global__ void k_identity(Grid g, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const idx_t n = g.count(), i = g.lin(x, y, z);
+    out[i] = static_cast<double>(x) * g.h[0];
+    out[n + i] = static_cast<double>(y) * g.h[1];
+    out[2 * n + i] = static_cast<double>(z) * g.h[2];
+}
+
+// volume.cpp:123-160
+__global__ void k_downsample(Grid f, Grid c, const double* __restrict__ v, double* __restrict__ out) {
+    idx_t i, j, k;
+    if (!coords(c, i, j, k)) return;
+    double sum = 0.0;
+    int cnt = 0;
+    for (idx_t dz = 0; dz < 2; ++dz)
+        for (idx_t dy = 0; dy < 2; ++dy)
+            for (idx_t dx = 0; dx < 2; ++dx) {
+                const idx_t fi = 2 * i + dx, fj = 2 * j + dy, fk = 2 * k + dz;
+                if (fi < f.m[0] && fj < f.m[1] && fk < f.m[2]) {
+                    sum += v[f.lin(fi, fj, fk)];
+                    ++cnt;
+                }
+            }
+    out[c.lin(i, j, k)] = sum / cnt;
+}
+
+// multilevel.cpp:51-115 — u = y_c - x_c, y_f = x_f + nodal_interpolate(u, x_f)
+__global__ void k_prolong(Grid c, Grid f, const double* __restrict__ yc, double* __restrict__ yf) {
+    idx_t x, y, z;
+    if (!coords(f, x, y, z)) return;
+    const idx_t nf = f.count(), nc = c.count(), i = f.lin(x, y, z);
+    const double p[3] = {static_cast<double>(x) * f.h[0], static_cast<double>(y) * f.h[1],
+                         static_cast<double>(z) * f.h[2]};
+    idx_t b[3];
+    double w[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const idx_t ma = c.m[a];
+        double s = p[a] / c.h[a];
+        const double hi = static_cast<double>(ma - 1);
+        s = (s < 0.0) ? 0.0 : ((hi < s) ? hi : s);
+        idx_t base = static_cast<idx_t>(floor(s));
+        base = base < 0 ? 0 : (base > ma - 2 ? ma - 2 : base);
+        b[a] = base;
+        w[a] = s - static_cast<double>(base);
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double v = 0.0;
+        for (int cc = 0; cc < 2; ++cc)
+            for (int bb = 0; bb < 2; ++bb)
+                for (int aa = 0; aa < 2; ++aa) {
+                    const double weight =
+                        (aa ? w[0] : 1.0 - w[0]) * (bb ? w[1] : 1.0 - w[1]) * (cc ? w[2] : 1.0 - w[2]);
+                    const idx_t gx = b[0] + aa, gy = b[1] + bb, gz = b[2] + cc;
+                    const double xc = d == 0 ? static_cast<double>(gx) * c.h[0]
+                                             : (d == 1 ? static_cast<double>(gy) * c.h[1]
+                                                       : static_cast<double>(gz) * c.h[2]);
+                    const double u = yc[d * nc + c.lin(gx, gy, gz)] - xc;
+                    v += weight * u;
+                }
+        yf[d * nf + i] = p[d] + v;
+    }
+}
+
+// synthetic.cpp:15-63 (device libm: values agree with glibc to a few ulp; inputs
+// are generated once and shared by every arm that consumes them)
+__device__ __forceinline__ double soft_step(double x, double width) { return 1.0 / (1.0 + exp(-x / width)); }
+
+__global__ void k_phantom(Grid g, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    const double p[3] = {(static_cast<double>(x) + 0.5) * g.h[0], (static_cast<double>(y) + 0.5) * g.h[1],
+                         (static_cast<double>(z) + 0.5) * g.h[2]};
+    const double e[3] = {static_cast<double>(g.m[0]) * g.h[0], static_cast<double>(g.m[1]) * g.h[1],
+                         static_cast<double>(g.m[2]) * g.h[2]};
+    const double scale = fmin(fmin(e[0], e[1]), e[2]);
+    const double edge = 0.015 * scale;
+    const double sc[5][3] = {{0.35, 0.4, 0.45}, {0.68, 0.62, 0.40}, {0.55, 0.30, 0.68}, {0.30, 0.70, 0.62},
+                             {0.72, 0.35, 0.70}};
+    const double sr[5] = {0.22, 0.14, 0.10, 0.08, 0.06};
+    const double sw[5] = {1.0, -0.7, 0.8, 0.6, -0.5};
+    double val = 0.1 * (p[0] / e[0]) * (p[1] / e[1]);
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        double d2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double diff = p[a] - sc[s][a] * e[a];
+            d2 += diff * diff;
+        }
+        val += sw[s] * soft_step(sr[s] * scale - sqrt(d2), edge);
+    }
+    const double plane = (p[0] / e[0] + p[1] / e[1] + p[2] / e[2]) / 3.0 - 0.55;
+    val += 0.4 * soft_step(-fabs(plane) + 0.04, 0.01);
+    const double pi = 3.141592653589793;
+    const double tx = 2.0 * pi * p[0] / e[0];
+    const double ty = 2.0 * pi * p[1] / e[1];
+    const double tz = 2.0 * pi * p[2] / e[2];
+    val += 0.12 * sin(3.0 * tx + 0.8 * sin(2.0 * ty)) * cos(2.0 * ty + 0.6 * sin(3.0 * tz)) +
+           0.08 * cos(4.0 * tz + 0.7 * sin(2.0 * tx)) * sin(3.0 * ty + 0.5 * cos(2.0 * tx));
+    out[g.lin(x, y, z)] = val;
+}
+
+// synthetic.cpp:92-108 + 145-159
+__global__ void k_warp_with(Grid g, WarpTerms w, const double* __restrict__ T, double* __restrict__ out) {
+    idx_t x, y, z;
+    if (!coords(g, x, y, z)) return;
+    double p[3] = {(static_cast<double>(x) + 0.5) * g.h[0], (static_cast<double>(y) + 0.5) * g.h[1],
+                   (static_cast<double>(z) + 0.5) * g.h[2]};
+    const double pi = 3.141592653589793;
+    double u[3] = {0.0, 0.0, 0.0};
+    for (int t = 0; t < 3; ++t)
+        for (int d = 0; d < 3; ++d) {
+            double v = w.amp[t][d];
+            for (int a = 0; a < 3; ++a) {
+                const double xx = p[a] / w.extent[a];
+                v *= sin(pi * w.freq[t][a] * xx + w.phase[t][a] * xx * (1.0 - xx));
+            }
+            u[d] += v;
+        }
+    for (int d = 0; d < 3; ++d) p[d] += u[d];
+    double val, gx, gy, gz;
+    interpolate(T, g, p[0], p[1], p[2], val, gx, gy, gz);
+    out[g.lin(x, y, z)] = val;
+}
+
+std::atomic<long long> g_launches{0};
+
+}  // namespace
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+long long launch_counter() { return g_launches.load(); }
+
+// ------------------------------------------------------------------ host side
+
+HvTable make_hv_table(const Grid& g) {
+    // ngf.cpp:267-300: kappa = mu(db) - mu(da), grouped; groups ordered by kappa
+    // (std::map), pairs in (da outer, db inner) order. Grouping by 3-D offset
+    // instead of linear kappa only separates groups that collide on degenerate
+    // grids, and for every voxel at most one of a colliding set is non-zero.
+    auto mu = [&](int d) -> long long {
+        switch (d) {
+        case NEGZ: return -g.m[0] * g.m[1];
+        case NEGY: return -g.m[0];
+        case NEGX: return -1;
+        case CENTER: return 0;
+        case POSX: return 1;
+        case POSY: return g.m[0];
+        default: return g.m[0] * g.m[1];
+        }
+    };
+    struct G3 {
+        int dx, dy, dz;
+        long long kappa;
+        int first;
+        std::vector<std::pair<int, int>> pairs;
+    };
+    std::vector<G3> groups;
+    int order = 0;
+    for (int da = 0; da < 7; ++da)
+        for (int db = 0; db < 7; ++db) {
+            const int dx = dir_dx(db) - dir_dx(da), dy = dir_dy(db) - dir_dy(da), dz = dir_dz(db) - dir_dz(da);
+            auto it = std::find_if(groups.begin(), groups.end(),
+                                   [&](const G3& q) { return q.dx == dx && q.dy == dy && q.dz == dz; });
+            if (it == groups.end()) {
+                groups.push_back({dx, dy, dz, mu(db) - mu(da), order++, {}});
+                it = groups.end() - 1;
+            }
+            it->pairs.emplace_back(da, db);
+        }
+    std::stable_sort(groups.begin(), groups.end(), [](const G3& a, const G3& b) { return a.kappa < b.kappa; });
+    HvTable t{};
+    t.ngroups = static_cast<int>(groups.size());
+    for (int e = 0; e < t.ngroups; ++e) {
+        t.dx[e] = groups[e].dx;
+        t.dy[e] = groups[e].dy;
+        t.dz[e] = groups[e].dz;
+        t.npairs[e] = static_cast<int>(groups[e].pairs.size());
+        for (int q = 0; q < t.npairs[e]; ++q) {
+            t.pa[e][q] = groups[e].pairs[q].first;
+            t.pb[e][q] = groups[e].pairs[q].second;
+        }
+    }
+    return t;
+}
+
+void launch_transfer_apply(const DevPlan& P, const double* y, double* out, cudaStream_t s) {
+    note_launch(), k_transfer_apply<<<grid3(P.tgt), block3(), 0, s>>>(P, y, out);
+}
+void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s) {
+    note_launch(), k_transfer_T<<<grid3(P.src), block3(), 0, s>>>(P, w, out);
+}
+void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n, double* vals, double* dT,
+                   cudaStream_t s) {
+    note_launch(), k_sample<<<blocks1(n), 256, 0, s>>>(img, T, pts, n, vals, dT);
+}
+void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s) {
+    note_launch(), k_warp<<<grid3(P.tgt), block3(), 0, s>>>(P, y, T, Tw, dT);
+}
+void launch_ngf_ws(const Grid& img, const double* R, const double* Tw, double tau, double rho, double* r,
+                   double* inv1, double* inv2, double* rh, cudaStream_t s) {
+    note_launch(), k_ngf_ws<<<grid3(img), block3(), 0, s>>>(img, R, Tw, tau, rho, r, inv1, inv2, rh);
+}
+void launch_ngf_gradient(const Grid& img, const double* r, const double* rh, const double* dT, double* out,
+                         cudaStream_t s) {
+    const double scale = -2.0 * img.cell_volume();
+    note_launch(), k_ngf_gradient<<<grid3(img), block3(), 0, s>>>(img, scale, r, rh, dT, out);
+}
+void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv, cudaStream_t s) {
+    note_launch(), k_Pp_s<<<grid3(P.tgt), block3(), 0, s>>>(P, p, dT, sv);
+}
+void launch_hv_closed(const Grid& img, const HvTable& tab, const double* rh, const double* sv, const double* dT,
+                      double* out, cudaStream_t s) {
+    const double scale = 2.0 * img.cell_volume();
+    note_launch(), k_hv_closed<<<grid3(img), block3(), 0, s>>>(img, tab, scale, rh, sv, dT, out);
+}
+void launch_hv_factored(const Grid& img, const double* rh, const double* sv, const double* dT, double* wbuf,
+                        double* out, cudaStream_t s) {
+    const double scale = 2.0 * img.cell_volume();
+    note_launch(), k_hv_w<<<grid3(img), block3(), 0, s>>>(img, rh, sv, wbuf);
+    note_launch(), k_hv_z<<<grid3(img), block3(), 0, s>>>(img, scale, rh, wbuf, dT, out);
+}
+
+idx_t chunk_count(idx_t n) { return (n + kChunk - 1) / kChunk; }
+idx_t tree_blocks(idx_t n) { return std::max<idx_t>(1, (n + kTreeSpan - 1) / kTreeSpan); }
+
+void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
+                        double scale, cudaStream_t s) {
+    const idx_t nch = chunk_count(n);
+    if (nch > 0) note_launch(), k_chunks<<<blocks1(nch, 128), 128, 0, s>>>(kind, n, a, b, partials);
+    note_launch(), k_serial<<<1, 32, 0, s>>>(partials, nch, scale, out);
+}
+void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
+                     double scale, cudaStream_t s) {
+    const idx_t nb = tree_blocks(n);
+    note_launch(), k_tree_partials<<<static_cast<unsigned>(nb), kTreeThreads, 0, s>>>(kind, n, a, b, partials);
+    note_launch(), k_tree_final<<<1, 1024, 0, s>>>(partials, nb, scale, out);
+}
+void launch_inf_norm(idx_t n, const double* a, double scale, double* out, cudaStream_t s) {
+    note_launch(), k_inf_norm_init<<<1, 1, 0, s>>>(out);
+    const unsigned nb = static_cast<unsigned>(std::min<idx_t>(blocks1(n), 148 * 8));
+    note_launch(), k_inf_norm<<<nb, 256, 0, s>>>(n, a, scale, reinterpret_cast<unsigned long long*>(out));
+}
+
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s) {
+    note_launch(), k_lap3<<<grid3(g), block3(), 0, s>>>(g, u, out);
+}
+void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
+                  const double* p, double* out, cudaStream_t s) {
+    note_launch(), k_bilap<<<grid3(g), block3(), 0, s>>>(g, lap_u, scale, mode, alpha, gamma, p, out);
+}
+void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s) {
+    note_launch(), k_curv_finalize<<<1, 1, 0, s>>>(S3, cellvol, alpha, out);
+}
+void launch_add_scalars(const double* a, const double* b, double* out, cudaStream_t s) {
+    note_launch(), k_add_scalars<<<1, 1, 0, s>>>(a, b, out);
+}
+void launch_sub(idx_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+    note_launch(), k_sub<<<blocks1(n), 256, 0, s>>>(n, a, b, out);
+}
+void launch_neg(idx_t n, const double* a, double* out, cudaStream_t s) { note_launch(), k_neg<<<blocks1(n), 256, 0, s>>>(n, a, out); }
+void launch_axpy_to(idx_t n, const double* x, double a, const double* y, double* out, cudaStream_t s) {
+    note_launch(), k_axpy_to<<<blocks1(n), 256, 0, s>>>(n, x, a, y, out);
+}
+void launch_cg_update(idx_t n, double alpha, const double* p, const double* ap, double* x, double* r,
+                      cudaStream_t s) {
+    note_launch(), k_cg_update<<<blocks1(n), 256, 0, s>>>(n, alpha, p, ap, x, r);
+}
+void launch_scale_to(idx_t n, double a, const double* x, double* out, cudaStream_t s) {
+    note_launch(), k_scale_to<<<blocks1(n), 256, 0, s>>>(n, a, x, out);
+}
+void launch_scale_inplace(idx_t n, double a, double* x, cudaStream_t s) {
+    note_launch(), k_scale_inplace<<<blocks1(n), 256, 0, s>>>(n, a, x);
+}
+void launch_identity(const Grid& g, double* out, cudaStream_t s) { note_launch(), k_identity<<<grid3(g), block3(), 0, s>>>(g, out); }
+void launch_downsample(const Grid& fine, const Grid& coarse, const double* v, double* out, cudaStream_t s) {
+    note_launch(), k_downsample<<<grid3(coarse), block3(), 0, s>>>(fine, coarse, v, out);
+}
+void launch_prolong(const Grid& coarse, const Grid& fine, const double* yc, double* yf, cudaStream_t s) {
+    note_launch(), k_prolong<<<grid3(fine), block3(), 0, s>>>(coarse, fine, yc, yf);
+}
+void launch_phantom(const Grid& g, double* out, cudaStream_t s) { note_launch(), k_phantom<<<grid3(g), block3(), 0, s>>>(g, out); }
+void launch_warp_with(const Grid& g, const WarpTerms& w, const double* T, double* out, cudaStream_t s) {
+    note_launch(), k_warp_with<<<grid3(g), block3(), 0, s>>>(g, w, T, out);
+}
+
+}  // namespace mfreg_b200

@@ -1,0 +1,241 @@
+// DeviceObjective and its building blocks (see objective.cuh).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "objective.cuh"
+
+namespace mfreg_b200 {
+
+void check_launch(const char* what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void validate_grid(const Grid& g, bool nodal) {  // grid.hpp:103-119
+    for (int a = 0; a < 3; ++a) {
+        if (g.m[a] < 1) throw std::invalid_argument("GridDesc: all m components must be >= 1");
+        if (!(g.h[a] > 0.0)) throw std::invalid_argument("GridDesc: all h components must be > 0");
+    }
+    if (nodal)
+        for (int a = 0; a < 3; ++a)
+            if (g.m[a] < 2) throw std::invalid_argument("GridDesc: nodal grids need >= 2 points per axis");
+}
+
+Grid make_deform_grid(const Grid& image, const idx_t points[3]) {  // grid.hpp:131-146
+    Grid g{};
+    for (int a = 0; a < 3; ++a) {
+        g.m[a] = points[a];
+        if (points[a] < 2) throw std::invalid_argument("deformation grid needs >= 2 points per axis");
+        if (points[a] - 1 > image.m[a]) throw std::invalid_argument("deformation grid finer than image grid");
+        g.h[a] = (static_cast<double>(image.m[a]) * image.h[a]) / static_cast<double>(points[a] - 1);
+    }
+    return g;
+}
+
+Grid deformation_grid_for(const Grid& image, idx_t ratio) {  // multilevel.cpp:39-49
+    if (ratio < 1) throw std::invalid_argument("deformation_grid_for: ratio must be >= 1");
+    idx_t pts[3];
+    for (int a = 0; a < 3; ++a) pts[a] = std::max<idx_t>(2, (image.m[a] + ratio - 1) / ratio + 1);
+    return make_deform_grid(image, pts);
+}
+
+DevicePlanOwner::DevicePlanOwner(const Grid& nodal, const Grid& image) {
+    validate_grid(nodal, true);
+    validate_grid(image, false);
+    view_.src = nodal;
+    view_.tgt = image;
+    for (int a = 0; a < 3; ++a) {
+        const idx_t mt = image.m[a], ms = nodal.m[a];
+        auto& hb = host_base[a];
+        auto& hr = host_rem[a];
+        hb.resize(mt);
+        hr.resize(mt);
+        for (idx_t k = 0; k < mt; ++k) {  // transfer.cpp:24-39, same expression
+            const double c = (static_cast<double>(k) + 0.5) * static_cast<double>(ms - 1) / static_cast<double>(mt);
+            idx_t b = static_cast<idx_t>(std::floor(c));
+            b = std::clamp<idx_t>(b, 0, ms - 2);
+            hb[k] = static_cast<int>(b);
+            hr[k] = c - static_cast<double>(b);
+            if (hr[k] < 0.0 || hr[k] > 1.0) throw std::invalid_argument("transfer plan: coverage invariant violated");
+        }
+        std::vector<int> lo(ms - 1, 0), hi(ms - 1, 0);
+        for (idx_t k = 0; k < mt; ++k) {
+            const int c = hb[k];
+            if (lo[c] == hi[c]) lo[c] = static_cast<int>(k);
+            hi[c] = static_cast<int>(k) + 1;
+        }
+        base_[a].resize(mt);
+        rem_[a].resize(mt);
+        lo_[a].resize(ms - 1);
+        hi_[a].resize(ms - 1);
+        MFREG_CUDA(cudaMemcpy(base_[a].get(), hb.data(), mt * sizeof(int), cudaMemcpyHostToDevice));
+        MFREG_CUDA(cudaMemcpy(rem_[a].get(), hr.data(), mt * sizeof(double), cudaMemcpyHostToDevice));
+        MFREG_CUDA(cudaMemcpy(lo_[a].get(), lo.data(), (ms - 1) * sizeof(int), cudaMemcpyHostToDevice));
+        MFREG_CUDA(cudaMemcpy(hi_[a].get(), hi.data(), (ms - 1) * sizeof(int), cudaMemcpyHostToDevice));
+        view_.base[a] = base_[a].get();
+        view_.rem[a] = rem_[a].get();
+        view_.cell_lo[a] = lo_[a].get();
+        view_.cell_hi[a] = hi_[a].get();
+    }
+}
+
+Reducer::Reducer(Mode mode, idx_t max_n) : mode_(mode) {
+    partials_.resize(static_cast<std::size_t>(std::max<idx_t>(16, std::max(chunk_count(max_n), tree_blocks(max_n)))));
+}
+
+void Reducer::sum(int kind, idx_t n, const double* a, const double* b, double* out_dev, double scale,
+                  cudaStream_t s) {
+    const idx_t need = mode_ == Mode::Parity ? chunk_count(n) : tree_blocks(n);
+    if (static_cast<std::size_t>(need) > partials_.size()) partials_.resize(static_cast<std::size_t>(need));
+    if (mode_ == Mode::Parity) launch_chunked_sum(kind, n, a, b, partials_.get(), out_dev, scale, s);
+    else launch_tree_sum(kind, n, a, b, partials_.get(), out_dev, scale, s);
+    check_launch("reduction");
+}
+
+Scalars::Scalars(int n) : d_(static_cast<std::size_t>(n)) {
+    MFREG_CUDA(cudaMallocHost(&h_, n * sizeof(double)));
+    MFREG_CUDA(cudaMemset(d_.get(), 0, n * sizeof(double)));
+}
+Scalars::~Scalars() {
+    if (h_) cudaFreeHost(h_);
+}
+const double* Scalars::fetch(int n, cudaStream_t s) {
+    MFREG_CUDA(cudaMemcpyAsync(h_, d_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    MFREG_CUDA(cudaStreamSynchronize(s));
+    return h_;
+}
+
+// ------------------------------------------------------------------ DeviceNgf
+DeviceNgf::DeviceNgf(const Grid& img, const double* R_dev, double tau, double rho, Mode mode, cudaStream_t s)
+    : g_(img), tau_(tau), rho_(rho), mode_(mode), s_(s), R_(R_dev), red_(mode, img.count()) {
+    if (!(rho > 0.0)) throw std::invalid_argument("NGF: rho must be > 0");  // ngf.cpp:168-170
+    const std::size_t n = static_cast<std::size_t>(img.count());
+    Tw.resize(n);
+    dT.resize(3 * n);
+    r.resize(n);
+    inv1.resize(n);
+    inv2.resize(n);
+    rh.resize(7 * n);
+    sv.resize(n);
+    if (mode == Mode::Fast) wbuf.resize(n);
+    tab_ = make_hv_table(img);
+}
+
+void DeviceNgf::populate_points(const double* T_dev, const double* pts_dev) {
+    if (!(tau_ > 0.0) || !(rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
+    launch_sample(g_, T_dev, pts_dev, g_.count(), Tw.get(), dT.get(), s_);
+    launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_);
+    check_launch("populate_ngf_workspace");
+}
+
+void DeviceNgf::populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev) {
+    if (!(tau_ > 0.0) || !(rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
+    launch_warp(P, y_dev, T_dev, Tw.get(), dT.get(), s_);
+    launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_);
+    check_launch("warp + workspace");
+}
+
+void DeviceNgf::value_async(double* out_dev) {
+    red_.sum(SUM_ONE_MINUS_SQ, g_.count(), r.get(), nullptr, out_dev, g_.cell_volume(), s_);
+}
+
+void DeviceNgf::gradient(double* out3n) {
+    launch_ngf_gradient(g_, r.get(), rh.get(), dT.get(), out3n, s_);
+    check_launch("ngf_gradient");
+}
+
+void DeviceNgf::hessian_vec_image(const double* svp, double* out3n) {
+    if (mode_ == Mode::Parity) launch_hv_closed(g_, tab_, rh.get(), svp, dT.get(), out3n, s_);
+    else launch_hv_factored(g_, rh.get(), svp, dT.get(), wbuf.get(), out3n, s_);
+    check_launch("ngf_hessian_vec");
+}
+
+namespace {
+__global__ void k_dot3(long long n, const double* __restrict__ dT, const double* __restrict__ p,
+                       double* __restrict__ sv) {
+    const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) sv[i] = dT[i] * p[i] + dT[n + i] * p[n + i] + dT[2 * n + i] * p[2 * n + i];
+}
+}  // namespace
+
+void DeviceNgf::hessian_vec(const double* p3n, double* out3n) {
+    const idx_t n = g_.count();
+    note_launch(), k_dot3<<<static_cast<unsigned>((n + 255) / 256), 256, 0, s_>>>(n, dT.get(), p3n, sv.get());
+    hessian_vec_image(sv.get(), out3n);
+}
+
+// ------------------------------------------------------------ DeviceObjective
+DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform,
+                                 double tau, double rho, double alpha, Mode mode, cudaStream_t s)
+    : img_(image),
+      dg_(deform),
+      alpha_(alpha),
+      s_(s),
+      T_(T_dev),
+      plan_(deform, image),
+      ngf_(image, R_dev, tau, rho, mode, s) {
+    const std::size_t ny = static_cast<std::size_t>(dg_.count());
+    xid_.resize(3 * ny);
+    u_.resize(3 * ny);
+    lapu_.resize(3 * ny);
+    lapp_.resize(3 * ny);
+    img3_.resize(3 * static_cast<std::size_t>(img_.count()));
+    launch_identity(dg_, xid_.get(), s_);
+    check_launch("identity");
+}
+
+double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
+
+// optimizer.cpp:64-92
+double DeviceObjective::eval(const double* y, double* grad) {
+    const idx_t ny = dg_.count();
+    ngf_.populate_warp(plan_.view(), y, T_);
+    ngf_.value_async(sc_.dev(0));
+    launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
+    launch_lap3(dg_, u_.get(), lapu_.get(), s_);
+    for (int d = 0; d < 3; ++d) ngf_.reducer().sum(SUM_SQ, ny, lapu_.get() + d * ny, nullptr, sc_.dev(4 + d), 1.0, s_);
+    launch_curv_finalize(sc_.dev(4), dg_.cell_volume(), alpha_, sc_.dev(1), s_);
+    if (grad) {
+        ngf_.gradient(img3_.get());
+        launch_transfer_T(plan_.view(), img3_.get(), grad, s_);
+        if (alpha_ != 0.0) launch_bilap(dg_, lapu_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, grad, s_);
+    }
+    check_launch("Objective::eval");
+    const double* h = sc_.fetch(2, s_);
+    last_distance_ = h[0];
+    last_regularizer_ = h[1];
+    return last_distance_ + last_regularizer_;
+}
+
+// optimizer.cpp:94-104
+void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
+    launch_Pp_s(plan_.view(), p, ngf_.dT.get(), ngf_.sv.get(), s_);
+    ngf_.hessian_vec_image(ngf_.sv.get(), img3_.get());
+    launch_transfer_T(plan_.view(), img3_.get(), q, s_);
+    if (alpha_ != 0.0) {
+        launch_lap3(dg_, p, lapp_.get(), s_);
+        launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, q, s_);
+    }
+    check_launch("Objective::gn_hessian_vec");
+}
+
+// optimizer.cpp:106-111
+void DeviceObjective::seed_hessian_vec(const double* p, double gamma, double* q) {
+    launch_lap3(dg_, p, lapp_.get(), s_);
+    launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 2, 0.0, gamma, p, q, s_);
+    check_launch("Objective::seed_hessian_vec");
+}
+
+double DeviceObjective::dot(const double* a, const double* b) {
+    ngf_.reducer().sum(SUM_DOT, dof(), a, b, sc_.dev(8), 1.0, s_);
+    return sc_.fetch(9, s_)[8];
+}
+
+double DeviceObjective::inf_norm(const double* a, double scale) {
+    launch_inf_norm(dof(), a, scale, sc_.dev(10), s_);
+    check_launch("inf_norm");
+    return sc_.fetch(11, s_)[10];
+}
+
+}  // namespace mfreg_b200

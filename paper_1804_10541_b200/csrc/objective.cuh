@@ -1,0 +1,270 @@
+// Host-side C++ runtime for the device-resident hot path: device buffers, the
+// transfer plan, the NGF state, DeviceObjective (reference Objective,
+// optimizer.hpp:53-106), the device-resident solvers (optimizer.cpp:113-407) and
+// the multilevel driver (multilevel.cpp:117-145).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <deque>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace mfreg_b200 {
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define MFREG_CUDA(call)                                                                                  \
+    do {                                                                                                  \
+        cudaError_t e_ = (call);                                                                          \
+        if (e_ != cudaSuccess)                                                                            \
+            throw ::mfreg_b200::CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));          \
+    } while (0)
+
+void check_launch(const char* what);
+
+enum class Mode : int { Parity = 0, Fast = 1 };
+
+// RAII device array of doubles (or raw bytes).
+template <typename T>
+class DevArray {
+public:
+    DevArray() = default;
+    explicit DevArray(std::size_t n) { resize(n); }
+    ~DevArray() { release(); }
+    DevArray(const DevArray&) = delete;
+    DevArray& operator=(const DevArray&) = delete;
+    DevArray(DevArray&& o) noexcept : p_(o.p_), n_(o.n_) {
+        o.p_ = nullptr;
+        o.n_ = 0;
+    }
+    DevArray& operator=(DevArray&& o) noexcept {
+        if (this != &o) {
+            release();
+            p_ = o.p_;
+            n_ = o.n_;
+            o.p_ = nullptr;
+            o.n_ = 0;
+        }
+        return *this;
+    }
+    void resize(std::size_t n) {
+        if (n == n_) return;
+        release();
+        if (n) MFREG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        n_ = n;
+    }
+    void release() {
+        if (p_) cudaFree(p_);
+        p_ = nullptr;
+        n_ = 0;
+    }
+    T* get() { return p_; }
+    const T* get() const { return p_; }
+    std::size_t size() const { return n_; }
+
+private:
+    T* p_ = nullptr;
+    std::size_t n_ = 0;
+};
+using DVec = DevArray<double>;
+
+// Validation mirroring grid.hpp:103-146 (messages identical to the reference).
+void validate_grid(const Grid& g, bool nodal);
+Grid make_deform_grid(const Grid& image, const idx_t points[3]);
+Grid deformation_grid_for(const Grid& image, idx_t ratio);
+
+// transfer.cpp:11-47 computed on the host bit-identically, uploaded once per level.
+class DevicePlanOwner {
+public:
+    DevicePlanOwner(const Grid& nodal, const Grid& image);
+    const DevPlan& view() const { return view_; }
+    std::vector<int> host_base[3];
+    std::vector<double> host_rem[3];
+
+private:
+    DevArray<int> base_[3], lo_[3], hi_[3];
+    DVec rem_[3];
+    DevPlan view_{};
+};
+
+// Reduction helpers: exact 4096-chunk order (parity) or fixed-order tree (fast).
+class Reducer {
+public:
+    Reducer(Mode mode, idx_t max_n);
+    // device result into out_dev (scaled)
+    void sum(int kind, idx_t n, const double* a, const double* b, double* out_dev, double scale, cudaStream_t s);
+    Mode mode() const { return mode_; }
+
+private:
+    Mode mode_;
+    DVec partials_;
+};
+
+// Scalar staging: a few device doubles mirrored into pinned host memory.
+class Scalars {
+public:
+    explicit Scalars(int n = 32);
+    ~Scalars();
+    double* dev(int i) { return d_.get() + i; }
+    // copies [0, n) to host and synchronises the stream
+    const double* fetch(int n, cudaStream_t s);
+
+private:
+    DVec d_;
+    double* h_ = nullptr;
+};
+
+// Abstract problem the device-resident solvers drive (reference Problem,
+// optimizer.hpp:36-48), with the vector-space operations the solvers need so a
+// sharded implementation can reduce across GPUs.
+class DeviceProblem {
+public:
+    virtual ~DeviceProblem() = default;
+    virtual idx_t dof() const = 0;  // local length of y
+    virtual double eval(const double* y, double* grad) = 0;
+    virtual void gn_hessian_vec(const double* p, double* q) = 0;
+    virtual void seed_hessian_vec(const double* p, double gamma, double* q) = 0;
+    virtual double min_spacing() const = 0;
+    virtual double alpha() const = 0;
+    virtual double last_distance() const = 0;
+    virtual double last_regularizer() const = 0;
+    virtual double dot(const double* a, const double* b) = 0;  // vec_dot (optimizer.cpp:12-19)
+    virtual double inf_norm(const double* a, double scale) = 0;  // max |scale * a_i|
+    virtual cudaStream_t stream() const = 0;
+    double norm(const double* a) { return std::sqrt(dot(a, a)); }
+};
+
+// NGF state on the image grid: reference image (+ its owner), sampled template
+// state and the per-iterate workspace (ngf.hpp:21-37).
+class DeviceNgf {
+public:
+    DeviceNgf(const Grid& img, const double* R_dev, double tau, double rho, Mode mode, cudaStream_t s);
+    // populate from explicit sample points (ngf.cpp:185-214), both device pointers
+    void populate_points(const double* T_dev, const double* pts_dev);
+    // populate from the nodal deformation (transfer_apply + populate fused)
+    void populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev);
+    void value_async(double* out_dev);                 // D (ngf.cpp:225-231)
+    void gradient(double* out3n);                      // dD/dP (ngf.cpp:66-103)
+    void hessian_vec_image(const double* sv, double* out3n);  // from s = dT.(P p)
+    void hessian_vec(const double* p3n, double* out3n);        // image-grid p (ngf.cpp:253-258)
+    const Grid& grid() const { return g_; }
+    Mode mode() const { return mode_; }
+    cudaStream_t stream() const { return s_; }
+    Reducer& reducer() { return red_; }
+
+    Grid g_;
+    double tau_, rho_;
+    Mode mode_;
+    cudaStream_t s_;
+    const double* R_;  // borrowed
+    DVec Tw, dT, r, inv1, inv2, rh, sv, wbuf;
+    HvTable tab_;
+    Reducer red_;
+};
+
+class DeviceObjective : public DeviceProblem {
+public:
+    // R_dev/T_dev: device arrays over `image` that must outlive the objective
+    // (the reference Objective also stores references, optimizer.hpp:87-88).
+    DeviceObjective(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform, double tau,
+                    double rho, double alpha, Mode mode, cudaStream_t s);
+    idx_t dof() const override { return 3 * dg_.count(); }
+    double eval(const double* y, double* grad) override;
+    void gn_hessian_vec(const double* p, double* q) override;
+    void seed_hessian_vec(const double* p, double gamma, double* q) override;
+    double min_spacing() const override;
+    double alpha() const override { return alpha_; }
+    double last_distance() const override { return last_distance_; }
+    double last_regularizer() const override { return last_regularizer_; }
+    double dot(const double* a, const double* b) override;
+    double inf_norm(const double* a, double scale) override;
+    cudaStream_t stream() const override { return s_; }
+    const double* identity_dev() const { return xid_.get(); }
+    const Grid& image_grid() const { return img_; }
+    const Grid& deform_grid() const { return dg_; }
+    DeviceNgf& ngf() { return ngf_; }
+    const DevicePlanOwner& plan() const { return plan_; }
+
+private:
+    Grid img_, dg_;
+    double alpha_;
+    cudaStream_t s_;
+    const double* T_;
+    DevicePlanOwner plan_;
+    DeviceNgf ngf_;
+    DVec xid_, u_, lapu_, lapp_, img3_;
+    Scalars sc_;
+    double last_distance_ = 0.0, last_regularizer_ = 0.0;
+};
+
+// ---- solvers (optimizer.hpp:108-166), vectors on the device
+struct CgConfig {
+    int max_iters = 50;
+    double rel_tol = 1e-2;
+};
+struct CgResult {
+    int iters = 0;
+    double relres = 0.0;
+    bool breakdown = false;
+};
+struct ArmijoConfig {
+    double c1 = 1e-4;
+    double beta = 0.5;
+    int max_backtracks = 10;
+};
+struct OptimizerConfig {
+    int max_iters = 20;
+    ArmijoConfig armijo{};
+    CgConfig cg{50, 1e-2};
+    CgConfig h0_cg{20, 1e-2};
+    int lbfgs_history = 5;
+    double gamma = -1.0;
+    double tol_rel_j = 1e-4;
+    double tol_grad = 1e-4;
+    double tol_step = 1e-3;
+};
+struct IterationRecord {
+    int iter = 0;
+    int cg_iters = 0;
+    double j = 0.0, distance = 0.0, regularizer = 0.0, grad_norm = 0.0, step = 0.0;
+};
+struct MinimizeResult {
+    std::vector<IterationRecord> trace;
+    bool line_search_failed = false;
+};
+
+// op: 0 = Gauss-Newton operator, 1 = L-BFGS seed (Hess S + gamma I)
+CgResult cg_solve(DeviceProblem& P, int op, double gamma, const double* b, double* x, const CgConfig& cfg);
+MinimizeResult gauss_newton_minimize(DeviceProblem& P, const double* y0, double* y, const OptimizerConfig& cfg);
+MinimizeResult lbfgs_minimize(DeviceProblem& P, const double* y0, double* y, const OptimizerConfig& cfg);
+
+enum class Method : int { Lbfgs = 0, GaussNewton = 1 };
+struct MultilevelConfig {
+    int levels = 3;
+    idx_t deform_ratio = 4;
+    double tau = 10.0, rho = 10.0;
+    double alpha = 1.0;
+    Method method = Method::Lbfgs;
+    Mode mode = Mode::Parity;
+    OptimizerConfig opt{};
+};
+struct LevelResult {
+    Grid image_grid, deform_grid;
+    MinimizeResult result;
+};
+struct MultilevelResult {
+    DVec y;
+    Grid deform_grid;
+    std::vector<LevelResult> levels;  // coarsest first
+};
+MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, const Grid& image,
+                                     const MultilevelConfig& cfg, cudaStream_t s);
+
+}  // namespace mfreg_b200

@@ -1,0 +1,291 @@
+// Device-resident solvers (reference optimizer.cpp:113-407) and the multilevel
+// driver (multilevel.cpp:9-145). All vectors stay in HBM; only the scalars the
+// reference's control flow branches on cross to the host.
+#include <algorithm>
+#include <cmath>
+#include <deque>
+
+#include "objective.cuh"
+
+namespace mfreg_b200 {
+
+namespace {
+
+struct Work {
+    explicit Work(idx_t n) : n(n) {}
+    idx_t n;
+    DVec make() { return DVec(static_cast<std::size_t>(n)); }
+};
+
+double effective_gamma(const OptimizerConfig& cfg, double alpha) {  // optimizer.cpp:179-181
+    return cfg.gamma >= 0.0 ? cfg.gamma : 1e-3 * std::max(1.0, alpha);
+}
+
+bool should_stop(const OptimizerConfig& cfg, double g0, double min_hy, double j_prev, double j_cur, double gnorm,
+                 double step_inf) {  // optimizer.cpp:188-200
+    if (gnorm <= cfg.tol_grad * g0) return true;
+    if (std::abs(j_prev - j_cur) <= cfg.tol_rel_j * std::max(1.0, std::abs(j_prev))) return true;
+    if (step_inf <= cfg.tol_step * min_hy) return true;
+    return false;
+}
+
+void apply_op(DeviceProblem& P, int op, double gamma, const double* v, double* out) {
+    if (op == 1) P.seed_hessian_vec(v, gamma, out);
+    else P.gn_hessian_vec(v, out);
+}
+
+// optimizer.cpp:156-175 with phi(eta) = J(y + eta d), value-only evaluation
+bool armijo_search(DeviceProblem& P, const double* y, const double* dir, double* y_trial, double f0, double gdotd,
+                   const ArmijoConfig& cfg, double eta0, double& eta_out) {
+    if (!(gdotd < 0.0)) return false;
+    double eta = eta0;
+    for (int k = 0; k <= cfg.max_backtracks; ++k) {
+        launch_axpy_to(P.dof(), y, eta, dir, y_trial, P.stream());
+        const double f = P.eval(y_trial, nullptr);
+        if (std::isfinite(f) && f <= f0 + cfg.c1 * eta * gdotd) {
+            eta_out = eta;
+            return true;
+        }
+        eta *= cfg.beta;
+    }
+    return false;
+}
+
+}  // namespace
+
+// optimizer.cpp:113-154 — plain CG, x0 = 0
+CgResult cg_solve(DeviceProblem& P, int op, double gamma, const double* b, double* x, const CgConfig& cfg) {
+    const idx_t n = P.dof();
+    cudaStream_t s = P.stream();
+    CgResult res;
+    MFREG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
+    const double bnorm = P.norm(b);
+    if (bnorm == 0.0) return res;
+    DVec r(static_cast<std::size_t>(n)), p(static_cast<std::size_t>(n)), ap(static_cast<std::size_t>(n));
+    MFREG_CUDA(cudaMemcpyAsync(r.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MFREG_CUDA(cudaMemcpyAsync(p.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    MFREG_CUDA(cudaMemsetAsync(ap.get(), 0, n * sizeof(double), s));
+    double rr = P.dot(r.get(), r.get());
+    for (int it = 0; it < cfg.max_iters; ++it) {
+        apply_op(P, op, gamma, p.get(), ap.get());
+        const double pap = P.dot(p.get(), ap.get());
+        if (!std::isfinite(pap) || pap <= 0.0) {
+            res.breakdown = !std::isfinite(pap);
+            break;
+        }
+        const double alpha = rr / pap;
+        launch_cg_update(n, alpha, p.get(), ap.get(), x, r.get(), s);
+        ++res.iters;
+        const double rr_new = P.dot(r.get(), r.get());
+        res.relres = std::sqrt(rr_new) / bnorm;
+        if (!std::isfinite(rr_new)) {
+            res.breakdown = true;
+            break;
+        }
+        if (res.relres <= cfg.rel_tol) break;
+        const double beta = rr_new / rr;
+        launch_axpy_to(n, r.get(), beta, p.get(), p.get(), s);
+        rr = rr_new;
+    }
+    check_launch("cg_solve");
+    return res;
+}
+
+// optimizer.cpp:202-268 + 392-407
+MinimizeResult gauss_newton_minimize(DeviceProblem& P, const double* y0, double* y, const OptimizerConfig& cfg) {
+    const idx_t n = P.dof();
+    cudaStream_t s = P.stream();
+    MinimizeResult out;
+    MFREG_CUDA(cudaMemcpyAsync(y, y0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (cfg.max_iters <= 0) return out;
+    DVec grad(n), dir(n), y_trial(n), b(n);
+    double j = P.eval(y, grad.get());
+    const double g0 = P.norm(grad.get());
+    const double min_hy = P.min_spacing();
+    for (int it = 0; it < cfg.max_iters; ++it) {
+        IterationRecord rec;
+        rec.iter = it;
+        rec.j = j;
+        rec.distance = P.last_distance();
+        rec.regularizer = P.last_regularizer();
+        rec.grad_norm = P.norm(grad.get());
+        if (rec.grad_norm <= cfg.tol_grad * g0) {
+            out.trace.push_back(rec);
+            break;
+        }
+        launch_neg(n, grad.get(), b.get(), s);
+        const CgResult sol = cg_solve(P, 0, 0.0, b.get(), dir.get(), cfg.cg);
+        rec.cg_iters = sol.iters;
+        const double gdotd = P.dot(grad.get(), dir.get());
+        const double dinf = P.inf_norm(dir.get(), 1.0);
+        const double eta0 = dinf > 0.0 ? std::min(1.0, P.min_spacing() / dinf) : 1.0;
+        double eta = 0.0;
+        if (!armijo_search(P, y, dir.get(), y_trial.get(), j, gdotd, cfg.armijo, eta0, eta)) {
+            out.line_search_failed = true;
+            out.trace.push_back(rec);
+            break;
+        }
+        rec.step = eta;
+        const double j_prev = j;
+        launch_axpy_to(n, y, eta, dir.get(), y, s);
+        const double step_inf = P.inf_norm(dir.get(), eta);
+        j = P.eval(y, grad.get());
+        out.trace.push_back(rec);
+        if (should_stop(cfg, g0, min_hy, j_prev, j, P.norm(grad.get()), step_inf)) break;
+    }
+    return out;
+}
+
+// optimizer.cpp:272-390
+MinimizeResult lbfgs_minimize(DeviceProblem& P, const double* y0, double* y, const OptimizerConfig& cfg) {
+    const idx_t n = P.dof();
+    cudaStream_t s = P.stream();
+    const double gamma = effective_gamma(cfg, P.alpha());
+    const int hist = std::max(1, cfg.lbfgs_history);
+    MinimizeResult out;
+    MFREG_CUDA(cudaMemcpyAsync(y, y0, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    if (cfg.max_iters <= 0) return out;
+
+    // history slots: hist + 1 (one is filled before the oldest is popped)
+    std::vector<DVec> S, Yv;
+    for (int k = 0; k < hist + 1; ++k) {
+        S.emplace_back(static_cast<std::size_t>(n));
+        Yv.emplace_back(static_cast<std::size_t>(n));
+    }
+    struct Pair {
+        int slot;
+        double rho;
+    };
+    std::deque<Pair> history;
+    auto free_slot = [&]() {
+        for (int k = 0; k < hist + 1; ++k) {
+            bool used = false;
+            for (const auto& p : history) used |= (p.slot == k);
+            if (!used) return k;
+        }
+        return 0;
+    };
+
+    DVec grad(n), grad_new(n), dir(n), y_trial(n), q(n), r(n);
+    std::vector<double> alphas;
+    double j = P.eval(y, grad.get());
+    const double g0 = P.norm(grad.get());
+    const double min_hy = P.min_spacing();
+
+    for (int it = 0; it < cfg.max_iters; ++it) {
+        IterationRecord rec;
+        rec.iter = it;
+        rec.j = j;
+        rec.distance = P.last_distance();
+        rec.regularizer = P.last_regularizer();
+        rec.grad_norm = P.norm(grad.get());
+        if (rec.grad_norm <= cfg.tol_grad * g0) {
+            out.trace.push_back(rec);
+            break;
+        }
+        // two-loop recursion, optimizer.cpp:285-312
+        MFREG_CUDA(cudaMemcpyAsync(q.get(), grad.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        alphas.assign(history.size(), 0.0);
+        for (std::size_t k = history.size(); k-- > 0;) {
+            const auto& hp = history[k];
+            alphas[k] = hp.rho * P.dot(S[hp.slot].get(), q.get());
+            launch_axpy_to(n, q.get(), -alphas[k], Yv[hp.slot].get(), q.get(), s);
+        }
+        const CgResult h0 = cg_solve(P, 1, gamma, q.get(), r.get(), cfg.h0_cg);
+        for (std::size_t k = 0; k < history.size(); ++k) {
+            const auto& hp = history[k];
+            const double beta = hp.rho * P.dot(Yv[hp.slot].get(), r.get());
+            launch_axpy_to(n, r.get(), alphas[k] - beta, S[hp.slot].get(), r.get(), s);
+        }
+        launch_neg(n, r.get(), dir.get(), s);
+        rec.cg_iters = h0.iters;
+        const double gdotd = P.dot(grad.get(), dir.get());
+        const double dinf = P.inf_norm(dir.get(), 1.0);
+        const double eta0 = dinf > 0.0 ? std::min(1.0, P.min_spacing() / dinf) : 1.0;
+        double eta = 0.0;
+        if (!armijo_search(P, y, dir.get(), y_trial.get(), j, gdotd, cfg.armijo, eta0, eta)) {
+            out.line_search_failed = true;
+            out.trace.push_back(rec);
+            break;
+        }
+        rec.step = eta;
+        const double j_prev = j;
+        const int slot = free_slot();
+        double* sv = S[slot].get();
+        double* yv = Yv[slot].get();
+        launch_scale_to(n, eta, dir.get(), sv, s);  // s = eta*dir
+        launch_axpy_to(n, y, 1.0, sv, y, s);        // y += s (1.0*s is exact)
+        const double step_inf = P.inf_norm(sv, 1.0);
+        j = P.eval(y, grad_new.get());
+        launch_sub(n, grad_new.get(), grad.get(), yv, s);
+        const double sy = P.dot(sv, yv);
+        if (sy > 1e-10 * P.norm(sv) * P.norm(yv)) {
+            history.push_back({slot, 1.0 / sy});
+            while (static_cast<int>(history.size()) > hist) history.pop_front();
+        }
+        std::swap(grad, grad_new);
+        out.trace.push_back(rec);
+        if (should_stop(cfg, g0, min_hy, j_prev, j, P.norm(grad.get()), step_inf)) break;
+    }
+    return out;
+}
+
+// multilevel.cpp:9-37 (pyramid), :117-145 (driver), :78-115 (prolong)
+MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, const Grid& image,
+                                     const MultilevelConfig& cfg, cudaStream_t s) {
+    if (cfg.levels < 1) throw std::invalid_argument("build_pyramid: levels must be >= 1");
+    validate_grid(image, false);
+    for (int a = 0; a < 3; ++a) {
+        idx_t m = image.m[a];
+        for (int l = 1; l < cfg.levels; ++l) {
+            if (m < 2) throw std::invalid_argument("build_pyramid: too many levels for this size");
+            m = (m + 1) / 2;
+        }
+        if (m < 2) throw std::invalid_argument("build_pyramid: too many levels for this size");
+    }
+    std::vector<Grid> G(cfg.levels);
+    std::vector<DVec> R(cfg.levels), T(cfg.levels);
+    G[0] = image;
+    for (int l = 1; l < cfg.levels; ++l) {
+        for (int a = 0; a < 3; ++a) {
+            G[l].m[a] = (G[l - 1].m[a] + 1) / 2;
+            G[l].h[a] = 2.0 * G[l - 1].h[a];
+        }
+        R[l].resize(static_cast<std::size_t>(G[l].count()));
+        T[l].resize(static_cast<std::size_t>(G[l].count()));
+        const double* rp = l == 1 ? R_dev : R[l - 1].get();
+        const double* tp = l == 1 ? T_dev : T[l - 1].get();
+        launch_downsample(G[l - 1], G[l], rp, R[l].get(), s);
+        launch_downsample(G[l - 1], G[l], tp, T[l].get(), s);
+    }
+    check_launch("build_pyramid");
+
+    MultilevelResult out;
+    DVec y, y0;
+    Grid prev{};
+    bool have_prev = false;
+    for (int l = cfg.levels - 1; l >= 0; --l) {
+        const Grid dg = deformation_grid_for(G[l], cfg.deform_ratio);
+        const double* rp = l == 0 ? R_dev : R[l].get();
+        const double* tp = l == 0 ? T_dev : T[l].get();
+        DeviceObjective obj(rp, tp, G[l], dg, cfg.tau, cfg.rho, cfg.alpha, cfg.mode, s);
+        y0.resize(static_cast<std::size_t>(obj.dof()));
+        if (have_prev) launch_prolong(prev, dg, y.get(), y0.get(), s);
+        else MFREG_CUDA(cudaMemcpyAsync(y0.get(), obj.identity_dev(), obj.dof() * sizeof(double),
+                                        cudaMemcpyDeviceToDevice, s));
+        check_launch("prolong");
+        DVec yl(static_cast<std::size_t>(obj.dof()));
+        MinimizeResult res = cfg.method == Method::Lbfgs ? lbfgs_minimize(obj, y0.get(), yl.get(), cfg.opt)
+                                                         : gauss_newton_minimize(obj, y0.get(), yl.get(), cfg.opt);
+        MFREG_CUDA(cudaStreamSynchronize(s));
+        y = std::move(yl);
+        out.levels.push_back({G[l], dg, std::move(res)});
+        prev = dg;
+        have_prev = true;
+    }
+    out.y = std::move(y);
+    out.deform_grid = prev;
+    return out;
+}
+
+}  // namespace mfreg_b200
