@@ -1,0 +1,89 @@
+// Fused `fast`-mode kernels: one pass over the image grid per operator, with the
+// grid transfer P / P^T folded in, plus one small nodal finalize kernel.
+//
+// Factored Gauss-Newton product. With the directional
+// coefficients rho-hat_t(k) = h^_a (dR_k inv1_t - dT_k inv2_t), dX_k = X_{t+k} - X_t
+// (ngf.cpp:39-64; zero across the domain boundary, clamped neighbours) and
+// rho-hat_t(0) = -sum_k rho-hat_t(k) =: -sigma_t, the reference's closed-form
+// H^ p^ = 2h dT dr^T dr (dT . p^) (ngf.cpp:105-163) factors as
+//   w_t = (dr s)_t   = sum_k rho-hat_t(k) (s_{t+k} - s_t),           s = dT . P p
+//   z_i = (dr^T w)_i = sum_k rho-hat_{i+k}(-k) w_{i+k} - sigma_i w_i
+// and the NGF gradient (ngf.cpp:66-103) is -2h dT (dr^T r). The eval pass stores
+// the six rho-hat per voxel (48 B) next to dT (24 B); every Hv then streams
+// 72 B/voxel and needs ~40 flops/voxel.
+//
+// Execution: 2.5D column marching. A CTA owns a 32x8 output tile and a z range;
+// threads map to the tile columns first (warps 0-7), then the 1-voxel halo ring,
+// then the 2-voxel halo ring. Each thread marches its column in z with the
+// column's history in registers; only the in-plane neighbour data lives in
+// shared memory. Loads of plane k+1 are issued before plane k is processed.
+// P p is separable per column (x-y weights fixed, z blend per plane). P^T
+// accumulates z weights per column in registers and spreads over x-y in
+// shared memory once per completed nodal plane; per-tile partials are summed
+// per node in a fixed order by the finalize kernel (deterministic, no atomics).
+#pragma once
+
+#include "objective.cuh"
+
+namespace mfreg_b200 {
+
+constexpr int FT_X = 32;  // output tile (x) per CTA
+constexpr int FT_Y = 8;   // output tile (y) per CTA
+
+// Host-computed tiling of the image grid and the per-tile nodal footprints.
+struct TileMeta {
+    int ntx, nty, ntz;          // tiles per axis
+    int zc;                     // z planes per tile
+    int nlx, nly, nlz;          // max local nodes per tile per axis
+    std::size_t part_stride;    // doubles per tile partial (nlz*nly*nlx*3)
+    const int* node_tlo[3];     // per node: first touching tile
+    const int* node_thi[3];     // per node: last touching tile
+    const int* tile_n0[3];      // per tile: first local node (global index)
+};
+
+class FusedPlan {
+public:
+    explicit FusedPlan(const DevicePlanOwner& plan);
+    const TileMeta& meta() const { return meta_; }
+    double* partials() { return part_.get(); }
+    double* value_partials() { return vpart_.get(); }
+    double* red() { return red_.get(); }
+    unsigned int* counter() { return counter_.get(); }
+    int ntiles() const { return meta_.ntx * meta_.nty * meta_.ntz; }
+
+private:
+    TileMeta meta_{};
+    DevArray<int> tlo_[3], thi_[3], n0_[3];
+    DVec part_, vpart_, red_;
+    DevArray<unsigned int> counter_;
+};
+
+// Direction order of the stored coefficients: -x, +x, -y, +y, -z, +z.
+constexpr int kRhoDirs = 6;
+
+// Gauss-Newton Hv image pass: s = dT . P p -> w -> z -> q^ = 2h z dT -> P^T partials.
+void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
+                     cudaStream_t s);
+
+// Eval image pass on the warped state (T_w, dT from launch_warp): rho-hat (6 per
+// voxel, stored as Hv state), per-tile sums of (1 - r^2) and, when `grad`, the
+// NGF gradient -2h dT (dr^T r) spread by P^T into per-tile partials.
+void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
+                       double tau, double rho, double* frh, bool grad, cudaStream_t s);
+
+// Nodal finalize (one launch):
+//   out != null: out = gather(P^T partials) [+ alpha 2 h^y Lap(Lap v) when v != null];
+//   dot_a != null: sc[0] = <dot_a, out>;
+//   value: sc[0] = h D-sum over tiles, sc[1] = alpha h^y sum (Lap u)^2 with u = v (eval);
+// all reductions fixed-order (last-block pattern).
+struct FinalizeSpec {
+    const double* v = nullptr;  // curvature operand (p for Hv, u = y - x for eval)
+    double alpha = 0.0;
+    double* out = nullptr;      // nodal result
+    const double* dot_a = nullptr;
+    bool value = false;         // eval: D and S into sc[0], sc[1]
+    double* sc = nullptr;       // device scalars
+};
+void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s);
+
+}  // namespace mfreg_b200

@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "objective.cuh"
+#include "fused.cuh"
 
 namespace mfreg_b200 {
 
@@ -113,16 +114,26 @@ DeviceNgf::DeviceNgf(const Grid& img, const double* R_dev, double tau, double rh
     const std::size_t n = static_cast<std::size_t>(img.count());
     Tw.resize(n);
     dT.resize(3 * n);
+    if (mode == Mode::Parity) ensure_ws();
+    else frh.resize(6 * n);
+    tab_ = make_hv_table(img);
+}
+
+void DeviceNgf::ensure_ws() {
+    // per-voxel workspace of the unfused kernels (parity mode, and the kernel-level
+    // NGF API in either mode); the fused fast-mode objective only keeps frh.
+    const std::size_t n = static_cast<std::size_t>(g_.count());
+    if (r.size() == n) return;
     r.resize(n);
     inv1.resize(n);
     inv2.resize(n);
     rh.resize(7 * n);
     sv.resize(n);
-    if (mode == Mode::Fast) wbuf.resize(n);
-    tab_ = make_hv_table(img);
+    if (mode_ == Mode::Fast) wbuf.resize(n);
 }
 
 void DeviceNgf::populate_points(const double* T_dev, const double* pts_dev) {
+    ensure_ws();
     if (!(tau_ > 0.0) || !(rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
     launch_sample(g_, T_dev, pts_dev, g_.count(), Tw.get(), dT.get(), s_);
     launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_);
@@ -130,6 +141,7 @@ void DeviceNgf::populate_points(const double* T_dev, const double* pts_dev) {
 }
 
 void DeviceNgf::populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev) {
+    ensure_ws();
     if (!(tau_ > 0.0) || !(rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
     launch_warp(P, y_dev, T_dev, Tw.get(), dT.get(), s_);
     launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_);
@@ -183,13 +195,35 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     img3_.resize(3 * static_cast<std::size_t>(img_.count()));
     launch_identity(dg_, xid_.get(), s_);
     check_launch("identity");
+    if (mode == Mode::Fast) fused_ = std::make_unique<FusedPlan>(plan_);
 }
+
+DeviceObjective::~DeviceObjective() = default;
 
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
 
 // optimizer.cpp:64-92
 double DeviceObjective::eval(const double* y, double* grad) {
     const idx_t ny = dg_.count();
+    if (fused_) {
+        if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
+        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
+        launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
+        launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, ngf_.frh.get(),
+                          grad != nullptr, s_);
+        FinalizeSpec f;
+        f.v = u_.get();
+        f.alpha = alpha_;
+        f.out = grad;
+        f.value = true;
+        f.sc = sc_.dev(0);
+        launch_nodal_finalize(plan_, *fused_, f, s_);
+        check_launch("Objective::eval (fused)");
+        const double* h = sc_.fetch(2, s_);
+        last_distance_ = h[0];
+        last_regularizer_ = h[1];
+        return last_distance_ + last_regularizer_;
+    }
     ngf_.populate_warp(plan_.view(), y, T_);
     ngf_.value_async(sc_.dev(0));
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
@@ -210,6 +244,16 @@ double DeviceObjective::eval(const double* y, double* grad) {
 
 // optimizer.cpp:94-104
 void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
+    if (fused_) {
+        launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
+        FinalizeSpec f;
+        f.v = alpha_ != 0.0 ? p : nullptr;
+        f.alpha = alpha_;
+        f.out = q;
+        launch_nodal_finalize(plan_, *fused_, f, s_);
+        check_launch("Objective::gn_hessian_vec (fused)");
+        return;
+    }
     launch_Pp_s(plan_.view(), p, ngf_.dT.get(), ngf_.sv.get(), s_);
     ngf_.hessian_vec_image(ngf_.sv.get(), img3_.get());
     launch_transfer_T(plan_.view(), img3_.get(), q, s_);

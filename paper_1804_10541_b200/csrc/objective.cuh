@@ -6,8 +6,10 @@
 
 #include <cuda_runtime.h>
 
+#include <cmath>
 #include <cstdint>
 #include <deque>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -147,6 +149,7 @@ class DeviceNgf {
 public:
     DeviceNgf(const Grid& img, const double* R_dev, double tau, double rho, Mode mode, cudaStream_t s);
     // populate from explicit sample points (ngf.cpp:185-214), both device pointers
+    void ensure_ws();
     void populate_points(const double* T_dev, const double* pts_dev);
     // populate from the nodal deformation (transfer_apply + populate fused)
     void populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev);
@@ -165,6 +168,7 @@ public:
     cudaStream_t s_;
     const double* R_;  // borrowed
     DVec Tw, dT, r, inv1, inv2, rh, sv, wbuf;
+    DVec frh;  // fast mode: rho-hat [6][n] (-x,+x,-y,+y,-z,+z), the Hv state
     HvTable tab_;
     Reducer red_;
 };
@@ -175,6 +179,7 @@ public:
     // (the reference Objective also stores references, optimizer.hpp:87-88).
     DeviceObjective(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform, double tau,
                     double rho, double alpha, Mode mode, cudaStream_t s);
+    ~DeviceObjective() override;
     idx_t dof() const override { return 3 * dg_.count(); }
     double eval(const double* y, double* grad) override;
     void gn_hessian_vec(const double* p, double* q) override;
@@ -200,6 +205,7 @@ private:
     DevicePlanOwner plan_;
     DeviceNgf ngf_;
     DVec xid_, u_, lapu_, lapp_, img3_;
+    std::unique_ptr<class FusedPlan> fused_;  // fast mode: fused single-pass kernels
     Scalars sc_;
     double last_distance_ = 0.0, last_regularizer_ = 0.0;
 };
