@@ -1,7 +1,12 @@
 // Fused fast-mode kernels (see fused.cuh for the algebra and execution scheme).
 #include <algorithm>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <vector>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "fused.cuh"
 
@@ -9,11 +14,23 @@ namespace mfreg_b200 {
 
 namespace {
 
-constexpr int CX = FT_X + 4, CY = FT_Y + 4, NC = CX * CY;  // columns incl. 2-voxel halo (432)
-constexpr int NTH = 448;                                     // threads per CTA (>= NC, multiple of 32)
+constexpr int CX = FT_X + 4, CY = FT_Y + 4, NC = CX * CY;  // halo-2 column region (36 x 12 = 432)
+constexpr int C1X = FT_X + 2, C1Y = FT_Y + 2, NC1 = C1X * C1Y;  // halo-1 region (34 x 10 = 340)
 constexpr int TT = FT_X * FT_Y;                              // output columns (256)
-constexpr int NH1 = (FT_X + 2) * (FT_Y + 2);                 // columns incl. 1-voxel halo (340)
+// warp-aligned thread roles: tile (warps 0-7), halo-1 ring (warps 8-10), halo-2 ring (warps 11-13)
+constexpr int R1_0 = TT, R1_N = NC1 - TT;                    // 84 halo-1 ring columns
+constexpr int R2_0 = 352, R2_N = NC - NC1;                   // 92 halo-2 ring columns
+constexpr int NTH = 448;
+constexpr int DEPTH = 4;                                     // staging ring (TMA, loads 2 planes ahead)
+constexpr int NSLAB = 8;                                     // nodal-slab ring (planes, power of 2)
+constexpr int PAD = CX + 1;                                  // guard around the plane buffers
+constexpr int NB = NC + 2 * PAD;
 constexpr int kSMs = 148;
+// staging slot layouts (bytes, 128-aligned): TMA boxes land as [comp][y][x]
+constexpr int HV_DT = 3 * NC;                  // doubles: dT box 36x12x3
+constexpr int HV_RH = 6 * NC;                  // doubles: rho-hat box 36x12x6
+constexpr int HV_SLOT = HV_DT + HV_RH;         // 3888 doubles = 31104 B
+constexpr int EV_SLOT = 5 * NC;                // R, T_w, dT(3) boxes 36x12: 2160 doubles = 17280 B
 
 struct FArgs {
     Grid g;
@@ -32,125 +49,84 @@ struct FArgs {
     double* part;
     double* vpart;
     int grad;
+    int nxf, nyf;       // nodal slab footprint (max over tiles) per plane, x and y
+    int dbg;            // profiling switches (0 in production)
+};
+
+struct TmaMaps {
+    CUtensorMap a, b, c;  // Hv: dT, rho-hat; eval: R, T_w, dT
 };
 
 __device__ __forceinline__ double lerp(double t, double a, double b) { return fma(t, b - a, a); }
 
-// bilinear x-y interpolation of the 3 nodal components on nodal plane nz at a fixed column
-__device__ __forceinline__ void bilerp3(const double* __restrict__ p, long long ns, long long sm0, long long sm01,
-                                        int bx, int by, int nz, double rx, double ry, double out[3]) {
-    const long long c = bx + by * sm0 + nz * sm01;
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        const double* q = p + d * ns + c;
-        const double v0 = lerp(rx, __ldg(q), __ldg(q + 1));
-        const double v1 = lerp(rx, __ldg(q + sm0), __ldg(q + sm0 + 1));
-        out[d] = lerp(ry, v0, v1);
-    }
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// one elected lane of a converged warp (TMA must be issued from warp-uniform control flow)
+__device__ __forceinline__ bool elect_one() {
+    unsigned pred = 0;
+    asm volatile(
+        "{\n\t.reg .pred P;\n\t.reg .b32 r;\n\telect.sync r|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+        : "=r"(pred));
+    return pred != 0;
 }
 
-// Per-CTA precomputed task of the x-y spread (P^T in x then y): which local
-// node / row a thread reduces and the clipped voxel ranges of its two cells.
-struct SpreadTask {
-    int xrow, xl, xlo1, xhi1, xlo0, xhi0;  // x-collapse: row, local node, ranges for cells nx-1 (w = r), nx (w = 1-r)
-    int yl, yx, ylo1, yhi1, ylo0, yhi0;    // y-collapse: local node y, local node x, ranges
-    bool xon, yon;
-};
-
-__device__ SpreadTask make_spread_task(const DevPlan& P, int x0, int y0, int xe, int ye, int nxA, int nyA, int nlx_t,
-                                       int nly_t) {
-    SpreadTask t{};
-    const int tid = threadIdx.x;
-    const int nsx = static_cast<int>(P.src.m[0]) - 1, nsy = static_cast<int>(P.src.m[1]) - 1;
-    t.xon = tid < FT_Y * nlx_t;
-    if (t.xon) {
-        t.xrow = tid / nlx_t;
-        t.xl = tid % nlx_t;
-        const int nx = nxA + t.xl;
-        t.xlo1 = t.xhi1 = t.xlo0 = t.xhi0 = x0;
-        if (nx >= 1 && nx - 1 < nsx) {
-            t.xlo1 = max(x0, __ldg(&P.cell_lo[0][nx - 1]));
-            t.xhi1 = max(t.xlo1, min(xe, __ldg(&P.cell_hi[0][nx - 1])));
-        }
-        if (nx < nsx) {
-            t.xlo0 = max(x0, __ldg(&P.cell_lo[0][nx]));
-            t.xhi0 = max(t.xlo0, min(xe, __ldg(&P.cell_hi[0][nx])));
-        }
-        if (y0 + t.xrow >= ye) t.xhi1 = t.xlo1, t.xhi0 = t.xlo0;
-    }
-    t.yon = tid < nly_t * nlx_t;
-    if (t.yon) {
-        t.yl = tid / nlx_t;
-        t.yx = tid % nlx_t;
-        const int ny = nyA + t.yl;
-        t.ylo1 = t.yhi1 = t.ylo0 = t.yhi0 = y0;
-        if (ny >= 1 && ny - 1 < nsy) {
-            t.ylo1 = max(y0, __ldg(&P.cell_lo[1][ny - 1]));
-            t.yhi1 = max(t.ylo1, min(ye, __ldg(&P.cell_hi[1][ny - 1])));
-        }
-        if (ny < nsy) {
-            t.ylo0 = max(y0, __ldg(&P.cell_lo[1][ny]));
-            t.yhi0 = max(t.ylo0, min(ye, __ldg(&P.cell_hi[1][ny])));
-        }
-    }
-    return t;
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z, int w,
+                                            unsigned long long* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+            "r"(smem_u32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
+        : "memory");
 }
 
-// x-y spread of the per-column nodal-plane accumulators into the tile partial
-// (P^T in x and y; z weights were applied per column). Called by all threads.
-__device__ __noinline__ void spread_plane(const SpreadTask& st, const double* sremx, const double* sremy, double* sQ,
-                                             double* sQx, int nlx, const double acc[3], bool tile, int tcol, int x0,
-                                             int y0, double* dst) {
-    if (tile) {
-        sQ[tcol] = acc[0];
-        sQ[TT + tcol] = acc[1];
-        sQ[2 * TT + tcol] = acc[2];
-    }
-    __syncthreads();
-    if (st.xon) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double* q = sQ + d * TT + st.xrow * FT_X;
-            double s = 0.0;
-            for (int x = st.xlo1; x < st.xhi1; ++x) s = fma(sremx[x - x0], q[x - x0], s);
-            for (int x = st.xlo0; x < st.xhi0; ++x) s = fma(1.0 - sremx[x - x0], q[x - x0], s);
-            sQx[(d * FT_Y + st.xrow) * nlx + st.xl] = s;
-        }
-    }
-    __syncthreads();
-    if (st.yon) {
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const double* q = sQx + d * FT_Y * nlx + st.yx;
-            double s = 0.0;
-            for (int y = st.ylo1; y < st.yhi1; ++y) s = fma(sremy[y - y0], q[(y - y0) * nlx], s);
-            for (int y = st.ylo0; y < st.yhi0; ++y) s = fma(1.0 - sremy[y - y0], q[(y - y0) * nlx], s);
-            dst[(st.yl * nlx + st.yx) * 3 + d] = s;
-        }
-    }
-    __syncthreads();
-}
-
-// Shared-memory plane buffers are padded by PAD doubles on both sides so that
-// every active column may read its +-1 / +-CX neighbours without a guard.
-constexpr int PAD = CX + 1;
-constexpr int NB = NC + 2 * PAD;
-
-template <bool EVAL, int MINB>
-__global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
-    extern __shared__ double sm[];
-    double* sP0 = sm + PAD;            // [2][NB] Hv: s; eval: R (by plane parity)
-    double* sP1 = sP0 + 2 * NB;        // [2][NB] eval: T_w
-    double* sW = sP1 + 2 * NB;         // [2][NB] Hv: w; eval: r
-    double* sRh = sW + 2 * NB;         // [2][4][NB] in-plane rho-hat (-x,+x,-y,+y)
-    double* sDq = sRh + 8 * NB - PAD;  // [3][3][TT] dT of the tile columns
-    double* sQ = sDq + 9 * TT;         // [3][TT]
-    double* sQx = sQ + 3 * TT;         // [3][FT_Y][nlx]
-    double* sremx = sQx + 3 * FT_Y * a.tm.nlx;
-    double* sremy = sremx + FT_X;
-    __shared__ double sred[32];
-
+template <bool EVAL, bool TMA>
+__global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
+    extern __shared__ __align__(128) double sm[];
     const TileMeta& tm = a.tm;
+    const int nlx = tm.nlx;
+    // ---- shared memory carve-up (doubles); the staging ring comes first (128-byte aligned)
+    constexpr int SLOT = EVAL ? EV_SLOT : HV_SLOT;
+    double* stg = sm;                      // [DEPTH][SLOT]
+    double* sP0 = stg + DEPTH * SLOT + PAD;  // [2][NB] Hv: s; eval: R (by plane parity)
+    double* sP1 = sP0 + 2 * NB;            // [2][NB] eval: T_w
+    double* sW = sP1 + 2 * NB;             // [2][NB] Hv: w; eval: r
+    double* sRh = sW + 2 * NB;             // [2][4][NB] in-plane rho-hat (-x,+x,-y,+y)
+    double* sDq = sRh + 8 * NB - PAD;      // [3][3][TT] dT of the tile columns (planes k, k-1, k-2)
+    double* sQ = sDq + 9 * TT;             // [3][TT]
+    double* sQx = sQ + 3 * TT;             // [3][FT_Y][nlx]
+    double* sZr = sQx + 3 * FT_Y * nlx;    // [zc + 8] rem_z per plane
+    double* sremx = sZr + tm.zc + 8;
+    double* sremy = sremx + FT_X;
+    double* slab = sremy + FT_Y;          // [NSLAB][nxf*nyf*3] nodal p (Hv)
+    int* sZb = reinterpret_cast<int*>(slab + (EVAL ? 0 : NSLAB * a.nxf * a.nyf * 3));  // [zc + 8]
+    int* sXr = sZb + tm.zc + 8;            // [nlx][4] x ranges of the spread tasks
+    int* sYr = sXr + 4 * nlx;              // [nly][4]
+    unsigned long long* bars = reinterpret_cast<unsigned long long*>(
+        (reinterpret_cast<std::uintptr_t>(sYr + 4 * tm.nly) + 15) & ~static_cast<std::uintptr_t>(15));  // [DEPTH]
+    double* sred = reinterpret_cast<double*>(bars + DEPTH);  // [32]
+
     const int tid = threadIdx.x;
     const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
     const long long n = a.g.count(), plane = static_cast<long long>(mx) * my;
@@ -162,170 +138,303 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
     const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
     const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
     double* part = a.part + tile_id * tm.part_stride;
-    const std::size_t pstride = static_cast<std::size_t>(tm.nly) * tm.nlx * 3;
+    const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
 
-    // thread -> column: tile columns first (warps 0-7 run every phase), then the
-    // halo-1 ring (phase W), then the halo-2 ring (loads only)
-    const bool active = tid < NC;
+    // ---- thread -> column (roles are warp-aligned, so role branches are uniform)
+    const int role = tid < TT ? 0 : (tid < R2_0 ? 1 : 2);
+    bool active = true;
     int lx, ly;
-    if (tid < TT) {
+    if (role == 0) {
         lx = 2 + tid % FT_X;
         ly = 2 + tid / FT_X;
-    } else if (tid < NH1) {
-        const int r = tid - TT;  // 84 = 34 + 34 + 8 + 8
-        if (r < CX - 2) { lx = 1 + r; ly = 1; }
-        else if (r < 2 * (CX - 2)) { lx = 1 + r - (CX - 2); ly = CY - 2; }
-        else if (r < 2 * (CX - 2) + FT_Y) { lx = 1; ly = 2 + r - 2 * (CX - 2); }
-        else { lx = CX - 2; ly = 2 + r - 2 * (CX - 2) - FT_Y; }
+    } else if (role == 1) {
+        const int r = tid - R1_0;  // 84 = 34 + 34 + 8 + 8
+        active = r < R1_N;
+        if (r < C1X) { lx = 1 + r; ly = 1; }
+        else if (r < 2 * C1X) { lx = 1 + r - C1X; ly = CY - 2; }
+        else if (r < 2 * C1X + FT_Y) { lx = 1; ly = 2 + r - 2 * C1X; }
+        else if (r < R1_N) { lx = CX - 2; ly = 2 + r - 2 * C1X - FT_Y; }
+        else { lx = 1; ly = 1; }
     } else {
-        const int r = tid < NC ? tid - NH1 : 0;  // 92 = 36 + 36 + 10 + 10
+        const int r = tid - R2_0;  // 92 = 36 + 36 + 10 + 10
+        active = r < R2_N;
         if (r < CX) { lx = r; ly = 0; }
         else if (r < 2 * CX) { lx = r - CX; ly = CY - 1; }
         else if (r < 2 * CX + CY - 2) { lx = 0; ly = 1 + r - 2 * CX; }
-        else { lx = CX - 1; ly = 1 + r - 2 * CX - (CY - 2); }
+        else if (r < R2_N) { lx = CX - 1; ly = 1 + r - 2 * CX - (CY - 2); }
+        else { lx = 0; ly = 0; }
     }
-    const int c = lx + ly * CX;  // position in the plane buffers
-    const bool inW = tid < NH1;
-    const bool inZ = tid < TT;
+    const int c = lx + ly * CX;                // halo-2 layout index
+    const int c1 = (lx - 1) + (ly - 1) * C1X;  // halo-1 layout index (roles 0, 1)
     const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
     const bool indom = active && gx >= 0 && gx < mx && gy >= 0 && gy < my;
-    const bool tile = inZ && gx < mx && gy < my;
-    // clamped column (out-of-domain halo columns replicate the boundary column:
-    // differences across the boundary vanish exactly, as the reference's clamps)
-    const int gxc = min(max(gx, 0), mx - 1), gyc = min(max(gy, 0), my - 1);
-    const long long col = static_cast<long long>(gxc) + static_cast<long long>(gyc) * mx;
+    const bool tile = role == 0 && gx < mx && gy < my;
+    const long long col = indom ? static_cast<long long>(gx) + static_cast<long long>(gy) * mx : 0;
+    // boundary masks (staged values outside the volume are zero; differences across
+    // the boundary must vanish exactly, as the reference's clamped neighbours)
+    const double mxm = gx > 0 ? 1.0 : 0.0, mxp = gx + 1 < mx ? 1.0 : 0.0;
+    const double mym = gy > 0 ? 1.0 : 0.0, myp = gy + 1 < my ? 1.0 : 0.0;
 
+    // ---- per-CTA tables
+    for (int t = tid; t < tm.zc + 8; t += NTH) {
+        const int kk = min(max(z0 - 2 + t, 0), mz - 1);
+        sZb[t] = __ldg(&a.P.base[2][kk]);
+        sZr[t] = __ldg(&a.P.rem[2][kk]);
+    }
     if (tid < FT_X) sremx[tid] = x0 + tid < mx ? __ldg(&a.P.rem[0][x0 + tid]) : 0.0;
     if (tid < FT_Y) sremy[tid] = y0 + tid < my ? __ldg(&a.P.rem[1][y0 + tid]) : 0.0;
-    if (tid < 2 * PAD) {  // zero the guard pads of every padded buffer
+    {
+        const int nsx = static_cast<int>(a.P.src.m[0]) - 1, nsy = static_cast<int>(a.P.src.m[1]) - 1;
+        for (int t = tid; t < nlx_t; t += NTH) {  // cells nx-1 (weight r) and nx (weight 1-r), clipped to the tile
+            const int nx = nxA + t;
+            int lo1 = x0, hi1 = x0, lo0 = x0, hi0 = x0;
+            if (nx >= 1 && nx - 1 < nsx) {
+                lo1 = max(x0, __ldg(&a.P.cell_lo[0][nx - 1]));
+                hi1 = max(lo1, min(xe, __ldg(&a.P.cell_hi[0][nx - 1])));
+            }
+            if (nx < nsx) {
+                lo0 = max(x0, __ldg(&a.P.cell_lo[0][nx]));
+                hi0 = max(lo0, min(xe, __ldg(&a.P.cell_hi[0][nx])));
+            }
+            sXr[4 * t] = lo1 - x0;
+            sXr[4 * t + 1] = hi1 - x0;
+            sXr[4 * t + 2] = lo0 - x0;
+            sXr[4 * t + 3] = hi0 - x0;
+        }
+        for (int t = tid; t < nly_t; t += NTH) {
+            const int ny = nyA + t;
+            int lo1 = y0, hi1 = y0, lo0 = y0, hi0 = y0;
+            if (ny >= 1 && ny - 1 < nsy) {
+                lo1 = max(y0, __ldg(&a.P.cell_lo[1][ny - 1]));
+                hi1 = max(lo1, min(ye, __ldg(&a.P.cell_hi[1][ny - 1])));
+            }
+            if (ny < nsy) {
+                lo0 = max(y0, __ldg(&a.P.cell_lo[1][ny]));
+                hi0 = max(lo0, min(ye, __ldg(&a.P.cell_hi[1][ny])));
+            }
+            sYr[4 * t] = lo1 - y0;
+            sYr[4 * t + 1] = hi1 - y0;
+            sYr[4 * t + 2] = lo0 - y0;
+            sYr[4 * t + 3] = hi0 - y0;
+        }
+    }
+    if (tid < 2 * PAD) {  // zero the guard pads of the plane buffers
         const int o = tid < PAD ? -PAD + tid : NC + (tid - PAD);
         for (int b = 0; b < 14; ++b) sP0[b * NB + o] = 0.0;
     }
-    const SpreadTask st = make_spread_task(a.P, x0, y0, xe, ye, nxA, nyA, nlx_t, nly_t);
+    if (TMA && tid == 0) {
+        for (int b = 0; b < DEPTH; ++b) mbar_init(&bars[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
 
-    // separable P p (Hv): fixed x-y weights per column, z blend per plane
-    int pz = -1000;
-    double Pa0 = 0.0, Pa1 = 0.0, Pa2 = 0.0, Pb0 = 0.0, Pb1 = 0.0, Pb2 = 0.0;
+    // ---- nodal slab (Hv): x-y footprint of the halo-2 columns, ring of nodal planes
+    const int fx0 = __ldg(&a.P.base[0][max(x0 - 2, 0)]);
+    const int fy0 = __ldg(&a.P.base[1][max(y0 - 2, 0)]);
+    const int nxf = a.nxf, nyf = a.nyf, nsl = nxf * nyf * 3;
     const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = a.P.src.m[0] * a.P.src.m[1];
-    const int bx = __ldg(&a.P.base[0][gxc]), by = __ldg(&a.P.base[1][gyc]);
+    const int msx = static_cast<int>(a.P.src.m[0]), msy = static_cast<int>(a.P.src.m[1]);
+    const int msz = static_cast<int>(a.P.src.m[2]);
+    const int gxc = min(max(gx, 0), mx - 1), gyc = min(max(gy, 0), my - 1);
+    const int bxl = __ldg(&a.P.base[0][gxc]) - fx0, byl = __ldg(&a.P.base[1][gyc]) - fy0;
     const double rx = __ldg(&a.P.rem[0][gxc]), ry = __ldg(&a.P.rem[1][gyc]);
+    // per-thread slab element (up to 4 per thread; host guarantees nsl <= 4 * NTH)
+    double slab_v[4];
+    auto slab_load = [&](int nz) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = tid + u * NTH;
+            if (t < nsl) {
+                const int ix = t % nxf, iy = (t / nxf) % nyf, d = t / (nxf * nyf);
+                const int gxn = min(fx0 + ix, msx - 1), gyn = min(fy0 + iy, msy - 1);
+                slab_v[u] = __ldg(a.p + d * ns + gxn + gyn * sm0 + static_cast<long long>(nz) * sm01);
+            }
+        }
+    };
+    auto slab_store = [&](int nz) {
+        double* dst = slab + (nz & (NSLAB - 1)) * nsl;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int t = tid + u * NTH;
+            if (t < nsl) dst[t] = slab_v[u];
+        }
+    };
+    auto slab_bilerp = [&](int nz, double& o0, double& o1, double& o2) {
+        const double* q = slab + (nz & (NSLAB - 1)) * nsl + bxl + byl * nxf;
+        const int pl = nxf * nyf;
+        o0 = lerp(ry, lerp(rx, q[0], q[1]), lerp(rx, q[nxf], q[nxf + 1]));
+        o1 = lerp(ry, lerp(rx, q[pl], q[pl + 1]), lerp(rx, q[pl + nxf], q[pl + nxf + 1]));
+        o2 = lerp(ry, lerp(rx, q[2 * pl], q[2 * pl + 1]), lerp(rx, q[2 * pl + nxf], q[2 * pl + nxf + 1]));
+    };
+
+    // ---- staging of plane m into its ring slot: TMA (one thread, zero fill outside
+    // the volume) or, for row strides TMA cannot address, per-thread loads with the
+    // same zero-fill semantics
+    auto stage_issue = [&](int m) {
+        const int mr = m - (z0 - 2);
+        double* st = stg + (mr & (DEPTH - 1)) * SLOT;
+        if (TMA) {
+            if (tid < 32 && elect_one()) {  // warp 0 is converged here; one lane issues
+                unsigned long long* bar = &bars[mr & (DEPTH - 1)];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                if (EVAL) {
+                    mbar_expect_tx(bar, EV_SLOT * 8);
+                    tma_load_3d(st, &maps.a, x0 - 2, y0 - 2, m, bar);
+                    tma_load_3d(st + NC, &maps.b, x0 - 2, y0 - 2, m, bar);
+                    tma_load_4d(st + 2 * NC, &maps.c, x0 - 2, y0 - 2, m, 0, bar);
+                } else {
+                    mbar_expect_tx(bar, HV_SLOT * 8);
+                    tma_load_4d(st, &maps.a, x0 - 2, y0 - 2, m, 0, bar);
+                    tma_load_4d(st + HV_DT, &maps.b, x0 - 2, y0 - 2, m, 0, bar);
+                }
+            }
+        } else if (active) {
+            const bool ok = indom && m >= 0 && m < mz;
+            const long long o = col + static_cast<long long>(ok ? m : 0) * plane;
+            if (EVAL) {
+                st[c] = ok ? __ldg(a.R + o) : 0.0;
+                st[NC + c] = ok ? __ldg(a.Tw + o) : 0.0;
+                st[2 * NC + c] = ok ? __ldg(a.dT + o) : 0.0;
+                st[3 * NC + c] = ok ? __ldg(a.dT + n + o) : 0.0;
+                st[4 * NC + c] = ok ? __ldg(a.dT + 2 * n + o) : 0.0;
+            } else {
+                st[c] = ok ? __ldg(a.dT + o) : 0.0;
+                st[NC + c] = ok ? __ldg(a.dT + n + o) : 0.0;
+                st[2 * NC + c] = ok ? __ldg(a.dT + 2 * n + o) : 0.0;
+                if (role < 2) {
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) st[HV_DT + d * NC + c] = ok ? __ldg(a.frh + d * n + o) : 0.0;
+                }
+            }
+        }
+    };
+    auto stage_wait = [&](int m) {
+        if (TMA) {
+            const int mr = m - (z0 - 2);
+            mbar_wait(&bars[mr & (DEPTH - 1)], (mr / DEPTH) & 1);
+        }
+    };
+
+    __syncthreads();  // tables and barriers ready
+    int pz = -1000, slab_hi = -1;
+    double Pa0 = 0.0, Pa1 = 0.0, Pa2 = 0.0, Pb0 = 0.0, Pb1 = 0.0, Pb2 = 0.0;
+    if (!EVAL) {  // the first two nodal planes, synchronously
+        const int nz0 = sZb[0];
+        slab_load(nz0);
+        slab_store(nz0);
+        slab_load(min(nz0 + 1, msz - 1));
+        slab_store(min(nz0 + 1, msz - 1));
+        slab_hi = nz0 + 1;
+    }
+    stage_issue(z0 - 2);
+    stage_issue(z0 - 1);
+    __syncthreads();
+
+    // x-y spread of one completed nodal plane: per-column z-accumulated values ->
+    // sQ -> x-collapse (all threads) -> sQx -> y-collapse (all threads) -> partial
+    auto spread = [&](double v0, double v1, double v2, int nzp) {
+        if (role == 0) {
+            sQ[tid] = v0;
+            sQ[TT + tid] = v1;
+            sQ[2 * TT + tid] = v2;
+        }
+        __syncthreads();
+        for (int t = tid; t < 3 * FT_Y * nlx_t; t += NTH) {
+            const int lxn = t % nlx_t, row = (t / nlx_t) % FT_Y, d = t / (nlx_t * FT_Y);
+            const int* xr = sXr + 4 * lxn;
+            const double* q = sQ + d * TT + row * FT_X;
+            double s1 = 0.0, s2 = 0.0;
+            for (int x = xr[0]; x < xr[1]; ++x) s1 = fma(sremx[x], q[x], s1);
+            for (int x = xr[2]; x < xr[3]; ++x) s2 = fma(1.0 - sremx[x], q[x], s2);
+            sQx[(d * FT_Y + row) * nlx + lxn] = s1 + s2;
+        }
+        __syncthreads();
+        double* dst = part + static_cast<std::size_t>(nzp - nzA) * pstride;
+        for (int t = tid; t < 3 * nly_t * nlx_t; t += NTH) {
+            const int lxn = t % nlx_t, lyn = (t / nlx_t) % nly_t, d = t / (nlx_t * nly_t);
+            const int* yr = sYr + 4 * lyn;
+            const double* q = sQx + d * FT_Y * nlx + lxn;
+            double s1 = 0.0, s2 = 0.0;
+            for (int y = yr[0]; y < yr[1]; ++y) s1 = fma(sremy[y], q[y * nlx], s1);
+            for (int y = yr[2]; y < yr[3]; ++y) s2 = fma(1.0 - sremy[y], q[y * nlx], s2);
+            dst[(lyn * nlx + lxn) * 3 + d] = s1 + s2;
+        }
+    };
+    double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
 
     // column histories (plane index relative to the current iteration k)
-    double sh1 = 0.0, sh2 = 0.0;              // Hv: s_{k-1}, s_{k-2}
+    double sh1 = 0.0, sh2 = 0.0;                        // Hv: s_{k-1}, s_{k-2}
     double Rh1 = 0.0, Rh2 = 0.0, Th1 = 0.0, Th2 = 0.0;  // eval: R, T_w at k-1, k-2
-    double wh1 = 0.0, wh2 = 0.0;              // w (or r) at k-2, k-3
-    double sg1 = 0.0;                          // sigma at k-2
-    double pzh1 = 0.0, pzh2 = 0.0;             // rho-hat(+z) at k-2, k-3
-    double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
+    double wh1 = 0.0, wh2 = 0.0;                        // w (or r) at k-2, k-3
+    double sg1 = 0.0;                                   // sigma at k-2
+    double pzh1 = 0.0, pzh2 = 0.0;                      // rho-hat(+z) at k-2, k-3
     double dsum = 0.0;
-    int cur = nzA;
-
-    // prefetch registers: plane k+1 (clamped) streams, rho-hat of plane k (Hv)
-    double nA = 0.0, nB = 0.0, nD0 = 0.0, nD1 = 0.0, nD2 = 0.0;
-    double nr0 = 0.0, nr1 = 0.0, nr2 = 0.0, nr3 = 0.0, nr4 = 0.0, nr5 = 0.0;
-    const bool need_dT = EVAL ? inZ : active;
-    {
-        const long long o = col + static_cast<long long>(min(max(z0 - 2, 0), mz - 1)) * plane;
-        if (EVAL && active) {
-            nA = __ldg(a.R + o);
-            nB = __ldg(a.Tw + o);
-        }
-        if (need_dT) {
-            nD0 = __ldg(a.dT + o);
-            nD1 = __ldg(a.dT + n + o);
-            nD2 = __ldg(a.dT + 2 * n + o);
-        }
-        const int kr = z0 - 3;
-        if (!EVAL && inW && indom && kr >= 0 && kr < mz) {
-            const long long oi = col + static_cast<long long>(kr) * plane;
-            nr0 = __ldg(a.frh + oi);
-            nr1 = __ldg(a.frh + n + oi);
-            nr2 = __ldg(a.frh + 2 * n + oi);
-            nr3 = __ldg(a.frh + 3 * n + oi);
-            nr4 = __ldg(a.frh + 4 * n + oi);
-            nr5 = __ldg(a.frh + 5 * n + oi);
-        }
-    }
-    __syncthreads();
+    int cur = nzA;  // nodal plane held in accumulator slot 0
 
 #pragma unroll 1
     for (int k = z0 - 2; k <= z1 + 1; ++k) {
-        const int kc = min(max(k, 0), mz - 1);
-        // ---- rotate prefetched values in, issue the next loads
-        const double A0 = nA, B0 = nB, D0 = nD0, D1 = nD1, D2 = nD2;
-        const double r0 = nr0, r1 = nr1, r2 = nr2, r3 = nr3, r4 = nr4, r5 = nr5;  // Hv: rho-hat of plane k-1
-        {
-            const long long o = col + static_cast<long long>(min(k + 1, mz - 1) < 0 ? 0 : min(k + 1, mz - 1)) * plane;
-            if (EVAL && active) {
-                nA = __ldg(a.R + o);
-                nB = __ldg(a.Tw + o);
-            }
-            if (need_dT) {
-                nD0 = __ldg(a.dT + o);
-                nD1 = __ldg(a.dT + n + o);
-                nD2 = __ldg(a.dT + 2 * n + o);
-            }
-            if (!EVAL && inW) {
-                const bool ok = indom && k >= 0 && k < mz;
-                const long long oi = col + static_cast<long long>(kc) * plane;
-                nr0 = ok ? __ldg(a.frh + oi) : 0.0;
-                nr1 = ok ? __ldg(a.frh + n + oi) : 0.0;
-                nr2 = ok ? __ldg(a.frh + 2 * n + oi) : 0.0;
-                nr3 = ok ? __ldg(a.frh + 3 * n + oi) : 0.0;
-                nr4 = ok ? __ldg(a.frh + 4 * n + oi) : 0.0;
-                nr5 = ok ? __ldg(a.frh + 5 * n + oi) : 0.0;
+        const int kt = k - (z0 - 2);  // index into the per-CTA z tables
+        stage_issue(k + 2);
+        bool slab_pending = false;
+        int slab_nz = 0;
+        if (!EVAL) {  // nodal plane needed by plane k+3, loaded now, stored at the end of the iteration
+            const int nzq = min(sZb[kt + 3] + 1, msz - 1);
+            if (nzq > slab_hi) {
+                slab_load(nzq);
+                slab_pending = true;
+                slab_nz = nzq;
+                slab_hi = nzq;
             }
         }
+        stage_wait(k);
+        const double* st = stg + (kt & (DEPTH - 1)) * SLOT;
 
-        // ---- phase P: plane k into shared memory
-        double s0 = 0.0;
+        // ---- phase P: plane k into the plane buffers
+        double s0 = 0.0, A0 = 0.0, B0 = 0.0;
         if (!EVAL) {
-            const int bz = __ldg(&a.P.base[2][kc]);
-            const double rz = __ldg(&a.P.rem[2][kc]);
+            const int bz = sZb[kt];
+            const double rz = sZr[kt];
             if (bz != pz) {  // uniform across the CTA
-                double t[3];
                 if (bz == pz + 1) {
                     Pa0 = Pb0;
                     Pa1 = Pb1;
                     Pa2 = Pb2;
                 } else {
-                    bilerp3(a.p, ns, sm0, sm01, bx, by, bz, rx, ry, t);
-                    Pa0 = t[0];
-                    Pa1 = t[1];
-                    Pa2 = t[2];
+                    slab_bilerp(bz, Pa0, Pa1, Pa2);
                 }
-                bilerp3(a.p, ns, sm0, sm01, bx, by, bz + 1, rx, ry, t);
-                Pb0 = t[0];
-                Pb1 = t[1];
-                Pb2 = t[2];
+                slab_bilerp(min(bz + 1, msz - 1), Pb0, Pb1, Pb2);
                 pz = bz;
             }
+            const double D0 = st[c], D1 = st[NC + c], D2 = st[2 * NC + c];
             s0 = fma(D0, lerp(rz, Pa0, Pb0), fma(D1, lerp(rz, Pa1, Pb1), D2 * lerp(rz, Pa2, Pb2)));
-            if (active) sP0[(k & 1) * NB + c] = s0;
-            if (inW) {  // in-plane coefficients of plane k-1 for the neighbours' phase Z
-                double* rb = sRh + ((k - 1) & 1) * 4 * NB + c;
-                rb[0] = r0;
-                rb[NB] = r1;
-                rb[2 * NB] = r2;
-                rb[3 * NB] = r3;
+            sP0[(k & 1) * NB + c] = s0;
+            if (role == 0) {
+                double* dq = sDq + ((k + 3) % 3) * 3 * TT + tid;
+                dq[0] = D0;
+                dq[TT] = D1;
+                dq[2 * TT] = D2;
             }
-        } else if (active) {
+        } else {
+            A0 = st[c];
+            B0 = st[NC + c];
             sP0[(k & 1) * NB + c] = A0;
             sP1[(k & 1) * NB + c] = B0;
+            if (role == 0) {
+                double* dq = sDq + ((k + 3) % 3) * 3 * TT + tid;
+                dq[0] = st[2 * NC + c];
+                dq[TT] = st[3 * NC + c];
+                dq[2 * TT] = st[4 * NC + c];
+            }
         }
-        if (inZ) {
-            double* dq = sDq + ((k + 3) % 3) * 3 * TT + tid;
-            dq[0] = D0;
-            dq[TT] = D1;
-            dq[2 * TT] = D2;
-        }
-        __syncthreads();
+        // no barrier: phases W(k-1) and Z(k-2) only read shared buffers written in
+        // earlier iterations (plane-parity double buffers), so P, W and Z overlap
 
         // ---- phase W: w (Hv) or rho-hat and r (eval) of plane j = k-1
         const int j = k - 1;
         double wc = 0.0, sgc = 0.0, mzc = 0.0, pzc = 0.0;  // fresh values of plane j
-        if (inW) {
+        if (role < 2) {
             if (!EVAL) {
+                const double* sr = stg + ((kt - 1) & (DEPTH - 1)) * SLOT + HV_DT + c;  // rho-hat of plane k-1
+                const double r0 = sr[0], r1 = sr[NC], r2 = sr[2 * NC], r3 = sr[3 * NC], r4 = sr[4 * NC], r5 = sr[5 * NC];
                 const double* cs = sP0 + (j & 1) * NB;
                 const double sj = sh1;
                 wc = r0 * (cs[c - 1] - sj);
@@ -337,14 +446,22 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
                 sgc = ((r0 + r1) + (r2 + r3)) + (r4 + r5);
                 mzc = r4;
                 pzc = r5;
+                double* rb = sRh + (j & 1) * 4 * NB + c;
+                rb[0] = r0;
+                rb[NB] = r1;
+                rb[2 * NB] = r2;
+                rb[3 * NB] = r3;
             } else {
                 const double* cR = sP0 + (j & 1) * NB;
                 const double* cT = sP1 + (j & 1) * NB;
                 const double Rj = Rh1, Tj = Th1;
-                const double dR0 = cR[c - 1] - Rj, dR1 = cR[c + 1] - Rj, dR2 = cR[c - CX] - Rj, dR3 = cR[c + CX] - Rj;
-                const double dR4 = Rh2 - Rj, dR5 = A0 - Rj;
-                const double dT0 = cT[c - 1] - Tj, dT1 = cT[c + 1] - Tj, dT2 = cT[c - CX] - Tj, dT3 = cT[c + CX] - Tj;
-                const double dT4 = Th2 - Tj, dT5 = B0 - Tj;
+                const double mzm = j > 0 ? 1.0 : 0.0, mzp = j + 1 < mz ? 1.0 : 0.0;
+                const double dR0 = mxm * (cR[c - 1] - Rj), dR1 = mxp * (cR[c + 1] - Rj);
+                const double dR2 = mym * (cR[c - CX] - Rj), dR3 = myp * (cR[c + CX] - Rj);
+                const double dR4 = mzm * (Rh2 - Rj), dR5 = mzp * (A0 - Rj);
+                const double dT0 = mxm * (cT[c - 1] - Tj), dT1 = mxp * (cT[c + 1] - Tj);
+                const double dT2 = mym * (cT[c - CX] - Tj), dT3 = myp * (cT[c + CX] - Tj);
+                const double dT4 = mzm * (Th2 - Tj), dT5 = mzp * (B0 - Tj);
                 const double i0 = a.ih2[0], i1 = a.ih2[1], i2 = a.ih2[2];
                 const double stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
                 const double srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
@@ -385,13 +502,13 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
             }
             sW[(j & 1) * NB + c] = wc;
         }
-        __syncthreads();
 
-        // ---- phase Z: divergence at plane i = k-2, P^T accumulation
+        // ---- phase Z: divergence at plane i = k-2; z weights per column; x-y spread per nodal plane
         if (!EVAL || a.grad) {
             const int i = k - 2;
+            const bool iout = i >= z0 && i < z1;  // uniform
             double q0 = 0.0, q1 = 0.0, q2 = 0.0;
-            if (inZ) {
+            if (role == 0 && iout) {
                 const double* cw = sW + (i & 1) * NB;
                 const double* cr = sRh + (i & 1) * 4 * NB;
                 // neighbour coefficient toward i: +x neighbour holds (-x), -x neighbour holds (+x), ...
@@ -402,19 +519,17 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
                 z = fma(mzc, wc, z);      // rho-hat_{i+z}(-z) w_{i+z}
                 z = fma(pzh2, wh2, z);    // rho-hat_{i-z}(+z) w_{i-z}
                 z = fma(-sg1, wh1, z);    // -sigma_i w_i
-                const double sz = a.scale * z;
+                const double sz = tile ? a.scale * z : 0.0;
                 const double* dq = sDq + ((k + 1) % 3) * 3 * TT + tid;  // plane k-2
                 q0 = sz * dq[0];
                 q1 = sz * dq[TT];
                 q2 = sz * dq[2 * TT];
             }
-            if (i >= z0 && i < z1) {  // uniform
-                const int bz = __ldg(&a.P.base[2][i]);
-                const double rz = __ldg(&a.P.rem[2][i]);
-                if (bz > cur) {  // nodal plane `cur` complete: spread in x-y (all threads)
-                    const double acc[3] = {acc00, acc01, acc02};
-                    spread_plane(st, sremx, sremy, sQ, sQx, tm.nlx, acc, tile, tid, x0, y0,
-                                 part + static_cast<std::size_t>(cur - nzA) * pstride);
+            if (iout) {
+                const int bz = sZb[kt - 2];
+                const double rz = sZr[kt - 2];
+                if (bz > cur) {  // nodal plane `cur` complete: x-y spread (all threads)
+                    spread(acc00, acc01, acc02, cur);
                     acc00 = acc10;
                     acc01 = acc11;
                     acc02 = acc12;
@@ -429,6 +544,7 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
                 acc12 = fma(rz, q2, acc12);
             }
         }
+        if (slab_pending) slab_store(slab_nz);
         __syncthreads();
         // ---- rotate the column histories
         sh2 = sh1;
@@ -443,12 +559,14 @@ __global__ void __launch_bounds__(NTH, MINB) k_fused(FArgs a) {
         pzh2 = pzh1;
         pzh1 = pzc;
     }
-    if (!EVAL || a.grad) {
-        const double acc0[3] = {acc00, acc01, acc02}, acc1[3] = {acc10, acc11, acc12};
-        spread_plane(st, sremx, sremy, sQ, sQx, tm.nlx, acc0, tile, tid, x0, y0,
-                     part + static_cast<std::size_t>(cur - nzA) * pstride);
-        spread_plane(st, sremx, sremy, sQ, sQx, tm.nlx, acc1, tile, tid, x0, y0,
-                     part + static_cast<std::size_t>(cur + 1 - nzA) * pstride);
+    if (TMA) {  // drain the two look-ahead loads before the CTA exits
+        stage_wait(z1 + 2);
+        stage_wait(z1 + 3);
+    }
+    if (!EVAL || a.grad) {  // flush the last two nodal planes
+        spread(acc00, acc01, acc02, cur);
+        __syncthreads();
+        spread(acc10, acc11, acc12, cur + 1);
     }
     if (EVAL) {
 #pragma unroll
@@ -601,16 +719,12 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     }
 }
 
-std::size_t fused_smem_bytes(const TileMeta& tm) {
-    return sizeof(double) * (14 * NB + 9 * TT + 3 * TT + 3 * FT_Y * tm.nlx + FT_X + FT_Y);
-}
-
-int fused_occupancy() {
-    static const int occ = [] {
-        const char* e = std::getenv("MFREG_FUSED_OCC");
-        return (e && e[0] == '2') ? 2 : 1;
-    }();
-    return occ;
+std::size_t fused_smem_bytes(const TileMeta& tm, int nxf, int nyf, bool eval) {
+    const int slot = eval ? EV_SLOT : HV_SLOT;
+    std::size_t d = DEPTH * slot + 14 * NB + 9 * TT + 3 * TT + 3 * FT_Y * tm.nlx + tm.zc + 8 + FT_X + FT_Y +
+                    (eval ? 0 : NSLAB * nxf * nyf * 3);
+    std::size_t ints = tm.zc + 8 + 4 * tm.nlx + 4 * tm.nly;
+    return d * sizeof(double) + ints * sizeof(int) + 16 + DEPTH * 8 + 32 * 8;
 }
 
 FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
@@ -625,12 +739,15 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
     }
     a.part = fp.partials();
     a.vpart = fp.value_partials();
+    a.nxf = fp.slab_x();
+    a.nyf = fp.slab_y();
+    a.dbg = 0;
     return a;
 }
 
 }  // namespace
 
-FusedPlan::FusedPlan(const DevicePlanOwner& plan) {
+FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh) {
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
     TileMeta& t = meta_;
@@ -696,11 +813,68 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan) {
     red_.resize(static_cast<std::size_t>(2 * ((ny + FIN_THREADS - 1) / FIN_THREADS) + 2));
     counter_.resize(1);
     MFREG_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
-    const int smem = static_cast<int>(fused_smem_bytes(t));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    // nodal slab footprint of a tile's halo-2 columns (max over tiles), per axis
+    for (int a2 = 0; a2 < 2; ++a2) {
+        const auto& base = plan.host_base[a2];
+        const int m = static_cast<int>(g.m[a2]);
+        const int ts = a2 == 0 ? FT_X : FT_Y;
+        int mxf = 0;
+        for (int k = 0; k < ntl[a2]; ++k) {
+            const int lo = std::max(k * ts - 2, 0), hi = std::min(m - 1, k * ts + ts + 1);
+            mxf = std::max(mxf, base[hi] - base[lo] + 2);
+        }
+        slab_[a2] = mxf;
+    }
+    const std::size_t hv_smem = fused_smem_bytes(t, slab_[0], slab_[1], false);
+    const std::size_t ev_smem = fused_smem_bytes(t, slab_[0], slab_[1], true);
+    int dev = 0, max_optin = 0;
+    MFREG_CUDA(cudaGetDevice(&dev));
+    MFREG_CUDA(cudaDeviceGetAttribute(&max_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    if (hv_smem > static_cast<std::size_t>(max_optin) || ev_smem > static_cast<std::size_t>(max_optin))
+        throw std::invalid_argument("fused kernels: tile footprint exceeds shared memory (deformation grid too fine)");
+    if (static_cast<long long>(slab_[0]) * slab_[1] * 3 > 4LL * NTH)
+        throw std::invalid_argument("fused kernels: nodal slab footprint too large (deformation grid too fine)");
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hv_smem)));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev_smem)));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hv_smem)));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev_smem)));
+    // TMA needs 16-byte global strides: even mx (rows) and 16-byte aligned bases
+    const bool aligned = (g.m[0] % 2 == 0) && (reinterpret_cast<std::uintptr_t>(R) % 16 == 0) &&
+                         (reinterpret_cast<std::uintptr_t>(Tw) % 16 == 0) &&
+                         (reinterpret_cast<std::uintptr_t>(dT) % 16 == 0) && (reinterpret_cast<std::uintptr_t>(frh) % 16 == 0);
+    const char* off = std::getenv("MFREG_NO_TMA");
+    tma_ = aligned && !(off && off[0] == '1') && make_tma_maps(g, R, Tw, dT, frh);
+}
+
+bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh) {
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return false;
+    const cuuint64_t mx = g.m[0], my = g.m[1], mz = g.m[2], n = g.count();
+    auto enc = [&](CUtensorMap* m, const double* base, int rank, cuuint64_t comps, cuuint32_t bx, cuuint32_t by,
+                   cuuint32_t bc) {
+        const cuuint64_t dims[4] = {mx, my, mz, comps};
+        const cuuint64_t strides[3] = {mx * 8, mx * my * 8, n * 8};
+        const cuuint32_t box[4] = {bx, by, 1, bc};
+        const cuuint32_t es[4] = {1, 1, 1, 1};
+        return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box, es,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    TmaMaps hv{}, ev{};
+    bool ok = enc(&hv.a, dT, 4, 3, CX, CY, 3) && enc(&hv.b, frh, 4, 6, CX, CY, 6) && enc(&ev.a, R, 3, 1, CX, CY, 1) &&
+              enc(&ev.b, Tw, 3, 1, CX, CY, 1) && enc(&ev.c, dT, 4, 3, CX, CY, 3);
+    if (!ok) return false;
+    static_assert(sizeof(TmaMaps) <= sizeof(maps_hv_), "tensor-map storage");
+    std::memcpy(maps_hv_, &hv, sizeof(TmaMaps));
+    std::memcpy(maps_ev_, &ev, sizeof(TmaMaps));
+    return true;
 }
 
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
@@ -712,8 +886,10 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     a.p = p;
     const TileMeta& t = fp.meta();
     note_launch();
-    if (fused_occupancy() == 2) k_fused<false, 2><<<dim3(t.ntx, t.nty, t.ntz), NTH, fused_smem_bytes(t), s>>>(a);
-    else k_fused<false, 1><<<dim3(t.ntx, t.nty, t.ntz), NTH, fused_smem_bytes(t), s>>>(a);
+    const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
+    const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_hv());
+    if (fp.tma()) k_fused<false, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
+    else k_fused<false, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
 }
 
 void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
@@ -729,8 +905,10 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     a.grad = grad ? 1 : 0;
     const TileMeta& t = fp.meta();
     note_launch();
-    if (fused_occupancy() == 2) k_fused<true, 2><<<dim3(t.ntx, t.nty, t.ntz), NTH, fused_smem_bytes(t), s>>>(a);
-    else k_fused<true, 1><<<dim3(t.ntx, t.nty, t.ntz), NTH, fused_smem_bytes(t), s>>>(a);
+    const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, true);
+    const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_ev());
+    if (fp.tma()) k_fused<true, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
+    else k_fused<true, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
 }
 
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s) {

@@ -43,19 +43,31 @@ struct TileMeta {
 
 class FusedPlan {
 public:
-    explicit FusedPlan(const DevicePlanOwner& plan);
+    // R, Tw, dT, frh: the device arrays the fused kernels stream (tensor maps are
+    // built over them when TMA can address the grid)
+    FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh);
+    bool tma() const { return tma_; }
+    const void* maps_hv() const { return maps_hv_; }
+    const void* maps_ev() const { return maps_ev_; }
     const TileMeta& meta() const { return meta_; }
     double* partials() { return part_.get(); }
     double* value_partials() { return vpart_.get(); }
     double* red() { return red_.get(); }
     unsigned int* counter() { return counter_.get(); }
     int ntiles() const { return meta_.ntx * meta_.nty * meta_.ntz; }
+    int slab_x() const { return slab_[0]; }
+    int slab_y() const { return slab_[1]; }
 
 private:
     TileMeta meta_{};
     DevArray<int> tlo_[3], thi_[3], n0_[3];
     DVec part_, vpart_, red_;
     DevArray<unsigned int> counter_;
+    int slab_[2] = {0, 0};
+    bool tma_ = false;
+    alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
+    alignas(64) unsigned char maps_ev_[3 * 128];
+    bool make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh);
 };
 
 // Direction order of the stored coefficients: -x, +x, -y, +y, -z, +z.

@@ -195,7 +195,8 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     img3_.resize(3 * static_cast<std::size_t>(img_.count()));
     launch_identity(dg_, xid_.get(), s_);
     check_launch("identity");
-    if (mode == Mode::Fast) fused_ = std::make_unique<FusedPlan>(plan_);
+    if (mode == Mode::Fast)
+        fused_ = std::make_unique<FusedPlan>(plan_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.frh.get());
 }
 
 DeviceObjective::~DeviceObjective() = default;
