@@ -361,6 +361,22 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     };
     double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
 
+    // rotating buffer pointers (column position c folded in once)
+    double* bA_cur = sP0 + c;          // Hv: s; eval: R  -- plane k
+    double* bA_prv = sP0 + NB + c;     //                  -- plane k-1
+    double* bB_cur = sP1 + c;          // eval: T_w
+    double* bB_prv = sP1 + NB + c;
+    double* bW_new = sW + c;           // w / r of plane k-1 (written this iteration)
+    double* bW_old = sW + NB + c;      // w / r of plane k-2 (read this iteration)
+    double* bR_new = sRh + c;          // in-plane rho-hat of plane k-1
+    double* bR_old = sRh + 4 * NB + c; // in-plane rho-hat of plane k-2
+    double* dq_w = sDq + tid;          // tile dT ring: plane k (write)
+    double* dq_1 = sDq + 3 * TT + tid; //               plane k-1
+    double* dq_r = sDq + 6 * TT + tid; //               plane k-2 (read)
+    const double* st_k = stg + c;                        // staged plane k (dT / R,T)
+    const double* st_r = stg + (DEPTH - 1) * SLOT + HV_DT + c;  // staged rho-hat of plane k-1 (Hv)
+    const double hx = a.hh[0], hy = a.hh[1], hz = a.hh[2];
+
     // column histories (plane index relative to the current iteration k)
     double sh1 = 0.0, sh2 = 0.0;                        // Hv: s_{k-1}, s_{k-2}
     double Rh1 = 0.0, Rh2 = 0.0, Th1 = 0.0, Th2 = 0.0;  // eval: R, T_w at k-1, k-2
@@ -369,6 +385,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     double pzh1 = 0.0, pzh2 = 0.0;                      // rho-hat(+z) at k-2, k-3
     double dsum = 0.0;
     int cur = nzA;  // nodal plane held in accumulator slot 0
+    const bool do_z = !EVAL || a.grad;
 
 #pragma unroll 1
     for (int k = z0 - 2; k <= z1 + 1; ++k) {
@@ -384,16 +401,8 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
                 slab_nz = nzq;
                 slab_hi = nzq;
             }
-        }
-        stage_wait(k);
-        const double* st = stg + (kt & (DEPTH - 1)) * SLOT;
-
-        // ---- phase P: plane k into the plane buffers
-        double s0 = 0.0, A0 = 0.0, B0 = 0.0;
-        if (!EVAL) {
             const int bz = sZb[kt];
-            const double rz = sZr[kt];
-            if (bz != pz) {  // uniform across the CTA
+            if (bz != pz) {  // uniform across the CTA: new nodal plane pair for P p
                 if (bz == pz + 1) {
                     Pa0 = Pb0;
                     Pa1 = Pb1;
@@ -404,63 +413,63 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
                 slab_bilerp(min(bz + 1, msz - 1), Pb0, Pb1, Pb2);
                 pz = bz;
             }
-            const double D0 = st[c], D1 = st[NC + c], D2 = st[2 * NC + c];
-            s0 = fma(D0, lerp(rz, Pa0, Pb0), fma(D1, lerp(rz, Pa1, Pb1), D2 * lerp(rz, Pa2, Pb2)));
-            sP0[(k & 1) * NB + c] = s0;
-            if (role == 0) {
-                double* dq = sDq + ((k + 3) % 3) * 3 * TT + tid;
-                dq[0] = D0;
-                dq[TT] = D1;
-                dq[2 * TT] = D2;
-            }
-        } else {
-            A0 = st[c];
-            B0 = st[NC + c];
-            sP0[(k & 1) * NB + c] = A0;
-            sP1[(k & 1) * NB + c] = B0;
-            if (role == 0) {
-                double* dq = sDq + ((k + 3) % 3) * 3 * TT + tid;
-                dq[0] = st[2 * NC + c];
-                dq[TT] = st[3 * NC + c];
-                dq[2 * TT] = st[4 * NC + c];
-            }
         }
-        // no barrier: phases W(k-1) and Z(k-2) only read shared buffers written in
-        // earlier iterations (plane-parity double buffers), so P, W and Z overlap
+        const int i = k - 2, j = k - 1;
+        const bool iout = do_z && i >= z0 && i < z1;  // uniform
+        const double rzk = sZr[kt];
+        stage_wait(k);
 
-        // ---- phase W: w (Hv) or rho-hat and r (eval) of plane j = k-1
-        const int j = k - 1;
+        double s0 = 0.0, A0 = 0.0, B0 = 0.0;
         double wc = 0.0, sgc = 0.0, mzc = 0.0, pzc = 0.0;  // fresh values of plane j
+        double q0 = 0.0, q1 = 0.0, q2 = 0.0;
         if (role < 2) {
+            // ---- P: plane k
             if (!EVAL) {
-                const double* sr = stg + ((kt - 1) & (DEPTH - 1)) * SLOT + HV_DT + c;  // rho-hat of plane k-1
-                const double r0 = sr[0], r1 = sr[NC], r2 = sr[2 * NC], r3 = sr[3 * NC], r4 = sr[4 * NC], r5 = sr[5 * NC];
-                const double* cs = sP0 + (j & 1) * NB;
+                const double D0 = st_k[0], D1 = st_k[NC], D2 = st_k[2 * NC];
+                s0 = fma(D0, lerp(rzk, Pa0, Pb0), fma(D1, lerp(rzk, Pa1, Pb1), D2 * lerp(rzk, Pa2, Pb2)));
+                bA_cur[0] = s0;
+                if (role == 0) {
+                    dq_w[0] = D0;
+                    dq_w[TT] = D1;
+                    dq_w[2 * TT] = D2;
+                }
+            } else {
+                A0 = st_k[0];
+                B0 = st_k[NC];
+                bA_cur[0] = A0;
+                bB_cur[0] = B0;
+                if (role == 0) {
+                    dq_w[0] = st_k[2 * NC];
+                    dq_w[TT] = st_k[3 * NC];
+                    dq_w[2 * TT] = st_k[4 * NC];
+                }
+            }
+            // ---- W: plane j = k-1 (reads buffers of the previous iteration)
+            if (!EVAL) {
+                const double r0 = st_r[0], r1 = st_r[NC], r2 = st_r[2 * NC], r3 = st_r[3 * NC], r4 = st_r[4 * NC],
+                             r5 = st_r[5 * NC];
                 const double sj = sh1;
-                wc = r0 * (cs[c - 1] - sj);
-                wc = fma(r1, cs[c + 1] - sj, wc);
-                wc = fma(r2, cs[c - CX] - sj, wc);
-                wc = fma(r3, cs[c + CX] - sj, wc);
+                wc = r0 * (bA_prv[-1] - sj);
+                wc = fma(r1, bA_prv[1] - sj, wc);
+                wc = fma(r2, bA_prv[-CX] - sj, wc);
+                wc = fma(r3, bA_prv[CX] - sj, wc);
                 wc = fma(r4, sh2 - sj, wc);
                 wc = fma(r5, s0 - sj, wc);
                 sgc = ((r0 + r1) + (r2 + r3)) + (r4 + r5);
                 mzc = r4;
                 pzc = r5;
-                double* rb = sRh + (j & 1) * 4 * NB + c;
-                rb[0] = r0;
-                rb[NB] = r1;
-                rb[2 * NB] = r2;
-                rb[3 * NB] = r3;
+                bR_new[0] = r0;
+                bR_new[NB] = r1;
+                bR_new[2 * NB] = r2;
+                bR_new[3 * NB] = r3;
             } else {
-                const double* cR = sP0 + (j & 1) * NB;
-                const double* cT = sP1 + (j & 1) * NB;
                 const double Rj = Rh1, Tj = Th1;
                 const double mzm = j > 0 ? 1.0 : 0.0, mzp = j + 1 < mz ? 1.0 : 0.0;
-                const double dR0 = mxm * (cR[c - 1] - Rj), dR1 = mxp * (cR[c + 1] - Rj);
-                const double dR2 = mym * (cR[c - CX] - Rj), dR3 = myp * (cR[c + CX] - Rj);
+                const double dR0 = mxm * (bA_prv[-1] - Rj), dR1 = mxp * (bA_prv[1] - Rj);
+                const double dR2 = mym * (bA_prv[-CX] - Rj), dR3 = myp * (bA_prv[CX] - Rj);
                 const double dR4 = mzm * (Rh2 - Rj), dR5 = mzp * (A0 - Rj);
-                const double dT0 = mxm * (cT[c - 1] - Tj), dT1 = mxp * (cT[c + 1] - Tj);
-                const double dT2 = mym * (cT[c - CX] - Tj), dT3 = myp * (cT[c + CX] - Tj);
+                const double dT0 = mxm * (bB_prv[-1] - Tj), dT1 = mxp * (bB_prv[1] - Tj);
+                const double dT2 = mym * (bB_prv[-CX] - Tj), dT3 = myp * (bB_prv[CX] - Tj);
                 const double dT4 = mzm * (Th2 - Tj), dT5 = mzp * (B0 - Tj);
                 const double i0 = a.ih2[0], i1 = a.ih2[1], i2 = a.ih2[2];
                 const double stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
@@ -472,81 +481,81 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
                 const double in1 = itn * irn;
                 const double in2 = num * (itn * itn) * in1;
                 const bool ok = indom && j >= 0 && j < mz;
-                const double hx = a.hh[0], hy = a.hh[1], hz = a.hh[2];
-                const double q0 = ok ? hx * fma(dR0, in1, -dT0 * in2) : 0.0;
-                const double q1 = ok ? hx * fma(dR1, in1, -dT1 * in2) : 0.0;
-                const double q2 = ok ? hy * fma(dR2, in1, -dT2 * in2) : 0.0;
-                const double q3 = ok ? hy * fma(dR3, in1, -dT3 * in2) : 0.0;
-                const double q4 = ok ? hz * fma(dR4, in1, -dT4 * in2) : 0.0;
-                const double q5 = ok ? hz * fma(dR5, in1, -dT5 * in2) : 0.0;
+                const double e0 = ok ? hx * fma(dR0, in1, -dT0 * in2) : 0.0;
+                const double e1 = ok ? hx * fma(dR1, in1, -dT1 * in2) : 0.0;
+                const double e2 = ok ? hy * fma(dR2, in1, -dT2 * in2) : 0.0;
+                const double e3 = ok ? hy * fma(dR3, in1, -dT3 * in2) : 0.0;
+                const double e4 = ok ? hz * fma(dR4, in1, -dT4 * in2) : 0.0;
+                const double e5 = ok ? hz * fma(dR5, in1, -dT5 * in2) : 0.0;
                 const double r = ok ? num * in1 : 0.0;
                 wc = r;
-                sgc = ((q0 + q1) + (q2 + q3)) + (q4 + q5);
-                mzc = q4;
-                pzc = q5;
-                double* rb = sRh + (j & 1) * 4 * NB + c;
-                rb[0] = q0;
-                rb[NB] = q1;
-                rb[2 * NB] = q2;
-                rb[3 * NB] = q3;
+                sgc = ((e0 + e1) + (e2 + e3)) + (e4 + e5);
+                mzc = e4;
+                pzc = e5;
+                bR_new[0] = e0;
+                bR_new[NB] = e1;
+                bR_new[2 * NB] = e2;
+                bR_new[3 * NB] = e3;
                 if (tile && j >= z0 && j < z1) {
                     const long long gi = col + static_cast<long long>(j) * plane;
-                    a.frh_out[gi] = q0;
-                    a.frh_out[n + gi] = q1;
-                    a.frh_out[2 * n + gi] = q2;
-                    a.frh_out[3 * n + gi] = q3;
-                    a.frh_out[4 * n + gi] = q4;
-                    a.frh_out[5 * n + gi] = q5;
+                    a.frh_out[gi] = e0;
+                    a.frh_out[n + gi] = e1;
+                    a.frh_out[2 * n + gi] = e2;
+                    a.frh_out[3 * n + gi] = e3;
+                    a.frh_out[4 * n + gi] = e4;
+                    a.frh_out[5 * n + gi] = e5;
                     dsum += fma(-r, r, 1.0);
                 }
             }
-            sW[(j & 1) * NB + c] = wc;
-        }
-
-        // ---- phase Z: divergence at plane i = k-2; z weights per column; x-y spread per nodal plane
-        if (!EVAL || a.grad) {
-            const int i = k - 2;
-            const bool iout = i >= z0 && i < z1;  // uniform
-            double q0 = 0.0, q1 = 0.0, q2 = 0.0;
+            bW_new[0] = wc;
+            // ---- Z: plane i = k-2 (tile columns)
             if (role == 0 && iout) {
-                const double* cw = sW + (i & 1) * NB;
-                const double* cr = sRh + (i & 1) * 4 * NB;
                 // neighbour coefficient toward i: +x neighbour holds (-x), -x neighbour holds (+x), ...
-                double z = cr[NB + c - 1] * cw[c - 1];
-                z = fma(cr[c + 1], cw[c + 1], z);
-                z = fma(cr[3 * NB + c - CX], cw[c - CX], z);
-                z = fma(cr[2 * NB + c + CX], cw[c + CX], z);
+                double z = bR_old[NB - 1] * bW_old[-1];
+                z = fma(bR_old[1], bW_old[1], z);
+                z = fma(bR_old[3 * NB - CX], bW_old[-CX], z);
+                z = fma(bR_old[2 * NB + CX], bW_old[CX], z);
                 z = fma(mzc, wc, z);      // rho-hat_{i+z}(-z) w_{i+z}
                 z = fma(pzh2, wh2, z);    // rho-hat_{i-z}(+z) w_{i-z}
                 z = fma(-sg1, wh1, z);    // -sigma_i w_i
                 const double sz = tile ? a.scale * z : 0.0;
-                const double* dq = sDq + ((k + 1) % 3) * 3 * TT + tid;  // plane k-2
-                q0 = sz * dq[0];
-                q1 = sz * dq[TT];
-                q2 = sz * dq[2 * TT];
+                q0 = sz * dq_r[0];
+                q1 = sz * dq_r[TT];
+                q2 = sz * dq_r[2 * TT];
             }
-            if (iout) {
-                const int bz = sZb[kt - 2];
-                const double rz = sZr[kt - 2];
-                if (bz > cur) {  // nodal plane `cur` complete: x-y spread (all threads)
-                    spread(acc00, acc01, acc02, cur);
-                    acc00 = acc10;
-                    acc01 = acc11;
-                    acc02 = acc12;
-                    acc10 = acc11 = acc12 = 0.0;
-                    cur = bz;
-                }
-                acc00 = fma(1.0 - rz, q0, acc00);
-                acc10 = fma(rz, q0, acc10);
-                acc01 = fma(1.0 - rz, q1, acc01);
-                acc11 = fma(rz, q1, acc11);
-                acc02 = fma(1.0 - rz, q2, acc02);
-                acc12 = fma(rz, q2, acc12);
+        } else {
+            // halo-2 ring: P only
+            if (!EVAL) {
+                s0 = fma(st_k[0], lerp(rzk, Pa0, Pb0), fma(st_k[NC], lerp(rzk, Pa1, Pb1), st_k[2 * NC] * lerp(rzk, Pa2, Pb2)));
+                bA_cur[0] = s0;
+            } else {
+                A0 = st_k[0];
+                B0 = st_k[NC];
+                bA_cur[0] = A0;
+                bB_cur[0] = B0;
             }
+        }
+        if (iout) {
+            const int bz = sZb[kt - 2];
+            const double rz = sZr[kt - 2];
+            if (bz > cur) {  // nodal plane `cur` complete: x-y spread (all threads)
+                spread(acc00, acc01, acc02, cur);
+                acc00 = acc10;
+                acc01 = acc11;
+                acc02 = acc12;
+                acc10 = acc11 = acc12 = 0.0;
+                cur = bz;
+            }
+            acc00 = fma(1.0 - rz, q0, acc00);
+            acc10 = fma(rz, q0, acc10);
+            acc01 = fma(1.0 - rz, q1, acc01);
+            acc11 = fma(rz, q1, acc11);
+            acc02 = fma(1.0 - rz, q2, acc02);
+            acc12 = fma(rz, q2, acc12);
         }
         if (slab_pending) slab_store(slab_nz);
         __syncthreads();
-        // ---- rotate the column histories
+        // ---- rotate histories and buffer pointers
         sh2 = sh1;
         sh1 = s0;
         Rh2 = Rh1;
@@ -558,6 +567,16 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
         sg1 = sgc;
         pzh2 = pzh1;
         pzh1 = pzc;
+        {
+            double* t;
+            t = bA_cur; bA_cur = bA_prv; bA_prv = t;
+            t = bB_cur; bB_cur = bB_prv; bB_prv = t;
+            t = bW_new; bW_new = bW_old; bW_old = t;
+            t = bR_new; bR_new = bR_old; bR_old = t;
+            t = dq_r; dq_r = dq_1; dq_1 = dq_w; dq_w = t;
+            st_r = st_k + HV_DT;
+            st_k = (kt & (DEPTH - 1)) == DEPTH - 1 ? st_k - (DEPTH - 1) * SLOT : st_k + SLOT;
+        }
     }
     if (TMA) {  // drain the two look-ahead loads before the CTA exits
         stage_wait(z1 + 2);
@@ -592,7 +611,8 @@ struct FinArgs {
     double alpha;
     double scale_y;  // 2 h_bar^y
     double cell_y;   // h_bar^y
-    const double* v;
+    const double* add;  // nodal term added to out (alpha * curvature), nullable
+    const double* S;    // device scalar sum (Lap u)^2 (value), nullable
     double* out;
     const double* dot_a;
     int value;
@@ -666,28 +686,13 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
             double v = acc[d];
-            if (a.v != nullptr && (a.alpha != 0.0 || a.value)) {
-                const double* u = a.v + d * ny;
-                const double li = lapc(u, a.gy, nx, nyy, nz);
-                if (a.value) r1 = fma(li, li, r1);
-                if (a.out && a.alpha != 0.0) {
-                    const Grid& g = a.gy;
-                    double s = (lapc(u, g, clampl(nx - 1, mx - 1), nyy, nz) - 2.0 * li + lapc(u, g, clampl(nx + 1, mx - 1), nyy, nz)) /
-                               (g.h[0] * g.h[0]);
-                    s += (lapc(u, g, nx, clampl(nyy - 1, my - 1), nz) - 2.0 * li + lapc(u, g, nx, clampl(nyy + 1, my - 1), nz)) /
-                         (g.h[1] * g.h[1]);
-                    s += (lapc(u, g, nx, nyy, clampl(nz - 1, mzn - 1)) - 2.0 * li + lapc(u, g, nx, nyy, clampl(nz + 1, mzn - 1))) /
-                         (g.h[2] * g.h[2]);
-                    v = fma(a.alpha * a.scale_y, s, v);
-                }
-            }
+            if (a.add) v += a.add[d * ny + node];
             if (a.out) a.out[d * ny + node] = v;
             if (a.dot_a) r0 = fma(a.dot_a[d * ny + node], v, r0);
         }
     }
     if (a.sc == nullptr) return;
     r0 = block_reduce(r0, sh);
-    r1 = a.value ? block_reduce(r1, sh) : 0.0;
     if (threadIdx.x == 0) {
         a.red[2 * blockIdx.x] = r0;
         a.red[2 * blockIdx.x + 1] = r1;
@@ -711,7 +716,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     if (threadIdx.x == 0) {
         if (a.value) {
             a.sc[0] = a.hbar * sv;                    // D
-            a.sc[1] = a.alpha * (a.cell_y * s1);      // alpha S
+            a.sc[1] = a.S ? a.alpha * (a.cell_y * *a.S) : 0.0;  // alpha S
         } else {
             a.sc[0] = s0;                             // <dot_a, out>
         }
@@ -922,7 +927,8 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.alpha = spec.alpha;
     a.scale_y = 2.0 * a.gy.cell_volume();
     a.cell_y = a.gy.cell_volume();
-    a.v = spec.v;
+    a.add = spec.add;
+    a.S = spec.S;
     a.out = spec.out;
     a.dot_a = spec.dot_a;
     a.value = spec.value ? 1 : 0;

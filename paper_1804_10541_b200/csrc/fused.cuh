@@ -84,17 +84,18 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
                        double tau, double rho, double* frh, bool grad, cudaStream_t s);
 
 // Nodal finalize (one launch):
-//   out != null: out = gather(P^T partials) [+ alpha 2 h^y Lap(Lap v) when v != null];
+//   out != null: out = gather(P^T partials) [+ add];
 //   dot_a != null: sc[0] = <dot_a, out>;
-//   value: sc[0] = h D-sum over tiles, sc[1] = alpha h^y sum (Lap u)^2 with u = v (eval);
+//   value: sc[0] = h * sum over tiles of (1 - r^2) partials, sc[1] = alpha h^y S;
 // all reductions fixed-order (last-block pattern).
 struct FinalizeSpec {
-    const double* v = nullptr;  // curvature operand (p for Hv, u = y - x for eval)
+    const double* add = nullptr;  // nodal term added to out (alpha * curvature gradient / Hv)
+    const double* S = nullptr;    // device scalar: sum (Lap u)^2 over all components (value)
     double alpha = 0.0;
-    double* out = nullptr;      // nodal result
+    double* out = nullptr;        // nodal result
     const double* dot_a = nullptr;
-    bool value = false;         // eval: D and S into sc[0], sc[1]
-    double* sc = nullptr;       // device scalars
+    bool value = false;           // eval: D and alpha S into sc[0], sc[1]
+    double* sc = nullptr;         // device scalars
 };
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s);
 

@@ -195,11 +195,22 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     img3_.resize(3 * static_cast<std::size_t>(img_.count()));
     launch_identity(dg_, xid_.get(), s_);
     check_launch("identity");
-    if (mode == Mode::Fast)
+    if (mode == Mode::Fast) {
         fused_ = std::make_unique<FusedPlan>(plan_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.frh.get());
+        MFREG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
+        MFREG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
+        MFREG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
+        red2_ = std::make_unique<Reducer>(Mode::Fast, 3 * dg_.count());
+        curv_.resize(3 * ny);
+        sc2_.resize(4);
+    }
 }
 
-DeviceObjective::~DeviceObjective() = default;
+DeviceObjective::~DeviceObjective() {
+    if (ev_fork_) cudaEventDestroy(ev_fork_);
+    if (ev_join_) cudaEventDestroy(ev_join_);
+    if (s2_) cudaStreamDestroy(s2_);
+}
 
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
 
@@ -210,10 +221,20 @@ double DeviceObjective::eval(const double* y, double* grad) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
         launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
         launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
+        // curvature value / gradient on the side stream, overlapping the image pass
+        MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
+        MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+        launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
+        red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
+        if (grad && alpha_ != 0.0)
+            launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+        MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
         launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, ngf_.frh.get(),
                           grad != nullptr, s_);
+        MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         FinalizeSpec f;
-        f.v = u_.get();
+        f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
+        f.S = sc2_.get();
         f.alpha = alpha_;
         f.out = grad;
         f.value = true;
@@ -246,10 +267,17 @@ double DeviceObjective::eval(const double* y, double* grad) {
 // optimizer.cpp:94-104
 void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
     if (fused_) {
+        if (alpha_ != 0.0) {  // alpha 2 h^y Lap(Lap p) on the side stream, overlapping the image pass
+            MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
+            MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+            launch_lap3(dg_, p, lapp_.get(), s2_);
+            launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+            MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+        }
         launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
+        if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
         FinalizeSpec f;
-        f.v = alpha_ != 0.0 ? p : nullptr;
-        f.alpha = alpha_;
+        f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
         f.out = q;
         launch_nodal_finalize(plan_, *fused_, f, s_);
         check_launch("Objective::gn_hessian_vec (fused)");

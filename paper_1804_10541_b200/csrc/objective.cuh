@@ -206,6 +206,10 @@ private:
     DeviceNgf ngf_;
     DVec xid_, u_, lapu_, lapp_, img3_;
     std::unique_ptr<class FusedPlan> fused_;  // fast mode: fused single-pass kernels
+    cudaStream_t s2_ = nullptr;                // fast mode: side stream (nodal curvature terms)
+    cudaEvent_t ev_fork_ = nullptr, ev_join_ = nullptr;
+    std::unique_ptr<Reducer> red2_;
+    DVec curv_, sc2_;
     Scalars sc_;
     double last_distance_ = 0.0, last_regularizer_ = 0.0;
 };
