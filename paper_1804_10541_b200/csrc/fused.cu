@@ -51,6 +51,7 @@ struct FArgs {
     int grad;
     int nxf, nyf;       // nodal slab footprint (max over tiles) per plane, x and y
     int dbg;            // profiling switches (0 in production)
+    const int* skip;    // device flag: return immediately when set (CG already converged)
 };
 
 struct TmaMaps {
@@ -104,6 +105,7 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
 template <bool EVAL, bool TMA>
 __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
     extern __shared__ __align__(128) double sm[];
+    if (a.skip && *a.skip) return;  // uniform
     const TileMeta& tm = a.tm;
     const int nlx = tm.nlx;
     // ---- shared memory carve-up (doubles); the staging ring comes first (128-byte aligned)
@@ -619,6 +621,7 @@ struct FinArgs {
     double* sc;
     double* red;
     unsigned int* counter;
+    const int* skip;
 };
 
 __device__ __forceinline__ long long clampl(long long v, long long hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
@@ -655,6 +658,7 @@ __device__ double block_reduce(double v, double* sh) {
 __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     __shared__ double sh[32];
     __shared__ bool last;
+    if (a.skip && *a.skip) return;  // uniform
     const long long ny = a.gy.count();
     const long long node = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
     double r0 = 0.0, r1 = 0.0;  // reduction terms (dot or S)
@@ -883,8 +887,9 @@ bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, 
 }
 
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     cudaStream_t s) {
+                     cudaStream_t s, const int* skip) {
     FArgs a = make_args(plan, fp);
+    a.skip = skip;
     a.scale = 2.0 * a.g.cell_volume();
     a.frh = frh;
     a.dT = dT;
@@ -935,6 +940,7 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.sc = spec.sc;
     a.red = fp.red();
     a.counter = fp.counter();
+    a.skip = spec.skip;
     const long long ny = a.gy.count();
     note_launch();
     k_nodal_finalize<<<static_cast<unsigned>((ny + FIN_THREADS - 1) / FIN_THREADS), FIN_THREADS, 0, s>>>(a);

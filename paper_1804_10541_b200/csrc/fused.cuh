@@ -75,7 +75,7 @@ constexpr int kRhoDirs = 6;
 
 // Gauss-Newton Hv image pass: s = dT . P p -> w -> z -> q^ = 2h z dT -> P^T partials.
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     cudaStream_t s);
+                     cudaStream_t s, const int* skip = nullptr);
 
 // Eval image pass on the warped state (T_w, dT from launch_warp): rho-hat (6 per
 // voxel, stored as Hv state), per-tile sums of (1 - r^2) and, when `grad`, the
@@ -96,6 +96,7 @@ struct FinalizeSpec {
     const double* dot_a = nullptr;
     bool value = false;           // eval: D and alpha S into sc[0], sc[1]
     double* sc = nullptr;         // device scalars
+    const int* skip = nullptr;    // device flag: skip the launch when set
 };
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s);
 

@@ -4,6 +4,7 @@
 #include <cstring>
 
 #include "objective.cuh"
+#include "cg.cuh"
 #include "fused.cuh"
 
 namespace mfreg_b200 {
@@ -303,6 +304,40 @@ void DeviceObjective::seed_hessian_vec(const double* p, double gamma, double* q)
 double DeviceObjective::dot(const double* a, const double* b) {
     ngf_.reducer().sum(SUM_DOT, dof(), a, b, sc_.dev(8), 1.0, s_);
     return sc_.fetch(9, s_)[8];
+}
+
+void DeviceObjective::dot_async(const double* a, const double* b, double* out_dev) {
+    ngf_.reducer().sum(SUM_DOT, dof(), a, b, out_dev, 1.0, s_);
+}
+
+void DeviceObjective::apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) {
+    if (!fused_ || op != 0) {
+        DeviceProblem::apply_dot(op, gamma, p, q, pq_dev, skip);
+        return;
+    }
+    // fused GN Hv with <p, q> folded into the nodal finalize
+    if (alpha_ != 0.0) {
+        MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
+        MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+        launch_lap3(dg_, p, lapp_.get(), s2_);
+        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+        MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+    }
+    launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_, skip);
+    if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
+    FinalizeSpec f;
+    f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
+    f.out = q;
+    f.dot_a = p;
+    f.sc = pq_dev;
+    f.skip = skip;
+    launch_nodal_finalize(plan_, *fused_, f, s_);
+    check_launch("Objective::gn_hessian_vec (fused, dot)");
+}
+
+DeviceCg& DeviceProblem::cg_workspace() {
+    if (!cg_) cg_ = std::make_shared<DeviceCg>(dof());
+    return *cg_;
 }
 
 double DeviceObjective::inf_norm(const double* a, double scale) {

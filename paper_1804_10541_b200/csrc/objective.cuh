@@ -141,6 +141,23 @@ public:
     virtual double inf_norm(const double* a, double scale) = 0;  // max |scale * a_i|
     virtual cudaStream_t stream() const = 0;
     double norm(const double* a) { return std::sqrt(dot(a, a)); }
+    // asynchronous vec_dot with a device result (exact chunk order in parity mode)
+    virtual void dot_async(const double* a, const double* b, double* out_dev) = 0;
+    // fixed-order tree reductions allowed (fast mode)
+    virtual bool fast_reductions() const = 0;
+    // q = A p and <p, q> into pq_dev (A = GN operator, op 0, or seed operator, op 1);
+    // `skip` (device flag, nullable): work may be skipped when *skip != 0
+    virtual void apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) {
+        (void)skip;
+        if (op == 1) seed_hessian_vec(p, gamma, q);
+        else gn_hessian_vec(p, q);
+        dot_async(p, q, pq_dev);
+    }
+    // device-resident CG workspace (created on first use)
+    class DeviceCg& cg_workspace();
+
+private:
+    std::shared_ptr<class DeviceCg> cg_;
 };
 
 // NGF state on the image grid: reference image (+ its owner), sampled template
@@ -191,6 +208,9 @@ public:
     double dot(const double* a, const double* b) override;
     double inf_norm(const double* a, double scale) override;
     cudaStream_t stream() const override { return s_; }
+    void dot_async(const double* a, const double* b, double* out_dev) override;
+    bool fast_reductions() const override { return fused_ != nullptr; }
+    void apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) override;
     const double* identity_dev() const { return xid_.get(); }
     const Grid& image_grid() const { return img_; }
     const Grid& deform_grid() const { return dg_; }

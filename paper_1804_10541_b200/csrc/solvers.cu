@@ -5,17 +5,12 @@
 #include <cmath>
 #include <deque>
 
+#include "cg.cuh"
 #include "objective.cuh"
 
 namespace mfreg_b200 {
 
 namespace {
-
-struct Work {
-    explicit Work(idx_t n) : n(n) {}
-    idx_t n;
-    DVec make() { return DVec(static_cast<std::size_t>(n)); }
-};
 
 double effective_gamma(const OptimizerConfig& cfg, double alpha) {  // optimizer.cpp:179-181
     return cfg.gamma >= 0.0 ? cfg.gamma : 1e-3 * std::max(1.0, alpha);
@@ -27,11 +22,6 @@ bool should_stop(const OptimizerConfig& cfg, double g0, double min_hy, double j_
     if (std::abs(j_prev - j_cur) <= cfg.tol_rel_j * std::max(1.0, std::abs(j_prev))) return true;
     if (step_inf <= cfg.tol_step * min_hy) return true;
     return false;
-}
-
-void apply_op(DeviceProblem& P, int op, double gamma, const double* v, double* out) {
-    if (op == 1) P.seed_hessian_vec(v, gamma, out);
-    else P.gn_hessian_vec(v, out);
 }
 
 // optimizer.cpp:156-175 with phi(eta) = J(y + eta d), value-only evaluation
@@ -53,42 +43,9 @@ bool armijo_search(DeviceProblem& P, const double* y, const double* dir, double*
 
 }  // namespace
 
-// optimizer.cpp:113-154 — plain CG, x0 = 0
+// optimizer.cpp:113-154 — plain CG, x0 = 0, device-resident scalars (cg.cu)
 CgResult cg_solve(DeviceProblem& P, int op, double gamma, const double* b, double* x, const CgConfig& cfg) {
-    const idx_t n = P.dof();
-    cudaStream_t s = P.stream();
-    CgResult res;
-    MFREG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
-    const double bnorm = P.norm(b);
-    if (bnorm == 0.0) return res;
-    DVec r(static_cast<std::size_t>(n)), p(static_cast<std::size_t>(n)), ap(static_cast<std::size_t>(n));
-    MFREG_CUDA(cudaMemcpyAsync(r.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    MFREG_CUDA(cudaMemcpyAsync(p.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
-    MFREG_CUDA(cudaMemsetAsync(ap.get(), 0, n * sizeof(double), s));
-    double rr = P.dot(r.get(), r.get());
-    for (int it = 0; it < cfg.max_iters; ++it) {
-        apply_op(P, op, gamma, p.get(), ap.get());
-        const double pap = P.dot(p.get(), ap.get());
-        if (!std::isfinite(pap) || pap <= 0.0) {
-            res.breakdown = !std::isfinite(pap);
-            break;
-        }
-        const double alpha = rr / pap;
-        launch_cg_update(n, alpha, p.get(), ap.get(), x, r.get(), s);
-        ++res.iters;
-        const double rr_new = P.dot(r.get(), r.get());
-        res.relres = std::sqrt(rr_new) / bnorm;
-        if (!std::isfinite(rr_new)) {
-            res.breakdown = true;
-            break;
-        }
-        if (res.relres <= cfg.rel_tol) break;
-        const double beta = rr_new / rr;
-        launch_axpy_to(n, r.get(), beta, p.get(), p.get(), s);
-        rr = rr_new;
-    }
-    check_launch("cg_solve");
-    return res;
+    return P.cg_workspace().solve(P, op, gamma, b, x, cfg);
 }
 
 // optimizer.cpp:202-268 + 392-407
