@@ -1,4 +1,4 @@
-"""Summarise an ncu --csv launch list: per-kernel count, mean time, DRAM bytes."""
+"""Summarise an ncu --csv launch list (profiles helper): per-kernel count, mean time, DRAM bytes."""
 import csv, collections, sys
 rows = list(csv.reader(open(sys.argv[1])))
 start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
