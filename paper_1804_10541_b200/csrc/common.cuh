@@ -22,9 +22,13 @@ using idx_t = long long;
 struct Grid {
     idx_t m[3];
     double h[3];
+    double ih[3];  // RN(1 / h), for the correctly rounded division div_rn (kernels.cu)
     __host__ __device__ idx_t count() const { return m[0] * m[1] * m[2]; }
     __host__ __device__ double cell_volume() const { return h[0] * h[1] * h[2]; }
     __host__ __device__ idx_t lin(idx_t i, idx_t j, idx_t k) const { return i + j * m[0] + k * m[0] * m[1]; }
+    __host__ void set_inv() {
+        for (int a = 0; a < 3; ++a) ih[a] = 1.0 / h[a];
+    }
 };
 
 // Directions {-z,-y,-x,0,+x,+y,+z} (grid.hpp:16-18).

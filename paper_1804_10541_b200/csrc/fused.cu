@@ -239,26 +239,30 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     const int gxc = min(max(gx, 0), mx - 1), gyc = min(max(gy, 0), my - 1);
     const int bxl = __ldg(&a.P.base[0][gxc]) - fx0, byl = __ldg(&a.P.base[1][gyc]) - fy0;
     const double rx = __ldg(&a.P.rem[0][gxc]), ry = __ldg(&a.P.rem[1][gyc]);
-    // per-thread slab element (up to 4 per thread; host guarantees nsl <= 4 * NTH)
+    // per-thread slab elements (up to 4 per thread; host guarantees nsl <= 4 * NTH):
+    // global offsets precomputed once (no integer division in the plane loop)
     double slab_v[4];
+    long long slab_off[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int t = tid + u * NTH;
+        slab_off[u] = -1;
+        if (!EVAL && t < nsl) {
+            const int ix = t % nxf, iy = (t / nxf) % nyf, d = t / (nxf * nyf);
+            const int gxn = min(fx0 + ix, msx - 1), gyn = min(fy0 + iy, msy - 1);
+            slab_off[u] = d * ns + gxn + gyn * sm0;
+        }
+    }
     auto slab_load = [&](int nz) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int t = tid + u * NTH;
-            if (t < nsl) {
-                const int ix = t % nxf, iy = (t / nxf) % nyf, d = t / (nxf * nyf);
-                const int gxn = min(fx0 + ix, msx - 1), gyn = min(fy0 + iy, msy - 1);
-                slab_v[u] = __ldg(a.p + d * ns + gxn + gyn * sm0 + static_cast<long long>(nz) * sm01);
-            }
-        }
+        for (int u = 0; u < 4; ++u)
+            if (slab_off[u] >= 0) slab_v[u] = __ldg(a.p + slab_off[u] + static_cast<long long>(nz) * sm01);
     };
     auto slab_store = [&](int nz) {
         double* dst = slab + (nz & (NSLAB - 1)) * nsl;
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int t = tid + u * NTH;
-            if (t < nsl) dst[t] = slab_v[u];
-        }
+        for (int u = 0; u < 4; ++u)
+            if (slab_off[u] >= 0) dst[tid + u * NTH] = slab_v[u];
     };
     auto slab_bilerp = [&](int nz, double& o0, double& o1, double& o2) {
         const double* q = slab + (nz & (NSLAB - 1)) * nsl + bxl + byl * nxf;
@@ -333,6 +337,30 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
 
     // x-y spread of one completed nodal plane: per-column z-accumulated values ->
     // sQ -> x-collapse (all threads) -> sQx -> y-collapse (all threads) -> partial
+    // spread work items: x-collapse (d, row, local node x), y-collapse (d, local node y, x);
+    // the first item of each thread is decomposed once here, further items (fine
+    // deformation grids only) in the loop
+    const int nxi = 3 * FT_Y * nlx_t, nyi = 3 * nly_t * nlx_t;
+    const int x_lxn = tid % nlx_t, x_row = (tid / nlx_t) % FT_Y, x_d = tid / (nlx_t * FT_Y);
+    const int y_lxn = tid % nlx_t, y_lyn = (tid / nlx_t) % nly_t, y_d = tid / (nlx_t * nly_t);
+    auto xitem = [&](int lxn, int row, int d) {
+        const int* xr = sXr + 4 * lxn;
+        const double* q = sQ + d * TT + row * FT_X;
+        double s1 = 0.0, s2 = 0.0;
+        for (int x = xr[0]; x < xr[1]; ++x) s1 = fma(sremx[x], q[x], s1);
+        for (int x = xr[2]; x < xr[3]; ++x) s2 = fma(1.0 - sremx[x], q[x], s2);
+        sQx[(d * FT_Y + row) * nlx + lxn] = s1 + s2;
+    };
+    auto yitem = [&](int lxn, int lyn, int d, double* dst) {
+        const int* yr = sYr + 4 * lyn;
+        const double* q = sQx + d * FT_Y * nlx + lxn;
+        double s1 = 0.0, s2 = 0.0;
+        for (int y = yr[0]; y < yr[1]; ++y) s1 = fma(sremy[y], q[y * nlx], s1);
+        for (int y = yr[2]; y < yr[3]; ++y) s2 = fma(1.0 - sremy[y], q[y * nlx], s2);
+        dst[(lyn * nlx + lxn) * 3 + d] = s1 + s2;
+    };
+    // x-y spread of one completed nodal plane: per-column z-accumulated values ->
+    // sQ -> x-collapse (all threads) -> sQx -> y-collapse (all threads) -> partial
     auto spread = [&](double v0, double v1, double v2, int nzp) {
         if (role == 0) {
             sQ[tid] = v0;
@@ -340,26 +368,12 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
             sQ[2 * TT + tid] = v2;
         }
         __syncthreads();
-        for (int t = tid; t < 3 * FT_Y * nlx_t; t += NTH) {
-            const int lxn = t % nlx_t, row = (t / nlx_t) % FT_Y, d = t / (nlx_t * FT_Y);
-            const int* xr = sXr + 4 * lxn;
-            const double* q = sQ + d * TT + row * FT_X;
-            double s1 = 0.0, s2 = 0.0;
-            for (int x = xr[0]; x < xr[1]; ++x) s1 = fma(sremx[x], q[x], s1);
-            for (int x = xr[2]; x < xr[3]; ++x) s2 = fma(1.0 - sremx[x], q[x], s2);
-            sQx[(d * FT_Y + row) * nlx + lxn] = s1 + s2;
-        }
+        if (tid < nxi) xitem(x_lxn, x_row, x_d);
+        for (int t = tid + NTH; t < nxi; t += NTH) xitem(t % nlx_t, (t / nlx_t) % FT_Y, t / (nlx_t * FT_Y));
         __syncthreads();
         double* dst = part + static_cast<std::size_t>(nzp - nzA) * pstride;
-        for (int t = tid; t < 3 * nly_t * nlx_t; t += NTH) {
-            const int lxn = t % nlx_t, lyn = (t / nlx_t) % nly_t, d = t / (nlx_t * nly_t);
-            const int* yr = sYr + 4 * lyn;
-            const double* q = sQx + d * FT_Y * nlx + lxn;
-            double s1 = 0.0, s2 = 0.0;
-            for (int y = yr[0]; y < yr[1]; ++y) s1 = fma(sremy[y], q[y * nlx], s1);
-            for (int y = yr[2]; y < yr[3]; ++y) s2 = fma(1.0 - sremy[y], q[y * nlx], s2);
-            dst[(lyn * nlx + lxn) * 3 + d] = s1 + s2;
-        }
+        if (tid < nyi) yitem(y_lxn, y_lyn, y_d, dst);
+        for (int t = tid + NTH; t < nyi; t += NTH) yitem(t % nlx_t, (t / nlx_t) % nly_t, t / (nlx_t * nly_t), dst);
     };
     double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
 

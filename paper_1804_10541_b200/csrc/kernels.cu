@@ -40,6 +40,17 @@ __device__ __forceinline__ double sample_or_zero(const double* __restrict__ t, c
     return __ldg(&t[g.lin(i, j, k)]);
 }
 
+// Correctly rounded p / h from the correctly rounded reciprocal ih = RN(1/h)
+// (Markstein's correction: q0 = RN(p ih), r = p - q0 h exactly by FMA,
+// q = RN(q0 + r ih)); identical to IEEE division, ~4x cheaper than __ddiv_rn.
+// A zero quotient keeps the sign of p, as IEEE division does.
+__device__ __forceinline__ double div_rn(double p, double h, double ih) {
+    const double q0 = __dmul_rn(p, ih);
+    const double r = __fma_rn(-q0, h, p);
+    const double q = __fma_rn(r, ih, q0);
+    return q == 0.0 ? q0 : q;
+}
+
 // volume.cpp:29-74 — trilinear sample with Dirichlet zeros; ties go to the lower
 // cell (ceil(s)-1); IEEE division p/h (a reciprocal multiply flips ties).
 __device__ __forceinline__ void interpolate(const double* __restrict__ t, const Grid& g, double px, double py,
@@ -49,7 +60,7 @@ __device__ __forceinline__ void interpolate(const double* __restrict__ t, const 
     double f[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double s = __ddiv_rn(p[a], g.h[a]) - 0.5;
+        const double s = div_rn(p[a], g.h[a], g.ih[a]) - 0.5;
         const double c = ceil(s);
         base[a] = static_cast<idx_t>(c) - 1;
         f[a] = s - static_cast<double>(base[a]);
@@ -81,9 +92,9 @@ __device__ __forceinline__ void interpolate(const double* __restrict__ t, const 
     const double ggx = dxv[0] * (1.0 - fz) + dxv[1] * fz;
     const double ggy = dyv[0] * (1.0 - fz) + dyv[1] * fz;
     const double ggz = cy[1] - cy[0];
-    gx = __ddiv_rn(ggx, g.h[0]);
-    gy = __ddiv_rn(ggy, g.h[1]);
-    gz = __ddiv_rn(ggz, g.h[2]);
+    gx = div_rn(ggx, g.h[0], g.ih[0]);
+    gy = div_rn(ggy, g.h[1], g.ih[1]);
+    gz = div_rn(ggz, g.h[2], g.ih[2]);
 }
 
 // transfer.cpp:56-83 — acc += ((wx*wy)*wz)*y over corners in (g,b,a) order from 0.0
@@ -222,8 +233,8 @@ __device__ __forceinline__ void dgrad6(const double* __restrict__ v, const Grid&
                          g.lin(x, clampi(y + 1, g.m[1] - 1), z), g.lin(x, y, clampi(z + 1, g.m[2] - 1))};
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        r[a] = __ddiv_rn(vi - __ldg(&v[nb[a]]), g.h[a]);
-        r[a + 3] = __ddiv_rn(__ldg(&v[nb[a + 3]]) - vi, g.h[a]);
+        r[a] = div_rn(vi - __ldg(&v[nb[a]]), g.h[a], g.ih[a]);
+        r[a + 3] = div_rn(__ldg(&v[nb[a + 3]]) - vi, g.h[a], g.ih[a]);
     }
 }
 
@@ -730,15 +741,21 @@ void launch_transfer_apply(const DevPlan& P, const double* y, double* out, cudaS
 void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s) {
     note_launch(), k_transfer_T<<<grid3(P.src), block3(), 0, s>>>(P, w, out);
 }
-void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n, double* vals, double* dT,
+void launch_sample(const Grid& img0, const double* T, const double* pts, idx_t n, double* vals, double* dT,
                    cudaStream_t s) {
+    Grid img = img0;
+    img.set_inv();
     note_launch(), k_sample<<<blocks1(n), 256, 0, s>>>(img, T, pts, n, vals, dT);
 }
-void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s) {
+void launch_warp(const DevPlan& P0, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s) {
+    DevPlan P = P0;
+    P.tgt.set_inv();
     note_launch(), k_warp<<<grid3(P.tgt), block3(), 0, s>>>(P, y, T, Tw, dT);
 }
-void launch_ngf_ws(const Grid& img, const double* R, const double* Tw, double tau, double rho, double* r,
+void launch_ngf_ws(const Grid& img0, const double* R, const double* Tw, double tau, double rho, double* r,
                    double* inv1, double* inv2, double* rh, cudaStream_t s) {
+    Grid img = img0;
+    img.set_inv();
     note_launch(), k_ngf_ws<<<grid3(img), block3(), 0, s>>>(img, R, Tw, tau, rho, r, inv1, inv2, rh);
 }
 void launch_ngf_gradient(const Grid& img, const double* r, const double* rh, const double* dT, double* out,
@@ -820,7 +837,9 @@ void launch_prolong(const Grid& coarse, const Grid& fine, const double* yc, doub
     note_launch(), k_prolong<<<grid3(fine), block3(), 0, s>>>(coarse, fine, yc, yf);
 }
 void launch_phantom(const Grid& g, double* out, cudaStream_t s) { note_launch(), k_phantom<<<grid3(g), block3(), 0, s>>>(g, out); }
-void launch_warp_with(const Grid& g, const WarpTerms& w, const double* T, double* out, cudaStream_t s) {
+void launch_warp_with(const Grid& g0, const WarpTerms& w, const double* T, double* out, cudaStream_t s) {
+    Grid g = g0;
+    g.set_inv();
     note_launch(), k_warp_with<<<grid3(g), block3(), 0, s>>>(g, w, T, out);
 }
 
