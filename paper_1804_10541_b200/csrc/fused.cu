@@ -674,40 +674,33 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     __shared__ bool last;
     if (a.skip && *a.skip) return;  // uniform
     const long long ny = a.gy.count();
-    const long long node = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
-    double r0 = 0.0, r1 = 0.0;  // reduction terms (dot or S)
-    if (node < ny) {
-        const long long mx = a.gy.m[0], my = a.gy.m[1], mzn = a.gy.m[2];
+    // one thread per (component, node): component-major like the nodal vectors
+    const long long t = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
+    double r0 = 0.0, r1 = 0.0;
+    if (t < 3 * ny && a.out) {
+        const int d = static_cast<int>(t / ny);
+        const long long node = t - d * ny;
+        const long long mx = a.gy.m[0], my = a.gy.m[1];
         const long long nx = node % mx, nyy = (node / mx) % my, nz = node / (mx * my);
-        double acc[3] = {0.0, 0.0, 0.0};
-        if (a.out) {
-            const TileMeta& tm = a.tm;
-            const int tz0 = tm.node_tlo[2][nz], tz1 = tm.node_thi[2][nz];
-            const int ty0 = tm.node_tlo[1][nyy], ty1 = tm.node_thi[1][nyy];
-            const int tx0 = tm.node_tlo[0][nx], tx1 = tm.node_thi[0][nx];
-            for (int tz = tz0; tz <= tz1; ++tz) {
-                const int lz = static_cast<int>(nz) - tm.tile_n0[2][tz];
-                for (int ty = ty0; ty <= ty1; ++ty) {
-                    const int lyn = static_cast<int>(nyy) - tm.tile_n0[1][ty];
-                    for (int tx = tx0; tx <= tx1; ++tx) {
-                        const int lxn = static_cast<int>(nx) - tm.tile_n0[0][tx];
-                        const double* pp = a.part + ((static_cast<std::size_t>(tz) * tm.nty + ty) * tm.ntx + tx) *
-                                                        tm.part_stride +
-                                           ((static_cast<std::size_t>(lz) * tm.nly + lyn) * tm.nlx + lxn) * 3;
-                        acc[0] += pp[0];
-                        acc[1] += pp[1];
-                        acc[2] += pp[2];
-                    }
+        const TileMeta& tm = a.tm;
+        const int tz0 = __ldg(&tm.node_tlo[2][nz]), tz1 = __ldg(&tm.node_thi[2][nz]);
+        const int ty0 = __ldg(&tm.node_tlo[1][nyy]), ty1 = __ldg(&tm.node_thi[1][nyy]);
+        const int tx0 = __ldg(&tm.node_tlo[0][nx]), tx1 = __ldg(&tm.node_thi[0][nx]);
+        double v = 0.0;
+        for (int tz = tz0; tz <= tz1; ++tz) {
+            const int lz = static_cast<int>(nz) - __ldg(&tm.tile_n0[2][tz]);
+            for (int ty = ty0; ty <= ty1; ++ty) {
+                const int lyn = static_cast<int>(nyy) - __ldg(&tm.tile_n0[1][ty]);
+                for (int tx = tx0; tx <= tx1; ++tx) {
+                    const int lxn = static_cast<int>(nx) - __ldg(&tm.tile_n0[0][tx]);
+                    v += __ldg(a.part + ((static_cast<std::size_t>(tz) * tm.nty + ty) * tm.ntx + tx) * tm.part_stride +
+                               ((static_cast<std::size_t>(lz) * tm.nly + lyn) * tm.nlx + lxn) * 3 + d);
                 }
             }
         }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            double v = acc[d];
-            if (a.add) v += a.add[d * ny + node];
-            if (a.out) a.out[d * ny + node] = v;
-            if (a.dot_a) r0 = fma(a.dot_a[d * ny + node], v, r0);
-        }
+        if (a.add) v += a.add[t];
+        a.out[t] = v;
+        if (a.dot_a) r0 = a.dot_a[t] * v;
     }
     if (a.sc == nullptr) return;
     r0 = block_reduce(r0, sh);
@@ -833,7 +826,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     MFREG_CUDA(cudaMemset(part_.get(), 0, part_.size() * sizeof(double)));
     vpart_.resize(static_cast<std::size_t>(ntiles()));
     const long long ny = P.src.count();
-    red_.resize(static_cast<std::size_t>(2 * ((ny + FIN_THREADS - 1) / FIN_THREADS) + 2));
+    red_.resize(static_cast<std::size_t>(2 * ((3 * ny + FIN_THREADS - 1) / FIN_THREADS) + 2));
     counter_.resize(1);
     MFREG_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
     // nodal slab footprint of a tile's halo-2 columns (max over tiles), per axis
@@ -957,7 +950,7 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.skip = spec.skip;
     const long long ny = a.gy.count();
     note_launch();
-    k_nodal_finalize<<<static_cast<unsigned>((ny + FIN_THREADS - 1) / FIN_THREADS), FIN_THREADS, 0, s>>>(a);
+    k_nodal_finalize<<<static_cast<unsigned>((3 * ny + FIN_THREADS - 1) / FIN_THREADS), FIN_THREADS, 0, s>>>(a);
 }
 
 }  // namespace mfreg_b200
