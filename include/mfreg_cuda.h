@@ -164,6 +164,26 @@ int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, 
 int mfreg_cu_objective_seed_hessian_vec(mfreg_cu_objective* obj, const double* p, double gamma, double* q,
                                         int where);
 
+/* vec_dot(a, b) (optimizer.cpp:12-19) over the dof the objective owns (all of
+ * them, or the owned nodal planes of a z-slab objective) */
+int mfreg_cu_objective_dot(mfreg_cu_objective* obj, const double* a, const double* b, int where, double* out);
+
+/* ---- z-slab decomposition (multi-GPU) --------------------------
+ * No reference counterpart: the reference parallelises one address space with
+ * OpenMP (parallel.hpp:22-55); this splits the image z axis across processes.
+ * table[r*7 + 0..6] = zlo, zhi (image planes [zlo, zhi) of rank r), own_lo, own_hi
+ * (owned nodal planes), need_lo, need_hi (nodal operand planes read; the halo
+ * comes from ranks r-1 / r+1), bnd (P^T planes [own_hi, own_hi + bnd) shared with
+ * rank r+1, which adds them). Pure host computation. */
+int mfreg_cu_slab_partition(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int32_t* table);
+/* Objective over one slab (fast mode): ref/tpl are the whole volume (replicated);
+ * slab = {zlo, zhi, own_lo, own_hi} from the partition. eval / gn_hessian_vec
+ * return this rank's contributions: D and alpha S of its planes (via
+ * mfreg_cu_objective_last) and the nodal result on [min(own_lo, .), own_hi + bnd). */
+int mfreg_cu_objective_create_slab(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                   const mfreg_cu_grid* deform, double tau, double rho, double alpha,
+                                   const int32_t slab[4], int where, mfreg_cu_objective** out);
+
 /* ---- solvers (optimizer.hpp:123-166) ---------------------------------------- */
 /* cg_solve on the objective's GN operator (op = 0) or seed operator (op = 1, gamma) */
 int mfreg_cu_cg_solve(mfreg_cu_objective* obj, int op, double gamma, const double* b, int max_iters, double rel_tol,

@@ -106,6 +106,10 @@ _SIGS = {
     "mfreg_cu_objective_last": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_gn_hessian_vec": ([_vp, _dp, _dp, C.c_int], C.c_int),
     "mfreg_cu_objective_seed_hessian_vec": ([_vp, _dp, C.c_double, _dp, C.c_int], C.c_int),
+    "mfreg_cu_objective_dot": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_slab_partition": ([_gp, _gp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+    "mfreg_cu_objective_create_slab": ([_dp, _dp, _gp, _gp, C.c_double, C.c_double, C.c_double,
+                                        C.POINTER(C.c_int32), C.c_int, C.POINTER(_vp)], C.c_int),
     "mfreg_cu_cg_solve": ([_vp, C.c_int, C.c_double, _dp, C.c_int, C.c_double, _dp, C.POINTER(C.c_int),
                            C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int], C.c_int),
     "mfreg_cu_minimize": ([_vp, C.c_int, _dp, C.POINTER(_OptConfig), _dp, C.POINTER(_IterRecord), C.c_int,
@@ -530,6 +534,14 @@ class Objective:
         _check(lib().mfreg_cu_objective_seed_hessian_vec(self._h, _ptr(p)[0], float(gamma), _ptr(q)[0], w))
         return q
 
+    def dot(self, a, b) -> float:
+        """vec_dot (optimizer.cpp:12-19) over the dof this objective owns."""
+        w = _where_of(a, b)
+        a, b = _as_input(a, w), _as_input(b, w)
+        v = C.c_double()
+        _check(lib().mfreg_cu_objective_dot(self._h, _ptr(a)[0], _ptr(b)[0], w, C.byref(v)))
+        return v.value
+
 
 def cg_solve(obj: Objective, b, max_iters: int = 50, rel_tol: float = 1e-2, seed: bool = False, gamma: float = 0.0):
     """cg_solve (optimizer.cpp:113-154) on obj's GN operator (or the seed operator). Returns (x, iters, relres, breakdown)."""
@@ -622,3 +634,5 @@ def warp_sinusoid(vol, image: GridDesc, max_amp: float, seed: int):
     _check(lib().mfreg_cu_warp_sinusoid(C.byref(image.c()), _ptr(vol)[0], float(max_amp), C.c_uint64(seed),
                                         _ptr(out)[0], w))
     return out
+
+from . import slab  # noqa: E402  (z-slab decomposition, multi-GPU)

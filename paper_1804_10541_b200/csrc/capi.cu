@@ -394,6 +394,51 @@ int mfreg_cu_objective_create(const double* ref, const double* tpl, const mfreg_
         *out = h.release();
     });
 }
+int mfreg_cu_objective_create_slab(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                   const mfreg_cu_grid* deform, double tau, double rho, double alpha,
+                                   const int32_t slab[4], int where, mfreg_cu_objective** out) {
+    return guard([&] {
+        check_where(where);
+        if (!slab) throw std::invalid_argument("slab: null window");
+        auto h = std::make_unique<mfreg_cu_objective>();
+        h->img = to_grid(image);
+        h->dg = to_grid(deform);
+        validate_grid(h->img, false);
+        const std::size_t n = h->img.count();
+        h->R.resize(n);
+        h->T.resize(n);
+        const auto kind = where == MFREG_CU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        MFREG_CUDA(cudaMemcpy(h->R.get(), ref, n * sizeof(double), kind));
+        MFREG_CUDA(cudaMemcpy(h->T.get(), tpl, n * sizeof(double), kind));
+        SlabSpec sp;
+        sp.zlo = slab[0];
+        sp.zhi = slab[1];
+        sp.own_lo = slab[2];
+        sp.own_hi = slab[3];
+        h->obj = std::make_unique<DeviceObjective>(h->R.get(), h->T.get(), h->img, h->dg, tau, rho, alpha, Mode::Fast,
+                                                   kStream, sp);
+        MFREG_CUDA(cudaStreamSynchronize(kStream));
+        *out = h.release();
+    });
+}
+int mfreg_cu_slab_partition(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int32_t* table) {
+    return guard([&] {
+        const auto parts = slab_partition(to_grid(image), to_grid(deform), nranks);
+        for (int r = 0; r < nranks; ++r) {
+            const SlabInfo& s = parts[r];
+            const int32_t v[7] = {s.zlo, s.zhi, s.own_lo, s.own_hi, s.need_lo, s.need_hi, s.bnd};
+            std::memcpy(table + 7 * r, v, sizeof(v));
+        }
+    });
+}
+int mfreg_cu_objective_dot(mfreg_cu_objective* obj, const double* a, const double* b, int where, double* out) {
+    return guard([&] {
+        const idx_t nd = obj->obj->dof();
+        In ai(a, nd, where, kStream);
+        In bi(b, nd, where, kStream);
+        *out = obj->obj->dot(ai.ptr, bi.ptr);
+    });
+}
 int mfreg_cu_objective_destroy(mfreg_cu_objective* obj) {
     return guard([&] { delete obj; });
 }
@@ -452,6 +497,7 @@ int mfreg_cu_objective_seed_hessian_vec(mfreg_cu_objective* obj, const double* p
 int mfreg_cu_cg_solve(mfreg_cu_objective* obj, int op, double gamma, const double* b, int max_iters, double rel_tol,
                       double* x, int* iters, double* relres, int* breakdown, int where) {
     return guard([&] {
+        if (obj->obj->sliced()) throw std::logic_error("slab objectives are driven by the distributed solver (slab.py)");
         const idx_t nd = obj->obj->dof();
         In bi(b, nd, where, kStream);
         Out xo(x, nd, where);
@@ -467,6 +513,7 @@ int mfreg_cu_minimize(mfreg_cu_objective* obj, int method, const double* y0, con
                       double* y_out, mfreg_cu_iter_record* trace, int cap, int* ntrace, int* line_search_failed,
                       int where) {
     return guard([&] {
+        if (obj->obj->sliced()) throw std::logic_error("slab objectives are driven by the distributed solver (slab.py)");
         const idx_t nd = obj->obj->dof();
         In yi(y0, nd, where, kStream);
         Out yo(y_out, nd, where);

@@ -49,6 +49,7 @@ struct FArgs {
     double* part;
     double* vpart;
     int grad;
+    int olo, ohi;       // output image planes (z slab); the tiles may extend 2 planes beyond
     int nxf, nyf;       // nodal slab footprint (max over tiles) per plane, x and y
     int dbg;            // profiling switches (0 in production)
     const int* skip;    // device flag: return immediately when set (CG already converged)
@@ -133,7 +134,8 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
     const long long n = a.g.count(), plane = static_cast<long long>(mx) * my;
     const int x0 = blockIdx.x * FT_X, y0 = blockIdx.y * FT_Y;
-    const int z0 = blockIdx.z * tm.zc, z1 = min(mz, z0 + tm.zc);
+    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);  // planes with outputs (D, P^T)
     const int xe = min(mx, x0 + FT_X), ye = min(my, y0 + FT_Y);
     const int nxA = __ldg(&a.P.base[0][x0]), nyA = __ldg(&a.P.base[1][y0]), nzA = __ldg(&a.P.base[2][z0]);
     const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
@@ -431,7 +433,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
             }
         }
         const int i = k - 2, j = k - 1;
-        const bool iout = do_z && i >= z0 && i < z1;  // uniform
+        const bool iout = do_z && i >= ilo && i < ihi;  // uniform
         const double rzk = sZr[kt];
         stage_wait(k);
 
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
                     a.frh_out[3 * n + gi] = e3;
                     a.frh_out[4 * n + gi] = e4;
                     a.frh_out[5 * n + gi] = e5;
-                    dsum += fma(-r, r, 1.0);
+                    if (j >= ilo && j < ihi) dsum += fma(-r, r, 1.0);
                 }
             }
             bW_new[0] = wc;
@@ -636,6 +638,9 @@ struct FinArgs {
     double* red;
     unsigned int* counter;
     const int* skip;
+    int nS;                   // number of device scalars summed into S
+    long long fin_lo, nwin;   // finalize nodes [fin_lo, fin_lo + nwin) (per component)
+    long long add_lo, add_hi; // nodes where `add` applies and the dot counts (owned)
 };
 
 __device__ __forceinline__ long long clampl(long long v, long long hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
@@ -674,12 +679,14 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     __shared__ bool last;
     if (a.skip && *a.skip) return;  // uniform
     const long long ny = a.gy.count();
-    // one thread per (component, node): component-major like the nodal vectors
-    const long long t = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
+    // one thread per (component, node) of the window: component-major like the nodal vectors
+    const long long tw = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
     double r0 = 0.0, r1 = 0.0;
-    if (t < 3 * ny && a.out) {
-        const int d = static_cast<int>(t / ny);
-        const long long node = t - d * ny;
+    if (tw < 3 * a.nwin && a.out) {
+        const int d = static_cast<int>(tw / a.nwin);
+        const long long node = a.fin_lo + (tw - d * a.nwin);
+        const long long t = d * ny + node;
+        const bool owned = node >= a.add_lo && node < a.add_hi;
         const long long mx = a.gy.m[0], my = a.gy.m[1];
         const long long nx = node % mx, nyy = (node / mx) % my, nz = node / (mx * my);
         const TileMeta& tm = a.tm;
@@ -698,9 +705,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
                 }
             }
         }
-        if (a.add) v += a.add[t];
+        if (a.add && owned) v += a.add[t];
         a.out[t] = v;
-        if (a.dot_a) r0 = a.dot_a[t] * v;
+        if (a.dot_a && owned) r0 = a.dot_a[t] * v;
     }
     if (a.sc == nullptr) return;
     r0 = block_reduce(r0, sh);
@@ -727,7 +734,9 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     if (threadIdx.x == 0) {
         if (a.value) {
             a.sc[0] = a.hbar * sv;                    // D
-            a.sc[1] = a.S ? a.alpha * (a.cell_y * *a.S) : 0.0;  // alpha S
+            double S = 0.0;
+            for (int k = 0; a.S && k < a.nS; ++k) S += a.S[k];
+            a.sc[1] = a.S ? a.alpha * (a.cell_y * S) : 0.0;  // alpha S
         } else {
             a.sc[0] = s0;                             // <dot_a, out>
         }
@@ -755,6 +764,8 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
     }
     a.part = fp.partials();
     a.vpart = fp.value_partials();
+    a.olo = fp.out_lo();
+    a.ohi = fp.out_hi();
     a.nxf = fp.slab_x();
     a.nyf = fp.slab_y();
     a.dbg = 0;
@@ -763,15 +774,30 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
 
 }  // namespace
 
-FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh) {
+FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh,
+                     const SlabSpec& slab) {
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
     TileMeta& t = meta_;
     t.ntx = static_cast<int>((g.m[0] + FT_X - 1) / FT_X);
     t.nty = static_cast<int>((g.m[1] + FT_Y - 1) / FT_Y);
+    // z window: outputs on image planes [zlo, zhi); tiles also cover 2 halo planes each
+    // side so the stored Hv state (rho-hat, dT) is valid wherever the Hv stencil reads it
+    const int gmz = static_cast<int>(g.m[2]);
+    const int msz = static_cast<int>(P.src.m[2]);
+    const bool full = slab.full(gmz, msz);
+    out_lo_ = full ? 0 : slab.zlo;
+    out_hi_ = full ? gmz : slab.zhi;
+    t.zlo = full ? 0 : std::max(0, slab.zlo - 2);
+    t.zhi = full ? gmz : std::min(gmz, slab.zhi + 2);
+    const auto& bz = plan.host_base[2];
+    own_lo_ = full ? 0 : slab.own_lo;
+    own_hi_ = full ? msz : slab.own_hi;
+    fin_lo_ = full ? 0 : std::min(own_lo_, bz[out_lo_]);
+    fin_hi_ = full ? msz : std::max(own_hi_, bz[out_hi_ - 1] + 2);
     // z chunking: minimise waves(1 CTA/SM) x (planes per chunk + 4 halo planes)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
-    const int mz = static_cast<int>(g.m[2]);
+    const int mz = t.zhi - t.zlo;
     int best = 1;
     double best_cost = 1e300;
     for (int ntz = 1; ntz <= std::max(1, mz / 4); ++ntz) {
@@ -788,15 +814,15 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     t.ntz = (mz + t.zc - 1) / t.zc;
     const int tsz[3] = {FT_X, FT_Y, t.zc};
     const int ntl[3] = {t.ntx, t.nty, t.ntz};
+    const int org[3] = {0, 0, t.zlo}, end[3] = {static_cast<int>(g.m[0]), static_cast<int>(g.m[1]), t.zhi};
     int nl[3];
     for (int a = 0; a < 3; ++a) {
         const auto& base = plan.host_base[a];
         const int ms = static_cast<int>(P.src.m[a]);
-        const int m = static_cast<int>(g.m[a]);
         std::vector<int> n0(ntl[a]), n1(ntl[a]);
         nl[a] = 0;
         for (int k = 0; k < ntl[a]; ++k) {
-            const int x0 = k * tsz[a], x1 = std::min(m, x0 + tsz[a]);
+            const int x0 = org[a] + k * tsz[a], x1 = std::min(end[a], x0 + tsz[a]);
             n0[k] = base[x0];
             n1[k] = base[x1 - 1] + 1;
             nl[a] = std::max(nl[a], n1[k] - n0[k] + 1);
@@ -948,9 +974,15 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.red = fp.red();
     a.counter = fp.counter();
     a.skip = spec.skip;
-    const long long ny = a.gy.count();
+    a.nS = spec.nS;
+    const long long pn = a.gy.m[0] * a.gy.m[1];
+    a.fin_lo = fp.fin_lo() * pn;
+    a.nwin = (fp.fin_hi() - fp.fin_lo()) * pn;
+    a.add_lo = fp.own_lo() * pn;
+    a.add_hi = fp.own_hi() * pn;
     note_launch();
-    k_nodal_finalize<<<static_cast<unsigned>((3 * ny + FIN_THREADS - 1) / FIN_THREADS), FIN_THREADS, 0, s>>>(a);
+    k_nodal_finalize<<<static_cast<unsigned>(std::max(1LL, (3 * a.nwin + FIN_THREADS - 1) / FIN_THREADS)), FIN_THREADS,
+                       0, s>>>(a);
 }
 
 }  // namespace mfreg_b200

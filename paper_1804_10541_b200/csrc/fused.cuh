@@ -34,6 +34,7 @@ constexpr int FT_Y = 8;   // output tile (y) per CTA
 struct TileMeta {
     int ntx, nty, ntz;          // tiles per axis
     int zc;                     // z planes per tile
+    int zlo, zhi;               // image planes the tiles cover
     int nlx, nly, nlz;          // max local nodes per tile per axis
     std::size_t part_stride;    // doubles per tile partial (nlz*nly*nlx*3)
     const int* node_tlo[3];     // per node: first touching tile
@@ -45,7 +46,9 @@ class FusedPlan {
 public:
     // R, Tw, dT, frh: the device arrays the fused kernels stream (tensor maps are
     // built over them when TMA can address the grid)
-    FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh);
+    // `slab`: z window; the full domain when slab.full()
+    FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh,
+              const SlabSpec& slab);
     bool tma() const { return tma_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
@@ -57,6 +60,12 @@ public:
     int ntiles() const { return meta_.ntx * meta_.nty * meta_.ntz; }
     int slab_x() const { return slab_[0]; }
     int slab_y() const { return slab_[1]; }
+    int out_lo() const { return out_lo_; }   // image planes with outputs
+    int out_hi() const { return out_hi_; }
+    int fin_lo() const { return fin_lo_; }   // nodal planes the finalize writes
+    int fin_hi() const { return fin_hi_; }
+    int own_lo() const { return own_lo_; }   // owned nodal planes (curvature term, dots)
+    int own_hi() const { return own_hi_; }
 
 private:
     TileMeta meta_{};
@@ -64,6 +73,7 @@ private:
     DVec part_, vpart_, red_;
     DevArray<unsigned int> counter_;
     int slab_[2] = {0, 0};
+    int out_lo_ = 0, out_hi_ = 0, fin_lo_ = 0, fin_hi_ = 0, own_lo_ = 0, own_hi_ = 0;
     bool tma_ = false;
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
@@ -90,7 +100,8 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
 // all reductions fixed-order (last-block pattern).
 struct FinalizeSpec {
     const double* add = nullptr;  // nodal term added to out (alpha * curvature gradient / Hv)
-    const double* S = nullptr;    // device scalar: sum (Lap u)^2 over all components (value)
+    const double* S = nullptr;    // device scalars: sum (Lap u)^2 (value), nS partial sums added in order
+    int nS = 1;
     double alpha = 0.0;
     double* out = nullptr;        // nodal result
     const double* dot_a = nullptr;

@@ -134,9 +134,10 @@ __global__ void k_transfer_apply(DevPlan P, const double* __restrict__ y, double
 }
 
 __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __restrict__ T, double* __restrict__ Tw,
-                       double* __restrict__ dT) {
+                       double* __restrict__ dT, int zoff) {
     idx_t x, yy, z;
     if (!coords(P.tgt, x, yy, z)) return;
+    z += zoff;  // image-plane window (z slabs)
     double v[3];
     transfer_point(P, y, x, yy, z, v);
     double val, gx, gy, gz;
@@ -747,10 +748,15 @@ void launch_sample(const Grid& img0, const double* T, const double* pts, idx_t n
     img.set_inv();
     note_launch(), k_sample<<<blocks1(n), 256, 0, s>>>(img, T, pts, n, vals, dT);
 }
-void launch_warp(const DevPlan& P0, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s) {
+void launch_warp(const DevPlan& P0, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s, int zlo,
+                 int zhi) {
     DevPlan P = P0;
     P.tgt.set_inv();
-    note_launch(), k_warp<<<grid3(P.tgt), block3(), 0, s>>>(P, y, T, Tw, dT);
+    if (zhi < 0) zhi = static_cast<int>(P.tgt.m[2]);
+    dim3 gr = grid3(P.tgt);
+    gr.z = static_cast<unsigned>(zhi - zlo);
+    if (gr.z == 0) return;
+    note_launch(), k_warp<<<gr, block3(), 0, s>>>(P, y, T, Tw, dT, zlo);
 }
 void launch_ngf_ws(const Grid& img0, const double* R, const double* Tw, double tau, double rho, double* r,
                    double* inv1, double* inv2, double* rh, cudaStream_t s) {

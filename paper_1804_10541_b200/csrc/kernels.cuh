@@ -27,7 +27,9 @@ void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStrea
 void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n, double* vals, double* dT,
                    cudaStream_t s);
 // Fused P*y + trilinear sample: T_w and dT/dP (32 B/voxel) without materialising P*y.
-void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s);
+// image planes [zlo, zhi) (zhi < 0: all)
+void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
+                 int zlo = 0, int zhi = -1);
 
 // ---- NGF workspace (ngf.cpp:185-214) + rho-hat table (ngf.cpp:39-64)
 void launch_ngf_ws(const Grid& img, const double* R, const double* Tw, double tau, double rho, double* r,

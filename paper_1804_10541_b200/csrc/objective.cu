@@ -42,6 +42,53 @@ Grid deformation_grid_for(const Grid& image, idx_t ratio) {  // multilevel.cpp:3
     return make_deform_grid(image, pts);
 }
 
+std::vector<int> plan_base_axis(idx_t mt, idx_t ms) {
+    std::vector<int> hb(mt);
+    for (idx_t k = 0; k < mt; ++k) {  // transfer.cpp:24-35, same expression as DevicePlanOwner
+        const double c = (static_cast<double>(k) + 0.5) * static_cast<double>(ms - 1) / static_cast<double>(mt);
+        hb[k] = static_cast<int>(std::clamp<idx_t>(static_cast<idx_t>(std::floor(c)), 0, ms - 2));
+    }
+    return hb;
+}
+
+std::vector<SlabInfo> slab_partition(const Grid& img, const Grid& dg, int nr) {
+    validate_grid(dg, true);
+    validate_grid(img, false);
+    if (nr < 1) throw std::invalid_argument("slab_partition: nranks must be >= 1");
+    const int mz = static_cast<int>(img.m[2]), ms = static_cast<int>(dg.m[2]);
+    const std::vector<int> b = plan_base_axis(mz, ms);
+    // split planes: first image plane of a nodal cell, at or after the even split
+    std::vector<int> zb(nr + 1, 0);
+    zb[nr] = mz;
+    for (int r = 1; r < nr; ++r) {
+        int z = std::max(zb[r - 1] + 1, static_cast<int>((static_cast<long long>(r) * mz + nr / 2) / nr));
+        while (z < mz && b[z] == b[z - 1]) ++z;
+        if (z >= mz) throw std::invalid_argument("slab_partition: too many ranks for the z extent");
+        zb[r] = z;
+    }
+    std::vector<SlabInfo> out(nr);
+    for (int r = 0; r < nr; ++r) {
+        SlabInfo& s = out[r];
+        s.zlo = zb[r];
+        s.zhi = zb[r + 1];
+        s.own_lo = r == 0 ? 0 : b[s.zlo];
+        s.own_hi = r == nr - 1 ? ms : b[s.zhi];
+        s.bnd = r == nr - 1 ? 0 : std::max(0, b[s.zhi - 1] + 2 - s.own_hi);
+        // operand planes read: the warp over [zlo-3, zhi+3) and the curvature stencil
+        // (Lap Lap: +-2 nodal planes) of the owned planes
+        const int wlo = std::max(0, s.zlo - 3), whi = std::min(mz, s.zhi + 3);
+        s.need_lo = std::max(0, std::min(b[wlo], s.own_lo - 2));
+        s.need_hi = std::min(ms, std::max(b[whi - 1] + 2, s.own_hi + 2));
+    }
+    for (int r = 0; r < nr; ++r) {
+        const SlabInfo& s = out[r];
+        if ((r > 0 && s.need_lo < out[r - 1].own_lo) || (r + 1 < nr && s.need_hi > out[r + 1].own_hi) ||
+            (r + 1 < nr && s.own_hi + s.bnd > out[r + 1].own_hi) || s.own_hi <= s.own_lo)
+            throw std::invalid_argument("slab_partition: slabs thinner than the halo (too many ranks)");
+    }
+    return out;
+}
+
 DevicePlanOwner::DevicePlanOwner(const Grid& nodal, const Grid& image) {
     validate_grid(nodal, true);
     validate_grid(image, false);
@@ -51,14 +98,11 @@ DevicePlanOwner::DevicePlanOwner(const Grid& nodal, const Grid& image) {
         const idx_t mt = image.m[a], ms = nodal.m[a];
         auto& hb = host_base[a];
         auto& hr = host_rem[a];
-        hb.resize(mt);
+        hb = plan_base_axis(mt, ms);
         hr.resize(mt);
         for (idx_t k = 0; k < mt; ++k) {  // transfer.cpp:24-39, same expression
             const double c = (static_cast<double>(k) + 0.5) * static_cast<double>(ms - 1) / static_cast<double>(mt);
-            idx_t b = static_cast<idx_t>(std::floor(c));
-            b = std::clamp<idx_t>(b, 0, ms - 2);
-            hb[k] = static_cast<int>(b);
-            hr[k] = c - static_cast<double>(b);
+            hr[k] = c - static_cast<double>(hb[k]);
             if (hr[k] < 0.0 || hr[k] > 1.0) throw std::invalid_argument("transfer plan: coverage invariant violated");
         }
         std::vector<int> lo(ms - 1, 0), hi(ms - 1, 0);
@@ -180,9 +224,10 @@ void DeviceNgf::hessian_vec(const double* p3n, double* out3n) {
 
 // ------------------------------------------------------------ DeviceObjective
 DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform,
-                                 double tau, double rho, double alpha, Mode mode, cudaStream_t s)
+                                 double tau, double rho, double alpha, Mode mode, cudaStream_t s, const SlabSpec& slab)
     : img_(image),
       dg_(deform),
+      slab_(slab),
       alpha_(alpha),
       s_(s),
       T_(T_dev),
@@ -196,8 +241,18 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     img3_.resize(3 * static_cast<std::size_t>(img_.count()));
     launch_identity(dg_, xid_.get(), s_);
     check_launch("identity");
+    sliced_ = !slab.full(static_cast<int>(img_.m[2]), static_cast<int>(dg_.m[2]));
+    if (sliced_) {
+        if (mode != Mode::Fast) throw std::invalid_argument("z slabs require fast mode");
+        const auto parts = slab_partition(img_, dg_, 1);  // validates the grids
+        (void)parts;
+        const int mz = static_cast<int>(img_.m[2]), msz = static_cast<int>(dg_.m[2]);
+        if (!(0 <= slab.zlo && slab.zlo < slab.zhi && slab.zhi <= mz && 0 <= slab.own_lo &&
+              slab.own_lo < slab.own_hi && slab.own_hi <= msz))
+            throw std::invalid_argument("slab: invalid z window");
+    }
     if (mode == Mode::Fast) {
-        fused_ = std::make_unique<FusedPlan>(plan_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.frh.get());
+        fused_ = std::make_unique<FusedPlan>(plan_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.frh.get(), slab_);
         MFREG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
         MFREG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         MFREG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -220,13 +275,24 @@ double DeviceObjective::eval(const double* y, double* grad) {
     const idx_t ny = dg_.count();
     if (fused_) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
-        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
+        const int mz = static_cast<int>(img_.m[2]);
+        if (sliced_)  // the slab's planes + 3 halo planes (state of the 2 halo planes the Hv reads)
+            launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_, std::max(0, slab_.zlo - 3),
+                        std::min(mz, slab_.zhi + 3));
+        else
+            launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
         launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
         // curvature value / gradient on the side stream, overlapping the image pass
         MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
         MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
         launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
-        red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
+        const idx_t pn = dg_.m[0] * dg_.m[1];
+        if (sliced_)  // owned nodal planes only, per component
+            for (int d = 0; d < 3; ++d)
+                red2_->sum(SUM_SQ, (slab_.own_hi - slab_.own_lo) * pn, lapu_.get() + d * ny + slab_.own_lo * pn, nullptr,
+                           sc2_.get() + d, 1.0, s2_);
+        else
+            red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
         if (grad && alpha_ != 0.0)
             launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
         MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
@@ -236,6 +302,7 @@ double DeviceObjective::eval(const double* y, double* grad) {
         FinalizeSpec f;
         f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
         f.S = sc2_.get();
+        f.nS = sliced_ ? 3 : 1;
         f.alpha = alpha_;
         f.out = grad;
         f.value = true;
@@ -302,6 +369,14 @@ void DeviceObjective::seed_hessian_vec(const double* p, double gamma, double* q)
 }
 
 double DeviceObjective::dot(const double* a, const double* b) {
+    if (sliced_) {  // owned nodal planes, per component, added in component order
+        const idx_t ny = dg_.count(), pn = dg_.m[0] * dg_.m[1], off = slab_.own_lo * pn;
+        for (int d = 0; d < 3; ++d)
+            ngf_.reducer().sum(SUM_DOT, (slab_.own_hi - slab_.own_lo) * pn, a + d * ny + off, b + d * ny + off,
+                               sc_.dev(12 + d), 1.0, s_);
+        const double* h = sc_.fetch(15, s_);
+        return (h[12] + h[13]) + h[14];
+    }
     ngf_.reducer().sum(SUM_DOT, dof(), a, b, sc_.dev(8), 1.0, s_);
     return sc_.fetch(9, s_)[8];
 }

@@ -96,6 +96,24 @@ private:
     DevPlan view_{};
 };
 
+// transfer.cpp:24-35 on one axis: image index -> nodal cell (host, no device state)
+std::vector<int> plan_base_axis(idx_t image_m, idx_t nodal_m);
+
+// z-slab decomposition: rank r outputs the image planes
+// [zlo, zhi) (D and the P^T contributions of those planes) and owns the nodal
+// planes [own_lo, own_hi) (curvature term, dot products). Splits fall on nodal
+// cell boundaries, so neighbouring ranks share exactly the P^T planes
+// [own_hi, own_hi + bnd) (summed on the upper rank). Before an operator call the
+// nodal operand must be valid on [need_lo, need_hi) (halo from the neighbours).
+struct SlabSpec {
+    int zlo = 0, zhi = -1, own_lo = 0, own_hi = -1;
+    bool full(int mz, int msz) const { return zhi < 0 || (zlo == 0 && zhi == mz && own_lo == 0 && own_hi == msz); }
+};
+struct SlabInfo {
+    int zlo, zhi, own_lo, own_hi, need_lo, need_hi, bnd;
+};
+std::vector<SlabInfo> slab_partition(const Grid& image, const Grid& deform, int nranks);
+
 // Reduction helpers: exact 4096-chunk order (parity) or fixed-order tree (fast).
 class Reducer {
 public:
@@ -194,8 +212,9 @@ class DeviceObjective : public DeviceProblem {
 public:
     // R_dev/T_dev: device arrays over `image` that must outlive the objective
     // (the reference Objective also stores references, optimizer.hpp:87-88).
+    // `slab`: this rank's z window (fast mode only); default: the whole domain
     DeviceObjective(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform, double tau,
-                    double rho, double alpha, Mode mode, cudaStream_t s);
+                    double rho, double alpha, Mode mode, cudaStream_t s, const SlabSpec& slab = SlabSpec{});
     ~DeviceObjective() override;
     idx_t dof() const override { return 3 * dg_.count(); }
     double eval(const double* y, double* grad) override;
@@ -216,9 +235,12 @@ public:
     const Grid& deform_grid() const { return dg_; }
     DeviceNgf& ngf() { return ngf_; }
     const DevicePlanOwner& plan() const { return plan_; }
+    bool sliced() const { return sliced_; }
 
 private:
     Grid img_, dg_;
+    SlabSpec slab_;
+    bool sliced_ = false;
     double alpha_;
     cudaStream_t s_;
     const double* T_;

@@ -1,0 +1,203 @@
+"""GPU: z-slab decomposition (SURVEY §8 row e) against the single-domain objective.
+
+N slab objectives run as threads on one B200 (`LoopbackHub`: the same exchange
+plan `TorchComm` drives over NCCL). Assembled on the owned planes, their J,
+gradient, GN Hessian-vector product and dot products must equal the full-domain
+`fast` objective (and the CPU reference) to the north_star fp64 tolerance 1e-9;
+the only differences are the order of the per-tile / per-rank partial sums.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from conftest import max_rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-9
+
+
+def _run_ranks(n, body):
+    import paper_1804_10541_b200 as P
+    hub = P.slab.LoopbackHub(n)
+    out, errs = {}, []
+
+    def run(r):
+        try:
+            out[r] = body(r, hub.comm(r))
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+            hub._bar.abort()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(n)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=300)
+    assert not errs, errs
+    return out
+
+
+@pytest.mark.parametrize("m,h,n", [
+    ((64, 48, 72), (1.0, 1.0, 1.2), 2),
+    ((64, 48, 72), (1.0, 1.0, 1.2), 3),
+    ((40, 36, 96), (0.97, 0.97, 1.0), 4),
+])
+def test_slab_operators_match_full_domain(oracle, m, h, n):
+    import torch
+
+    import paper_1804_10541_b200 as P
+    img = P.make_image_grid(m, h)
+    dg = P.deformation_grid_for(img, 4)
+    R = oracle.make_phantom(m, h) * 1000.0
+    T = oracle.warp_sinusoid(R, m, h, 3.0, 42)
+    full = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), alpha=1.0, mode=P.Mode.FAST)
+    rng = np.random.default_rng(3)
+    y = full.identity() + rng.uniform(-0.4, 0.4, full.dof())
+    p = rng.standard_normal(full.dof())
+    g_ref = np.empty(full.dof())
+    J_ref = full.eval(y, g_ref)
+    D_ref, S_ref = full.last_distance(), full.last_regularizer()
+    q_ref = full.gn_hessian_vec(p)
+    pq_ref = float(np.dot(p, q_ref))
+    # the CPU reference agrees with the full-domain fast objective (anchor)
+    oo = oracle.objective(R, T, m, h, tuple(dg.m))
+    J_o, _, _, g_o = oo.eval(y)
+    assert abs(J_ref - J_o) <= TOL * abs(J_o)
+    assert max_rel(g_ref, g_o) <= TOL
+
+    Rd, Td = torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda()
+    ms = tuple(dg.m)
+
+    def body(r, comm):
+        so = P.slab.SlabObjective(Rd, Td, img, dg, P.NgfParams(10.0, 10.0), alpha=1.0, comm=comm)
+        s = so.info
+        # each rank starts with only its owned planes valid (the rest poisoned)
+        def local(v):
+            t = torch.full((so.dof(),), float("nan"), dtype=torch.float64, device="cuda")
+            src = torch.from_numpy(v).cuda()
+            so.owned(t).copy_(so.owned(src))
+            return t
+        yl, pl = local(y), local(p)
+        g = torch.zeros(so.dof(), dtype=torch.float64, device="cuda")
+        J = so.eval(yl, g)
+        D, S = so.last_distance(), so.last_regularizer()
+        q = so.gn_hessian_vec(pl)
+        pq = so.dot(pl, q)
+        torch.cuda.synchronize()
+        return s, J, D, S, so.owned(g).cpu().numpy(), so.owned(q).cpu().numpy(), pq
+
+    res = _run_ranks(n, body)
+    gv = g_ref.reshape(3, ms[2], ms[1], ms[0])
+    qv = q_ref.reshape(3, ms[2], ms[1], ms[0])
+    g_scale, q_scale = np.max(np.abs(g_ref)), np.max(np.abs(q_ref))
+    covered = 0
+    for r in range(n):
+        s, J, D, S, g, q, pq = res[r]
+        assert J == res[0][1] and pq == res[0][6]          # identical on every rank
+        assert abs(J - J_ref) <= TOL * abs(J_ref)
+        assert abs(D - D_ref) <= TOL * abs(D_ref) and abs(S - S_ref) <= TOL * max(abs(S_ref), 1e-300)
+        assert np.all(np.isfinite(g)) and np.all(np.isfinite(q))
+        assert np.max(np.abs(g - gv[:, s.own_lo:s.own_hi])) <= TOL * g_scale
+        assert np.max(np.abs(q - qv[:, s.own_lo:s.own_hi])) <= TOL * q_scale
+        assert abs(pq - pq_ref) <= TOL * abs(pq_ref)
+        covered += s.own_hi - s.own_lo
+    assert covered == ms[2]
+
+
+def test_slab_requires_fast_mode_and_valid_window():
+    import ctypes as C
+
+    import paper_1804_10541_b200 as P
+    img = P.make_image_grid((32, 32, 32))
+    dg = P.deformation_grid_for(img, 4)
+    R = np.ones(img.count())
+    h = P._vp()
+    bad = (C.c_int32 * 4)(10, 5, 0, 3)
+    rc = P.lib().mfreg_cu_objective_create_slab(R.ctypes.data, R.ctypes.data, C.byref(img.c()), C.byref(dg.c()),
+                                                10.0, 10.0, 1.0, bad, P.HOST, C.byref(h))
+    assert rc == 1 and b"slab" in P.lib().mfreg_cu_last_error()
+
+
+def _gloo_gpu_worker(rank, world, port, queue, m, h):
+    """One process per rank on the same device, torch.distributed (gloo, CUDA planes
+    staged through the host): the TorchComm path NCCL takes on multi-GPU nodes."""
+    import os
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1804_10541_b200 as P
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        torch.cuda.set_device(0)
+        img = P.make_image_grid(m, h)
+        dg = P.deformation_grid_for(img, 4)
+        R = P.make_phantom(img, device=True) * 1000.0
+        T = P.warp_sinusoid(R, img, 3.0, 42)
+        gen = torch.Generator(device="cuda").manual_seed(5)
+        y = torch.from_numpy(dg.point_coords()).cuda() + (torch.rand(3 * dg.count(), generator=gen, device="cuda",
+                                                                     dtype=torch.float64) - 0.5) * 0.6
+        p = torch.rand(3 * dg.count(), generator=gen, device="cuda", dtype=torch.float64) - 0.5
+        so = P.slab.SlabObjective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.slab.TorchComm())
+        g = torch.zeros_like(y)
+        J = so.eval(y.clone(), g)
+        q = so.gn_hessian_vec(p.clone())
+        pq = so.dot(p, q)
+        queue.put((rank, (so.info, J, pq, so.owned(g).cpu().numpy(), so.owned(q).cpu().numpy())))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_torch_distributed_two_processes():
+    import socket
+
+    import torch
+    import torch.multiprocessing as mp
+
+    import paper_1804_10541_b200 as P
+    m, h, world = (64, 64, 80), (1.0, 1.0, 1.0), 2
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    qu = ctx.Queue()
+    procs = [ctx.Process(target=_gloo_gpu_worker, args=(r, world, port, qu, m, h)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    res = {}
+    try:
+        for _ in range(world):
+            r, v = qu.get(timeout=300)
+            res[r] = v
+    finally:
+        for pr in procs:
+            pr.join(timeout=60)
+            if pr.is_alive():
+                pr.kill()
+    # single-domain reference on the same inputs
+    img = P.make_image_grid(m, h)
+    dg = P.deformation_grid_for(img, 4)
+    R = P.make_phantom(img, device=True) * 1000.0
+    T = P.warp_sinusoid(R, img, 3.0, 42)
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    y = torch.from_numpy(dg.point_coords()).cuda() + (torch.rand(3 * dg.count(), generator=gen, device="cuda",
+                                                                 dtype=torch.float64) - 0.5) * 0.6
+    p = torch.rand(3 * dg.count(), generator=gen, device="cuda", dtype=torch.float64) - 0.5
+    full = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.Mode.FAST)
+    g = torch.empty_like(y)
+    J_ref = full.eval(y, g)
+    q = full.gn_hessian_vec(p)
+    pq_ref = float(torch.dot(p, q))
+    ms = tuple(dg.m)
+    gv = g.cpu().numpy().reshape(3, ms[2], ms[1], ms[0])
+    qv = q.cpu().numpy().reshape(3, ms[2], ms[1], ms[0])
+    for r in range(world):
+        s, J, pq, gl, ql = res[r]
+        assert abs(J - J_ref) <= TOL * abs(J_ref) and abs(pq - pq_ref) <= TOL * abs(pq_ref)
+        assert np.max(np.abs(gl - gv[:, s.own_lo:s.own_hi])) <= TOL * np.max(np.abs(gv))
+        assert np.max(np.abs(ql - qv[:, s.own_lo:s.own_hi])) <= TOL * np.max(np.abs(qv))
