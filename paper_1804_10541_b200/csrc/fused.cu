@@ -876,10 +876,12 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
         throw std::invalid_argument("fused kernels: tile footprint exceeds shared memory (deformation grid too fine)");
     if (static_cast<long long>(slab_[0]) * slab_[1] * 3 > 4LL * NTH)
         throw std::invalid_argument("fused kernels: nodal slab footprint too large (deformation grid too fine)");
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hv_smem)));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev_smem)));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(hv_smem)));
-    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ev_smem)));
+    // the cap is per kernel (process-wide): set it to the device limit so plans of
+    // different footprints (levels, slabs, threads) never lower each other's
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
+    MFREG_CUDA(cudaFuncSetAttribute(k_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_optin));
     // TMA needs 16-byte global strides: even mx (rows) and 16-byte aligned bases
     const bool aligned = (g.m[0] % 2 == 0) && (reinterpret_cast<std::uintptr_t>(R) % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(Tw) % 16 == 0) &&

@@ -225,10 +225,12 @@ class SlabObjective:
         self._last = (0.0, 0.0)
 
     def __del__(self):
-        from . import _lib
-        if getattr(self, "_h", None) and _lib is not None:
-            lib().mfreg_cu_objective_destroy(self._h)
-            self._h = None
+        try:
+            if getattr(self, "_h", None):
+                lib().mfreg_cu_objective_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
 
     def dof(self) -> int:
         return self._dof
@@ -286,3 +288,111 @@ class SlabObjective:
     def owned(self, v):
         """View of v's owned nodal planes, shape (3, own_hi - own_lo, my, mx)."""
         return self.ex._planes(v, self.info.own_lo, self.info.own_hi)
+
+    def inf_norm(self, a, scale: float = 1.0) -> float:
+        """max |scale * a_i| over all ranks' owned planes."""
+        v = float((self.owned(a) * scale).abs().max())
+        return max(row[0] for row in self.comm.allgather([v], a))
+
+    def min_spacing(self) -> float:
+        return min(self.deform.h)
+
+
+# ------------------------------------------------------------------ distributed solvers
+def cg_solve(so: SlabObjective, b, max_iters: int = 50, rel_tol: float = 1e-2):
+    """cg_solve (optimizer.cpp:113-154) on the sharded GN operator: x0 = 0, the
+    reference's scalar logic (breakdown on non-finite / non-positive <p,Ap>,
+    relres = ||r|| / ||b||, beta = rr_new / rr); every dot is a sharded reduction.
+    Returns (x, iters, relres, breakdown)."""
+    import math
+
+    import torch
+    x = torch.zeros_like(b)
+    r, p = b.clone(), b.clone()
+    rr = so.dot(b, b)
+    bnorm = math.sqrt(rr)
+    iters, relres, breakdown = 0, 0.0, False
+    if bnorm == 0.0:
+        return x, iters, relres, breakdown
+    ap = torch.zeros_like(b)
+    for _ in range(max_iters):
+        so.gn_hessian_vec(p, ap)
+        pap = so.dot(p, ap)
+        if not math.isfinite(pap) or pap <= 0.0:
+            breakdown = not math.isfinite(pap)
+            break
+        alpha = rr / pap
+        x.add_(p, alpha=alpha)
+        r.add_(ap, alpha=-alpha)
+        rr_new = so.dot(r, r)
+        iters += 1
+        relres = math.sqrt(rr_new) / bnorm
+        if not math.isfinite(rr_new):
+            breakdown = True
+            break
+        if relres <= rel_tol:
+            break
+        beta = rr_new / rr
+        rr = rr_new
+        p.mul_(beta).add_(r)
+    return x, iters, relres, breakdown
+
+
+def gauss_newton_minimize(so: SlabObjective, y0, cfg=None):
+    """gauss_newton_minimize (optimizer.cpp:202-268) over z slabs: same control flow,
+    stopping rules (optimizer.cpp:188-200) and Armijo backtracking
+    (optimizer.cpp:156-175); J, norms and dots are global. Returns (y, trace,
+    line_search_failed), identical on every rank."""
+    import math
+
+    from . import IterationRecord, OptimizerConfig
+    cfg = cfg or OptimizerConfig()
+    y = y0.clone()
+    trace, lsf = [], False
+    if cfg.max_iters <= 0:
+        return y, trace, lsf
+    grad = y.new_zeros(y.shape)
+    y_trial = y.clone()
+    j = so.eval(y, grad)
+    g0 = math.sqrt(so.dot(grad, grad))
+    min_hy = so.min_spacing()
+    for it in range(cfg.max_iters):
+        gnorm = math.sqrt(so.dot(grad, grad))
+        rec = IterationRecord(it, 0, j, so.last_distance(), so.last_regularizer(), gnorm, 0.0)
+        if gnorm <= cfg.tol_grad * g0:
+            trace.append(rec)
+            break
+        d, rec.cg_iters, _, _ = cg_solve(so, -grad, cfg.cg_max_iters, cfg.cg_rel_tol)
+        gdotd = so.dot(grad, d)
+        dinf = so.inf_norm(d)
+        eta = min(1.0, min_hy / dinf) if dinf > 0.0 else 1.0
+        ok = False
+        if gdotd < 0.0:
+            for _ in range(cfg.max_backtracks + 1):
+                torch_axpy_to(y, eta, d, y_trial)
+                f = so.eval(y_trial, None)
+                if math.isfinite(f) and f <= j + cfg.c1 * eta * gdotd:
+                    ok = True
+                    break
+                eta *= cfg.beta
+        if not ok:
+            lsf = True
+            trace.append(rec)
+            break
+        rec.step = eta
+        j_prev = j
+        torch_axpy_to(y, eta, d, y)
+        step_inf = so.inf_norm(d, eta)
+        j = so.eval(y, grad)
+        trace.append(rec)
+        gn = math.sqrt(so.dot(grad, grad))
+        if (gn <= cfg.tol_grad * g0 or abs(j_prev - j) <= cfg.tol_rel_j * max(1.0, abs(j_prev))
+                or step_inf <= cfg.tol_step * min_hy):
+            break
+    return y, trace, lsf
+
+
+def torch_axpy_to(y, eta: float, d, out) -> None:
+    """out = y + eta * d (optimizer.cpp:170, elementwise)."""
+    import torch
+    torch.add(y, d, alpha=eta, out=out)
