@@ -56,15 +56,18 @@ void check_where(int where) {
 }
 
 // Read-only input: device view of a host or device array of n doubles.
+// `cache`: a per-handle staging buffer reused across calls (no cudaMalloc/cudaFree
+// on the per-iteration path); null = a temporary.
 struct In {
-    In(const double* p, std::size_t n, int where, cudaStream_t s) {
+    In(const double* p, std::size_t n, int where, cudaStream_t s, DVec* cache = nullptr) {
         check_where(where);
         if (where == MFREG_CU_DEVICE || !p) {
             ptr = p;
         } else {
-            buf.resize(n);
-            MFREG_CUDA(cudaMemcpyAsync(buf.get(), p, n * sizeof(double), cudaMemcpyHostToDevice, s));
-            ptr = buf.get();
+            DVec& b = cache ? *cache : buf;
+            if (b.size() < n) b.resize(n);
+            MFREG_CUDA(cudaMemcpyAsync(b.get(), p, n * sizeof(double), cudaMemcpyHostToDevice, s));
+            ptr = b.get();
         }
     }
     DVec buf;
@@ -73,18 +76,19 @@ struct In {
 
 // Output: device buffer written by kernels, copied back on finish() for host.
 struct Out {
-    Out(double* p, std::size_t n, int where) : host(p), n(n), where(where) {
+    Out(double* p, std::size_t n, int where, DVec* cache = nullptr) : host(p), n(n), where(where) {
         check_where(where);
         if (where == MFREG_CU_DEVICE || !p) {
             ptr = p;
         } else {
-            buf.resize(n);
-            ptr = buf.get();
+            DVec& b = cache ? *cache : buf;
+            if (b.size() < n) b.resize(n);
+            ptr = b.get();
         }
     }
     void finish(cudaStream_t s) {
         if (where == MFREG_CU_HOST && host) {
-            MFREG_CUDA(cudaMemcpyAsync(host, buf.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+            MFREG_CUDA(cudaMemcpyAsync(host, ptr, n * sizeof(double), cudaMemcpyDeviceToHost, s));
             MFREG_CUDA(cudaStreamSynchronize(s));
         }
     }
@@ -164,7 +168,7 @@ struct mfreg_cu_objective {
     Grid img, dg;
     DVec R, T;
     std::unique_ptr<DeviceObjective> obj;
-    DVec stage_a, stage_b;
+    DVec stage[4];  // host-call staging (y / p in, grad / q out), reused
 };
 
 extern "C" {
@@ -461,8 +465,8 @@ int mfreg_cu_objective_eval(mfreg_cu_objective* obj, const double* y, double* gr
     return guard([&] {
         const idx_t nd = obj->obj->dof();
         if (!y) throw std::invalid_argument("Objective::eval: y length mismatch");
-        In yi(y, nd, where, kStream);
-        Out g(grad, nd, where);
+        In yi(y, nd, where, kStream, &obj->stage[0]);
+        Out g(grad, nd, where, &obj->stage[1]);
         const double v = obj->obj->eval(yi.ptr, g.ptr);
         g.finish(kStream);
         if (j) *j = v;
@@ -477,8 +481,8 @@ int mfreg_cu_objective_last(mfreg_cu_objective* obj, double* distance, double* r
 int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, double* q, int where) {
     return guard([&] {
         const idx_t nd = obj->obj->dof();
-        In pi(p, nd, where, kStream);
-        Out o(q, nd, where);
+        In pi(p, nd, where, kStream, &obj->stage[2]);
+        Out o(q, nd, where, &obj->stage[3]);
         obj->obj->gn_hessian_vec(pi.ptr, o.ptr);
         o.finish(kStream);
     });
@@ -487,7 +491,7 @@ int mfreg_cu_objective_seed_hessian_vec(mfreg_cu_objective* obj, const double* p
                                         int where) {
     return guard([&] {
         const idx_t nd = obj->obj->dof();
-        In pi(p, nd, where, kStream);
+        In pi(p, nd, where, kStream, &obj->stage[2]);
         Out o(q, nd, where);
         obj->obj->seed_hessian_vec(pi.ptr, gamma, o.ptr);
         o.finish(kStream);

@@ -19,6 +19,7 @@ HvTable make_hv_table(const Grid& g);
 
 // launch accounting (mfreg_cu_launch_count)
 void note_launch();
+void note_launches(long long n);
 long long launch_counter();
 
 // ---- grid transfer and warp (transfer.cpp:49-150, volume.cpp:29-94)

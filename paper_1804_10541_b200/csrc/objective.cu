@@ -1,6 +1,7 @@
 // DeviceObjective and its building blocks (see objective.cuh).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "objective.cuh"
@@ -270,45 +271,75 @@ DeviceObjective::~DeviceObjective() {
 
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
 
+// fast mode: the launch sequence of eval (captured once per (y, grad) into a CUDA graph)
+void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStream_t s) {
+    const idx_t ny = dg_.count();
+    const int mz = static_cast<int>(img_.m[2]);
+    if (sliced_)  // the slab's planes + 3 halo planes (state of the 2 halo planes the Hv reads)
+        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, std::max(0, slab_.zlo - 3),
+                    std::min(mz, slab_.zhi + 3));
+    else
+        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s);
+    launch_sub(3 * ny, y, xid_.get(), u_.get(), s);
+    // curvature value / gradient on the side stream, overlapping the image pass
+    MFREG_CUDA(cudaEventRecord(ev_fork_, s));
+    MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+    launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
+    const idx_t pn = dg_.m[0] * dg_.m[1];
+    if (sliced_)  // owned nodal planes only, per component
+        for (int d = 0; d < 3; ++d)
+            red2_->sum(SUM_SQ, (slab_.own_hi - slab_.own_lo) * pn, lapu_.get() + d * ny + slab_.own_lo * pn, nullptr,
+                       sc2_.get() + d, 1.0, s2_);
+    else
+        red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
+    if (grad && alpha_ != 0.0)
+        launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+    MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+    launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, ngf_.frh.get(),
+                      grad != nullptr, s);
+    MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    FinalizeSpec f;
+    f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
+    f.S = sc2_.get();
+    f.nS = sliced_ ? 3 : 1;
+    f.alpha = alpha_;
+    f.out = grad;
+    f.value = true;
+    f.sc = sc_.dev(0);
+    launch_nodal_finalize(plan_, *fused_, f, s);
+    check_launch("Objective::eval (fused)");
+}
+
+// fast mode: GN Hv (alpha 2 h^y Lap(Lap p) on the side stream, overlapping the image
+// pass), optionally <dot_a, q> into sc
+void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip,
+                                      cudaStream_t s) {
+    if (alpha_ != 0.0) {
+        MFREG_CUDA(cudaEventRecord(ev_fork_, s));
+        MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+        launch_lap3(dg_, p, lapp_.get(), s2_);
+        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+        MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+    }
+    launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s, skip);
+    if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    FinalizeSpec f;
+    f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
+    f.out = q;
+    f.dot_a = dot_a;
+    f.sc = sc;
+    f.skip = skip;
+    launch_nodal_finalize(plan_, *fused_, f, s);
+    check_launch("Objective::gn_hessian_vec (fused)");
+}
+
 // optimizer.cpp:64-92
 double DeviceObjective::eval(const double* y, double* grad) {
     const idx_t ny = dg_.count();
     if (fused_) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
-        const int mz = static_cast<int>(img_.m[2]);
-        if (sliced_)  // the slab's planes + 3 halo planes (state of the 2 halo planes the Hv reads)
-            launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_, std::max(0, slab_.zlo - 3),
-                        std::min(mz, slab_.zhi + 3));
-        else
-            launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
-        launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
-        // curvature value / gradient on the side stream, overlapping the image pass
-        MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
-        MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
-        launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
-        const idx_t pn = dg_.m[0] * dg_.m[1];
-        if (sliced_)  // owned nodal planes only, per component
-            for (int d = 0; d < 3; ++d)
-                red2_->sum(SUM_SQ, (slab_.own_hi - slab_.own_lo) * pn, lapu_.get() + d * ny + slab_.own_lo * pn, nullptr,
-                           sc2_.get() + d, 1.0, s2_);
-        else
-            red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
-        if (grad && alpha_ != 0.0)
-            launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
-        MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
-        launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, ngf_.frh.get(),
-                          grad != nullptr, s_);
-        MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        FinalizeSpec f;
-        f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
-        f.S = sc2_.get();
-        f.nS = sliced_ ? 3 : 1;
-        f.alpha = alpha_;
-        f.out = grad;
-        f.value = true;
-        f.sc = sc_.dev(0);
-        launch_nodal_finalize(plan_, *fused_, f, s_);
-        check_launch("Objective::eval (fused)");
+        graphs_.run({y, grad, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(1)}, s_,
+                    [&](cudaStream_t cs) { enqueue_eval_fast(y, grad, cs); });
         const double* h = sc_.fetch(2, s_);
         last_distance_ = h[0];
         last_regularizer_ = h[1];
@@ -335,20 +366,8 @@ double DeviceObjective::eval(const double* y, double* grad) {
 // optimizer.cpp:94-104
 void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
     if (fused_) {
-        if (alpha_ != 0.0) {  // alpha 2 h^y Lap(Lap p) on the side stream, overlapping the image pass
-            MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
-            MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
-            launch_lap3(dg_, p, lapp_.get(), s2_);
-            launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
-            MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
-        }
-        launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
-        if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-        FinalizeSpec f;
-        f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
-        f.out = q;
-        launch_nodal_finalize(plan_, *fused_, f, s_);
-        check_launch("Objective::gn_hessian_vec (fused)");
+        graphs_.run({p, q, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(2)}, s_,
+                    [&](cudaStream_t cs) { enqueue_hv_fast(p, q, nullptr, nullptr, nullptr, cs); });
         return;
     }
     launch_Pp_s(plan_.view(), p, ngf_.dT.get(), ngf_.sv.get(), s_);
@@ -391,23 +410,66 @@ void DeviceObjective::apply_dot(int op, double gamma, const double* p, double* q
         return;
     }
     // fused GN Hv with <p, q> folded into the nodal finalize
-    if (alpha_ != 0.0) {
-        MFREG_CUDA(cudaEventRecord(ev_fork_, s_));
-        MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
-        launch_lap3(dg_, p, lapp_.get(), s2_);
-        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
-        MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+    graphs_.run({p, q, pq_dev, skip, nullptr, reinterpret_cast<const void*>(3)}, s_,
+                [&](cudaStream_t cs) { enqueue_hv_fast(p, q, p, pq_dev, skip, cs); });
+}
+
+// ------------------------------------------------------------------ GraphCache
+GraphCache::GraphCache(std::size_t cap) : cap_(cap) {
+    const char* off = std::getenv("MFREG_NO_GRAPHS");
+    enabled_ = !(off && off[0] == '1');
+}
+
+GraphCache::~GraphCache() {
+    for (auto& e : entries_)
+        if (e.exec) cudaGraphExecDestroy(e.exec);
+    if (cs_) cudaStreamDestroy(cs_);
+}
+
+GraphCache::Entry* GraphCache::find(const Key& k) {
+    for (auto& e : entries_)
+        if (e.key == k) {
+            e.last_use = ++clock_;
+            return &e;
+        }
+    return nullptr;
+}
+
+void GraphCache::begin() {
+    if (!cs_) MFREG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+    l0_ = launch_counter();
+    MFREG_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
+}
+
+void GraphCache::abort() {
+    cudaGraph_t g = nullptr;
+    cudaStreamEndCapture(cs_, &g);
+    if (g) cudaGraphDestroy(g);
+    cudaGetLastError();
+}
+
+GraphCache::Entry* GraphCache::end(const Key& k) {
+    cudaGraph_t g = nullptr;
+    MFREG_CUDA(cudaStreamEndCapture(cs_, &g));
+    cudaGraphExec_t ex = nullptr;
+    const cudaError_t err = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    MFREG_CUDA(err);
+    const long long n = launch_counter() - l0_;
+    note_launches(-n);  // counted again on every replay
+    if (entries_.size() >= cap_) {  // evict the least recently used
+        auto it = std::min_element(entries_.begin(), entries_.end(),
+                                   [](const Entry& a, const Entry& b) { return a.last_use < b.last_use; });
+        cudaGraphExecDestroy(it->exec);
+        entries_.erase(it);
     }
-    launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_, skip);
-    if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s_, ev_join_, 0));
-    FinalizeSpec f;
-    f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
-    f.out = q;
-    f.dot_a = p;
-    f.sc = pq_dev;
-    f.skip = skip;
-    launch_nodal_finalize(plan_, *fused_, f, s_);
-    check_launch("Objective::gn_hessian_vec (fused, dot)");
+    entries_.push_back(Entry{k, ex, n, ++clock_});
+    return &entries_.back();
+}
+
+void GraphCache::launch(Entry* e, cudaStream_t s) {
+    MFREG_CUDA(cudaGraphLaunch(e->exec, s));
+    note_launches(e->launches);
 }
 
 DeviceCg& DeviceProblem::cg_workspace() {

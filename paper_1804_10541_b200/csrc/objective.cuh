@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <array>
 #include <cmath>
 #include <cstdint>
 #include <deque>
@@ -113,6 +114,55 @@ struct SlabInfo {
     int zlo, zhi, own_lo, own_hi, need_lo, need_hi, bnd;
 };
 std::vector<SlabInfo> slab_partition(const Grid& image, const Grid& deform, int nranks);
+
+// CUDA graphs for fixed launch sequences, keyed by the pointers they bake in
+// (replayed on the caller's stream; LRU-bounded). MFREG_NO_GRAPHS=1 disables.
+class GraphCache {
+public:
+    using Key = std::array<const void*, 6>;
+    explicit GraphCache(std::size_t cap = 8);
+    ~GraphCache();
+    GraphCache(const GraphCache&) = delete;
+    GraphCache& operator=(const GraphCache&) = delete;
+    template <class F>
+    void run(const Key& k, cudaStream_t s, F&& enqueue) {
+        if (!enabled_) {
+            enqueue(s);
+            return;
+        }
+        Entry* e = find(k);
+        if (!e) {
+            begin();
+            try {
+                enqueue(cs_);
+            } catch (...) {
+                abort();
+                throw;
+            }
+            e = end(k);
+        }
+        launch(e, s);
+    }
+
+private:
+    struct Entry {
+        Key key;
+        cudaGraphExec_t exec;
+        long long launches;
+        unsigned long long last_use;
+    };
+    Entry* find(const Key& k);
+    void begin();
+    void abort();
+    Entry* end(const Key& k);
+    void launch(Entry* e, cudaStream_t s);
+    std::vector<Entry> entries_;
+    std::size_t cap_;
+    bool enabled_ = true;
+    cudaStream_t cs_ = nullptr;
+    long long l0_ = 0;
+    unsigned long long clock_ = 0;
+};
 
 // Reduction helpers: exact 4096-chunk order (parity) or fixed-order tree (fast).
 class Reducer {
@@ -238,6 +288,8 @@ public:
     bool sliced() const { return sliced_; }
 
 private:
+    void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s);
+    void enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip, cudaStream_t s);
     Grid img_, dg_;
     SlabSpec slab_;
     bool sliced_ = false;
@@ -253,6 +305,7 @@ private:
     std::unique_ptr<Reducer> red2_;
     DVec curv_, sc2_;
     Scalars sc_;
+    GraphCache graphs_;
     double last_distance_ = 0.0, last_regularizer_ = 0.0;
 };
 
