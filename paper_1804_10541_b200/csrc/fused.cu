@@ -3,6 +3,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 #include <cuda.h>
@@ -21,7 +22,10 @@ constexpr int TT = FT_X * FT_Y;                              // output columns (
 constexpr int R1_0 = TT, R1_N = NC1 - TT;                    // 84 halo-1 ring columns
 constexpr int R2_0 = 352, R2_N = NC - NC1;                   // 92 halo-2 ring columns
 constexpr int NTH = 448;
-constexpr int DEPTH = 4;                                     // staging ring (TMA, loads 2 planes ahead)
+constexpr int DEPTH_EV = 4;  // staging ring, eval pass (TMA, loads 2 planes ahead)
+constexpr int DEPTH_HV = 5;  // Hv pass: also keeps plane k-2 (rho-hat of the Z stage, dT of q^)
+constexpr int NBUF_EV = 14;  // plane buffers (NB doubles): eval R, T_w, r (x2), rho-hat in-plane (x8)
+constexpr int NBUF_HV = 6;   // Hv: s, w (x2) (+2 unused)
 constexpr int NSLAB = 8;                                     // nodal-slab ring (planes, power of 2)
 constexpr int PAD = CX + 1;                                  // guard around the plane buffers
 constexpr int NB = NC + 2 * PAD;
@@ -111,13 +115,15 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     const int nlx = tm.nlx;
     // ---- shared memory carve-up (doubles); the staging ring comes first (128-byte aligned)
     constexpr int SLOT = EVAL ? EV_SLOT : HV_SLOT;
+    constexpr int DEPTH = EVAL ? DEPTH_EV : DEPTH_HV;
+    constexpr int NBUF = EVAL ? NBUF_EV : NBUF_HV;
     double* stg = sm;                      // [DEPTH][SLOT]
     double* sP0 = stg + DEPTH * SLOT + PAD;  // [2][NB] Hv: s; eval: R (by plane parity)
     double* sP1 = sP0 + 2 * NB;            // [2][NB] eval: T_w
     double* sW = sP1 + 2 * NB;             // [2][NB] Hv: w; eval: r
     double* sRh = sW + 2 * NB;             // [2][4][NB] in-plane rho-hat (-x,+x,-y,+y)
-    double* sDq = sRh + 8 * NB - PAD;      // [3][3][TT] dT of the tile columns (planes k, k-1, k-2)
-    double* sQ = sDq + 9 * TT;             // [3][TT]
+    double* sDq = sP0 + NBUF * NB - PAD;   // eval: [3][3][TT] dT of the tile columns (planes k, k-1, k-2)
+    double* sQ = sDq + (EVAL ? 9 * TT : 0);  // [3][TT]
     double* sQx = sQ + 3 * TT;             // [3][FT_Y][nlx]
     double* sZr = sQx + 3 * FT_Y * nlx;    // [zc + 8] rem_z per plane
     double* sremx = sZr + tm.zc + 8;
@@ -224,7 +230,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     }
     if (tid < 2 * PAD) {  // zero the guard pads of the plane buffers
         const int o = tid < PAD ? -PAD + tid : NC + (tid - PAD);
-        for (int b = 0; b < 14; ++b) sP0[b * NB + o] = 0.0;
+        for (int b = 0; b < NBUF; ++b) sP0[b * NB + o] = 0.0;
     }
     if (TMA && tid == 0) {
         for (int b = 0; b < DEPTH; ++b) mbar_init(&bars[b], 1);
@@ -279,10 +285,10 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     // same zero-fill semantics
     auto stage_issue = [&](int m) {
         const int mr = m - (z0 - 2);
-        double* st = stg + (mr & (DEPTH - 1)) * SLOT;
+        double* st = stg + (mr % DEPTH) * SLOT;
         if (TMA) {
             if (tid < 32 && elect_one()) {  // warp 0 is converged here; one lane issues
-                unsigned long long* bar = &bars[mr & (DEPTH - 1)];
+                unsigned long long* bar = &bars[mr % DEPTH];
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 if (EVAL) {
                     mbar_expect_tx(bar, EV_SLOT * 8);
@@ -318,7 +324,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     auto stage_wait = [&](int m) {
         if (TMA) {
             const int mr = m - (z0 - 2);
-            mbar_wait(&bars[mr & (DEPTH - 1)], (mr / DEPTH) & 1);
+            mbar_wait(&bars[mr % DEPTH], (mr / DEPTH) & 1);
         }
     };
 
@@ -405,6 +411,7 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     int cur = nzA;  // nodal plane held in accumulator slot 0
     const bool do_z = !EVAL || a.grad;
 
+  if constexpr (EVAL) {
 #pragma unroll 1
     for (int k = z0 - 2; k <= z1 + 1; ++k) {
         const int kt = k - (z0 - 2);  // index into the per-CTA z tables
@@ -596,6 +603,116 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
             st_k = (kt & (DEPTH - 1)) == DEPTH - 1 ? st_k - (DEPTH - 1) * SLOT : st_k + SLOT;
         }
     }
+  } else {
+    // ---- Hv: P (plane k) -> W (plane j = k-1) -> Z (plane i = k-2), one barrier per plane.
+    // The staging ring keeps planes k-2 .. k+2, so the Z stage reads its neighbours'
+    // rho-hat and its own dT straight from the staged slot of plane i. The loop is
+    // unrolled by two with parity-named registers / buffers (no rotation moves):
+    // on entry to a step of parity P, s_{k-2} = sr[P], s_{k-1} = sr[1-P],
+    // w_{k-2} = wr[P], w_{k-3} = wr[1-P], rho-hat_{k-3}(+z) = pr[1-P], sigma_{k-2} = gr[P].
+    double sr[2] = {0.0, 0.0}, wr[2] = {0.0, 0.0}, pr[2] = {0.0, 0.0}, gr[2] = {0.0, 0.0};
+    double* const sS = sP0 + c;  // s planes [2][NB] (by plane parity)
+    double* const sWv = sW + c;  // w planes [2][NB]
+    const int kfirst = z0 - 2, klast = z1 + 1;
+    auto slot_of = [&](int m) { return stg + ((m - kfirst + DEPTH) % DEPTH) * SLOT + c; };  // m >= kfirst - 2
+    auto step = [&](auto parc, int k) {
+        constexpr int P = decltype(parc)::value;
+        const int kt = k - kfirst;
+        stage_issue(k + 2);
+        bool slab_pending = false;
+        int slab_nz = 0;
+        {  // nodal plane needed by plane k+3, loaded now, stored at the end of the step
+            const int nzq = min(sZb[kt + 3] + 1, msz - 1);
+            if (nzq > slab_hi) {
+                slab_load(nzq);
+                slab_pending = true;
+                slab_nz = nzq;
+                slab_hi = nzq;
+            }
+            const int bz = sZb[kt];
+            if (bz != pz) {  // uniform: new nodal plane pair for P p
+                if (bz == pz + 1) {
+                    Pa0 = Pb0;
+                    Pa1 = Pb1;
+                    Pa2 = Pb2;
+                } else {
+                    slab_bilerp(bz, Pa0, Pa1, Pa2);
+                }
+                slab_bilerp(min(bz + 1, msz - 1), Pb0, Pb1, Pb2);
+                pz = bz;
+            }
+        }
+        const int i = k - 2;
+        const bool iout = i >= ilo && i < ihi;  // uniform
+        const double rzk = sZr[kt];
+        stage_wait(k);
+        const double* stk = slot_of(k);
+        // ---- P: plane k (all columns)
+        const double s0 = fma(stk[0], lerp(rzk, Pa0, Pb0),
+                              fma(stk[NC], lerp(rzk, Pa1, Pb1), stk[2 * NC] * lerp(rzk, Pa2, Pb2)));
+        sS[P * NB] = s0;
+        double wc = 0.0, sgc = 0.0, pzc = 0.0, q0 = 0.0, q1 = 0.0, q2 = 0.0;
+        if (role < 2) {
+            // ---- W: plane j = k-1 (own rho-hat from the ring, neighbours' s of plane j)
+            const double* rj = slot_of(k - 1) + HV_DT;
+            const double r0 = rj[0], r1 = rj[NC], r2 = rj[2 * NC], r3 = rj[3 * NC], r4 = rj[4 * NC], r5 = rj[5 * NC];
+            const double* sn = sS + (1 - P) * NB;
+            const double sj = sr[1 - P];
+            const double w01 = fma(r1, sn[1] - sj, r0 * (sn[-1] - sj));
+            const double w23 = fma(r3, sn[CX] - sj, r2 * (sn[-CX] - sj));
+            const double w45 = fma(r5, s0 - sj, r4 * (sr[P] - sj));
+            wc = (w01 + w23) + w45;
+            sgc = ((r0 + r1) + (r2 + r3)) + (r4 + r5);
+            pzc = r5;
+            sWv[(1 - P) * NB] = wc;
+            // ---- Z: plane i = k-2 (tile columns)
+            if (role == 0 && iout) {
+                const double* ri = slot_of(k - 2);  // dT [3][NC], then rho-hat [6][NC]
+                const double* rh = ri + HV_DT;
+                const double* wn = sWv + P * NB;
+                // neighbour coefficient toward i: -x neighbour holds (+x), +x neighbour (-x), ...
+                const double z01 = fma(rh[NC - 1], wn[-1], rh[1] * wn[1]);
+                const double z23 = fma(rh[3 * NC - CX], wn[-CX], rh[2 * NC + CX] * wn[CX]);
+                const double z45 = fma(r4, wc, pr[1 - P] * wr[1 - P]);  // rho-hat_{i+z}(-z) w_{i+z}, _{i-z}(+z) w_{i-z}
+                const double z = fma(-gr[P], wr[P], (z01 + z23) + z45);
+                const double sz = tile ? a.scale * z : 0.0;
+                q0 = sz * ri[0];
+                q1 = sz * ri[NC];
+                q2 = sz * ri[2 * NC];
+            }
+        }
+        if (iout) {
+            const int bz = sZb[kt - 2];
+            const double rz = sZr[kt - 2];
+            if (bz > cur) {  // nodal plane `cur` complete: x-y spread (all threads)
+                spread(acc00, acc01, acc02, cur);
+                acc00 = acc10;
+                acc01 = acc11;
+                acc02 = acc12;
+                acc10 = acc11 = acc12 = 0.0;
+                cur = bz;
+            }
+            acc00 = fma(1.0 - rz, q0, acc00);
+            acc10 = fma(rz, q0, acc10);
+            acc01 = fma(1.0 - rz, q1, acc01);
+            acc11 = fma(rz, q1, acc11);
+            acc02 = fma(1.0 - rz, q2, acc02);
+            acc12 = fma(rz, q2, acc12);
+        }
+        if (slab_pending) slab_store(slab_nz);
+        // histories (parity-named: no moves)
+        sr[P] = s0;
+        wr[1 - P] = wc;
+        pr[1 - P] = pzc;
+        gr[1 - P] = sgc;
+        __syncthreads();
+    };
+#pragma unroll 1
+    for (int k = kfirst; k <= klast; k += 2) {
+        step(std::integral_constant<int, 0>{}, k);
+        if (k + 1 <= klast) step(std::integral_constant<int, 1>{}, k + 1);
+    }
+  }
     if (TMA) {  // drain the two look-ahead loads before the CTA exits
         stage_wait(z1 + 2);
         stage_wait(z1 + 3);
@@ -687,27 +804,33 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
         const long long node = a.fin_lo + (tw - d * a.nwin);
         const long long t = d * ny + node;
         const bool owned = node >= a.add_lo && node < a.add_hi;
-        const long long mx = a.gy.m[0], my = a.gy.m[1];
-        const long long nx = node % mx, nyy = (node / mx) % my, nz = node / (mx * my);
+        const int mx = static_cast<int>(a.gy.m[0]), pn = static_cast<int>(a.gy.m[0] * a.gy.m[1]);
+        const int nz = static_cast<int>(node / pn), rem = static_cast<int>(node - static_cast<long long>(nz) * pn);
+        const int nyy = rem / mx, nx = rem - nyy * mx;
         const TileMeta& tm = a.tm;
-        const int tz0 = __ldg(&tm.node_tlo[2][nz]), tz1 = __ldg(&tm.node_thi[2][nz]);
-        const int ty0 = __ldg(&tm.node_tlo[1][nyy]), ty1 = __ldg(&tm.node_thi[1][nyy]);
-        const int tx0 = __ldg(&tm.node_tlo[0][nx]), tx1 = __ldg(&tm.node_thi[0][nx]);
+        // operands issued first so their latency overlaps the gather
+        const double addv = (a.add && owned) ? __ldg(a.add + t) : 0.0;
+        const double dotv = (a.dot_a && owned) ? __ldg(a.dot_a + t) : 0.0;
+        // gather lists (independent loads, no dependent index chains)
+        const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
+        const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
+        const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
         double v = 0.0;
-        for (int tz = tz0; tz <= tz1; ++tz) {
-            const int lz = static_cast<int>(nz) - __ldg(&tm.tile_n0[2][tz]);
-            for (int ty = ty0; ty <= ty1; ++ty) {
-                const int lyn = static_cast<int>(nyy) - __ldg(&tm.tile_n0[1][ty]);
-                for (int tx = tx0; tx <= tx1; ++tx) {
-                    const int lxn = static_cast<int>(nx) - __ldg(&tm.tile_n0[0][tx]);
-                    v += __ldg(a.part + ((static_cast<std::size_t>(tz) * tm.nty + ty) * tm.ntx + tx) * tm.part_stride +
-                               ((static_cast<std::size_t>(lz) * tm.nly + lyn) * tm.nlx + lxn) * 3 + d);
+        for (int ez = zb; ez < ze; ++ez) {
+            const int2 Z = __ldg(&tm.g_ent[2][ez]);
+            for (int ey = yb; ey < ye; ++ey) {
+                const int2 Y = __ldg(&tm.g_ent[1][ey]);
+                const std::size_t tile_row = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx;
+                const std::size_t loc_row = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx;
+                for (int ex = xb; ex < xe; ++ex) {
+                    const int2 X = __ldg(&tm.g_ent[0][ex]);
+                    v += __ldg(a.part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3 + d);
                 }
             }
         }
-        if (a.add && owned) v += a.add[t];
+        if (a.add && owned) v += addv;
         a.out[t] = v;
-        if (a.dot_a && owned) r0 = a.dot_a[t] * v;
+        if (a.dot_a && owned) r0 = dotv * v;
     }
     if (a.sc == nullptr) return;
     r0 = block_reduce(r0, sh);
@@ -746,10 +869,11 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
 
 std::size_t fused_smem_bytes(const TileMeta& tm, int nxf, int nyf, bool eval) {
     const int slot = eval ? EV_SLOT : HV_SLOT;
-    std::size_t d = DEPTH * slot + 14 * NB + 9 * TT + 3 * TT + 3 * FT_Y * tm.nlx + tm.zc + 8 + FT_X + FT_Y +
-                    (eval ? 0 : NSLAB * nxf * nyf * 3);
+    const int depth = eval ? DEPTH_EV : DEPTH_HV;
+    std::size_t d = depth * slot + (eval ? NBUF_EV : NBUF_HV) * NB + (eval ? 9 * TT : 0) + 3 * TT +
+                    3 * FT_Y * tm.nlx + tm.zc + 8 + FT_X + FT_Y + (eval ? 0 : NSLAB * nxf * nyf * 3);
     std::size_t ints = tm.zc + 8 + 4 * tm.nlx + 4 * tm.nly;
-    return d * sizeof(double) + ints * sizeof(int) + 16 + DEPTH * 8 + 32 * 8;
+    return d * sizeof(double) + ints * sizeof(int) + 16 + depth * 8 + 32 * 8;
 }
 
 FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
@@ -827,22 +951,21 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
             n1[k] = base[x1 - 1] + 1;
             nl[a] = std::max(nl[a], n1[k] - n0[k] + 1);
         }
-        std::vector<int> lo(ms, 0), hi(ms, -1);
-        for (int nd = 0; nd < ms; ++nd)
+        // finalize gather lists: for node nd, every tile k whose footprint holds it
+        std::vector<int> off(ms + 1, 0);
+        std::vector<int2> ent;
+        for (int nd = 0; nd < ms; ++nd) {
             for (int k = 0; k < ntl[a]; ++k)
-                if (n0[k] <= nd && nd <= n1[k]) {
-                    if (hi[nd] < 0) lo[nd] = k;
-                    hi[nd] = k;
-                }
-        tlo_[a].resize(ms);
-        thi_[a].resize(ms);
-        n0_[a].resize(ntl[a]);
-        MFREG_CUDA(cudaMemcpy(tlo_[a].get(), lo.data(), ms * sizeof(int), cudaMemcpyHostToDevice));
-        MFREG_CUDA(cudaMemcpy(thi_[a].get(), hi.data(), ms * sizeof(int), cudaMemcpyHostToDevice));
-        MFREG_CUDA(cudaMemcpy(n0_[a].get(), n0.data(), ntl[a] * sizeof(int), cudaMemcpyHostToDevice));
-        t.node_tlo[a] = tlo_[a].get();
-        t.node_thi[a] = thi_[a].get();
-        t.tile_n0[a] = n0_[a].get();
+                if (n0[k] <= nd && nd <= n1[k]) ent.push_back(make_int2(k, nd - n0[k]));
+            off[nd + 1] = static_cast<int>(ent.size());
+        }
+        goff_[a].resize(ms + 1);
+        gent_[a].resize(std::max<std::size_t>(1, ent.size()));
+        MFREG_CUDA(cudaMemcpy(goff_[a].get(), off.data(), (ms + 1) * sizeof(int), cudaMemcpyHostToDevice));
+        if (!ent.empty())
+            MFREG_CUDA(cudaMemcpy(gent_[a].get(), ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
+        t.g_off[a] = goff_[a].get();
+        t.g_ent[a] = gent_[a].get();
     }
     t.nlx = nl[0];
     t.nly = nl[1];

@@ -37,9 +37,8 @@ struct TileMeta {
     int zlo, zhi;               // image planes the tiles cover
     int nlx, nly, nlz;          // max local nodes per tile per axis
     std::size_t part_stride;    // doubles per tile partial (nlz*nly*nlx*3)
-    const int* node_tlo[3];     // per node: first touching tile
-    const int* node_thi[3];     // per node: last touching tile
-    const int* tile_n0[3];      // per tile: first local node (global index)
+    const int* g_off[3];        // per axis, CSR over nodes: entries [g_off[n], g_off[n+1])
+    const int2* g_ent[3];       //   entry = (tile index along the axis, local node index in that tile)
 };
 
 class FusedPlan {
@@ -69,7 +68,8 @@ public:
 
 private:
     TileMeta meta_{};
-    DevArray<int> tlo_[3], thi_[3], n0_[3];
+    DevArray<int> goff_[3];
+    DevArray<int2> gent_[3];
     DVec part_, vpart_, red_;
     DevArray<unsigned int> counter_;
     int slab_[2] = {0, 0};

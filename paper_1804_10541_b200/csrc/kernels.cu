@@ -149,6 +149,95 @@ __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __
     dT[2 * n + i] = gz;
 }
 
+// fast mode warp: the same P y (transfer.cpp:56-83 operation order, corner weights
+// shared by the three components) and the same cell choice as the reference
+// (IEEE p/h via div_rn, ties to the lower cell: at the identity every sample sits
+// on a tie, and the one-sided gradient there depends on that choice), then the
+// trilinear value / gradient with fused arithmetic (continuous in the cell
+// fraction, so contraction only moves the last bits).
+__global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __restrict__ y,
+                                                   const double* __restrict__ T, double* __restrict__ Tw,
+                                                   double* __restrict__ dT, int zoff) {
+    const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
+    const int x = blockIdx.x * 32 + threadIdx.x, yy = blockIdx.y * 8 + threadIdx.y;
+    const int z = blockIdx.z + zoff;
+    if (x >= mx || yy >= my) return;
+    const int bx = __ldg(&P.base[0][x]), by = __ldg(&P.base[1][yy]), bz = __ldg(&P.base[2][z]);
+    const double rx = __ldg(&P.rem[0][x]), ry = __ldg(&P.rem[1][yy]), rz = __ldg(&P.rem[2][z]);
+    const double wx[2] = {1.0 - rx, rx}, wy[2] = {1.0 - ry, ry}, wz[2] = {1.0 - rz, rz};
+    double w[8];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int a = 0; a < 2; ++a) w[(g * 2 + b) * 2 + a] = wx[a] * wy[b] * wz[g];
+    const long long ns = P.src.count();
+    const int sm0 = static_cast<int>(P.src.m[0]), sm01 = static_cast<int>(P.src.m[0] * P.src.m[1]);
+    const long long c0 = bx + static_cast<long long>(by) * sm0 + static_cast<long long>(bz) * sm01;
+    double pt[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        const double* yd = y + d * ns + c0;
+        double acc = 0.0;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) acc += w[(g * 2 + b) * 2 + a] * __ldg(yd + a + b * sm0 + g * sm01);
+        pt[d] = acc;
+    }
+    const int m3[3] = {mx, my, mz};
+    int i0[3];
+    double f[3];
+    bool ok0[3], ok1[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double sa = div_rn(pt[a], P.tgt.h[a], P.tgt.ih[a]) - 0.5;
+        const double c = fmin(fmax(ceil(sa), -4.0), static_cast<double>(m3[a]) + 4.0);  // far outside: all zero
+        const int b0 = static_cast<int>(c) - 1;
+        f[a] = sa - static_cast<double>(static_cast<long long>(ceil(sa)) - 1);
+        ok0[a] = b0 >= 0 && b0 < m3[a];
+        ok1[a] = b0 + 1 >= 0 && b0 + 1 < m3[a];
+        i0[a] = b0;
+    }
+    const long long plane = static_cast<long long>(mx) * my;
+    double t[2][2][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int a = 0; a < 2; ++a) {
+                const bool ok = (a ? ok1[0] : ok0[0]) && (b ? ok1[1] : ok0[1]) && (g ? ok1[2] : ok0[2]);
+                const long long o = (i0[0] + a) + static_cast<long long>(i0[1] + b) * mx + (i0[2] + g) * plane;
+                t[g][b][a] = ok ? __ldg(T + o) : 0.0;
+            }
+    const double fx = f[0], fy = f[1], fz = f[2];
+    double cx[2][2], dx[2][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+            dx[g][b] = t[g][b][1] - t[g][b][0];
+            cx[g][b] = fma(fx, dx[g][b], t[g][b][0]);
+        }
+    double cy[2], dyv[2], dxv[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        dyv[g] = cx[g][1] - cx[g][0];
+        cy[g] = fma(fy, dyv[g], cx[g][0]);
+        dxv[g] = fma(fy, dx[g][1] - dx[g][0], dx[g][0]);
+    }
+    const double gzv = cy[1] - cy[0];
+    const long long i = x + static_cast<long long>(yy) * mx + z * plane, n = plane * mz;
+    Tw[i] = fma(fz, gzv, cy[0]);
+    dT[i] = fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0];
+    dT[n + i] = fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1];
+    dT[2 * n + i] = gzv * P.tgt.ih[2];
+}
+
 __global__ void k_sample(Grid g, const double* __restrict__ T, const double* __restrict__ pts, idx_t n,
                          double* __restrict__ vals, double* __restrict__ dT) {
     const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -758,6 +847,16 @@ void launch_warp(const DevPlan& P0, const double* y, const double* T, double* Tw
     gr.z = static_cast<unsigned>(zhi - zlo);
     if (gr.z == 0) return;
     note_launch(), k_warp<<<gr, block3(), 0, s>>>(P, y, T, Tw, dT, zlo);
+}
+void launch_warp_fast(const DevPlan& P0, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
+                      int zlo, int zhi) {
+    DevPlan P = P0;
+    P.tgt.set_inv();
+    if (zhi < 0) zhi = static_cast<int>(P.tgt.m[2]);
+    if (zhi <= zlo) return;
+    const dim3 gr(static_cast<unsigned>((P.tgt.m[0] + 31) / 32), static_cast<unsigned>((P.tgt.m[1] + 7) / 8),
+                  static_cast<unsigned>(zhi - zlo));
+    note_launch(), k_warp_fast<<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo);
 }
 void launch_ngf_ws(const Grid& img0, const double* R, const double* Tw, double tau, double rho, double* r,
                    double* inv1, double* inv2, double* rh, cudaStream_t s) {

@@ -29,6 +29,8 @@ void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n,
                    cudaStream_t s);
 // Fused P*y + trilinear sample: T_w and dT/dP (32 B/voxel) without materialising P*y.
 // image planes [zlo, zhi) (zhi < 0: all)
+void launch_warp_fast(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
+                      int zlo = 0, int zhi = -1);
 void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
                  int zlo = 0, int zhi = -1);
 

@@ -276,10 +276,10 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     const idx_t ny = dg_.count();
     const int mz = static_cast<int>(img_.m[2]);
     if (sliced_)  // the slab's planes + 3 halo planes (state of the 2 halo planes the Hv reads)
-        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, std::max(0, slab_.zlo - 3),
-                    std::min(mz, slab_.zhi + 3));
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, std::max(0, slab_.zlo - 3),
+                         std::min(mz, slab_.zhi + 3));
     else
-        launch_warp(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s);
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s);
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s);
     // curvature value / gradient on the side stream, overlapping the image pass
     MFREG_CUDA(cudaEventRecord(ev_fork_, s));
