@@ -10,10 +10,20 @@
 #include <cudaTypedefs.h>
 
 #include "fused.cuh"
+#include "fused_dev.cuh"
 
 namespace mfreg_b200 {
 
+// hv_fast.cu
+std::size_t hv2_smem_bytes(int nlx, int nsl);
+int hv2_nsl_max();
+int hv2_threads();
+void hv2_set_smem_cap(int bytes);
+void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s);
+
 namespace {
+
+using namespace fdev;
 
 constexpr int CX = FT_X + 4, CY = FT_Y + 4, NC = CX * CY;  // halo-2 column region (36 x 12 = 432)
 constexpr int C1X = FT_X + 2, C1Y = FT_Y + 2, NC1 = C1X * C1Y;  // halo-1 region (34 x 10 = 340)
@@ -35,77 +45,6 @@ constexpr int HV_DT = 3 * NC;                  // doubles: dT box 36x12x3
 constexpr int HV_RH = 6 * NC;                  // doubles: rho-hat box 36x12x6
 constexpr int HV_SLOT = HV_DT + HV_RH;         // 3888 doubles = 31104 B
 constexpr int EV_SLOT = 5 * NC;                // R, T_w, dT(3) boxes 36x12: 2160 doubles = 17280 B
-
-struct FArgs {
-    Grid g;
-    DevPlan P;
-    TileMeta tm;
-    double hh[3];   // h^_a = 1 / (2 h_a^2)
-    double ih2[3];  // 1 / h_a^2
-    double scale;   // Hv: 2 h_bar; eval gradient: -2 h_bar
-    double tau, rho;
-    const double* R;    // eval
-    const double* Tw;   // eval
-    const double* dT;
-    const double* frh;  // Hv input: rho-hat [6][n]
-    const double* p;    // Hv nodal operand
-    double* frh_out;    // eval output
-    double* part;
-    double* vpart;
-    int grad;
-    int olo, ohi;       // output image planes (z slab); the tiles may extend 2 planes beyond
-    int nxf, nyf;       // nodal slab footprint (max over tiles) per plane, x and y
-    int dbg;            // profiling switches (0 in production)
-    const int* skip;    // device flag: return immediately when set (CG already converged)
-};
-
-struct TmaMaps {
-    CUtensorMap a, b, c;  // Hv: dT, rho-hat; eval: R, T_w, dT
-};
-
-__device__ __forceinline__ double lerp(double t, double a, double b) { return fma(t, b - a, a); }
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
-
-__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-// one elected lane of a converged warp (TMA must be issued from warp-uniform control flow)
-__device__ __forceinline__ bool elect_one() {
-    unsigned pred = 0;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t.reg .b32 r;\n\telect.sync r|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
-        : "=r"(pred));
-    return pred != 0;
-}
-
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int x, int y, int z,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
-            "r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, int x, int y, int z, int w,
-                                            unsigned long long* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
-            "r"(smem_u32(dst)),
-        "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
-        : "memory");
-}
 
 template <bool EVAL, bool TMA>
 __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
@@ -332,12 +271,13 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
     int pz = -1000, slab_hi = -1;
     double Pa0 = 0.0, Pa1 = 0.0, Pa2 = 0.0, Pb0 = 0.0, Pb1 = 0.0, Pb2 = 0.0;
     if (!EVAL) {  // the first two nodal planes, synchronously
+        // every nodal plane the first three planes read (later steps prefetch for plane k+3)
         const int nz0 = sZb[0];
-        slab_load(nz0);
-        slab_store(nz0);
-        slab_load(min(nz0 + 1, msz - 1));
-        slab_store(min(nz0 + 1, msz - 1));
-        slab_hi = nz0 + 1;
+        slab_hi = min(sZb[2] + 1, msz - 1);
+        for (int nz = nz0; nz <= slab_hi; ++nz) {
+            slab_load(nz);
+            slab_store(nz);
+        }
     }
     stage_issue(z0 - 2);
     stage_issue(z0 - 1);
@@ -420,11 +360,10 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
         int slab_nz = 0;
         if (!EVAL) {  // nodal plane needed by plane k+3, loaded now, stored at the end of the iteration
             const int nzq = min(sZb[kt + 3] + 1, msz - 1);
-            if (nzq > slab_hi) {
-                slab_load(nzq);
+            if (nzq > slab_hi) {  // next plane now; any further ones (cells of 1 plane) at the store
+                slab_load(slab_hi + 1);
                 slab_pending = true;
                 slab_nz = nzq;
-                slab_hi = nzq;
             }
             const int bz = sZb[kt];
             if (bz != pz) {  // uniform across the CTA: new nodal plane pair for P p
@@ -578,7 +517,14 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
             acc02 = fma(1.0 - rz, q2, acc02);
             acc12 = fma(rz, q2, acc12);
         }
-        if (slab_pending) slab_store(slab_nz);
+        if (slab_pending) {
+            slab_store(slab_hi + 1);
+            for (int nz = slab_hi + 2; nz <= slab_nz; ++nz) {
+                slab_load(nz);
+                slab_store(nz);
+            }
+            slab_hi = slab_nz;
+        }
         __syncthreads();
         // ---- rotate histories and buffer pointers
         sh2 = sh1;
@@ -623,11 +569,10 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
         int slab_nz = 0;
         {  // nodal plane needed by plane k+3, loaded now, stored at the end of the step
             const int nzq = min(sZb[kt + 3] + 1, msz - 1);
-            if (nzq > slab_hi) {
-                slab_load(nzq);
+            if (nzq > slab_hi) {  // next plane now; any further ones (cells of 1 plane) at the store
+                slab_load(slab_hi + 1);
                 slab_pending = true;
                 slab_nz = nzq;
-                slab_hi = nzq;
             }
             const int bz = sZb[kt];
             if (bz != pz) {  // uniform: new nodal plane pair for P p
@@ -699,7 +644,14 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
             acc02 = fma(1.0 - rz, q2, acc02);
             acc12 = fma(rz, q2, acc12);
         }
-        if (slab_pending) slab_store(slab_nz);
+        if (slab_pending) {
+            slab_store(slab_hi + 1);
+            for (int nz = slab_hi + 2; nz <= slab_nz; ++nz) {
+                slab_load(nz);
+                slab_store(nz);
+            }
+            slab_hi = slab_nz;
+        }
         // histories (parity-named: no moves)
         sr[P] = s0;
         wr[1 - P] = wc;
@@ -893,6 +845,7 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
     a.nxf = fp.slab_x();
     a.nyf = fp.slab_y();
     a.dbg = 0;
+    a.segw = fp.seg_width();
     return a;
 }
 
@@ -919,7 +872,8 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     own_hi_ = full ? msz : slab.own_hi;
     fin_lo_ = full ? 0 : std::min(own_lo_, bz[out_lo_]);
     fin_hi_ = full ? msz : std::max(own_hi_, bz[out_hi_ - 1] + 2);
-    // z chunking: minimise waves(1 CTA/SM) x (planes per chunk + 4 halo planes)
+    // z chunking: minimise waves x (planes per chunk + 4 halo planes), waves of the
+    // Hv kernel (2 CTAs/SM; the eval kernel then runs two waves of half the height)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
     const int mz = t.zhi - t.zlo;
     int best = 1;
@@ -927,7 +881,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     for (int ntz = 1; ntz <= std::max(1, mz / 4); ++ntz) {
         const int zc = (mz + ntz - 1) / ntz;
         const int real_ntz = (mz + zc - 1) / zc;
-        const double waves = std::ceil(static_cast<double>(nxy * real_ntz) / kSMs);
+        const double waves = std::ceil(static_cast<double>(nxy * real_ntz) / (2 * kSMs));
         const double cost = waves * (zc + 4);
         if (cost < best_cost - 1e-9) {
             best_cost = cost;
@@ -1011,6 +965,30 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
                          (reinterpret_cast<std::uintptr_t>(dT) % 16 == 0) && (reinterpret_cast<std::uintptr_t>(frh) % 16 == 0);
     const char* off = std::getenv("MFREG_NO_TMA");
     tma_ = aligned && !(off && off[0] == '1') && make_tma_maps(g, R, Tw, dT, frh);
+    // two-CTA/SM Hv kernel (hv_fast.cu): TMA only; the nodal z cells must span >= 2 image
+    // planes (x-collapse buffer reuse, nodal ring of 4), and the y collapse needs one
+    // thread per tile-local node
+    bool zok = true;
+    for (int k = 0; k < gmz; ++k) {
+        const auto& bzv = plan.host_base[2];
+        if (bzv[std::min(k + 2, gmz - 1)] - bzv[k] > 1) zok = false;  // cells of >= 2 planes
+        if (bzv[std::min(k + 3, gmz - 1)] - bzv[k] > 2) zok = false;
+    }
+    {  // longest run of image columns sharing a nodal x cell
+        const auto& bx = plan.host_base[0];
+        int run = 1;
+        segw_ = 1;
+        for (std::size_t k = 1; k < bx.size(); ++k) {
+            run = bx[k] == bx[k - 1] ? run + 1 : 1;
+            segw_ = std::max(segw_, run);
+        }
+    }
+    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3);
+    const char* no2 = std::getenv("MFREG_NO_HV2");
+    hv2_ = tma_ && zok && !(no2 && no2[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() &&
+           slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= 115712;
+    hv2_smem_ = hv2_smem;
+    if (hv2_) hv2_set_smem_cap(static_cast<int>(hv2_smem));
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh) {
@@ -1037,7 +1015,10 @@ bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, 
     TmaMaps hv{}, ev{};
     bool ok = enc(&hv.a, dT, 4, 3, CX, CY, 3) && enc(&hv.b, frh, 4, 6, CX, CY, 6) && enc(&ev.a, R, 3, 1, CX, CY, 1) &&
               enc(&ev.b, Tw, 3, 1, CX, CY, 1) && enc(&ev.c, dT, 4, 3, CX, CY, 3);
+    TmaMaps hv2{};
+    ok = ok && enc(&hv2.a, dT, 4, 3, CX, CY, 3) && enc(&hv2.b, frh, 4, 6, CX, C1Y, 6);
     if (!ok) return false;
+    std::memcpy(maps_hv2_, &hv2, sizeof(TmaMaps));
     static_assert(sizeof(TmaMaps) <= sizeof(maps_hv_), "tensor-map storage");
     std::memcpy(maps_hv_, &hv, sizeof(TmaMaps));
     std::memcpy(maps_ev_, &ev, sizeof(TmaMaps));
@@ -1055,6 +1036,10 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     const TileMeta& t = fp.meta();
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
+    if (fp.hv2()) {
+        hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, t.ntz), fp.hv2_smem(), s);
+        return;
+    }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_hv());
     if (fp.tma()) k_fused<false, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
     else k_fused<false, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);

@@ -49,6 +49,10 @@ public:
     FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh,
               const SlabSpec& slab);
     bool tma() const { return tma_; }
+    bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
+    std::size_t hv2_smem() const { return hv2_smem_; }
+    int seg_width() const { return segw_; }
+    const void* maps_hv2() const { return maps_hv2_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
     const TileMeta& meta() const { return meta_; }
@@ -75,6 +79,10 @@ private:
     int slab_[2] = {0, 0};
     int out_lo_ = 0, out_hi_ = 0, fin_lo_ = 0, fin_hi_ = 0, own_lo_ = 0, own_hi_ = 0;
     bool tma_ = false;
+    bool hv2_ = false;
+    std::size_t hv2_smem_ = 0;
+    int segw_ = 32;
+    alignas(64) unsigned char maps_hv2_[3 * 128];
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
     bool make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh);

@@ -68,3 +68,9 @@ def oracle():
         from oracle.oracle import build
         build()
     return Oracle("ref") if available("ref") else Oracle("port")
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_1804_10541_b200 as P
+    return P

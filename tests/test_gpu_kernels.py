@@ -1,0 +1,60 @@
+"""Kernel-variant parity: the two-CTA/SM fast kernels against the legacy fused
+kernels (MFREG_NO_HV2=1) and the CPU oracle, on shapes that exercise partial
+tiles, anisotropic spacing, thin volumes, coarse/fine deformation grids and z
+slabs. Fast-mode tolerance as DESIGN.md §3 (max-rel 1e-9)."""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FAST_TOL = 1e-9
+
+SHAPES = [((64, 48, 40), (1.0, 1.0, 1.0), 4), ((70, 30, 23), (0.97, 0.97, 2.5), 4), ((96, 40, 9), (1.0, 1.2, 0.8), 3),
+          ((34, 10, 64), (1.0, 1.0, 1.0), 4), ((128, 64, 50), (1.0, 1.0, 1.0), 5), ((40, 24, 30), (0.7, 0.7, 0.7), 2)]
+
+
+def max_rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300))
+
+
+def _objective(P, R, T, m, h, ratio, legacy):
+    old = os.environ.get("MFREG_NO_HV2")
+    os.environ["MFREG_NO_HV2"] = "1" if legacy else "0"
+    try:
+        img = P.make_image_grid(m, h)
+        dg = P.deformation_grid_for(img, ratio)
+        return P.Objective(R, T, img, dg, P.NgfParams(), 1.0, P.Mode.FAST)
+    finally:
+        if old is None:
+            del os.environ["MFREG_NO_HV2"]
+        else:
+            os.environ["MFREG_NO_HV2"] = old
+
+
+@pytest.mark.parametrize("case", SHAPES, ids=lambda c: "x".join(map(str, c[0])) + f"_r{c[2]}")
+def test_hv_kernel_variants(P, oracle, case):
+    m, h, ratio = case
+    R = oracle.make_phantom(m, h) * 1000.0
+    T = oracle.warp_sinusoid(R, m, h, 3.0, 42)
+    my, _ = oracle.deformation_grid_for(m, h, ratio)
+    o = oracle.objective(R, T, m, h, my, 10.0, 10.0, 1.0)
+    rng = np.random.default_rng(11)
+    y = o.identity() + rng.uniform(-0.4, 0.4, o.dof)
+    p = rng.uniform(-1, 1, o.dof)
+    J, _, _, grad = o.eval(y)
+    hv = o.gn_hessian_vec(p)
+    res = []
+    for legacy in (True, False):
+        obj = _objective(P, R, T, m, h, ratio, legacy)
+        g = np.empty(obj.dof())
+        j = obj.eval(y, g)
+        q = obj.gn_hessian_vec(p)
+        q2 = obj.gn_hessian_vec(p)
+        assert np.array_equal(q, q2)  # deterministic
+        assert max_rel(j, J) <= FAST_TOL and max_rel(g, grad) <= FAST_TOL
+        assert max_rel(q, hv) <= FAST_TOL, (legacy, max_rel(q, hv))
+        res.append(q)
+    assert max_rel(res[1], res[0]) <= 1e-12
