@@ -38,6 +38,9 @@ RATIO = 4
 LEVELS = 3
 B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
+# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
+# capture of the same workload (profiles/), or None when not captured for this build
+TRAFFIC = {}
 METRIC = "NGF+curvature derivative eval Gvoxel/s (%HBM roofline); full GN registration wall s"
 
 
@@ -258,13 +261,31 @@ def run_ours(args, rank, world, local):
            "d2h_bytes_per_step": 2 * nd * 8 + 16, "ms_per_step": e2e_s * 1e3}
 
     peak, peak_kind = measured_hbm_peak()
-    achieved = B_CANON_HV * n / (ms_hv * 1e-3) / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "gn_hessian_vec (P p, dT, dr, dr^T, dT^T, P^T, alpha curvature Hv)",
-                "algorithmic_bytes_per_voxel": B_CANON_HV, "peak_source": peak_kind,
-                "grad_eval": {"achieved": B_CANON_GRAD * n / (ms_eval * 1e-3) / 1e9,
-                              "frac": B_CANON_GRAD * n / (ms_eval * 1e-3) / 1e9 / peak,
-                              "algorithmic_bytes_per_voxel": B_CANON_GRAD}}
+    roofline = None
+    if mode == P.Mode.FAST:
+        # per-kernel device time: CUDA events recorded on the launching stream inside the
+        # library, L2 flushed (256 MB write) before every launch (outside the interval)
+        reps = max(5, args.steps)
+        obj.eval(y, grad)
+        k_ms = {"hv_pass": obj.profile_kernel(0, p, reps), "eval_pass": obj.profile_kernel(1, p, reps),
+                "warp": obj.profile_kernel(2, y, reps)}
+        obj.eval(y, grad)
+        # algorithmic bytes per image voxel: Hv pass reads the
+        # canonical state R, T_w, dT (40 B); eval pass reads R, T_w, dT (40 B); warp reads T
+        # and writes T_w, dT (8 + 32 B)
+        b_alg = {"hv_pass": B_CANON_HV, "eval_pass": 40.0, "warp": 40.0}
+        kern = {k: {"ms": v, "achieved_gbs": b_alg[k] * n / (v * 1e-3) / 1e9, "algorithmic_bytes_per_voxel": b_alg[k],
+                    "frac": b_alg[k] * n / (v * 1e-3) / 1e9 / peak} for k, v in k_ms.items()}
+        dom = max(k_ms, key=k_ms.get)
+        names = {"hv_pass": "k_hv2 (GN Hv image pass: P p, dr, dr^T, dT, P^T partials)",
+                 "eval_pass": "k_fused<eval> (rho-hat, r, D partials, gradient dr^T r, P^T partials)",
+                 "warp": "k_warp_fast (P y, trilinear T, dT/dP)"}
+        roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
+                    "frac": kern[dom]["frac"], "traffic": TRAFFIC.get(dom), "kernel": names[dom],
+                    "algorithmic_bytes_per_voxel": b_alg[dom], "units_per_launch": n, "peak_source": peak_kind,
+                    "kernels": kern,
+                    "operators": {"gn_hessian_vec": {"ms": ms_hv, "frac": B_CANON_HV * n / (ms_hv * 1e-3) / 1e9 / peak},
+                                  "eval_grad": {"ms": ms_eval, "frac": B_CANON_GRAD * n / (ms_eval * 1e-3) / 1e9 / peak}}}
 
     gn = None
     if not args.no_gn:

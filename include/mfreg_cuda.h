@@ -158,6 +158,12 @@ int mfreg_cu_objective_identity(mfreg_cu_objective* obj, double* out, int where)
 int mfreg_cu_objective_eval(mfreg_cu_objective* obj, const double* y, double* grad, int where, double* j);
 /* last_distance() / last_regularizer() */
 int mfreg_cu_objective_last(mfreg_cu_objective* obj, double* distance, double* regularizer);
+/* Bench support (no reference counterpart): average device time in ms, CUDA events on
+ * the launching stream, of one fast-mode image-pass kernel: which = 0 GN Hv pass
+ * (operand = p), 1 eval pass, 2 warp (operand = y); flush_bytes > 0 writes a scratch
+ * buffer of that size before every launch (L2 flush, outside the timed interval). */
+int mfreg_cu_objective_profile_kernel(mfreg_cu_objective* obj, int which, const double* operand, int reps,
+                                      long long flush_bytes, double* ms);
 /* Objective::gn_hessian_vec(p, q) at the last evaluated iterate */
 int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, double* q, int where);
 /* Objective::seed_hessian_vec(p, gamma, q) */

@@ -105,6 +105,7 @@ _SIGS = {
     "mfreg_cu_objective_eval": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_last": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_gn_hessian_vec": ([_vp, _dp, _dp, C.c_int], C.c_int),
+    "mfreg_cu_objective_profile_kernel": ([_vp, C.c_int, _dp, C.c_int, C.c_longlong, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_seed_hessian_vec": ([_vp, _dp, C.c_double, _dp, C.c_int], C.c_int),
     "mfreg_cu_objective_dot": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_slab_partition": ([_gp, _gp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
@@ -526,6 +527,14 @@ class Objective:
         q = _empty_like_kind(p, self._dof) if q is None else q
         _check(lib().mfreg_cu_objective_gn_hessian_vec(self._h, _ptr(p)[0], _ptr(q)[0], w))
         return q
+
+    def profile_kernel(self, which: int, operand, reps: int = 10, flush_bytes: int = 256 << 20) -> float:
+        """Average device ms of one fast-mode image-pass kernel (0 Hv, 1 eval, 2 warp),
+        CUDA events recorded on the launching stream inside the library (bench support)."""
+        ms = C.c_double(0.0)
+        _check(lib().mfreg_cu_objective_profile_kernel(self._h, int(which), _ptr(operand)[0], int(reps),
+                                                         int(flush_bytes), C.byref(ms)))
+        return ms.value
 
     def seed_hessian_vec(self, p, gamma: float, q=None):
         w = _where_of(p)

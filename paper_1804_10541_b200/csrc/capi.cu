@@ -487,6 +487,22 @@ int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, 
         o.finish(kStream);
     });
 }
+int mfreg_cu_objective_profile_kernel(mfreg_cu_objective* obj, int which, const double* operand, int reps,
+                                      long long flush_bytes, double* ms) {
+    return guard([&] {
+        const idx_t nd = obj->obj->dof();
+        const double* dev = operand;
+        DVec tmp;
+        if (cudaPointerAttributes at{}; cudaPointerGetAttributes(&at, operand) != cudaSuccess ||
+                                         at.type != cudaMemoryTypeDevice) {
+            cudaGetLastError();
+            tmp.resize(nd);
+            MFREG_CUDA(cudaMemcpy(tmp.get(), operand, nd * sizeof(double), cudaMemcpyHostToDevice));
+            dev = tmp.get();
+        }
+        *ms = obj->obj->profile_kernel(which, dev, reps, static_cast<std::size_t>(std::max(0LL, flush_bytes)));
+    });
+}
 int mfreg_cu_objective_seed_hessian_vec(mfreg_cu_objective* obj, const double* p, double gamma, double* q,
                                         int where) {
     return guard([&] {

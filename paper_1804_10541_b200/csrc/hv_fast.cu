@@ -100,7 +100,8 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
     // ---- shared memory (doubles): ring | s planes | fluxes | x-collapsed rows | nodal ring | row tables | barriers
     double* const stg = sm;
-    double* const sS = stg + RING * SLOT;       // [2][NS] by plane parity
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (4 doubles)
+    double* const sS = stg + RING * SLOT + 4;   // [2][NS] by plane parity
     double* const sF = sS + 2 * NS;             // [2][2][NT] consumer-indexed y fluxes by plane parity
     double* const sE = sF + 2 * 2 * NT;         // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
     double* const sQ1 = sE + 2 * 2 * TY;        // [6][NX_P] item-1 P p at nodal planes bz, bz+1
@@ -108,8 +109,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     double* const slab = sQx + 3 * TY * nlx;    // [NSL][nsl]
     double* const sry = slab + NSL * nsl;       // [TY]
     int* const sby = reinterpret_cast<int*>(sry + TY);  // [TY]
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(
-        (reinterpret_cast<std::uintptr_t>(sby + TY) + 15) & ~static_cast<std::uintptr_t>(15));
+    const unsigned bar0 = smem_u32(bars);
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
     const int tx = lane, ty = row;
@@ -198,15 +198,15 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const int kfirst = z0 - 2, klast = z1 + 1;
     // step m: dT of plane m, rho-hat of plane m-1 (one thread; inlined so the tensor
     // maps stay in the kernel's parameter space)
-#define HV2_ISSUE(m_)                                                                   \
+#define HV2_ISSUE(m_, r_)                                                               \
     do {                                                                                \
         if (tid == 0) {                                                                 \
-            const int r_ = ((m_) - kfirst) % RING;                                      \
-            double* st_ = stg + r_ * SLOT;                                              \
+            const int rr_ = (r_);                                                       \
+            double* st_ = stg + rr_ * SLOT;                                              \
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");               \
-            mbar_expect_tx(&bars[r_], (SLOT_DT + SLOT_RH) * 8);                         \
-            tma_load_4d(st_, &maps.a, x0 - 2, y0 - 2, (m_), 0, &bars[r_]);              \
-            tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - 2, y0 - 1, (m_) - 1, 0, &bars[r_]); \
+            mbar_expect_tx(&bars[rr_], (SLOT_DT + SLOT_RH) * 8);                         \
+            tma_load_4d(st_, &maps.a, x0 - 2, y0 - 2, (m_), 0, &bars[rr_]);              \
+            tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - 2, y0 - 1, (m_) - 1, 0, &bars[rr_]); \
         }                                                                               \
     } while (0)
     auto zbase = [&](int k) { return __ldg(&a.P.base[2][min(max(k, 0), mz - 1)]); };
@@ -270,8 +270,10 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             slab_store(nz);
         }
     }
-    HV2_ISSUE(kfirst);
-    if (kfirst + 1 <= klast) HV2_ISSUE(kfirst + 1);
+    HV2_ISSUE(kfirst, 0);
+    if (kfirst + 1 <= klast) HV2_ISSUE(kfirst + 1, 1);
+    int slot = 0;         // ring slot of the current step
+    unsigned phase = 0;   // its mbarrier phase parity
     __syncthreads();
 
     // ---- loop state (parity-named histories, P = (k - kfirst) & 1)
@@ -288,8 +290,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
     auto step = [&](auto parc, int k) {
         constexpr int P = decltype(parc)::P;
-        const int mr = k - kfirst;
-        if (k + 2 <= klast) HV2_ISSUE(k + 2);
+        if (k + 2 <= klast) HV2_ISSUE(k + 2, slot == 0 ? 2 : slot - 1);
         if (ypend >= 0) {  // y collapse of the plane completed last step (sQx published by the barrier)
             ycollapse(ypend);
             ypend = -1;
@@ -325,9 +326,8 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             if (has1) bilerp(bz1, gx1, gy1, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
             pz = bzk;
         }
-        const int r = mr % RING;
-        mbar_wait(&bars[r], (mr / RING) & 1);
-        const double* st = stg + r * SLOT;
+        mbar_wait_at(bar0 + 8 * slot, phase);
+        const double* st = stg + slot * SLOT;
         // ---- P: plane k
         const double pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
         const double D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
@@ -409,6 +409,10 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         fzp[P] = fzp_new;
         sw = sw_new;
         gx = gx_new;
+        if (++slot == RING) {
+            slot = 0;
+            phase ^= 1u;
+        }
         if (slab_pending) slab_store(slab_nz);
         __syncthreads();
     };
@@ -435,7 +439,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 std::size_t hv2_smem_bytes(int nlx, int nsl) {
     const std::size_t d = static_cast<std::size_t>(RING) * SLOT + 2 * NS + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P + 3 * TY * nlx +
                           static_cast<std::size_t>(NSL) * nsl + TY;
-    return d * sizeof(double) + TY * sizeof(int) + 16 + RING * 8;
+    return (d + 4) * sizeof(double) + TY * sizeof(int);
 }
 
 int hv2_nsl_max() { return 2 * NT; }

@@ -333,6 +333,35 @@ void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* 
     check_launch("Objective::gn_hessian_vec (fused)");
 }
 
+double DeviceObjective::profile_kernel(int which, const double* p, int reps, std::size_t flush_bytes) {
+    if (!fused_) throw std::logic_error("profile_kernel: fast mode only");
+    DevArray<unsigned char> scratch(flush_bytes);
+    cudaEvent_t e0, e1;
+    MFREG_CUDA(cudaEventCreate(&e0));
+    MFREG_CUDA(cudaEventCreate(&e1));
+    double total = 0.0;
+    for (int r = 0; r < reps; ++r) {
+        if (flush_bytes) MFREG_CUDA(cudaMemsetAsync(scratch.get(), r & 0xff, flush_bytes, s_));
+        MFREG_CUDA(cudaEventRecord(e0, s_));
+        if (which == 0)
+            launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
+        else if (which == 1)
+            launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
+                              ngf_.frh.get(), true, s_);
+        else
+            launch_warp_fast(plan_.view(), p, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
+        MFREG_CUDA(cudaEventRecord(e1, s_));
+        MFREG_CUDA(cudaEventSynchronize(e1));
+        float ms = 0.0f;
+        MFREG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        total += ms;
+    }
+    check_launch("profile_kernel");
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return total / std::max(1, reps);
+}
+
 // optimizer.cpp:64-92
 double DeviceObjective::eval(const double* y, double* grad) {
     const idx_t ny = dg_.count();

@@ -286,6 +286,11 @@ public:
     DeviceNgf& ngf() { return ngf_; }
     const DevicePlanOwner& plan() const { return plan_; }
     bool sliced() const { return sliced_; }
+    // bench support: average device time (CUDA events on the launching stream) of one
+    // image-pass kernel of the fast path: 0 = GN Hv pass (operand p), 1 = eval pass
+    // (gradient), 2 = warp; `flush_bytes` > 0 writes a scratch buffer that large before
+    // every timed launch (L2 flush, outside the timed interval). Needs a prior eval.
+    double profile_kernel(int which, const double* p, int reps, std::size_t flush_bytes);
 
 private:
     void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s);
