@@ -1,0 +1,374 @@
+// NGF eval image pass, two CTAs per SM (fast mode).
+//
+// Same algebra and outputs as k_fused<true> (fused.cu): per voxel the six
+// coefficients rho-hat (ngf.cpp:39-64, stored as the Hv state), the residual
+// r = num inv1 (ngf.cpp:204-211), the per-tile sums of (1 - r^2) (ngf_value,
+// ngf.cpp:225-231) and, when `grad`, the NGF gradient -2h dT (dr^T r)
+// (ngf.cpp:66-103) spread by P^T into per-tile partials. Execution mirrors
+// k_hv2 (hv_fast.cu):
+//  * one thread per tile column (32x8 tile) plus the 80 ring-1 edge columns as
+//    second items of threads 0..79 (their coefficients only feed the fluxes
+//    toward the tile);
+//  * the staging ring (5 slots, 3 steps ahead) holds per step k the R and T_w
+//    boxes of plane k (36x12) and the tile's dT of plane k-2 (32x8x3): stage A
+//    of plane j = k-1 reads its in-plane neighbours from the previous step's
+//    slot, its z neighbours from this slot and a register, and the dr^T stage
+//    of plane i = k-2 reads dT from this slot;
+//  * dr^T r: x fluxes by warp shuffles, y fluxes through consumer-indexed
+//    shared arrays, z fluxes and sigma r in registers;
+//  * P^T: z weights in registers, segmented-scan x collapse per warp, y
+//    collapse one step later (no extra barriers in the plane loop).
+// Boundary handling as the reference's clamped neighbours: differences across
+// the volume boundary are masked to zero, coefficients outside are zero.
+#include <cstdint>
+
+#include "fused_dev.cuh"
+
+namespace mfreg_b200 {
+
+namespace {
+
+using namespace fdev;
+
+constexpr int TX = FT_X, TY = FT_Y;                    // 32 x 8 output tile
+constexpr int SX = TX + 4, SY = TY + 4, NS = SX * SY;  // R / T_w box 36 x 12
+constexpr int NT = TX * TY;                            // 256 threads
+constexpr int RING = 5;                                // staging slots (3 steps ahead)
+constexpr int SLOT_R = 0, SLOT_T = NS, SLOT_D = 2 * NS;  // doubles: R, T_w [12][36], dT [3][8][32]
+constexpr int SLOT = 2 * NS + 3 * NT;                  // 1632 doubles = 13056 B
+constexpr int NX_A = 80;                               // extra items: ring-1 edge columns
+static_assert((SLOT * 8) % 128 == 0 && (SLOT_T * 8) % 128 == 0 && (SLOT_D * 8) % 128 == 0, "TMA alignment");
+
+// extra item e in [0, 80) -> ring-1 edge column (lx, ly) in the box frame and the
+// consumer flux array (0: +x, 1: -x, 2: +y, 3: -y)
+__device__ __forceinline__ void edge_item(int e, int& lx, int& ly, int& dir) {
+    if (e < 32) { lx = 2 + e; ly = 1; dir = 2; }
+    else if (e < 64) { lx = 2 + e - 32; ly = SY - 2; dir = 3; }
+    else if (e < 72) { lx = 1; ly = 2 + e - 64; dir = 0; }
+    else { lx = SX - 2; ly = 2 + e - 72; dir = 1; }
+}
+
+template <int P_>
+struct Par {
+    static constexpr int P = P_;
+};
+
+// NGF coefficients of one column at plane j from the six clamped differences
+struct Coef {
+    double e[6];  // rho-hat: -x, +x, -y, +y, -z, +z
+    double r;     // residual
+};
+
+__device__ __forceinline__ Coef ngf_coef(const FArgs& a, double dR0, double dR1, double dR2, double dR3, double dR4,
+                                         double dR5, double dT0, double dT1, double dT2, double dT3, double dT4,
+                                         double dT5, bool ok) {
+    const double i0 = a.ih2[0], i1 = a.ih2[1], i2 = a.ih2[2];
+    const double stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
+    const double srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
+    const double num = fma(0.5, fma(fma(dT0, dR0, dT1 * dR1), i0, fma(fma(dT2, dR2, dT3 * dR3), i1, fma(dT4, dR4, dT5 * dR5) * i2)),
+                           a.tau * a.rho);
+    const double itn = rsqrt(fma(0.5, stt, a.tau * a.tau));
+    const double irn = rsqrt(fma(0.5, srr, a.rho * a.rho));
+    const double in1 = itn * irn;
+    const double in2 = num * (itn * itn) * in1;
+    const double hx = a.hh[0], hy = a.hh[1], hz = a.hh[2];
+    Coef c;
+    c.e[0] = ok ? hx * fma(dR0, in1, -dT0 * in2) : 0.0;
+    c.e[1] = ok ? hx * fma(dR1, in1, -dT1 * in2) : 0.0;
+    c.e[2] = ok ? hy * fma(dR2, in1, -dT2 * in2) : 0.0;
+    c.e[3] = ok ? hy * fma(dR3, in1, -dT3 * in2) : 0.0;
+    c.e[4] = ok ? hz * fma(dR4, in1, -dT4 * in2) : 0.0;
+    c.e[5] = ok ? hz * fma(dR5, in1, -dT5 * in2) : 0.0;
+    c.r = ok ? num * in1 : 0.0;
+    return c;
+}
+
+__global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
+    extern __shared__ __align__(128) double sm[];
+    const TileMeta& tm = a.tm;
+    const int nlx = tm.nlx;
+    const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
+    const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
+    const long long n = a.g.count(), plane = static_cast<long long>(mx) * my;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);
+    const int xe = min(mx, x0 + TX), ye = min(my, y0 + TY);
+    const int nxA = __ldg(&a.P.base[0][x0]), nyA = __ldg(&a.P.base[1][y0]), nzA = __ldg(&a.P.base[2][z0]);
+    const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
+    const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
+    const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
+    double* const part = a.part + tile_id * tm.part_stride;
+    const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
+    const int segw = a.segw;
+    const bool grad = a.grad != 0;
+
+    // ---- shared memory (doubles): ring | barriers | y fluxes | x edge fluxes | x-collapsed rows | row tables
+    double* const stg = sm;
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (6 doubles)
+    double* const sF = stg + RING * SLOT + 6;   // [2][2][NT] consumer-indexed y fluxes by plane parity
+    double* const sE = sF + 2 * 2 * NT;         // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
+    double* const sQx = sE + 2 * 2 * TY;        // [3][TY][nlx]
+    double* const sry = sQx + 3 * TY * nlx;     // [TY]
+    double* const sred = sry + TY;              // [NT / 32]
+    int* const sby = reinterpret_cast<int*>(sred + NT / 32);  // [TY]
+    const unsigned bar0 = smem_u32(bars);
+
+    // ---- columns: item 0 = tile column (lane, row); item 1 (threads < 80) = ring-1 edge column
+    const int tx = lane, ty = row;
+    const int c0 = (tx + 2) + (ty + 2) * SX;
+    const int gx0 = x0 + tx, gy0 = y0 + ty;
+    const bool w1 = tid < NX_A;
+    int lx1 = 2, ly1 = 2, dir1 = 0;
+    if (w1) edge_item(tid, lx1, ly1, dir1);
+    const int c1 = lx1 + ly1 * SX;
+    const int gx1 = x0 - 2 + lx1, gy1 = y0 - 2 + ly1;
+    const bool xedge = dir1 == 0 || dir1 == 1;
+    const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
+                         : (dir1 - 2) * NT + min(max(lx1 - 2, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+    // boundary masks of the in-plane differences (reference clamped neighbours) and
+    // "inside the volume" flags of the two columns
+    const double m0xm = gx0 > 0 ? 1.0 : 0.0, m0xp = gx0 + 1 < mx ? 1.0 : 0.0;
+    const double m0ym = gy0 > 0 ? 1.0 : 0.0, m0yp = gy0 + 1 < my ? 1.0 : 0.0;
+    const double m1xm = gx1 > 0 ? 1.0 : 0.0, m1xp = gx1 + 1 < mx ? 1.0 : 0.0;
+    const double m1ym = gy1 > 0 ? 1.0 : 0.0, m1yp = gy1 + 1 < my ? 1.0 : 0.0;
+    const bool in0 = gx0 < mx && gy0 < my;
+    const bool in1c = gx1 >= 0 && gx1 < mx && gy1 >= 0 && gy1 < my;
+    const long long col0 = in0 ? static_cast<long long>(gx0) + static_cast<long long>(gy0) * mx : 0;
+
+    // x collapse geometry (as k_hv2)
+    const int gxc0 = min(gx0, mx - 1);
+    const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
+    const int bx = xin ? __ldg(&a.P.base[0][gxc0]) - nxA : 1024 + lane;
+    const double rxq = __ldg(&a.P.rem[0][gxc0]);
+    const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
+    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
+    const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+    const bool send = lane == 31 || ((starts >> (lane + 1)) & 1u);
+
+    if (tid < TY) {
+        const int gyc = min(y0 + tid, my - 1);
+        sby[tid] = __ldg(&a.P.base[1][gyc]) - nyA;
+        sry[tid] = __ldg(&a.P.rem[1][gyc]);
+    }
+    if (tid == 0) {
+        for (int b = 0; b < RING; ++b) mbar_init(&bars[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+
+    const int kfirst = z0 - 2, klast = z1 + 1;
+    // step m: R, T_w of plane m, the tile's dT of plane m-2 (one thread)
+#define EV2_ISSUE(m_, r_)                                                          \
+    do {                                                                           \
+        if (tid == 0) {                                                            \
+            const int rr_ = (r_);                                                  \
+            double* st_ = stg + rr_ * SLOT;                                         \
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");          \
+            mbar_expect_tx(&bars[rr_], SLOT * 8);                                  \
+            tma_load_3d(st_ + SLOT_R, &maps.a, x0 - 2, y0 - 2, (m_), &bars[rr_]);   \
+            tma_load_3d(st_ + SLOT_T, &maps.b, x0 - 2, y0 - 2, (m_), &bars[rr_]);   \
+            tma_load_4d(st_ + SLOT_D, &maps.c, x0, y0, (m_) - 2, 0, &bars[rr_]);    \
+        }                                                                          \
+    } while (0)
+
+    auto xcollapse = [&](double v0, double v1, double v2) {
+        double* dst = sQx + row * nlx;
+        double A[3] = {(1.0 - rxq) * v0, (1.0 - rxq) * v1, (1.0 - rxq) * v2};
+        double B[3] = {rxq * v0, rxq * v1, rxq * v2};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            if (o >= segw) break;  // uniform
+            const bool in = lane - o >= sst;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const double ua = __shfl_up_sync(0xffffffffu, A[d], o);
+                const double ub = __shfl_up_sync(0xffffffffu, B[d], o);
+                A[d] = in ? A[d] + ua : A[d];
+                B[d] = in ? B[d] + ub : B[d];
+            }
+        }
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const double bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
+            if (send && xin) {
+                dst[d * TY * nlx + bx] = sst > 0 ? A[d] + bp : A[d];
+                if (xlast) dst[d * TY * nlx + bx + 1] = B[d];
+            }
+        }
+    };
+    const int nyi = 3 * nly_t * nlx_t;
+    auto ycollapse = [&](int nzp) {
+        if (tid < nyi) {
+            const int lxn = tid % nlx_t, lyn = (tid / nlx_t) % nly_t, d = tid / (nlx_t * nly_t);
+            const double* q = sQx + d * TY * nlx + lxn;
+            double v = 0.0;
+#pragma unroll
+            for (int r = 0; r < TY; ++r) {
+                const int b = sby[r];
+                const double ry = sry[r];
+                const double wgt = b == lyn ? 1.0 - ry : (b == lyn - 1 ? ry : 0.0);
+                v = fma(wgt, q[r * nlx], v);
+            }
+            part[static_cast<std::size_t>(nzp - nzA) * pstride + (lyn * nlx + lxn) * 3 + d] = v;
+        }
+    };
+    auto zbase = [&](int k) { return __ldg(&a.P.base[2][min(max(k, 0), mz - 1)]); };
+    auto zrem = [&](int k) { return __ldg(&a.P.rem[2][min(max(k, 0), mz - 1)]); };
+
+    __syncthreads();  // tables, barriers
+    for (int m = 0; m < RING - 2; ++m)
+        if (kfirst + m <= klast) EV2_ISSUE(kfirst + m, m);
+    int slot = 0, slot_prev = RING - 1;  // ring slots of this step and the previous one
+    unsigned phase = 0;
+
+    // ---- loop state (P = (k - kfirst) & 1)
+    double Rm0 = 0.0, Tm0 = 0.0, Rm1 = 0.0, Tm1 = 0.0;  // own R, T_w at plane k-2 (items 0, 1)
+    double fzp[2] = {0.0, 0.0};                        // rho-hat(+z) r of planes k-2, k-3
+    double sw = 0.0;                                   // sigma r of plane k-2
+    double gx = 0.0;                                   // in-row x fluxes into the column, plane k-2
+    double dsum = 0.0;
+    double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
+    int cur = nzA, ypend = -1;
+    const double scale = a.scale;
+
+    auto step = [&](auto parc, int k) {
+        constexpr int P = decltype(parc)::P;
+        if (k + RING - 2 <= klast) EV2_ISSUE(k + RING - 2, slot >= 2 ? slot - 2 : slot + RING - 2);
+        if (ypend >= 0) {  // y collapse of the plane completed last step
+            ycollapse(ypend);
+            ypend = -1;
+        }
+        mbar_wait_at(bar0 + 8 * slot, phase);
+        const double* st = stg + slot * SLOT;       // plane k (R, T_w), dT of plane k-2
+        const double* sp = stg + slot_prev * SLOT;  // plane k-1 (R, T_w)
+        // ---- A: plane j = k-1
+        const int j = k - 1;
+        const double mzm = j > 0 ? 1.0 : 0.0, mzp = j + 1 < mz ? 1.0 : 0.0;
+        const bool jin = j >= 0 && j < mz;
+        double fzm, fzp_new, sw_new, gx_new;
+        {
+            const double Rj = sp[SLOT_R + c0], Tj = sp[SLOT_T + c0];
+            const double Rp = st[SLOT_R + c0], Tp = st[SLOT_T + c0];
+            const Coef cf = ngf_coef(a, m0xm * (sp[SLOT_R + c0 - 1] - Rj), m0xp * (sp[SLOT_R + c0 + 1] - Rj),
+                                     m0ym * (sp[SLOT_R + c0 - SX] - Rj), m0yp * (sp[SLOT_R + c0 + SX] - Rj),
+                                     mzm * (Rm0 - Rj), mzp * (Rp - Rj), m0xm * (sp[SLOT_T + c0 - 1] - Tj),
+                                     m0xp * (sp[SLOT_T + c0 + 1] - Tj), m0ym * (sp[SLOT_T + c0 - SX] - Tj),
+                                     m0yp * (sp[SLOT_T + c0 + SX] - Tj), mzm * (Tm0 - Tj), mzp * (Tp - Tj),
+                                     in0 && jin);
+            Rm0 = Rj;
+            Tm0 = Tj;
+            if (in0 && j >= z0 && j < z1) {  // Hv state of the tile voxel
+                const long long gi = col0 + static_cast<long long>(j) * plane;
+#pragma unroll
+                for (int d = 0; d < 6; ++d) a.frh_out[d * n + gi] = cf.e[d];
+                if (j >= ilo && j < ihi) dsum += fma(-cf.r, cf.r, 1.0);
+            }
+            const double r = cf.r;
+            const double fpx = __shfl_up_sync(0xffffffffu, cf.e[1] * r, 1);
+            const double fmx = __shfl_down_sync(0xffffffffu, cf.e[0] * r, 1);
+            gx_new = (tx > 0 ? fpx : 0.0) + (tx + 1 < TX ? fmx : 0.0);
+            double* const Fj = sF + (1 - P) * 2 * NT;
+            if (ty + 1 < TY) Fj[tid + TX] = cf.e[3] * r;  // +y flux -> (tx, ty+1)
+            if (ty > 0) Fj[NT + tid - TX] = cf.e[2] * r;  // -y flux -> (tx, ty-1)
+            fzm = cf.e[4] * r;
+            fzp_new = cf.e[5] * r;
+            sw_new = (((cf.e[0] + cf.e[1]) + (cf.e[2] + cf.e[3])) + (cf.e[4] + cf.e[5])) * r;
+        }
+        if (w1) {  // ring-1 edge column: the flux toward the tile
+            const double Rj = sp[SLOT_R + c1], Tj = sp[SLOT_T + c1];
+            const double Rp = st[SLOT_R + c1], Tp = st[SLOT_T + c1];
+            const Coef cf = ngf_coef(a, m1xm * (sp[SLOT_R + c1 - 1] - Rj), m1xp * (sp[SLOT_R + c1 + 1] - Rj),
+                                     m1ym * (sp[SLOT_R + c1 - SX] - Rj), m1yp * (sp[SLOT_R + c1 + SX] - Rj),
+                                     mzm * (Rm1 - Rj), mzp * (Rp - Rj), m1xm * (sp[SLOT_T + c1 - 1] - Tj),
+                                     m1xp * (sp[SLOT_T + c1 + 1] - Tj), m1ym * (sp[SLOT_T + c1 - SX] - Tj),
+                                     m1yp * (sp[SLOT_T + c1 + SX] - Tj), mzm * (Tm1 - Tj), mzp * (Tp - Tj),
+                                     in1c && jin);
+            Rm1 = Rj;
+            Tm1 = Tj;
+            const double e = dir1 == 0 ? cf.e[1] : (dir1 == 1 ? cf.e[0] : (dir1 == 2 ? cf.e[3] : cf.e[2]));
+            if (xedge) sE[(1 - P) * 2 * TY + f1] = e * cf.r;
+            else sF[(1 - P) * 2 * NT + f1] = e * cf.r;
+        }
+        // ---- Z: plane i = k-2 (tile columns): gradient -2h dT (dr^T r) -> P^T
+        const int i = k - 2;
+        if (grad && i >= ilo && i < ihi) {  // uniform
+            const double* Fi = sF + P * 2 * NT;
+            const double* Ei = sE + P * 2 * TY + ty;
+            const double ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : 0.0);
+            const double z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
+            const double sz = scale * z;  // dT vanishes outside the volume (TMA zero fill)
+            const double* dq = st + SLOT_D + tid;
+            const double q0 = sz * dq[0], q1 = sz * dq[NT], q2 = sz * dq[2 * NT];
+            const int bz = zbase(i);
+            const double rz = zrem(i);
+            if (bz > cur) {
+                xcollapse(acc00, acc01, acc02);
+                ypend = cur;
+                acc00 = acc10;
+                acc01 = acc11;
+                acc02 = acc12;
+                acc10 = acc11 = acc12 = 0.0;
+                cur = bz;
+            }
+            acc00 = fma(1.0 - rz, q0, acc00);
+            acc10 = fma(rz, q0, acc10);
+            acc01 = fma(1.0 - rz, q1, acc01);
+            acc11 = fma(rz, q1, acc11);
+            acc02 = fma(1.0 - rz, q2, acc02);
+            acc12 = fma(rz, q2, acc12);
+        }
+        fzp[P] = fzp_new;
+        sw = sw_new;
+        gx = gx_new;
+        slot_prev = slot;
+        if (++slot == RING) {
+            slot = 0;
+            phase ^= 1u;
+        }
+        __syncthreads();
+    };
+#pragma unroll 1
+    for (int k = kfirst; k <= klast; k += 2) {
+        step(Par<0>{}, k);
+        if (k + 1 <= klast) step(Par<1>{}, k + 1);
+    }
+#undef EV2_ISSUE
+    if (grad) {  // flush: pending y collapse, then the last two nodal planes
+        if (ypend >= 0) ycollapse(ypend);
+        __syncthreads();
+        xcollapse(acc00, acc01, acc02);
+        __syncthreads();
+        ycollapse(cur);
+        __syncthreads();
+        xcollapse(acc10, acc11, acc12);
+        __syncthreads();
+        ycollapse(cur + 1);
+    }
+    // per-tile sum of (1 - r^2), fixed order
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, o);
+    if (lane == 0) sred[row] = dsum;
+    __syncthreads();
+    if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < NT / 32; ++w) s += sred[w];
+        a.vpart[tile_id] = s;
+    }
+}
+
+}  // namespace
+
+std::size_t ev2_smem_bytes(int nlx) {
+    const std::size_t d = static_cast<std::size_t>(RING) * SLOT + 6 + 2 * 2 * NT + 2 * 2 * TY + 3 * TY * nlx + TY + NT / 32;
+    return d * sizeof(double) + TY * sizeof(int);
+}
+
+void ev2_set_smem_cap(int bytes) {
+    MFREG_CUDA(cudaFuncSetAttribute(k_ev2, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void ev2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s) {
+    k_ev2<<<grid, NT, smem, s>>>(a, maps);
+}
+
+}  // namespace mfreg_b200

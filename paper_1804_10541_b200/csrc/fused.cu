@@ -20,6 +20,10 @@ int hv2_nsl_max();
 int hv2_threads();
 void hv2_set_smem_cap(int bytes);
 void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s);
+// ev_fast.cu
+std::size_t ev2_smem_bytes(int nlx);
+void ev2_set_smem_cap(int bytes);
+void ev2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s);
 
 namespace {
 
@@ -989,6 +993,11 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
            slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= 115712;
     hv2_smem_ = hv2_smem;
     if (hv2_) hv2_set_smem_cap(static_cast<int>(hv2_smem));
+    // two-CTA/SM eval kernel (ev_fast.cu): same conditions
+    ev2_smem_ = ev2_smem_bytes(t.nlx);
+    const char* noe = std::getenv("MFREG_NO_EV2");
+    ev2_ = tma_ && zok && !(noe && noe[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= 115712;
+    if (ev2_) ev2_set_smem_cap(static_cast<int>(ev2_smem_));
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh) {
@@ -1015,10 +1024,12 @@ bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, 
     TmaMaps hv{}, ev{};
     bool ok = enc(&hv.a, dT, 4, 3, CX, CY, 3) && enc(&hv.b, frh, 4, 6, CX, CY, 6) && enc(&ev.a, R, 3, 1, CX, CY, 1) &&
               enc(&ev.b, Tw, 3, 1, CX, CY, 1) && enc(&ev.c, dT, 4, 3, CX, CY, 3);
-    TmaMaps hv2{};
+    TmaMaps hv2{}, ev2{};
     ok = ok && enc(&hv2.a, dT, 4, 3, CX, CY, 3) && enc(&hv2.b, frh, 4, 6, CX, C1Y, 6);
+    ok = ok && enc(&ev2.a, R, 3, 1, CX, CY, 1) && enc(&ev2.b, Tw, 3, 1, CX, CY, 1) && enc(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3);
     if (!ok) return false;
     std::memcpy(maps_hv2_, &hv2, sizeof(TmaMaps));
+    std::memcpy(maps_ev2_, &ev2, sizeof(TmaMaps));
     static_assert(sizeof(TmaMaps) <= sizeof(maps_hv_), "tensor-map storage");
     std::memcpy(maps_hv_, &hv, sizeof(TmaMaps));
     std::memcpy(maps_ev_, &ev, sizeof(TmaMaps));
@@ -1059,6 +1070,10 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     const TileMeta& t = fp.meta();
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, true);
+    if (fp.ev2()) {
+        ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s);
+        return;
+    }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_ev());
     if (fp.tma()) k_fused<true, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
     else k_fused<true, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);

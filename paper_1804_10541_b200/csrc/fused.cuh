@@ -52,6 +52,9 @@ public:
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
     int seg_width() const { return segw_; }
+    bool ev2() const { return ev2_; }  // two-CTA/SM eval kernel (ev_fast.cu)
+    std::size_t ev2_smem() const { return ev2_smem_; }
+    const void* maps_ev2() const { return maps_ev2_; }
     const void* maps_hv2() const { return maps_hv2_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
@@ -82,6 +85,9 @@ private:
     bool hv2_ = false;
     std::size_t hv2_smem_ = 0;
     int segw_ = 32;
+    bool ev2_ = false;
+    std::size_t ev2_smem_ = 0;
+    alignas(64) unsigned char maps_ev2_[3 * 128];
     alignas(64) unsigned char maps_hv2_[3 * 128];
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];

@@ -1,5 +1,5 @@
 """Kernel-variant parity: the two-CTA/SM fast kernels against the legacy fused
-kernels (MFREG_NO_HV2=1) and the CPU oracle, on shapes that exercise partial
+kernels (MFREG_NO_HV2=1, MFREG_NO_EV2=1) and the CPU oracle, on shapes that exercise partial
 tiles, anisotropic spacing, thin volumes, coarse/fine deformation grids and z
 slabs. Fast-mode tolerance as DESIGN.md §3 (max-rel 1e-9)."""
 import os
@@ -21,17 +21,20 @@ def max_rel(a, b):
 
 
 def _objective(P, R, T, m, h, ratio, legacy):
-    old = os.environ.get("MFREG_NO_HV2")
-    os.environ["MFREG_NO_HV2"] = "1" if legacy else "0"
+    keys = ("MFREG_NO_HV2", "MFREG_NO_EV2")
+    old = {k: os.environ.get(k) for k in keys}
+    for k in keys:
+        os.environ[k] = "1" if legacy else "0"
     try:
         img = P.make_image_grid(m, h)
         dg = P.deformation_grid_for(img, ratio)
         return P.Objective(R, T, img, dg, P.NgfParams(), 1.0, P.Mode.FAST)
     finally:
-        if old is None:
-            del os.environ["MFREG_NO_HV2"]
-        else:
-            os.environ["MFREG_NO_HV2"] = old
+        for k, v in old.items():
+            if v is None:
+                del os.environ[k]
+            else:
+                os.environ[k] = v
 
 
 @pytest.mark.parametrize("case", SHAPES, ids=lambda c: "x".join(map(str, c[0])) + f"_r{c[2]}")
@@ -56,5 +59,9 @@ def test_hv_kernel_variants(P, oracle, case):
         assert np.array_equal(q, q2)  # deterministic
         assert max_rel(j, J) <= FAST_TOL and max_rel(g, grad) <= FAST_TOL
         assert max_rel(q, hv) <= FAST_TOL, (legacy, max_rel(q, hv))
-        res.append(q)
-    assert max_rel(res[1], res[0]) <= 1e-12
+        j2 = obj.eval(y, None)  # value-only eval refreshes the same state
+        assert max_rel(j2, j) <= 1e-14
+        assert np.array_equal(obj.gn_hessian_vec(p), q)
+        res.append((j, g, q))
+    for a_, b_ in zip(res[1], res[0]):
+        assert max_rel(a_, b_) <= 1e-12
