@@ -714,6 +714,8 @@ struct FinArgs {
     int nS;                   // number of device scalars summed into S
     long long fin_lo, nwin;   // finalize nodes [fin_lo, fin_lo + nwin) (per component)
     long long add_lo, add_hi; // nodes where `add` applies and the dot counts (owned)
+    const int* flat;          // per-node partial offsets [node][flat_k] (-1 padded), or null
+    int flat_k;
 };
 
 __device__ __forceinline__ long long clampl(long long v, long long hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
@@ -767,11 +769,22 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
         // operands issued first so their latency overlaps the gather
         const double addv = (a.add && owned) ? __ldg(a.add + t) : 0.0;
         const double dotv = (a.dot_a && owned) ? __ldg(a.dot_a + t) : 0.0;
+        double v = 0.0;
+        if (a.flat) {  // flat per-node offset list (one dependent load level)
+            const int4* fl = reinterpret_cast<const int4*>(a.flat + node * a.flat_k);
+            for (int q = 0; q < a.flat_k / 4; ++q) {
+                const int4 o = __ldg(fl + q);
+                if (o.x >= 0) v += __ldg(a.part + o.x + d);
+                if (o.y >= 0) v += __ldg(a.part + o.y + d);
+                if (o.z >= 0) v += __ldg(a.part + o.z + d);
+                if (o.w >= 0) v += __ldg(a.part + o.w + d);
+                if (o.w < 0) break;
+            }
+        } else {
         // gather lists (independent loads, no dependent index chains)
         const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
         const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
         const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
-        double v = 0.0;
         for (int ez = zb; ez < ze; ++ez) {
             const int2 Z = __ldg(&tm.g_ent[2][ez]);
             for (int ey = yb; ey < ye; ++ey) {
@@ -783,6 +796,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
                     v += __ldg(a.part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3 + d);
                 }
             }
+        }
         }
         if (a.add && owned) v += addv;
         a.out[t] = v;
@@ -898,6 +912,8 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     const int ntl[3] = {t.ntx, t.nty, t.ntz};
     const int org[3] = {0, 0, t.zlo}, end[3] = {static_cast<int>(g.m[0]), static_cast<int>(g.m[1]), t.zhi};
     int nl[3];
+    std::vector<int> hoff[3];
+    std::vector<int2> hent[3];
     for (int a = 0; a < 3; ++a) {
         const auto& base = plan.host_base[a];
         const int ms = static_cast<int>(P.src.m[a]);
@@ -924,12 +940,44 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
             MFREG_CUDA(cudaMemcpy(gent_[a].get(), ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
         t.g_off[a] = goff_[a].get();
         t.g_ent[a] = gent_[a].get();
+        hoff[a] = std::move(off);
+        hent[a] = std::move(ent);
     }
     t.nlx = nl[0];
     t.nly = nl[1];
     t.nlz = nl[2];
     t.part_stride = static_cast<std::size_t>(t.nlz) * t.nly * t.nlx * 3;
     part_.resize(t.part_stride * static_cast<std::size_t>(ntiles()));
+    // flat finalize gather lists: per node, the partial offsets in CSR order (z tiles,
+    // then y, then x), padded with -1 to a multiple of 4 entries (one dependent load
+    // level in the finalize instead of three nested CSR walks)
+    {
+        int kmax[3] = {0, 0, 0};
+        for (int a = 0; a < 3; ++a)
+            for (std::size_t nd = 0; nd + 1 < hoff[a].size(); ++nd) kmax[a] = std::max(kmax[a], hoff[a][nd + 1] - hoff[a][nd]);
+        const int K = ((kmax[0] * kmax[1] * kmax[2] + 3) / 4) * 4;
+        const long long msx = P.src.m[0], msy = P.src.m[1], msz = P.src.m[2], nn = msx * msy * msz;
+        if (part_.size() < (1ull << 31) && K > 0 && static_cast<double>(nn) * K < 4e9) {
+            std::vector<int> flat(static_cast<std::size_t>(nn) * K, -1);
+            for (long long nz = 0; nz < msz; ++nz)
+                for (long long nyy = 0; nyy < msy; ++nyy)
+                    for (long long nx = 0; nx < msx; ++nx) {
+                        int* dst = flat.data() + ((nz * msy + nyy) * msx + nx) * K;
+                        int c = 0;
+                        for (int ez = hoff[2][nz]; ez < hoff[2][nz + 1]; ++ez)
+                            for (int ey = hoff[1][nyy]; ey < hoff[1][nyy + 1]; ++ey)
+                                for (int ex = hoff[0][nx]; ex < hoff[0][nx + 1]; ++ex) {
+                                    const int2 Z = hent[2][ez], Y = hent[1][ey], X = hent[0][ex];
+                                    const std::size_t tile = (static_cast<std::size_t>(Z.x) * t.nty + Y.x) * t.ntx + X.x;
+                                    const std::size_t loc = (static_cast<std::size_t>(Z.y) * t.nly + Y.y) * t.nlx + X.y;
+                                    dst[c++] = static_cast<int>(tile * t.part_stride + loc * 3);
+                                }
+                    }
+            flat_.resize(flat.size());
+            MFREG_CUDA(cudaMemcpy(flat_.get(), flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice));
+            flat_k_ = K;
+        }
+    }
     MFREG_CUDA(cudaMemset(part_.get(), 0, part_.size() * sizeof(double)));
     vpart_.resize(static_cast<std::size_t>(ntiles()));
     const long long ny = P.src.count();
@@ -1105,6 +1153,8 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.nwin = (fp.fin_hi() - fp.fin_lo()) * pn;
     a.add_lo = fp.own_lo() * pn;
     a.add_hi = fp.own_hi() * pn;
+    a.flat = fp.flat();
+    a.flat_k = fp.flat_k();
     note_launch();
     k_nodal_finalize<<<static_cast<unsigned>(std::max(1LL, (3 * a.nwin + FIN_THREADS - 1) / FIN_THREADS)), FIN_THREADS,
                        0, s>>>(a);

@@ -464,6 +464,14 @@ GraphCache::Entry* GraphCache::find(const Key& k) {
     return nullptr;
 }
 
+bool GraphCache::promote(const Key& k) {
+    for (auto& e : seen_)
+        if (e.first == k) return ++e.second >= kPromote;
+    if (seen_.size() >= 4 * cap_) seen_.erase(seen_.begin());
+    seen_.emplace_back(k, 1);
+    return kPromote <= 1;
+}
+
 void GraphCache::begin() {
     if (!cs_) MFREG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
     l0_ = launch_counter();

@@ -131,6 +131,10 @@ public:
             return;
         }
         Entry* e = find(k);
+        if (!e && !promote(k)) {  // keys seen fewer than kPromote times run eagerly
+            enqueue(s);
+            return;
+        }
         if (!e) {
             begin();
             try {
@@ -152,6 +156,9 @@ private:
         unsigned long long last_use;
     };
     Entry* find(const Key& k);
+    bool promote(const Key& k);  // counts a miss; true once the key is worth a graph
+    static constexpr int kPromote = 3;
+    std::vector<std::pair<Key, int>> seen_;
     void begin();
     void abort();
     Entry* end(const Key& k);
