@@ -40,7 +40,7 @@ B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # capture of the same workload (profiles/), or None when not captured for this build
-TRAFFIC = {}
+TRAFFIC = {"hv_pass": 170.44e6, "eval_pass": 145.98e6, "warp": 28.79e6}  # bytes/launch, profiles/r1b_ncu_full.md
 METRIC = "NGF+curvature derivative eval Gvoxel/s (%HBM roofline); full GN registration wall s"
 
 
@@ -278,10 +278,11 @@ def run_ours(args, rank, world, local):
                     "frac": b_alg[k] * n / (v * 1e-3) / 1e9 / peak} for k, v in k_ms.items()}
         dom = max(k_ms, key=k_ms.get)
         names = {"hv_pass": "k_hv2 (GN Hv image pass: P p, dr, dr^T, dT, P^T partials)",
-                 "eval_pass": "k_fused<eval> (rho-hat, r, D partials, gradient dr^T r, P^T partials)",
+                 "eval_pass": "k_ev2 (NGF eval pass: rho-hat, r, D partials, gradient dr^T r, P^T partials)",
                  "warp": "k_warp_fast (P y, trilinear T, dT/dP)"}
         roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                    "frac": kern[dom]["frac"], "traffic": TRAFFIC.get(dom), "kernel": names[dom],
+                    "frac": kern[dom]["frac"], "traffic": TRAFFIC.get(dom), "traffic_unit": "bytes/launch (ncu dram read+write)",
+                    "algorithmic_bytes_per_launch": b_alg[dom] * n, "kernel": names[dom],
                     "algorithmic_bytes_per_voxel": b_alg[dom], "units_per_launch": n, "peak_source": peak_kind,
                     "kernels": kern,
                     "operators": {"gn_hessian_vec": {"ms": ms_hv, "frac": B_CANON_HV * n / (ms_hv * 1e-3) / 1e9 / peak},
