@@ -15,7 +15,7 @@
 namespace mfreg_b200 {
 
 // hv_fast.cu
-std::size_t hv2_smem_bytes(int nlx, int nsl);
+std::size_t hv2_smem_bytes(int nlx, int nsl, int zc);
 int hv2_nsl_max();
 int hv2_threads();
 void hv2_set_smem_cap(int bytes);
@@ -44,6 +44,7 @@ constexpr int NSLAB = 8;                                     // nodal-slab ring 
 constexpr int PAD = CX + 1;                                  // guard around the plane buffers
 constexpr int NB = NC + 2 * PAD;
 constexpr int kSMs = 148;
+constexpr int kSmem2Cta = 115712;  // dynamic shared memory per CTA with two CTAs per SM (228 KB - 2 x 1 KB reserved)
 // staging slot layouts (bytes, 128-aligned): TMA boxes land as [comp][y][x]
 constexpr int HV_DT = 3 * NC;                  // doubles: dT box 36x12x3
 constexpr int HV_RH = 6 * NC;                  // doubles: rho-hat box 36x12x6
@@ -894,9 +895,10 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
     // Hv kernel (2 CTAs/SM; the eval kernel then runs two waves of half the height)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
     const int mz = t.zhi - t.zlo;
-    int best = 1;
+    int best = (mz + 255) / 256;
     double best_cost = 1e300;
-    for (int ntz = 1; ntz <= std::max(1, mz / 4); ++ntz) {
+    // (chunks of <= 256 planes: the two-CTA kernels keep per-chunk z tables in shared memory)
+    for (int ntz = (mz + 255) / 256; ntz <= std::max((mz + 255) / 256, mz / 4); ++ntz) {
         const int zc = (mz + ntz - 1) / ntz;
         const int real_ntz = (mz + zc - 1) / zc;
         const double waves = std::ceil(static_cast<double>(nxy * real_ntz) / (2 * kSMs));
@@ -1035,17 +1037,18 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
             segw_ = std::max(segw_, run);
         }
     }
-    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3);
+    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3, t.zc);
     const char* no2 = std::getenv("MFREG_NO_HV2");
     hv2_ = tma_ && zok && !(no2 && no2[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() &&
-           slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= 115712;
+           slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= static_cast<std::size_t>(kSmem2Cta);
     hv2_smem_ = hv2_smem;
-    if (hv2_) hv2_set_smem_cap(static_cast<int>(hv2_smem));
+    // (process-wide per-kernel cap: always the 2-CTA bound, so plans never lower each other's)
+    if (hv2_) hv2_set_smem_cap(kSmem2Cta);
     // two-CTA/SM eval kernel (ev_fast.cu): same conditions
     ev2_smem_ = ev2_smem_bytes(t.nlx);
     const char* noe = std::getenv("MFREG_NO_EV2");
-    ev2_ = tma_ && zok && !(noe && noe[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= 115712;
-    if (ev2_) ev2_set_smem_cap(static_cast<int>(ev2_smem_));
+    ev2_ = tma_ && zok && !(noe && noe[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
+    if (ev2_) ev2_set_smem_cap(kSmem2Cta);
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh) {

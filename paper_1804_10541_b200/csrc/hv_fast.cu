@@ -108,7 +108,9 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     double* const sQx = sQ1 + 6 * NX_P;         // [3][TY][nlx] (completions >= 2 steps apart)
     double* const slab = sQx + 3 * TY * nlx;    // [NSL][nsl]
     double* const sry = slab + NSL * nsl;       // [TY]
-    int* const sby = reinterpret_cast<int*>(sry + TY);  // [TY]
+    double* const sZr = sry + TY;               // [zc + 8] rem_z of the planes kfirst ..
+    int* const sby = reinterpret_cast<int*>(sZr + tm.zc + 8);  // [TY]
+    int* const sZb = sby + TY;                  // [zc + 8] base_z of the planes kfirst ..
     const unsigned bar0 = smem_u32(bars);
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
@@ -163,10 +165,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         for (int u = 0; u < 2; ++u)
             if (slab_off[u] >= 0) dst[tid + u * NT] = slab_v[u];
     };
-    auto bilerp = [&](int nz, int gx, int gy, double& o0, double& o1, double& o2) {
-        int off;
-        double rx, ry;
-        col_geom(gx, gy, off, rx, ry);
+    auto bilerp = [&](int nz, int off, double rx, double ry, double& o0, double& o1, double& o2) {
         const double* q = slab + (nz & (NSL - 1)) * nsl + off;
         const int pl = nxf * nyf;
         o0 = lerp(ry, lerp(rx, q[0], q[1]), lerp(rx, q[nxf], q[nxf + 1]));
@@ -178,7 +177,8 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     // (columns past the volume form one-lane segments of their own and write nothing)
     const int gxc0 = min(gx0, mx - 1);
     const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
-    const int bx = xin ? __ldg(&a.P.base[0][gxc0]) - nxA : 1024 + lane;
+    const int bxc = __ldg(&a.P.base[0][gxc0]) - nxA;
+    const int bx = xin ? bxc : 1024 + lane;
     const double rxq = __ldg(&a.P.rem[0][gxc0]);
     const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
     const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
@@ -189,6 +189,11 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         const int gyc = min(y0 + tid, my - 1);
         sby[tid] = __ldg(&a.P.base[1][gyc]) - nyA;
         sry[tid] = __ldg(&a.P.rem[1][gyc]);
+    }
+    for (int t = tid; t < tm.zc + 8; t += NT) {
+        const int kk = min(max(z0 - 2 + t, 0), mz - 1);
+        sZb[t] = __ldg(&a.P.base[2][kk]);
+        sZr[t] = __ldg(&a.P.rem[2][kk]);
     }
     if (tid == 0) {
         for (int b = 0; b < RING; ++b) mbar_init(&bars[b], 1);
@@ -209,8 +214,8 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - 2, y0 - 1, (m_) - 1, 0, &bars[rr_]); \
         }                                                                               \
     } while (0)
-    auto zbase = [&](int k) { return __ldg(&a.P.base[2][min(max(k, 0), mz - 1)]); };
-    auto zrem = [&](int k) { return __ldg(&a.P.rem[2][min(max(k, 0), mz - 1)]); };
+    auto zbase = [&](int k) { return sZb[k - kfirst]; };  // k in [kfirst, klast + 3]
+    auto zrem = [&](int k) { return sZr[k - kfirst]; };
 
     // x collapse of one completed nodal plane (tile row = warp) into sQx[par]
     auto xcollapse = [&](double v0, double v1, double v2) {
@@ -310,6 +315,12 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         const double rzk = zrem(k);
         if (bzk != pz) {  // uniform: new nodal plane pair
             double* q1 = sQ1 + tid;  // item 1: [0..2] plane bz, [3..5] plane bz+1 (own entries only)
+            // item 0 geometry from the x-collapse registers and the row tables; item 1 from global
+            const int off0 = (bxc + nxA - fx0) + (sby[row] + nyA - fy0) * nxf;
+            const double ry0 = sry[row];
+            int off1 = 0;
+            double rx1 = 0.0, ry1 = 0.0;
+            if (has1) col_geom(gx1, gy1, off1, rx1, ry1);
             if (bzk == pz + 1) {
                 Pa0 = Pb0; Pa1 = Pb1; Pa2 = Pb2;
                 if (has1) {
@@ -318,12 +329,12 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
                     q1[2 * NX_P] = q1[5 * NX_P];
                 }
             } else {
-                bilerp(bzk, gx0, gy0, Pa0, Pa1, Pa2);
-                if (has1) bilerp(bzk, gx1, gy1, q1[0], q1[NX_P], q1[2 * NX_P]);
+                bilerp(bzk, off0, rxq, ry0, Pa0, Pa1, Pa2);
+                if (has1) bilerp(bzk, off1, rx1, ry1, q1[0], q1[NX_P], q1[2 * NX_P]);
             }
             const int bz1 = min(bzk + 1, msz - 1);
-            bilerp(bz1, gx0, gy0, Pb0, Pb1, Pb2);
-            if (has1) bilerp(bz1, gx1, gy1, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
+            bilerp(bz1, off0, rxq, ry0, Pb0, Pb1, Pb2);
+            if (has1) bilerp(bz1, off1, rx1, ry1, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
             pz = bzk;
         }
         mbar_wait_at(bar0 + 8 * slot, phase);
@@ -436,10 +447,10 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
 }  // namespace
 
-std::size_t hv2_smem_bytes(int nlx, int nsl) {
+std::size_t hv2_smem_bytes(int nlx, int nsl, int zc) {
     const std::size_t d = static_cast<std::size_t>(RING) * SLOT + 2 * NS + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P + 3 * TY * nlx +
                           static_cast<std::size_t>(NSL) * nsl + TY;
-    return (d + 4) * sizeof(double) + TY * sizeof(int);
+    return (d + 4 + zc + 8) * sizeof(double) + (TY + zc + 8) * sizeof(int);
 }
 
 int hv2_nsl_max() { return 2 * NT; }
