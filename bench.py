@@ -244,9 +244,12 @@ def run_ours(args, rank, world, local):
     value = 2.0 * n * world / (ms_step * 1e-3) / 1e9
     clocks = ck.summary()
 
-    # e2e through the C ABI with HOST buffers (copies inside the timed region)
-    yh, ph = y.cpu().numpy(), p.cpu().numpy()
-    gh, qh = np.empty(nd), np.empty(nd)
+    # e2e through the C ABI with HOST buffers (pinned; H2D of y, p and D2H of grad, q inside
+    # the timed region, every step)
+    yh = y.cpu().pin_memory().numpy()
+    ph = p.cpu().pin_memory().numpy()
+    gh = torch.empty(nd, dtype=torch.float64).pin_memory().numpy()
+    qh = torch.empty(nd, dtype=torch.float64).pin_memory().numpy()
     for _ in range(2):
         obj.eval(yh, gh)
         obj.gn_hessian_vec(ph, qh)

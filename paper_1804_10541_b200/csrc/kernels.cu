@@ -2,6 +2,7 @@
 // Compiled with --fmad=false (see common.cuh): every expression below keeps the
 // reference's operation order and rounding so `parity` results are bitwise
 // identical to the CPU reference.
+#include <cstdlib>
 #include <algorithm>
 #include <atomic>
 #include <cmath>
@@ -172,20 +173,25 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
         for (int b = 0; b < 2; ++b)
 #pragma unroll
             for (int a = 0; a < 2; ++a) w[(g * 2 + b) * 2 + a] = wx[a] * wy[b] * wz[g];
-    const long long ns = P.src.count();
+    // 32-bit element offsets (nodal arrays and image volumes are < 2^31 elements)
+    const int ns = static_cast<int>(P.src.count());
     const int sm0 = static_cast<int>(P.src.m[0]), sm01 = static_cast<int>(P.src.m[0] * P.src.m[1]);
-    const long long c0 = bx + static_cast<long long>(by) * sm0 + static_cast<long long>(bz) * sm01;
+    // four corner-row pointers (b, g); the a = 1 corner is an immediate offset
+    const double* yr[2][2];
+    yr[0][0] = y + (bx + by * sm0 + bz * sm01);
+    yr[0][1] = yr[0][0] + sm0;
+    yr[1][0] = yr[0][0] + sm01;
+    yr[1][1] = yr[1][0] + sm0;
     double pt[3];
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const double* yd = y + d * ns + c0;
         double acc = 0.0;
 #pragma unroll
         for (int g = 0; g < 2; ++g)
 #pragma unroll
             for (int b = 0; b < 2; ++b)
 #pragma unroll
-                for (int a = 0; a < 2; ++a) acc += w[(g * 2 + b) * 2 + a] * __ldg(yd + a + b * sm0 + g * sm01);
+                for (int a = 0; a < 2; ++a) acc += w[(g * 2 + b) * 2 + a] * __ldg(yr[g][b] + d * ns + a);
         pt[d] = acc;
     }
     const int m3[3] = {mx, my, mz};
@@ -202,8 +208,13 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
         ok1[a] = b0 + 1 >= 0 && b0 + 1 < m3[a];
         i0[a] = b0;
     }
-    const long long plane = static_cast<long long>(mx) * my;
+    const int plane = mx * my;
     double t[2][2][2];
+    const double* tr[2][2];
+    tr[0][0] = T + (i0[0] + i0[1] * mx + i0[2] * plane);
+    tr[0][1] = tr[0][0] + mx;
+    tr[1][0] = tr[0][0] + plane;
+    tr[1][1] = tr[1][0] + mx;
 #pragma unroll
     for (int g = 0; g < 2; ++g)
 #pragma unroll
@@ -211,8 +222,7 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
 #pragma unroll
             for (int a = 0; a < 2; ++a) {
                 const bool ok = (a ? ok1[0] : ok0[0]) && (b ? ok1[1] : ok0[1]) && (g ? ok1[2] : ok0[2]);
-                const long long o = (i0[0] + a) + static_cast<long long>(i0[1] + b) * mx + (i0[2] + g) * plane;
-                t[g][b][a] = ok ? __ldg(T + o) : 0.0;
+                t[g][b][a] = ok ? __ldg(tr[g][b] + a) : 0.0;
             }
     const double fx = f[0], fy = f[1], fz = f[2];
     double cx[2][2], dx[2][2];
@@ -231,7 +241,8 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
         dxv[g] = fma(fy, dx[g][1] - dx[g][0], dx[g][0]);
     }
     const double gzv = cy[1] - cy[0];
-    const long long i = x + static_cast<long long>(yy) * mx + z * plane, n = plane * mz;
+    const long long i = x + static_cast<long long>(yy) * mx + static_cast<long long>(z) * plane,
+                    n = static_cast<long long>(plane) * mz;
     Tw[i] = fma(fz, gzv, cy[0]);
     dT[i] = fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0];
     dT[n + i] = fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1];

@@ -65,3 +65,4 @@ def test_hv_kernel_variants(P, oracle, case):
         res.append((j, g, q))
     for a_, b_ in zip(res[1], res[0]):
         assert max_rel(a_, b_) <= 1e-12
+
