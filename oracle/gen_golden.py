@@ -87,6 +87,25 @@ def solver_case(o: Oracle, name, m, h, my, tau, rho, alpha, method, max_iters):
     print(f"solve_{name}: {method} iters={len(trace)} lsf={lsf} J={trace[-1][2]:.6g}")
 
 
+def config_case(o: Oracle, name, m, h, ratio, method, max_iters):
+    """BASELINE configs[0] (C1: 256x256 single-level GN) and its quasi-2D variant C1'
+    (SURVEY §8(d)). The test regenerates the inputs with the reference library (oracle
+    fixture), so only their hashes are stored next to the trace and the final y."""
+    import hashlib
+    m, h = tuple(m), tuple(h)
+    ref = o.make_phantom(m, h) * 1000.0
+    tpl = o.warp_sinusoid(ref, m, h, 3.0, 42)
+    my, _ = o.deformation_grid_for(m, h, ratio)
+    obj = o.objective(ref, tpl, m, h, my, 10.0, 10.0, 1.0)
+    cfg = OptConfig.defaults(max_iters=max_iters)
+    y, trace, lsf = obj.minimize(obj.identity(), method, cfg)
+    np.savez_compressed(os.path.join(OUT, f"cfg_{name}.npz"), m=np.array(m), h=np.array(h), my=np.array(my),
+                        ratio=ratio, method=method, max_iters=max_iters, y=y, trace=np.array(trace, dtype=np.float64),
+                        lsf=lsf, ref_sha=hashlib.sha256(ref.tobytes()).hexdigest(),
+                        tpl_sha=hashlib.sha256(tpl.tobytes()).hexdigest())
+    print(f"cfg_{name}: {method} iters={len(trace)} lsf={lsf} J={trace[-1][2] if trace else None}")
+
+
 def multilevel_case(o: Oracle, name, m, h, levels, method, max_iters):
     m, h = tuple(m), tuple(h)
     ref = o.make_phantom(m, h) * 1000.0
@@ -102,6 +121,12 @@ def multilevel_case(o: Oracle, name, m, h, levels, method, max_iters):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "configs":  # only the config cases
+        o = Oracle("ref")
+        o.set_threads(os.cpu_count() or 1)
+        config_case(o, "c1", (256, 256, 1), (1.0, 1.0, 1.0), 4, "gn", 20)
+        config_case(o, "c1p", (256, 256, 8), (1.0, 1.0, 1.0), 4, "gn", 3)
+        return
     o = Oracle("ref")
     o.set_threads(1)
     operator_case(o, "rand_aniso", (7, 6, 5), (1.0, 1.3, 0.8), (4, 4, 3), 1.0, 1.0, 1.0, "random", 11, 0.4)
@@ -116,6 +141,9 @@ def main():
     solver_case(o, "lbfgs", (10, 9, 8), (1.0, 1.0, 1.0), (4, 4, 3), 10.0, 10.0, 1.0, "lbfgs", 8)
     multilevel_case(o, "gn2", (16, 14, 12), (1.0, 1.0, 1.0), 2, "gn", 4)
     multilevel_case(o, "lbfgs2", (18, 16, 14), (0.97, 0.97, 2.5), 2, "lbfgs", 6)
+    o.set_threads(os.cpu_count() or 1)  # the reference's results are thread-count invariant
+    config_case(o, "c1", (256, 256, 1), (1.0, 1.0, 1.0), 4, "gn", 20)
+    config_case(o, "c1p", (256, 256, 8), (1.0, 1.0, 1.0), 4, "gn", 3)
 
 
 if __name__ == "__main__":
