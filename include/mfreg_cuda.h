@@ -217,6 +217,35 @@ int mfreg_cu_warp_sinusoid(const mfreg_cu_grid* image, const double* vol, double
                            int where);
 int mfreg_cu_scale(int64_t n, double a, double* x, int where);
 
+
+/* ---- volume / deformation / landmark files (reference io.hpp).
+ * File-format errors map to MFREG_CU_EOTHER with the reference's std::runtime_error text. */
+
+/* io::read_volume (io.cpp:111-164): MetaImage (MET_SHORT/USHORT/FLOAT/DOUBLE, LOCAL or
+ * sibling raw). Fills `grid`; `data` (count() doubles, host or device) may be NULL to
+ * query the grid (all checks still run). Elements are converted to fp64 on the GPU. */
+int mfreg_cu_read_volume(const char* path, mfreg_cu_grid* grid, double* data, int where);
+/* io::write_volume (io.cpp:166-188): MET_DOUBLE, LOCAL payload, byte-identical files */
+int mfreg_cu_write_volume(const char* path, const mfreg_cu_grid* grid, const double* data, int where);
+/* io::write_deformation (io.cpp:200-229): raw doubles + "<path>.meta" sidecar; n = length of y */
+int mfreg_cu_write_deformation(const char* path, const double* y, int64_t n, const mfreg_cu_grid* nodal, int where);
+/* io::read_deformation_grid (io.cpp:231-253) */
+int mfreg_cu_read_deformation_grid(const char* path, mfreg_cu_grid* nodal);
+/* io::read_deformation (io.cpp:255-274): y = 3 * nodal.count() doubles */
+int mfreg_cu_read_deformation(const char* path, const mfreg_cu_grid* nodal, double* y, int where);
+/* io::read_landmarks (io.cpp:276-303): up to `cap` physical points (x, y, z interleaved)
+ * into `out` (host, may be NULL); *count = number of landmarks in the file */
+int mfreg_cu_read_landmarks(const char* path, const double spacing[3], double* out, int64_t cap, int64_t* count);
+/* io::landmark_error (io.cpp:305-348): fixed/moving are host (x, y, z) triples; y (length ny)
+ * host or device; per-landmark errors on the GPU, mean / stddev in landmark order */
+int mfreg_cu_landmark_error(const double* fixed, int64_t n_fixed, const double* moving, int64_t n_moving,
+                            const double* y, int64_t ny, const mfreg_cu_grid* nodal, int where, double* mean,
+                            double* stddev, int64_t* count);
+/* mfreg CLI `warp` (tools/mfreg_cli.cpp:112-135) without the file IO: out = vol(P y) on the
+ * volume's grid (transfer_apply + sample_deformed, reference order); extents must match */
+int mfreg_cu_warp_volume(const double* vol, const mfreg_cu_grid* image, const double* y, const mfreg_cu_grid* nodal,
+                         double* out, int where);
+
 #ifdef __cplusplus
 }
 #endif

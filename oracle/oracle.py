@@ -293,6 +293,53 @@ class Oracle:
         self._call("prolong", _dptr(yc), _arr_i64(mc), _arr_d(hc), _arr_i64(mf), _arr_d(hf), _dptr(out))
         return out
 
+    # ---------------- io.hpp (reference library only)
+    def io_read_volume(self, path):
+        """io::read_volume -> (data, m, h)"""
+        m = (C.c_int64 * 3)()
+        h = (C.c_double * 3)()
+        self._call("io_read_volume", os.fsencode(str(path)), m, h, None)
+        out = np.empty(int(m[0] * m[1] * m[2]))
+        self._call("io_read_volume", os.fsencode(str(path)), m, h, _dptr(out))
+        return out, tuple(int(v) for v in m), tuple(float(v) for v in h)
+
+    def io_write_volume(self, path, data, m, h):
+        data = np.ascontiguousarray(data, dtype=np.float64)
+        self._call("io_write_volume", os.fsencode(str(path)), _arr_i64(m), _arr_d(h), _dptr(data))
+
+    def io_write_deformation(self, path, y, m, h):
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        self._call("io_write_deformation", os.fsencode(str(path)), _dptr(y), C.c_int64(y.size), _arr_i64(m), _arr_d(h))
+
+    def io_read_deformation_grid(self, path):
+        m = (C.c_int64 * 3)()
+        h = (C.c_double * 3)()
+        self._call("io_read_deformation_grid", os.fsencode(str(path)), m, h)
+        return tuple(int(v) for v in m), tuple(float(v) for v in h)
+
+    def io_read_deformation(self, path, m, h):
+        out = np.empty(3 * int(np.prod(m)))
+        self._call("io_read_deformation", os.fsencode(str(path)), _arr_i64(m), _arr_d(h), _dptr(out))
+        return out
+
+    def io_read_landmarks(self, path, spacing):
+        n = C.c_int64()
+        self._call("io_read_landmarks", os.fsencode(str(path)), _arr_d(spacing), None, C.c_int64(0), C.byref(n))
+        out = np.empty((n.value, 3))
+        self._call("io_read_landmarks", os.fsencode(str(path)), _arr_d(spacing), _dptr(out) if n.value else None,
+                   C.c_int64(n.value), C.byref(n))
+        return out
+
+    def io_landmark_error(self, fixed, moving, y, m, h):
+        f = np.ascontiguousarray(np.asarray(fixed, dtype=np.float64).reshape(-1, 3))
+        mv = np.ascontiguousarray(np.asarray(moving, dtype=np.float64).reshape(-1, 3))
+        y = np.ascontiguousarray(y, dtype=np.float64)
+        mean, sd, cnt = C.c_double(), C.c_double(), C.c_int64()
+        self._call("io_landmark_error", _dptr(f) if len(f) else None, C.c_int64(len(f)), _dptr(mv) if len(mv) else None,
+                   C.c_int64(len(mv)), _dptr(y), C.c_int64(y.size), _arr_i64(m), _arr_d(h), C.byref(mean),
+                   C.byref(sd), C.byref(cnt))
+        return mean.value, sd.value, cnt.value
+
     # ---------------- contexts
     def ngf(self, ref, m, h, tau=10.0, rho=10.0) -> "NgfCtx":
         return NgfCtx(self, ref, m, h, tau, rho)

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "mfreg/curvature.hpp"
+#include "mfreg/io.hpp"
 #include "mfreg/multilevel.hpp"
 #include "mfreg/ngf.hpp"
 #include "mfreg/optimizer.hpp"
@@ -549,6 +550,75 @@ int mref_register_multilevel(const double* ref, const double* tpl, const std::in
             ls_failed[l] = res.levels[l].result.line_search_failed ? 1 : 0;
             off += k;
         }
+    });
+}
+
+// ---- io.hpp
+// io::read_volume (io.cpp:111-164); data may be NULL (dims / spacing only)
+int mref_io_read_volume(const char* path, std::int64_t* m, double* h, double* data) {
+    return guard([&] {
+        const Volume v = io::read_volume(path);
+        for (int a = 0; a < 3; ++a) {
+            m[a] = v.grid.m[a];
+            h[a] = v.grid.h[a];
+        }
+        if (data) std::memcpy(data, v.data.data(), v.data.size() * sizeof(double));
+    });
+}
+
+// io::write_volume (io.cpp:166-188)
+int mref_io_write_volume(const char* path, const std::int64_t* m, const double* h, const double* data) {
+    return guard([&] { io::write_volume(path, make_vol(data, m, h)); });
+}
+
+// io::write_deformation (io.cpp:200-229)
+int mref_io_write_deformation(const char* path, const double* y, std::int64_t n, const std::int64_t* m,
+                              const double* h) {
+    return guard([&] { io::write_deformation(path, {y, static_cast<std::size_t>(n)}, nodal(m, h)); });
+}
+
+// io::read_deformation_grid (io.cpp:231-253)
+int mref_io_read_deformation_grid(const char* path, std::int64_t* m, double* h) {
+    return guard([&] {
+        const GridDesc g = io::read_deformation_grid(path);
+        for (int a = 0; a < 3; ++a) {
+            m[a] = g.m[a];
+            h[a] = g.h[a];
+        }
+    });
+}
+
+// io::read_deformation (io.cpp:255-274)
+int mref_io_read_deformation(const char* path, const std::int64_t* m, const double* h, double* y) {
+    return guard([&] {
+        const auto v = io::read_deformation(path, nodal(m, h));
+        std::memcpy(y, v.data(), v.size() * sizeof(double));
+    });
+}
+
+// io::read_landmarks (io.cpp:276-303)
+int mref_io_read_landmarks(const char* path, const double* spacing, double* out, std::int64_t cap,
+                           std::int64_t* count) {
+    return guard([&] {
+        const auto v = io::read_landmarks(path, {spacing[0], spacing[1], spacing[2]});
+        *count = static_cast<std::int64_t>(v.size());
+        for (std::size_t i = 0; out && i < v.size() && static_cast<std::int64_t>(i) < cap; ++i)
+            for (int a = 0; a < 3; ++a) out[3 * i + a] = v[i][a];
+    });
+}
+
+// io::landmark_error (io.cpp:305-348)
+int mref_io_landmark_error(const double* fixed, std::int64_t nf, const double* moving, std::int64_t nm,
+                           const double* y, std::int64_t ny, const std::int64_t* m, const double* h, double* mean,
+                           double* stddev, std::int64_t* count) {
+    return guard([&] {
+        std::vector<std::array<double, 3>> f(static_cast<std::size_t>(nf)), mv(static_cast<std::size_t>(nm));
+        for (std::int64_t i = 0; i < nf; ++i) f[i] = {fixed[3 * i], fixed[3 * i + 1], fixed[3 * i + 2]};
+        for (std::int64_t i = 0; i < nm; ++i) mv[i] = {moving[3 * i], moving[3 * i + 1], moving[3 * i + 2]};
+        const auto st = io::landmark_error(f, mv, {y, static_cast<std::size_t>(ny)}, nodal(m, h));
+        *mean = st.mean;
+        *stddev = st.stddev;
+        *count = static_cast<std::int64_t>(st.count);
     });
 }
 

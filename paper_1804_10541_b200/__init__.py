@@ -105,6 +105,15 @@ _SIGS = {
     "mfreg_cu_objective_eval": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_last": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_gn_hessian_vec": ([_vp, _dp, _dp, C.c_int], C.c_int),
+    "mfreg_cu_read_volume": ([C.c_char_p, C.POINTER(_Grid), _dp, C.c_int], C.c_int),
+    "mfreg_cu_write_volume": ([C.c_char_p, C.POINTER(_Grid), _dp, C.c_int], C.c_int),
+    "mfreg_cu_write_deformation": ([C.c_char_p, _dp, C.c_int64, C.POINTER(_Grid), C.c_int], C.c_int),
+    "mfreg_cu_read_deformation_grid": ([C.c_char_p, C.POINTER(_Grid)], C.c_int),
+    "mfreg_cu_read_deformation": ([C.c_char_p, C.POINTER(_Grid), _dp, C.c_int], C.c_int),
+    "mfreg_cu_read_landmarks": ([C.c_char_p, C.POINTER(C.c_double), _dp, C.c_int64, C.POINTER(C.c_int64)], C.c_int),
+    "mfreg_cu_landmark_error": ([_dp, C.c_int64, _dp, C.c_int64, _dp, C.c_int64, C.POINTER(_Grid), C.c_int,
+                                 C.POINTER(C.c_double), C.POINTER(C.c_double), C.POINTER(C.c_int64)], C.c_int),
+    "mfreg_cu_warp_volume": ([_dp, C.POINTER(_Grid), _dp, C.POINTER(_Grid), _dp, C.c_int], C.c_int),
     "mfreg_cu_objective_profile_kernel": ([_vp, C.c_int, _dp, C.c_int, C.c_longlong, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_objective_seed_hessian_vec": ([_vp, _dp, C.c_double, _dp, C.c_int], C.c_int),
     "mfreg_cu_objective_dot": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
@@ -645,3 +654,4 @@ def warp_sinusoid(vol, image: GridDesc, max_amp: float, seed: int):
     return out
 
 from . import slab  # noqa: E402  (z-slab decomposition, multi-GPU)
+from . import io  # noqa: E402  (volume / deformation / landmark files)

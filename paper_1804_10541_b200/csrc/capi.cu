@@ -7,6 +7,7 @@
 #include <string>
 
 #include "../../include/mfreg_cuda.h"
+#include "io.cuh"
 #include "objective.cuh"
 
 using namespace mfreg_b200;
@@ -640,5 +641,103 @@ int mfreg_cu_scale(int64_t n, double a, double* x, int where) {
 }
 
 int64_t mfreg_cu_launch_count(void) { return mfreg_b200::launch_counter(); }
+
+// ---- volume / deformation / landmark files (io.cuh)
+int mfreg_cu_read_volume(const char* path, mfreg_cu_grid* grid, double* data, int where) {
+    return guard([&] {
+        check_where(where);
+        const io::VolumeHeader h = io::read_volume_header(path);
+        if (grid) from_grid(h.grid, grid);
+        if (!data) return;
+        if (where == MFREG_CU_DEVICE) {
+            io::read_volume(path, data, kStream);
+        } else {
+            DVec d(h.grid.count());
+            io::read_volume(path, d.get(), kStream);
+            MFREG_CUDA(cudaMemcpy(data, d.get(), h.grid.count() * sizeof(double), cudaMemcpyDeviceToHost));
+        }
+    });
+}
+
+int mfreg_cu_write_volume(const char* path, const mfreg_cu_grid* grid, const double* data, int where) {
+    return guard([&] {
+        check_where(where);
+        const Grid g = to_grid(grid);
+        validate_grid(g, false);
+        if (where == MFREG_CU_DEVICE) {
+            std::vector<double> h(g.count());
+            MFREG_CUDA(cudaMemcpy(h.data(), data, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            io::write_volume(path, g, h.data());
+        } else {
+            io::write_volume(path, g, data);
+        }
+    });
+}
+
+int mfreg_cu_write_deformation(const char* path, const double* y, int64_t n, const mfreg_cu_grid* nodal, int where) {
+    return guard([&] {
+        check_where(where);
+        const Grid g = to_grid(nodal);
+        if (where == MFREG_CU_DEVICE && n == 3 * g.count()) {
+            std::vector<double> h(static_cast<std::size_t>(n));
+            MFREG_CUDA(cudaMemcpy(h.data(), y, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+            io::write_deformation(path, h.data(), h.size(), g);
+        } else {
+            io::write_deformation(path, y, static_cast<std::size_t>(std::max<int64_t>(0, n)), g);
+        }
+    });
+}
+
+int mfreg_cu_read_deformation_grid(const char* path, mfreg_cu_grid* nodal) {
+    return guard([&] { from_grid(io::read_deformation_grid(path), nodal); });
+}
+
+int mfreg_cu_read_deformation(const char* path, const mfreg_cu_grid* nodal, double* y, int where) {
+    return guard([&] {
+        check_where(where);
+        const std::vector<double> v = io::read_deformation(path, to_grid(nodal));
+        MFREG_CUDA(cudaMemcpy(y, v.data(), v.size() * sizeof(double),
+                              where == MFREG_CU_DEVICE ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+    });
+}
+
+int mfreg_cu_read_landmarks(const char* path, const double spacing[3], double* out, int64_t cap, int64_t* count) {
+    return guard([&] {
+        const auto v = io::read_landmarks(path, {spacing[0], spacing[1], spacing[2]});
+        *count = static_cast<int64_t>(v.size());
+        for (std::size_t i = 0; out && i < v.size() && static_cast<int64_t>(i) < cap; ++i)
+            for (int a = 0; a < 3; ++a) out[3 * i + a] = v[i][a];
+    });
+}
+
+int mfreg_cu_landmark_error(const double* fixed, int64_t n_fixed, const double* moving, int64_t n_moving,
+                            const double* y, int64_t ny, const mfreg_cu_grid* nodal, int where, double* mean,
+                            double* stddev, int64_t* count) {
+    return guard([&] {
+        if (n_fixed != n_moving) throw std::invalid_argument("landmark_error: list sizes differ");
+        Grid g = to_grid(nodal);
+        if (ny != 3 * g.count()) throw std::invalid_argument("landmark_error: field length mismatch");
+        In yi(y, static_cast<std::size_t>(ny), where, kStream);
+        const io::LandmarkStats st =
+            io::landmark_error(fixed, moving, static_cast<std::size_t>(n_fixed), yi.ptr, g, kStream);
+        *mean = st.mean;
+        *stddev = st.stddev;
+        *count = static_cast<int64_t>(st.count);
+    });
+}
+
+int mfreg_cu_warp_volume(const double* vol, const mfreg_cu_grid* image, const double* y, const mfreg_cu_grid* nodal,
+                         double* out, int where) {
+    return guard([&] {
+        Grid gi = to_grid(image), gn = to_grid(nodal);
+        validate_grid(gi, false);
+        validate_grid(gn, true);
+        In vi(vol, gi.count(), where, kStream);
+        In yi(y, 3 * gn.count(), where, kStream);
+        Out o(out, gi.count(), where);
+        io::warp_volume(vi.ptr, gi, yi.ptr, gn, o.ptr, kStream);
+        o.finish(kStream);
+    });
+}
 
 }  // extern "C"
