@@ -12,6 +12,7 @@
 #define MFREG_B200_HPP
 
 #include <array>
+#include <filesystem>
 #include <cstdint>
 #include <span>
 #include <stdexcept>
@@ -317,6 +318,66 @@ inline MultilevelResult register_multilevel(const Volume& reference, const Volum
     }
     return out;
 }
+
+// ---- io.hpp (volume / deformation / landmark files; io.cpp:111-348)
+namespace io {
+
+inline Volume read_volume(const std::filesystem::path& path) {  // io.cpp:111-164
+    mfreg_cu_grid g{};
+    detail::check(mfreg_cu_read_volume(path.c_str(), &g, nullptr, MFREG_CU_HOST));
+    Volume v{from_c(g, GridKind::CellCentered), {}};
+    v.data.resize(static_cast<std::size_t>(v.grid.count()));
+    detail::check(mfreg_cu_read_volume(path.c_str(), &g, v.data.data(), MFREG_CU_HOST));
+    return v;
+}
+inline void write_volume(const std::filesystem::path& path, const Volume& v) {  // io.cpp:166-188
+    const mfreg_cu_grid g = v.grid.c();
+    detail::check(mfreg_cu_write_volume(path.c_str(), &g, v.data.data(), MFREG_CU_HOST));
+}
+inline void write_deformation(const std::filesystem::path& path, std::span<const double> y,
+                              const GridDesc& grid) {  // io.cpp:200-229
+    const mfreg_cu_grid g = grid.c();
+    detail::check(mfreg_cu_write_deformation(path.c_str(), y.data(), static_cast<int64_t>(y.size()), &g, MFREG_CU_HOST));
+}
+inline GridDesc read_deformation_grid(const std::filesystem::path& path) {  // io.cpp:231-253
+    mfreg_cu_grid g{};
+    detail::check(mfreg_cu_read_deformation_grid(path.c_str(), &g));
+    return from_c(g, GridKind::Nodal);
+}
+inline std::vector<double> read_deformation(const std::filesystem::path& path, const GridDesc& grid) {
+    const mfreg_cu_grid g = grid.c();  // io.cpp:255-274
+    std::vector<double> y(static_cast<std::size_t>(3 * grid.count()));
+    detail::check(mfreg_cu_read_deformation(path.c_str(), &g, y.data(), MFREG_CU_HOST));
+    return y;
+}
+inline std::vector<std::array<double, 3>> read_landmarks(const std::filesystem::path& path,
+                                                         const std::array<double, 3>& spacing) {  // io.cpp:276-303
+    int64_t n = 0;
+    detail::check(mfreg_cu_read_landmarks(path.c_str(), spacing.data(), nullptr, 0, &n));
+    std::vector<std::array<double, 3>> out(static_cast<std::size_t>(n));
+    detail::check(mfreg_cu_read_landmarks(path.c_str(), spacing.data(), out.empty() ? nullptr : out[0].data(), n, &n));
+    return out;
+}
+struct LandmarkStats {
+    double mean = 0.0;
+    double stddev = 0.0;
+    std::size_t count = 0;
+};
+inline LandmarkStats landmark_error(const std::vector<std::array<double, 3>>& fixed,
+                                    const std::vector<std::array<double, 3>>& moving, std::span<const double> y,
+                                    const GridDesc& grid) {  // io.cpp:305-348
+    const mfreg_cu_grid g = grid.c();
+    LandmarkStats st;
+    int64_t cnt = 0;
+    detail::check(mfreg_cu_landmark_error(fixed.empty() ? nullptr : fixed[0].data(), static_cast<int64_t>(fixed.size()),
+                                          moving.empty() ? nullptr : moving[0].data(),
+                                          static_cast<int64_t>(moving.size()), y.data(), static_cast<int64_t>(y.size()),
+                                          &g, MFREG_CU_HOST, &st.mean, &st.stddev, &cnt));
+    st.count = static_cast<std::size_t>(cnt);
+    return st;
+}
+
+}  // namespace io
 
 }  // namespace mfreg_b200
 

@@ -696,8 +696,10 @@ int mfreg_cu_read_deformation(const char* path, const mfreg_cu_grid* nodal, doub
     return guard([&] {
         check_where(where);
         const std::vector<double> v = io::read_deformation(path, to_grid(nodal));
-        MFREG_CUDA(cudaMemcpy(y, v.data(), v.size() * sizeof(double),
-                              where == MFREG_CU_DEVICE ? cudaMemcpyHostToDevice : cudaMemcpyHostToHost));
+        if (where == MFREG_CU_DEVICE)
+            MFREG_CUDA(cudaMemcpy(y, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice));
+        else
+            std::memcpy(y, v.data(), v.size() * sizeof(double));
     });
 }
 

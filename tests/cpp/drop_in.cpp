@@ -23,6 +23,20 @@ int main(int argc, char** argv) {
     } catch (const std::invalid_argument& e) {
         std::printf("invalid_argument: %s\n", e.what());
     }
+    {  // io.hpp on the host side: deformation file + sidecar round trip, landmark parsing
+        std::vector<double> yy(static_cast<std::size_t>(3 * dg.count()), 0.25);
+        const std::string base = std::string(argc > 2 ? argv[2] : "/tmp") + "/drop_in.def";
+        mfreg::io::write_deformation(base, yy, dg);
+        const auto g2 = mfreg::io::read_deformation_grid(base);
+        const auto y2 = mfreg::io::read_deformation(base, g2);
+        std::printf("io deform %lld %lld %lld %zu %.17g\n", (long long)g2.m[0], (long long)g2.m[1], (long long)g2.m[2],
+                    y2.size(), y2[5]);
+        try {
+            mfreg::io::read_deformation_grid(base + ".missing");
+        } catch (const std::runtime_error& e) {
+            std::printf("runtime_error: %s\n", e.what());
+        }
+    }
     if (!gpu) return 0;
     // inputs: ref = phantom x 1000 (synthetic.cpp:15-63), tpl = sinusoid-warped ref
     const auto g = mfreg::make_image_grid({24, 20, 18}, {0.97, 0.97, 2.5});

@@ -26,9 +26,11 @@ def _build(tmp_path):
 
 
 def test_drop_in_compiles_and_maps_errors(tmp_path):
-    out = subprocess.run([_build(tmp_path), "host"], capture_output=True, text=True, check=True).stdout
+    out = subprocess.run([_build(tmp_path), "host", str(tmp_path)], capture_output=True, text=True, check=True).stdout
     assert "deform 17 17 17 h 4" in out
     assert "invalid_argument: deformation grid finer than image grid" in out
+    assert "io deform 17 17 17 14739 0.25" in out
+    assert f"runtime_error: cannot open sidecar {tmp_path}/drop_in.def.missing.meta" in out
 
 
 @pytest.mark.gpu
