@@ -67,10 +67,11 @@ __device__ __forceinline__ Coef ngf_coef(const FArgs& a, double dR0, double dR1,
     const double srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
     const double num = fma(0.5, fma(fma(dT0, dR0, dT1 * dR1), i0, fma(fma(dT2, dR2, dT3 * dR3), i1, fma(dT4, dR4, dT5 * dR5) * i2)),
                            a.tau * a.rho);
-    const double itn = rsqrt(fma(0.5, stt, a.tau * a.tau));
-    const double irn = rsqrt(fma(0.5, srr, a.rho * a.rho));
-    const double in1 = itn * irn;
-    const double in2 = num * (itn * itn) * in1;
+    // one reciprocal square root: in1 = 1/(|T| |R|) = rsqrt(|T|^2 |R|^2) and
+    // in2 = num / (|T|^3 |R|) = num in1^3 |R|^2
+    const double nt2 = fma(0.5, stt, a.tau * a.tau), nr2 = fma(0.5, srr, a.rho * a.rho);
+    const double in1 = rsqrt(nt2 * nr2);
+    const double in2 = num * ((in1 * in1) * (in1 * nr2));
     const double hx = a.hh[0], hy = a.hh[1], hz = a.hh[2];
     Coef c;
     c.e[0] = ok ? hx * fma(dR0, in1, -dT0 * in2) : 0.0;
