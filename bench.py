@@ -63,9 +63,16 @@ def dist_init(n):
     if world > 1:
         import torch
         import torch.distributed as dist
+        # one GPU per rank; MFREG_BENCH_BACKEND=gloo (with ranks sharing devices) exercises the
+        # N > 1 code path on a single-GPU box — never used for reported numbers
+        backend = os.environ.get("MFREG_BENCH_BACKEND", "nccl")
+        local = local % max(1, torch.cuda.device_count()) if backend != "nccl" else local
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     return rank, world, local
 
 
@@ -74,7 +81,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cuda" if dist.get_backend() == "nccl" else "cpu")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
