@@ -43,6 +43,7 @@ extern "C" {
 
 #define MFREG_CU_PARITY 0
 #define MFREG_CU_FAST 1
+#define MFREG_CU_FAST32 2 /* fused kernels on single-precision image state (tolerance 1e-4) */
 
 #define MFREG_CU_LBFGS 0       /* mfreg::Method::Lbfgs (multilevel.hpp:36) */
 #define MFREG_CU_GAUSS_NEWTON 1 /* mfreg::Method::GaussNewton */

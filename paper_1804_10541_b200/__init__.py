@@ -34,6 +34,7 @@ HOST, DEVICE = 0, 1
 class Mode:
     PARITY = PARITY  # bitwise replica of the reference
     FAST = FAST      # tree reductions + factored GN Hv (max-rel <= 1e-9)
+    FAST32 = 2       # FAST on single-precision image state and arithmetic (max-rel <= 1e-4)
 
 
 class Method:

@@ -101,7 +101,8 @@ struct Out {
 };
 
 Mode to_mode(int mode) {
-    if (mode != MFREG_CU_PARITY && mode != MFREG_CU_FAST) throw std::invalid_argument("mode must be PARITY or FAST");
+    if (mode != MFREG_CU_PARITY && mode != MFREG_CU_FAST && mode != MFREG_CU_FAST32)
+        throw std::invalid_argument("mode must be PARITY, FAST or FAST32");
     return static_cast<Mode>(mode);
 }
 

@@ -31,21 +31,30 @@ namespace {
 using namespace fdev;
 
 constexpr int TX = FT_X, TY = FT_Y;                    // 32 x 8 output tile
-constexpr int SX = TX + 4, SY = TY + 4, NS = SX * SY;  // R / T_w box 36 x 12
+constexpr int SY = TY + 4;                             // R / T_w box rows
 constexpr int NT = TX * TY;                            // 256 threads
 constexpr int RING = 5;                                // staging slots (3 steps ahead)
-constexpr int SLOT_R = 0, SLOT_T = NS, SLOT_D = 2 * NS;  // doubles: R, T_w [12][36], dT [3][8][32]
-constexpr int SLOT = 2 * NS + 3 * NT;                  // 1632 doubles = 13056 B
 constexpr int NX_A = 80;                               // extra items: ring-1 edge columns
-static_assert((SLOT * 8) % 128 == 0 && (SLOT_T * 8) % 128 == 0 && (SLOT_D * 8) % 128 == 0, "TMA alignment");
 
-// extra item e in [0, 80) -> ring-1 edge column (lx, ly) in the box frame and the
-// consumer flux array (0: +x, 1: -x, 2: +y, 3: -y)
+// Box geometry per state precision (TMA boxes start 16-byte aligned in x: x0 - XO)
+template <typename Real>
+struct Geo {
+    static constexpr int XO = sizeof(Real) == 8 ? 2 : 4;
+    static constexpr int SX = TX + 2 * XO, NS = SX * SY;
+    static constexpr int SLOT_R = 0, SLOT_T = NS, SLOT_D = 2 * NS;  // R, T_w [12][SX], dT [3][8][32]
+    static constexpr int SLOT = 2 * NS + 3 * NT;
+    static_assert((SLOT * sizeof(Real)) % 128 == 0 && (SLOT_T * sizeof(Real)) % 128 == 0 &&
+                      (SLOT_D * sizeof(Real)) % 128 == 0, "TMA alignment");
+};
+
+// extra item e in [0, 80) -> ring-1 edge column (lx, ly) in the box frame (tile columns at
+// lx = XO .. XO+31) and the consumer flux array (0: +x, 1: -x, 2: +y, 3: -y)
+template <int XO>
 __device__ __forceinline__ void edge_item(int e, int& lx, int& ly, int& dir) {
-    if (e < 32) { lx = 2 + e; ly = 1; dir = 2; }
-    else if (e < 64) { lx = 2 + e - 32; ly = SY - 2; dir = 3; }
-    else if (e < 72) { lx = 1; ly = 2 + e - 64; dir = 0; }
-    else { lx = SX - 2; ly = 2 + e - 72; dir = 1; }
+    if (e < 32) { lx = XO + e; ly = 1; dir = 2; }
+    else if (e < 64) { lx = XO + e - 32; ly = SY - 2; dir = 3; }
+    else if (e < 72) { lx = XO - 1; ly = 2 + e - 64; dir = 0; }
+    else { lx = XO + TX; ly = 2 + e - 72; dir = 1; }
 }
 
 template <int P_>
@@ -53,39 +62,49 @@ struct Par {
     static constexpr int P = P_;
 };
 
+__device__ __forceinline__ double rsq(double v) { return rsqrt(v); }
+__device__ __forceinline__ float rsq(float v) { return rsqrtf(v); }
+
 // NGF coefficients of one column at plane j from the six clamped differences
+template <typename Real>
 struct Coef {
-    double e[6];  // rho-hat: -x, +x, -y, +y, -z, +z
-    double r;     // residual
+    Real e[6];  // rho-hat: -x, +x, -y, +y, -z, +z
+    Real r;     // residual
 };
 
-__device__ __forceinline__ Coef ngf_coef(const FArgs& a, double dR0, double dR1, double dR2, double dR3, double dR4,
-                                         double dR5, double dT0, double dT1, double dT2, double dT3, double dT4,
-                                         double dT5, bool ok) {
-    const double i0 = a.ih2[0], i1 = a.ih2[1], i2 = a.ih2[2];
-    const double stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
-    const double srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
-    const double num = fma(0.5, fma(fma(dT0, dR0, dT1 * dR1), i0, fma(fma(dT2, dR2, dT3 * dR3), i1, fma(dT4, dR4, dT5 * dR5) * i2)),
-                           a.tau * a.rho);
+template <typename Real>
+__device__ __forceinline__ Coef<Real> ngf_coef(const FArgs& a, Real dR0, Real dR1, Real dR2, Real dR3, Real dR4,
+                                               Real dR5, Real dT0, Real dT1, Real dT2, Real dT3, Real dT4, Real dT5,
+                                               bool ok) {
+    const Real i0 = static_cast<Real>(a.ih2[0]), i1 = static_cast<Real>(a.ih2[1]), i2 = static_cast<Real>(a.ih2[2]);
+    const Real stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
+    const Real srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
+    const Real num = fma(Real(0.5), fma(fma(dT0, dR0, dT1 * dR1), i0, fma(fma(dT2, dR2, dT3 * dR3), i1, fma(dT4, dR4, dT5 * dR5) * i2)),
+                         static_cast<Real>(a.tau * a.rho));
     // one reciprocal square root: in1 = 1/(|T| |R|) = rsqrt(|T|^2 |R|^2) and
     // in2 = num / (|T|^3 |R|) = num in1^3 |R|^2
-    const double nt2 = fma(0.5, stt, a.tau * a.tau), nr2 = fma(0.5, srr, a.rho * a.rho);
-    const double in1 = rsqrt(nt2 * nr2);
-    const double in2 = num * ((in1 * in1) * (in1 * nr2));
-    const double hx = a.hh[0], hy = a.hh[1], hz = a.hh[2];
-    Coef c;
-    c.e[0] = ok ? hx * fma(dR0, in1, -dT0 * in2) : 0.0;
-    c.e[1] = ok ? hx * fma(dR1, in1, -dT1 * in2) : 0.0;
-    c.e[2] = ok ? hy * fma(dR2, in1, -dT2 * in2) : 0.0;
-    c.e[3] = ok ? hy * fma(dR3, in1, -dT3 * in2) : 0.0;
-    c.e[4] = ok ? hz * fma(dR4, in1, -dT4 * in2) : 0.0;
-    c.e[5] = ok ? hz * fma(dR5, in1, -dT5 * in2) : 0.0;
-    c.r = ok ? num * in1 : 0.0;
+    const Real nt2 = fma(Real(0.5), stt, static_cast<Real>(a.tau * a.tau));
+    const Real nr2 = fma(Real(0.5), srr, static_cast<Real>(a.rho * a.rho));
+    const Real in1 = rsq(nt2 * nr2);
+    const Real in2 = num * ((in1 * in1) * (in1 * nr2));
+    const Real hx = static_cast<Real>(a.hh[0]), hy = static_cast<Real>(a.hh[1]), hz = static_cast<Real>(a.hh[2]);
+    Coef<Real> c;
+    c.e[0] = ok ? hx * fma(dR0, in1, -dT0 * in2) : Real(0);
+    c.e[1] = ok ? hx * fma(dR1, in1, -dT1 * in2) : Real(0);
+    c.e[2] = ok ? hy * fma(dR2, in1, -dT2 * in2) : Real(0);
+    c.e[3] = ok ? hy * fma(dR3, in1, -dT3 * in2) : Real(0);
+    c.e[4] = ok ? hz * fma(dR4, in1, -dT4 * in2) : Real(0);
+    c.e[5] = ok ? hz * fma(dR5, in1, -dT5 * in2) : Real(0);
+    c.r = ok ? num * in1 : Real(0);
     return c;
 }
 
+template <typename Real>
 __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
-    extern __shared__ __align__(128) double sm[];
+    using G = Geo<Real>;
+    constexpr int XO = G::XO, SX = G::SX, NS = G::NS, SLOT_R = G::SLOT_R, SLOT_T = G::SLOT_T, SLOT_D = G::SLOT_D,
+                  SLOT = G::SLOT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const TileMeta& tm = a.tm;
     const int nlx = tm.nlx;
     const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
@@ -99,40 +118,41 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
     const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
     const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
     const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
-    double* const part = a.part + tile_id * tm.part_stride;
+    Real* const part = reinterpret_cast<Real*>(a.part) + tile_id * tm.part_stride;
+    Real* const frh_out = reinterpret_cast<Real*>(a.frh_out);
     const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
     const int segw = a.segw;
     const bool grad = a.grad != 0;
 
-    // ---- shared memory (doubles): ring | barriers | y fluxes | x edge fluxes | x-collapsed rows | row tables
-    double* const stg = sm;
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (6 doubles)
-    double* const sF = stg + RING * SLOT + 6;   // [2][2][NT] consumer-indexed y fluxes by plane parity
-    double* const sE = sF + 2 * 2 * NT;         // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
-    double* const sQx = sE + 2 * 2 * TY;        // [3][TY][nlx]
-    double* const sry = sQx + 3 * TY * nlx;     // [TY]
+    // ---- shared memory: ring | barriers | row tables, reduction (fp64) | fluxes, x-collapsed rows (Real) | ints
+    Real* const stg = reinterpret_cast<Real*>(smem_raw);
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (48 B)
+    double* const sry = reinterpret_cast<double*>(bars + 6);  // [TY]
     double* const sred = sry + TY;              // [NT / 32]
-    int* const sby = reinterpret_cast<int*>(sred + NT / 32);  // [TY]
+    Real* const sF = reinterpret_cast<Real*>(sred + NT / 32);  // [2][2][NT] consumer-indexed y fluxes
+    Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
+    Real* const sQx = sE + 2 * 2 * TY;          // [3][TY][nlx]
+    int* const sby = reinterpret_cast<int*>(sQx + 3 * TY * nlx);  // [TY]
     const unsigned bar0 = smem_u32(bars);
 
     // ---- columns: item 0 = tile column (lane, row); item 1 (threads < 80) = ring-1 edge column
     const int tx = lane, ty = row;
-    const int c0 = (tx + 2) + (ty + 2) * SX;
+    const int c0 = (tx + XO) + (ty + 2) * SX;
     const int gx0 = x0 + tx, gy0 = y0 + ty;
     const bool w1 = tid < NX_A;
-    int lx1 = 2, ly1 = 2, dir1 = 0;
-    if (w1) edge_item(tid, lx1, ly1, dir1);
+    int lx1 = XO, ly1 = 2, dir1 = 0;
+    if (w1) edge_item<XO>(tid, lx1, ly1, dir1);
     const int c1 = lx1 + ly1 * SX;
-    const int gx1 = x0 - 2 + lx1, gy1 = y0 - 2 + ly1;
+    const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
     const bool xedge = dir1 == 0 || dir1 == 1;
     const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
-                         : (dir1 - 2) * NT + min(max(lx1 - 2, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+                         : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
     // boundary masks of the in-plane differences (reference clamped neighbours) and
     // "inside the volume" flags of the two columns
-    const double m0xm = gx0 > 0 ? 1.0 : 0.0, m0xp = gx0 + 1 < mx ? 1.0 : 0.0;
-    const double m0ym = gy0 > 0 ? 1.0 : 0.0, m0yp = gy0 + 1 < my ? 1.0 : 0.0;
-    const double m1xm = gx1 > 0 ? 1.0 : 0.0, m1xp = gx1 + 1 < mx ? 1.0 : 0.0;
-    const double m1ym = gy1 > 0 ? 1.0 : 0.0, m1yp = gy1 + 1 < my ? 1.0 : 0.0;
+    const Real m0xm = gx0 > 0 ? Real(1) : Real(0), m0xp = gx0 + 1 < mx ? Real(1) : Real(0);
+    const Real m0ym = gy0 > 0 ? Real(1) : Real(0), m0yp = gy0 + 1 < my ? Real(1) : Real(0);
+    const Real m1xm = gx1 > 0 ? Real(1) : Real(0), m1xp = gx1 + 1 < mx ? Real(1) : Real(0);
+    const Real m1ym = gy1 > 0 ? Real(1) : Real(0), m1yp = gy1 + 1 < my ? Real(1) : Real(0);
     const bool in0 = gx0 < mx && gy0 < my;
     const bool in1c = gx1 >= 0 && gx1 < mx && gy1 >= 0 && gy1 < my;
     const long long col0 = in0 ? static_cast<long long>(gx0) + static_cast<long long>(gy0) * mx : 0;
@@ -141,7 +161,7 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
     const int gxc0 = min(gx0, mx - 1);
     const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
     const int bx = xin ? __ldg(&a.P.base[0][gxc0]) - nxA : 1024 + lane;
-    const double rxq = __ldg(&a.P.rem[0][gxc0]);
+    const Real rxq = __ldg(&a.P.rem[0][gxc0]);
     const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
     const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
     const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
@@ -163,34 +183,34 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
     do {                                                                           \
         if (tid == 0) {                                                            \
             const int rr_ = (r_);                                                  \
-            double* st_ = stg + rr_ * SLOT;                                         \
+            Real* st_ = stg + rr_ * SLOT;                                         \
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");          \
-            mbar_expect_tx(&bars[rr_], SLOT * 8);                                  \
-            tma_load_3d(st_ + SLOT_R, &maps.a, x0 - 2, y0 - 2, (m_), &bars[rr_]);   \
-            tma_load_3d(st_ + SLOT_T, &maps.b, x0 - 2, y0 - 2, (m_), &bars[rr_]);   \
+            mbar_expect_tx(&bars[rr_], SLOT * sizeof(Real));                       \
+            tma_load_3d(st_ + SLOT_R, &maps.a, x0 - XO, y0 - 2, (m_), &bars[rr_]);  \
+            tma_load_3d(st_ + SLOT_T, &maps.b, x0 - XO, y0 - 2, (m_), &bars[rr_]);  \
             tma_load_4d(st_ + SLOT_D, &maps.c, x0, y0, (m_) - 2, 0, &bars[rr_]);    \
         }                                                                          \
     } while (0)
 
-    auto xcollapse = [&](double v0, double v1, double v2) {
-        double* dst = sQx + row * nlx;
-        double A[3] = {(1.0 - rxq) * v0, (1.0 - rxq) * v1, (1.0 - rxq) * v2};
-        double B[3] = {rxq * v0, rxq * v1, rxq * v2};
+    auto xcollapse = [&](Real v0, Real v1, Real v2) {
+        Real* dst = sQx + row * nlx;
+        Real A[3] = {(Real(1) - rxq) * v0, (Real(1) - rxq) * v1, (Real(1) - rxq) * v2};
+        Real B[3] = {rxq * v0, rxq * v1, rxq * v2};
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             if (o >= segw) break;  // uniform
             const bool in = lane - o >= sst;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                const double ua = __shfl_up_sync(0xffffffffu, A[d], o);
-                const double ub = __shfl_up_sync(0xffffffffu, B[d], o);
+                const Real ua = __shfl_up_sync(0xffffffffu, A[d], o);
+                const Real ub = __shfl_up_sync(0xffffffffu, B[d], o);
                 A[d] = in ? A[d] + ua : A[d];
                 B[d] = in ? B[d] + ub : B[d];
             }
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
+            const Real bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
             if (send && xin) {
                 dst[d * TY * nlx + bx] = sst > 0 ? A[d] + bp : A[d];
                 if (xlast) dst[d * TY * nlx + bx + 1] = B[d];
@@ -201,13 +221,13 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
     auto ycollapse = [&](int nzp) {
         if (tid < nyi) {
             const int lxn = tid % nlx_t, lyn = (tid / nlx_t) % nly_t, d = tid / (nlx_t * nly_t);
-            const double* q = sQx + d * TY * nlx + lxn;
-            double v = 0.0;
+            const Real* q = sQx + d * TY * nlx + lxn;
+            Real v = 0.0;
 #pragma unroll
             for (int r = 0; r < TY; ++r) {
                 const int b = sby[r];
-                const double ry = sry[r];
-                const double wgt = b == lyn ? 1.0 - ry : (b == lyn - 1 ? ry : 0.0);
+                const Real ry = sry[r];
+                const Real wgt = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
                 v = fma(wgt, q[r * nlx], v);
             }
             part[static_cast<std::size_t>(nzp - nzA) * pstride + (lyn * nlx + lxn) * 3 + d] = v;
@@ -223,14 +243,14 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
     unsigned phase = 0;
 
     // ---- loop state (P = (k - kfirst) & 1)
-    double Rm0 = 0.0, Tm0 = 0.0, Rm1 = 0.0, Tm1 = 0.0;  // own R, T_w at plane k-2 (items 0, 1)
-    double fzp[2] = {0.0, 0.0};                        // rho-hat(+z) r of planes k-2, k-3
-    double sw = 0.0;                                   // sigma r of plane k-2
-    double gx = 0.0;                                   // in-row x fluxes into the column, plane k-2
+    Real Rm0 = 0.0, Tm0 = 0.0, Rm1 = 0.0, Tm1 = 0.0;  // own R, T_w at plane k-2 (items 0, 1)
+    Real fzp[2] = {0.0, 0.0};                        // rho-hat(+z) r of planes k-2, k-3
+    Real sw = 0.0;                                   // sigma r of plane k-2
+    Real gx = 0.0;                                   // in-row x fluxes into the column, plane k-2
     double dsum = 0.0;
-    double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
+    Real acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
     int cur = nzA, ypend = -1;
-    const double scale = a.scale;
+    const Real scale = a.scale;
 
     auto step = [&](auto parc, int k) {
         constexpr int P = decltype(parc)::P;
@@ -240,16 +260,16 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
             ypend = -1;
         }
         mbar_wait_at(bar0 + 8 * slot, phase);
-        const double* st = stg + slot * SLOT;       // plane k (R, T_w), dT of plane k-2
-        const double* sp = stg + slot_prev * SLOT;  // plane k-1 (R, T_w)
+        const Real* st = stg + slot * SLOT;       // plane k (R, T_w), dT of plane k-2
+        const Real* sp = stg + slot_prev * SLOT;  // plane k-1 (R, T_w)
         // ---- A: plane j = k-1
         const int j = k - 1;
-        const double mzm = j > 0 ? 1.0 : 0.0, mzp = j + 1 < mz ? 1.0 : 0.0;
+        const Real mzm = j > 0 ? Real(1) : Real(0), mzp = j + 1 < mz ? Real(1) : Real(0);
         const bool jin = j >= 0 && j < mz;
-        double fzm, fzp_new, sw_new, gx_new;
+        Real fzm, fzp_new, sw_new, gx_new;
         {
-            const double Rj = sp[SLOT_R + c0], Tj = sp[SLOT_T + c0];
-            const double Rp = st[SLOT_R + c0], Tp = st[SLOT_T + c0];
+            const Real Rj = sp[SLOT_R + c0], Tj = sp[SLOT_T + c0];
+            const Real Rp = st[SLOT_R + c0], Tp = st[SLOT_T + c0];
             const Coef cf = ngf_coef(a, m0xm * (sp[SLOT_R + c0 - 1] - Rj), m0xp * (sp[SLOT_R + c0 + 1] - Rj),
                                      m0ym * (sp[SLOT_R + c0 - SX] - Rj), m0yp * (sp[SLOT_R + c0 + SX] - Rj),
                                      mzm * (Rm0 - Rj), mzp * (Rp - Rj), m0xm * (sp[SLOT_T + c0 - 1] - Tj),
@@ -261,14 +281,14 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
             if (in0 && j >= z0 && j < z1) {  // Hv state of the tile voxel
                 const long long gi = col0 + static_cast<long long>(j) * plane;
 #pragma unroll
-                for (int d = 0; d < 6; ++d) a.frh_out[d * n + gi] = cf.e[d];
-                if (j >= ilo && j < ihi) dsum += fma(-cf.r, cf.r, 1.0);
+                for (int d = 0; d < 6; ++d) frh_out[d * n + gi] = cf.e[d];
+                if (j >= ilo && j < ihi) dsum += fma(-static_cast<double>(cf.r), static_cast<double>(cf.r), 1.0);
             }
-            const double r = cf.r;
-            const double fpx = __shfl_up_sync(0xffffffffu, cf.e[1] * r, 1);
-            const double fmx = __shfl_down_sync(0xffffffffu, cf.e[0] * r, 1);
-            gx_new = (tx > 0 ? fpx : 0.0) + (tx + 1 < TX ? fmx : 0.0);
-            double* const Fj = sF + (1 - P) * 2 * NT;
+            const Real r = cf.r;
+            const Real fpx = __shfl_up_sync(0xffffffffu, cf.e[1] * r, 1);
+            const Real fmx = __shfl_down_sync(0xffffffffu, cf.e[0] * r, 1);
+            gx_new = (tx > 0 ? fpx : Real(0)) + (tx + 1 < TX ? fmx : Real(0));
+            Real* const Fj = sF + (1 - P) * 2 * NT;
             if (ty + 1 < TY) Fj[tid + TX] = cf.e[3] * r;  // +y flux -> (tx, ty+1)
             if (ty > 0) Fj[NT + tid - TX] = cf.e[2] * r;  // -y flux -> (tx, ty-1)
             fzm = cf.e[4] * r;
@@ -276,8 +296,8 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
             sw_new = (((cf.e[0] + cf.e[1]) + (cf.e[2] + cf.e[3])) + (cf.e[4] + cf.e[5])) * r;
         }
         if (w1) {  // ring-1 edge column: the flux toward the tile
-            const double Rj = sp[SLOT_R + c1], Tj = sp[SLOT_T + c1];
-            const double Rp = st[SLOT_R + c1], Tp = st[SLOT_T + c1];
+            const Real Rj = sp[SLOT_R + c1], Tj = sp[SLOT_T + c1];
+            const Real Rp = st[SLOT_R + c1], Tp = st[SLOT_T + c1];
             const Coef cf = ngf_coef(a, m1xm * (sp[SLOT_R + c1 - 1] - Rj), m1xp * (sp[SLOT_R + c1 + 1] - Rj),
                                      m1ym * (sp[SLOT_R + c1 - SX] - Rj), m1yp * (sp[SLOT_R + c1 + SX] - Rj),
                                      mzm * (Rm1 - Rj), mzp * (Rp - Rj), m1xm * (sp[SLOT_T + c1 - 1] - Tj),
@@ -286,22 +306,22 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
                                      in1c && jin);
             Rm1 = Rj;
             Tm1 = Tj;
-            const double e = dir1 == 0 ? cf.e[1] : (dir1 == 1 ? cf.e[0] : (dir1 == 2 ? cf.e[3] : cf.e[2]));
+            const Real e = dir1 == 0 ? cf.e[1] : (dir1 == 1 ? cf.e[0] : (dir1 == 2 ? cf.e[3] : cf.e[2]));
             if (xedge) sE[(1 - P) * 2 * TY + f1] = e * cf.r;
             else sF[(1 - P) * 2 * NT + f1] = e * cf.r;
         }
         // ---- Z: plane i = k-2 (tile columns): gradient -2h dT (dr^T r) -> P^T
         const int i = k - 2;
         if (grad && i >= ilo && i < ihi) {  // uniform
-            const double* Fi = sF + P * 2 * NT;
-            const double* Ei = sE + P * 2 * TY + ty;
-            const double ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : 0.0);
-            const double z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
-            const double sz = scale * z;  // dT vanishes outside the volume (TMA zero fill)
-            const double* dq = st + SLOT_D + tid;
-            const double q0 = sz * dq[0], q1 = sz * dq[NT], q2 = sz * dq[2 * NT];
+            const Real* Fi = sF + P * 2 * NT;
+            const Real* Ei = sE + P * 2 * TY + ty;
+            const Real ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : 0.0);
+            const Real z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
+            const Real sz = scale * z;  // dT vanishes outside the volume (TMA zero fill)
+            const Real* dq = st + SLOT_D + tid;
+            const Real q0 = sz * dq[0], q1 = sz * dq[NT], q2 = sz * dq[2 * NT];
             const int bz = zbase(i);
-            const double rz = zrem(i);
+            const Real rz = zrem(i);
             if (bz > cur) {
                 xcollapse(acc00, acc01, acc02);
                 ypend = cur;
@@ -311,11 +331,11 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
                 acc10 = acc11 = acc12 = 0.0;
                 cur = bz;
             }
-            acc00 = fma(1.0 - rz, q0, acc00);
+            acc00 = fma(Real(1) - rz, q0, acc00);
             acc10 = fma(rz, q0, acc10);
-            acc01 = fma(1.0 - rz, q1, acc01);
+            acc01 = fma(Real(1) - rz, q1, acc01);
             acc11 = fma(rz, q1, acc11);
-            acc02 = fma(1.0 - rz, q2, acc02);
+            acc02 = fma(Real(1) - rz, q2, acc02);
             acc12 = fma(rz, q2, acc12);
         }
         fzp[P] = fzp_new;
@@ -359,17 +379,25 @@ __global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, 
 
 }  // namespace
 
-std::size_t ev2_smem_bytes(int nlx) {
-    const std::size_t d = static_cast<std::size_t>(RING) * SLOT + 6 + 2 * 2 * NT + 2 * 2 * TY + 3 * TY * nlx + TY + NT / 32;
-    return d * sizeof(double) + TY * sizeof(int);
+namespace {
+template <typename Real>
+std::size_t smem_bytes(int nlx) {
+    using G = Geo<Real>;
+    return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 48 + (TY + NT / 32) * sizeof(double) +
+           (2 * 2 * NT + 2 * 2 * TY + 3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real) + TY * sizeof(int);
 }
+}  // namespace
+
+std::size_t ev2_smem_bytes(int nlx, bool fp32) { return fp32 ? smem_bytes<float>(nlx) : smem_bytes<double>(nlx); }
 
 void ev2_set_smem_cap(int bytes) {
-    MFREG_CUDA(cudaFuncSetAttribute(k_ev2, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_ev2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_ev2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-void ev2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s) {
-    k_ev2<<<grid, NT, smem, s>>>(a, maps);
+void ev2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
+    if (fp32) k_ev2<float><<<grid, NT, smem, s>>>(a, maps);
+    else k_ev2<double><<<grid, NT, smem, s>>>(a, maps);
 }
 
 }  // namespace mfreg_b200

@@ -15,15 +15,16 @@
 namespace mfreg_b200 {
 
 // hv_fast.cu
-std::size_t hv2_smem_bytes(int nlx, int nsl, int zc);
+std::size_t hv2_smem_bytes(int nlx, int nsl, int zc, bool fp32);
+int hv2_box_origin(bool fp32);
 int hv2_nsl_max();
 int hv2_threads();
 void hv2_set_smem_cap(int bytes);
-void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s);
+void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
 // ev_fast.cu
-std::size_t ev2_smem_bytes(int nlx);
+std::size_t ev2_smem_bytes(int nlx, bool fp32);
 void ev2_set_smem_cap(int bytes);
-void ev2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s);
+void ev2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
 
 namespace {
 
@@ -750,7 +751,9 @@ __device__ double block_reduce(double v, double* sh) {
     return v;
 }
 
+template <typename PT>  // partial element type (fp32 partials in FAST32 mode)
 __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
+    const PT* const part = reinterpret_cast<const PT*>(a.part);
     __shared__ double sh[32];
     __shared__ bool last;
     if (a.skip && *a.skip) return;  // uniform
@@ -775,10 +778,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
             const int4* fl = reinterpret_cast<const int4*>(a.flat + node * a.flat_k);
             for (int q = 0; q < a.flat_k / 4; ++q) {
                 const int4 o = __ldg(fl + q);
-                if (o.x >= 0) v += __ldg(a.part + o.x + d);
-                if (o.y >= 0) v += __ldg(a.part + o.y + d);
-                if (o.z >= 0) v += __ldg(a.part + o.z + d);
-                if (o.w >= 0) v += __ldg(a.part + o.w + d);
+                if (o.x >= 0) v += static_cast<double>(__ldg(part + o.x + d));
+                if (o.y >= 0) v += static_cast<double>(__ldg(part + o.y + d));
+                if (o.z >= 0) v += static_cast<double>(__ldg(part + o.z + d));
+                if (o.w >= 0) v += static_cast<double>(__ldg(part + o.w + d));
                 if (o.w < 0) break;
             }
         } else {
@@ -794,7 +797,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
                 const std::size_t loc_row = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx;
                 for (int ex = xb; ex < xe; ++ex) {
                     const int2 X = __ldg(&tm.g_ent[0][ex]);
-                    v += __ldg(a.part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3 + d);
+                    v += static_cast<double>(__ldg(part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3 + d));
                 }
             }
         }
@@ -870,8 +873,9 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
 
 }  // namespace
 
-FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh,
-                     const SlabSpec& slab) {
+FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
+                     const SlabSpec& slab, bool fp32)
+    : fp32_(fp32) {
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
     TileMeta& t = meta_;
@@ -1018,7 +1022,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
                          (reinterpret_cast<std::uintptr_t>(Tw) % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(dT) % 16 == 0) && (reinterpret_cast<std::uintptr_t>(frh) % 16 == 0);
     const char* off = std::getenv("MFREG_NO_TMA");
-    tma_ = aligned && !(off && off[0] == '1') && make_tma_maps(g, R, Tw, dT, frh);
+    tma_ = aligned && (fp32 || !(off && off[0] == '1')) && make_tma_maps(g, R, Tw, dT, frh);
     // two-CTA/SM Hv kernel (hv_fast.cu): TMA only; the nodal z cells must span >= 2 image
     // planes (x-collapse buffer reuse, nodal ring of 4), and the y collapse needs one
     // thread per tile-local node
@@ -1037,21 +1041,26 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const double* R, const double*
             segw_ = std::max(segw_, run);
         }
     }
-    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3, t.zc);
+    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3, t.zc, fp32_);
     const char* no2 = std::getenv("MFREG_NO_HV2");
-    hv2_ = tma_ && zok && !(no2 && no2[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() &&
+    hv2_ = tma_ && zok && (fp32_ || !(no2 && no2[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() &&
            slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= static_cast<std::size_t>(kSmem2Cta);
     hv2_smem_ = hv2_smem;
     // (process-wide per-kernel cap: always the 2-CTA bound, so plans never lower each other's)
     if (hv2_) hv2_set_smem_cap(kSmem2Cta);
     // two-CTA/SM eval kernel (ev_fast.cu): same conditions
-    ev2_smem_ = ev2_smem_bytes(t.nlx);
+    ev2_smem_ = ev2_smem_bytes(t.nlx, fp32_);
     const char* noe = std::getenv("MFREG_NO_EV2");
-    ev2_ = tma_ && zok && !(noe && noe[0] == '1') && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
+    ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
     if (ev2_) ev2_set_smem_cap(kSmem2Cta);
+    // FAST32 runs only on the two-CTA kernels (the legacy fused kernels are fp64)
+    if (fp32_ && !(hv2_ && ev2_))
+        throw std::invalid_argument(
+            "FAST32: the grid is not supported by the single-precision kernels (odd x size or nodal z cells "
+            "spanning < 2 image planes)");
 }
 
-bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh) {
+bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh) {
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -1062,16 +1071,32 @@ bool FusedPlan::make_tma_maps(const Grid& g, const double* R, const double* Tw, 
     }();
     if (!encode) return false;
     const cuuint64_t mx = g.m[0], my = g.m[1], mz = g.m[2], n = g.count();
-    auto enc = [&](CUtensorMap* m, const double* base, int rank, cuuint64_t comps, cuuint32_t bx, cuuint32_t by,
-                   cuuint32_t bc) {
+    auto encw = [&](CUtensorMap* m, const void* base, int rank, cuuint64_t comps, cuuint32_t bx, cuuint32_t by,
+                    cuuint32_t bc, int es_bytes) {
+        const cuuint64_t e = static_cast<cuuint64_t>(es_bytes);
         const cuuint64_t dims[4] = {mx, my, mz, comps};
-        const cuuint64_t strides[3] = {mx * 8, mx * my * 8, n * 8};
+        const cuuint64_t strides[3] = {mx * e, mx * my * e, n * e};
         const cuuint32_t box[4] = {bx, by, 1, bc};
         const cuuint32_t es[4] = {1, 1, 1, 1};
-        return encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(base), dims, strides, box, es,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+        return encode(m, es_bytes == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rank,
+                      const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
+    if (fp32_) {  // single-precision state: only the two-CTA kernels' maps (boxes start at x0 - 4)
+        if ((g.m[0] * 4) % 16 != 0) return false;
+        const int XO = hv2_box_origin(true), SXf = FT_X + 2 * XO;
+        TmaMaps hv2{}, ev2{};
+        const bool ok = encw(&hv2.a, dT, 4, 3, SXf, CY, 3, 4) && encw(&hv2.b, frh, 4, 6, SXf, C1Y, 6, 4) &&
+                        encw(&ev2.a, R, 3, 1, SXf, CY, 1, 4) && encw(&ev2.b, Tw, 3, 1, SXf, CY, 1, 4) &&
+                        encw(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3, 4);
+        if (!ok) return false;
+        std::memcpy(maps_hv2_, &hv2, sizeof(TmaMaps));
+        std::memcpy(maps_ev2_, &ev2, sizeof(TmaMaps));
+        return true;
+    }
+    auto enc = [&](CUtensorMap* m, const void* base, int rank, cuuint64_t comps, cuuint32_t bx, cuuint32_t by,
+                   cuuint32_t bc) { return encw(m, base, rank, comps, bx, by, bc, 8); };
     TmaMaps hv{}, ev{};
     bool ok = enc(&hv.a, dT, 4, 3, CX, CY, 3) && enc(&hv.b, frh, 4, 6, CX, CY, 6) && enc(&ev.a, R, 3, 1, CX, CY, 1) &&
               enc(&ev.b, Tw, 3, 1, CX, CY, 1) && enc(&ev.c, dT, 4, 3, CX, CY, 3);
@@ -1099,7 +1124,8 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
     if (fp.hv2()) {
-        hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, t.ntz), fp.hv2_smem(), s);
+        hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, t.ntz), fp.hv2_smem(), s,
+                   fp.fp32());
         return;
     }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_hv());
@@ -1122,7 +1148,8 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, true);
     if (fp.ev2()) {
-        ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s);
+        ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s,
+                   fp.fp32());
         return;
     }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_ev());
@@ -1159,8 +1186,9 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.flat = fp.flat();
     a.flat_k = fp.flat_k();
     note_launch();
-    k_nodal_finalize<<<static_cast<unsigned>(std::max(1LL, (3 * a.nwin + FIN_THREADS - 1) / FIN_THREADS)), FIN_THREADS,
-                       0, s>>>(a);
+    const unsigned blocks = static_cast<unsigned>(std::max(1LL, (3 * a.nwin + FIN_THREADS - 1) / FIN_THREADS));
+    if (fp.fp32()) k_nodal_finalize<float><<<blocks, FIN_THREADS, 0, s>>>(a);
+    else k_nodal_finalize<double><<<blocks, FIN_THREADS, 0, s>>>(a);
 }
 
 }  // namespace mfreg_b200

@@ -46,8 +46,10 @@ public:
     // R, Tw, dT, frh: the device arrays the fused kernels stream (tensor maps are
     // built over them when TMA can address the grid)
     // `slab`: z window; the full domain when slab.full()
-    FusedPlan(const DevicePlanOwner& plan, const double* R, const double* Tw, const double* dT, const double* frh,
-              const SlabSpec& slab);
+    // fp32: the state arrays are single precision (FAST32 mode; two-CTA kernels only)
+    FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
+              const SlabSpec& slab, bool fp32 = false);
+    bool fp32() const { return fp32_; }
     bool tma() const { return tma_; }
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
@@ -95,7 +97,8 @@ private:
     alignas(64) unsigned char maps_hv2_[3 * 128];
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
-    bool make_tma_maps(const Grid& g, const double* R, const double* Tw, const double* dT, const double* frh);
+    bool fp32_ = false;
+    bool make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh);
 };
 
 // Direction order of the stored coefficients: -x, +x, -y, +y, -z, +z.

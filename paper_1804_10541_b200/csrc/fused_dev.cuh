@@ -39,6 +39,7 @@ struct TmaMaps {
 };
 
 __device__ __forceinline__ double lerp(double t, double a, double b) { return fma(t, b - a, a); }
+__device__ __forceinline__ float lerp(float t, float a, float b) { return fmaf(t, b - a, a); }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 

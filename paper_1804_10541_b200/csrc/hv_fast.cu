@@ -38,37 +38,45 @@ namespace {
 using namespace fdev;
 
 constexpr int TX = FT_X, TY = FT_Y;                    // 32 x 8 output tile
-constexpr int SX = TX + 4, SY = TY + 4, NS = SX * SY;  // s region 36 x 12
-constexpr int WY = TY + 2, NW = SX * WY;              // rho-hat box 36 x 10 (x from x0-2: a TMA box
-                                                       // must start 16-byte aligned in x)
+constexpr int SY = TY + 4, WY = TY + 2;                // s region rows / rho-hat rows
 constexpr int NT = TX * TY;                            // 256 threads
 constexpr int RING = 3;                                // staging slots (2 planes ahead)
-constexpr int SLOT_DT = 3 * NS;                        // dT box [3][12][36]
-constexpr int SLOT_RH = 6 * NW;                        // rho-hat box [6][10][36]
-constexpr int SLOT = ((SLOT_DT + SLOT_RH + 15) / 16) * 16;  // doubles, 128-byte multiple
 constexpr int NX_W = 80;                               // extra items [0, 80): ring-1 edges (P + W)
 constexpr int NX_P = 164;                              // extra items [80, 164): P only
 constexpr int NSL = 4;                                 // nodal plane ring (power of 2)
-static_assert((SLOT_DT * 8) % 128 == 0, "rho-hat box must land 128-byte aligned");
 
-// extra work item e -> column (lx, ly) in the s frame; `dir` = consumer flux array of
-// a ring-1 edge item (0: +x, 1: -x, 2: +y, 3: -y)
+// Box geometry per state precision: a TMA box must start 16-byte aligned in x, so the
+// boxes start XO columns left of the tile (x0 - 2 for fp64, x0 - 4 for fp32) and are
+// SX = 32 + 2 XO wide; the s frame is SX x 12, the rho-hat box SX x 10 (one row lower).
+template <typename Real>
+struct Geo {
+    static constexpr int XO = sizeof(Real) == 8 ? 2 : 4;
+    static constexpr int SX = TX + 2 * XO, NS = SX * SY, NW = SX * WY;
+    static constexpr int SLOT_DT = 3 * NS;              // dT box [3][12][SX]
+    static constexpr int SLOT_RH = 6 * NW;              // rho-hat box [6][10][SX]
+    static constexpr int SLOT = static_cast<int>(((SLOT_DT + SLOT_RH) * sizeof(Real) + 127) / 128 * 128 / sizeof(Real));
+    static_assert((SLOT_DT * sizeof(Real)) % 128 == 0, "rho-hat box must land 128-byte aligned");
+};
+
+// extra work item e -> column (lx, ly) in the s frame (tile columns at lx = XO .. XO+31);
+// `dir` = consumer flux array of a ring-1 edge item (0: +x, 1: -x, 2: +y, 3: -y)
+template <int XO>
 __device__ __forceinline__ void extra_item(int e, int& lx, int& ly, int& dir) {
     dir = -1;
-    if (e < 32) { lx = 2 + e; ly = 1; dir = 2; }                        // ring-1, y = -1 row: feeds +y
-    else if (e < 64) { lx = 2 + e - 32; ly = SY - 2; dir = 3; }         // ring-1, y = TY row: feeds -y
-    else if (e < 72) { lx = 1; ly = 2 + e - 64; dir = 0; }              // ring-1, x = -1: feeds +x
-    else if (e < 80) { lx = SX - 2; ly = 2 + e - 72; dir = 1; }         // ring-1, x = TX: feeds -x
+    if (e < 32) { lx = XO + e; ly = 1; dir = 2; }                       // ring-1, y = -1 row: feeds +y
+    else if (e < 64) { lx = XO + e - 32; ly = SY - 2; dir = 3; }        // ring-1, y = TY row: feeds -y
+    else if (e < 72) { lx = XO - 1; ly = 2 + e - 64; dir = 0; }         // ring-1, x = -1: feeds +x
+    else if (e < 80) { lx = XO + TX; ly = 2 + e - 72; dir = 1; }        // ring-1, x = TX: feeds -x
     else if (e < 84) {                                                  // ring-1 corners
         const int q = e - 80;
-        lx = (q & 1) ? SX - 2 : 1;
+        lx = (q & 1) ? XO + TX : XO - 1;
         ly = (q & 2) ? SY - 2 : 1;
     } else {                                                            // ring-2 edges
         const int r = e - 84;
-        if (r < 32) { lx = 2 + r; ly = 0; }
-        else if (r < 64) { lx = 2 + r - 32; ly = SY - 1; }
-        else if (r < 72) { lx = 0; ly = 2 + r - 64; }
-        else { lx = SX - 1; ly = 2 + r - 72; }
+        if (r < 32) { lx = XO + r; ly = 0; }
+        else if (r < 64) { lx = XO + r - 32; ly = SY - 1; }
+        else if (r < 72) { lx = XO - 2; ly = 2 + r - 64; }
+        else { lx = XO + TX + 1; ly = 2 + r - 72; }
     }
 }
 
@@ -77,8 +85,12 @@ struct Par {
     static constexpr int P = P_;
 };
 
+template <typename Real>
 __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
-    extern __shared__ __align__(128) double sm[];
+    using G = Geo<Real>;
+    constexpr int XO = G::XO, SX = G::SX, NS = G::NS, NW = G::NW, SLOT_DT = G::SLOT_DT, SLOT_RH = G::SLOT_RH,
+                  SLOT = G::SLOT;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     if (a.skip && *a.skip) return;  // uniform
     const TileMeta& tm = a.tm;
     const int nlx = tm.nlx;
@@ -92,39 +104,40 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
     const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
     const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
-    double* const part = a.part + tile_id * tm.part_stride;
+    Real* const part = reinterpret_cast<Real*>(a.part) + tile_id * tm.part_stride;
     const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
     const int msx = static_cast<int>(a.P.src.m[0]), msy = static_cast<int>(a.P.src.m[1]);
     const int msz = static_cast<int>(a.P.src.m[2]);
     const int nxf = a.nxf, nyf = a.nyf, nsl = nxf * nyf * 3, segw = a.segw;
 
-    // ---- shared memory (doubles): ring | s planes | fluxes | x-collapsed rows | nodal ring | row tables | barriers
-    double* const stg = sm;
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (4 doubles)
-    double* const sS = stg + RING * SLOT + 4;   // [2][NS] by plane parity
-    double* const sF = sS + 2 * NS;             // [2][2][NT] consumer-indexed y fluxes by plane parity
-    double* const sE = sF + 2 * 2 * NT;         // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
-    double* const sQ1 = sE + 2 * 2 * TY;        // [6][NX_P] item-1 P p at nodal planes bz, bz+1
-    double* const sQx = sQ1 + 6 * NX_P;         // [3][TY][nlx] (completions >= 2 steps apart)
-    double* const slab = sQx + 3 * TY * nlx;    // [NSL][nsl]
+    // ---- shared memory: ring | barriers | nodal ring, row/z tables (fp64) | s planes, fluxes,
+    // item-1 interpolants, x-collapsed rows (Real) | int tables
+    Real* const stg = reinterpret_cast<Real*>(smem_raw);
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (32 B)
+    double* const slab = reinterpret_cast<double*>(bars + 4);  // [NSL][nsl] nodal p
     double* const sry = slab + NSL * nsl;       // [TY]
     double* const sZr = sry + TY;               // [zc + 8] rem_z of the planes kfirst ..
-    int* const sby = reinterpret_cast<int*>(sZr + tm.zc + 8);  // [TY]
+    Real* const sS = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [2][NS] by plane parity
+    Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
+    Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
+    Real* const sQ1 = sE + 2 * 2 * TY;          // [6][NX_P] item-1 P p at nodal planes bz, bz+1
+    Real* const sQx = sQ1 + 6 * NX_P;           // [3][TY][nlx] (completions >= 2 steps apart)
+    int* const sby = reinterpret_cast<int*>(sQx + 3 * TY * nlx);  // [TY]
     int* const sZb = sby + TY;                  // [zc + 8] base_z of the planes kfirst ..
     const unsigned bar0 = smem_u32(bars);
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
     const int tx = lane, ty = row;
-    const int c0 = (tx + 2) + (ty + 2) * SX, w0 = c0 - SX;  // s frame / rho-hat frame (one row lower)
+    const int c0 = (tx + XO) + (ty + 2) * SX, w0 = c0 - SX;  // s frame / rho-hat frame (one row lower)
     const int gx0 = x0 + tx, gy0 = y0 + ty;
     const bool has1 = tid < NX_P, w1 = tid < NX_W;  // warp-aligned except warp 2 (split P+W / P) and warp 5
     int lx1 = 0, ly1 = 0, dir1 = -1;
-    if (has1) extra_item(tid, lx1, ly1, dir1);
+    if (has1) extra_item<XO>(tid, lx1, ly1, dir1);
     const int c1 = lx1 + ly1 * SX, w1i = c1 - SX;
     // where the ring-1 edge flux goes: y edges -> consumer-indexed sF (+y: 0, -y: 1), x edges -> sE
     const bool xedge = dir1 == 0 || dir1 == 1;
     const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
-                         : (dir1 - 2) * NT + min(max(lx1 - 2, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+                         : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
 
     // nodal slab geometry (P p): x-y footprint of the s region, bilinear weights per column
     const int fx0 = __ldg(&a.P.base[0][max(x0 - 2, 0)]);
@@ -135,7 +148,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         rx = __ldg(&a.P.rem[0][gxc]);
         ry = __ldg(&a.P.rem[1][gyc]);
     };
-    const int gx1 = x0 - 2 + lx1, gy1 = y0 - 2 + ly1;
+    const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
 
     // nodal p elements this thread loads (<= 2 per thread; host guarantees nsl <= 2 * NT)
     const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = sm0 * a.P.src.m[1];
@@ -165,12 +178,13 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         for (int u = 0; u < 2; ++u)
             if (slab_off[u] >= 0) dst[tid + u * NT] = slab_v[u];
     };
-    auto bilerp = [&](int nz, int off, double rx, double ry, double& o0, double& o1, double& o2) {
+    auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
         const double* q = slab + (nz & (NSL - 1)) * nsl + off;
         const int pl = nxf * nyf;
-        o0 = lerp(ry, lerp(rx, q[0], q[1]), lerp(rx, q[nxf], q[nxf + 1]));
-        o1 = lerp(ry, lerp(rx, q[pl], q[pl + 1]), lerp(rx, q[pl + nxf], q[pl + nxf + 1]));
-        o2 = lerp(ry, lerp(rx, q[2 * pl], q[2 * pl + 1]), lerp(rx, q[2 * pl + nxf], q[2 * pl + nxf + 1]));
+        auto v = [&](int i) { return static_cast<Real>(q[i]); };
+        o0 = lerp(ry, lerp(rx, v(0), v(1)), lerp(rx, v(nxf), v(nxf + 1)));
+        o1 = lerp(ry, lerp(rx, v(pl), v(pl + 1)), lerp(rx, v(pl + nxf), v(pl + nxf + 1)));
+        o2 = lerp(ry, lerp(rx, v(2 * pl), v(2 * pl + 1)), lerp(rx, v(2 * pl + nxf), v(2 * pl + nxf + 1)));
     };
 
     // x collapse geometry of the tile column: nodal cell, weight, segment of equal cells in the warp
@@ -179,7 +193,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
     const int bxc = __ldg(&a.P.base[0][gxc0]) - nxA;
     const int bx = xin ? bxc : 1024 + lane;
-    const double rxq = __ldg(&a.P.rem[0][gxc0]);
+    const Real rxq = __ldg(&a.P.rem[0][gxc0]);
     const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
     const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
     const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // first lane of my segment
@@ -207,21 +221,21 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     do {                                                                                \
         if (tid == 0) {                                                                 \
             const int rr_ = (r_);                                                       \
-            double* st_ = stg + rr_ * SLOT;                                              \
+            Real* st_ = stg + rr_ * SLOT;                                              \
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");               \
-            mbar_expect_tx(&bars[rr_], (SLOT_DT + SLOT_RH) * 8);                         \
-            tma_load_4d(st_, &maps.a, x0 - 2, y0 - 2, (m_), 0, &bars[rr_]);              \
-            tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - 2, y0 - 1, (m_) - 1, 0, &bars[rr_]); \
+            mbar_expect_tx(&bars[rr_], (SLOT_DT + SLOT_RH) * sizeof(Real));              \
+            tma_load_4d(st_, &maps.a, x0 - XO, y0 - 2, (m_), 0, &bars[rr_]);             \
+            tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - XO, y0 - 1, (m_) - 1, 0, &bars[rr_]); \
         }                                                                               \
     } while (0)
     auto zbase = [&](int k) { return sZb[k - kfirst]; };  // k in [kfirst, klast + 3]
     auto zrem = [&](int k) { return sZr[k - kfirst]; };
 
     // x collapse of one completed nodal plane (tile row = warp) into sQx[par]
-    auto xcollapse = [&](double v0, double v1, double v2) {
-        double* dst = sQx + row * nlx;
-        double A[3] = {(1.0 - rxq) * v0, (1.0 - rxq) * v1, (1.0 - rxq) * v2};
-        double B[3] = {rxq * v0, rxq * v1, rxq * v2};
+    auto xcollapse = [&](Real v0, Real v1, Real v2) {
+        Real* dst = sQx + row * nlx;
+        Real A[3] = {(Real(1) - rxq) * v0, (Real(1) - rxq) * v1, (Real(1) - rxq) * v2};
+        Real B[3] = {rxq * v0, rxq * v1, rxq * v2};
         // segmented inclusive scan over the lanes of equal nodal cell (segments <= segw lanes)
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -229,15 +243,15 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             const bool in = lane - o >= sst;
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
-                const double ua = __shfl_up_sync(0xffffffffu, A[d], o);
-                const double ub = __shfl_up_sync(0xffffffffu, B[d], o);
+                const Real ua = __shfl_up_sync(0xffffffffu, A[d], o);
+                const Real ub = __shfl_up_sync(0xffffffffu, B[d], o);
                 A[d] = in ? A[d] + ua : A[d];
                 B[d] = in ? B[d] + ub : B[d];
             }
         }
 #pragma unroll
         for (int d = 0; d < 3; ++d) {
-            const double bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
+            const Real bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
             if (send && xin) {
                 dst[d * TY * nlx + bx] = sst > 0 ? A[d] + bp : A[d];
                 if (xlast) dst[d * TY * nlx + bx + 1] = B[d];
@@ -249,13 +263,13 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     auto ycollapse = [&](int nzp) {
         if (tid < nyi) {
             const int lxn = tid % nlx_t, lyn = (tid / nlx_t) % nly_t, d = tid / (nlx_t * nly_t);
-            const double* q = sQx + d * TY * nlx + lxn;
-            double v = 0.0;
+            const Real* q = sQx + d * TY * nlx + lxn;
+            Real v = 0.0;
 #pragma unroll
             for (int r = 0; r < TY; ++r) {
                 const int b = sby[r];
-                const double ry = sry[r];
-                const double wgt = b == lyn ? 1.0 - ry : (b == lyn - 1 ? ry : 0.0);
+                const Real ry = sry[r];
+                const Real wgt = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
                 v = fma(wgt, q[r * nlx], v);
             }
             part[static_cast<std::size_t>(nzp - nzA) * pstride + (lyn * nlx + lxn) * 3 + d] = v;
@@ -283,15 +297,15 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
     // ---- loop state (parity-named histories, P = (k - kfirst) & 1)
     int pz = -1000;
-    double Pa0 = 0.0, Pa1 = 0.0, Pa2 = 0.0, Pb0 = 0.0, Pb1 = 0.0, Pb2 = 0.0;  // item 0: P p at nodal planes bz, bz+1
-    double sh0[2] = {0.0, 0.0}, sh1[2] = {0.0, 0.0};   // s history (item 0, item 1)
-    double dq[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // dT of planes k-1, k-2 (item 0)
-    double fzp[2] = {0.0, 0.0};                        // rho-hat(+z) w of planes k-2, k-3
-    double gx = 0.0;                                   // in-row x fluxes into the column, plane k-2
-    double sw = 0.0;                                   // sigma w of plane k-2
-    double acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
+    Real Pa0 = 0.0, Pa1 = 0.0, Pa2 = 0.0, Pb0 = 0.0, Pb1 = 0.0, Pb2 = 0.0;  // item 0: P p at nodal planes bz, bz+1
+    Real sh0[2] = {0.0, 0.0}, sh1[2] = {0.0, 0.0};   // s history (item 0, item 1)
+    Real dq[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};  // dT of planes k-1, k-2 (item 0)
+    Real fzp[2] = {0.0, 0.0};                        // rho-hat(+z) w of planes k-2, k-3
+    Real gx = 0.0;                                   // in-row x fluxes into the column, plane k-2
+    Real sw = 0.0;                                   // sigma w of plane k-2
+    Real acc00 = 0.0, acc01 = 0.0, acc02 = 0.0, acc10 = 0.0, acc11 = 0.0, acc12 = 0.0;
     int cur = nzA, ypend = -1;
-    const double scale = a.scale;
+    const Real scale = a.scale;
 
     auto step = [&](auto parc, int k) {
         constexpr int P = decltype(parc)::P;
@@ -312,15 +326,16 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             }
         }
         const int bzk = zbase(k);
-        const double rzk = zrem(k);
+        const Real rzk = zrem(k);
         if (bzk != pz) {  // uniform: new nodal plane pair
-            double* q1 = sQ1 + tid;  // item 1: [0..2] plane bz, [3..5] plane bz+1 (own entries only)
+            Real* q1 = sQ1 + tid;  // item 1: [0..2] plane bz, [3..5] plane bz+1 (own entries only)
             // item 0 geometry from the x-collapse registers and the row tables; item 1 from global
             const int off0 = (bxc + nxA - fx0) + (sby[row] + nyA - fy0) * nxf;
-            const double ry0 = sry[row];
+            const Real ry0 = sry[row];
             int off1 = 0;
             double rx1 = 0.0, ry1 = 0.0;
             if (has1) col_geom(gx1, gy1, off1, rx1, ry1);
+            const Real rx1r = static_cast<Real>(rx1), ry1r = static_cast<Real>(ry1);
             if (bzk == pz + 1) {
                 Pa0 = Pb0; Pa1 = Pb1; Pa2 = Pb2;
                 if (has1) {
@@ -330,43 +345,43 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
                 }
             } else {
                 bilerp(bzk, off0, rxq, ry0, Pa0, Pa1, Pa2);
-                if (has1) bilerp(bzk, off1, rx1, ry1, q1[0], q1[NX_P], q1[2 * NX_P]);
+                if (has1) bilerp(bzk, off1, rx1r, ry1r, q1[0], q1[NX_P], q1[2 * NX_P]);
             }
             const int bz1 = min(bzk + 1, msz - 1);
             bilerp(bz1, off0, rxq, ry0, Pb0, Pb1, Pb2);
-            if (has1) bilerp(bz1, off1, rx1, ry1, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
+            if (has1) bilerp(bz1, off1, rx1r, ry1r, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
             pz = bzk;
         }
         mbar_wait_at(bar0 + 8 * slot, phase);
-        const double* st = stg + slot * SLOT;
+        const Real* st = stg + slot * SLOT;
         // ---- P: plane k
-        const double pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
-        const double D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
-        const double s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
+        const Real pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
+        const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
+        const Real s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
         sS[P * NS + c0] = s0;
-        double s1 = 0.0;
+        Real s1 = 0.0;
         if (has1) {
-            const double* q1 = sQ1 + tid;
+            const Real* q1 = sQ1 + tid;
             s1 = fma(st[c1], lerp(rzk, q1[0], q1[3 * NX_P]),
                      fma(st[NS + c1], lerp(rzk, q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * lerp(rzk, q1[2 * NX_P], q1[5 * NX_P])));
             sS[P * NS + c1] = s1;
         }
         // ---- W: plane j = k-1 (in-plane neighbours' s from the other parity buffer)
-        const double* sn = sS + (1 - P) * NS;
-        const double* rh = st + SLOT_DT + w0;  // rho-hat of plane j, [6][NW]
-        double* const Fj = sF + (1 - P) * 2 * NT;
-        double fzm, fzp_new, sw_new, gx_new;
+        const Real* sn = sS + (1 - P) * NS;
+        const Real* rh = st + SLOT_DT + w0;  // rho-hat of plane j, [6][NW]
+        Real* const Fj = sF + (1 - P) * 2 * NT;
+        Real fzm, fzp_new, sw_new, gx_new;
         {
-            const double sj = sh0[1 - P];
-            const double wa = fma(rh[1 * NW], sn[c0 + 1] - sj, rh[0] * (sn[c0 - 1] - sj));
-            const double wb = fma(rh[3 * NW], sn[c0 + SX] - sj, rh[2 * NW] * (sn[c0 - SX] - sj));
-            const double wc = fma(rh[5 * NW], s0 - sj, rh[4 * NW] * (sh0[P] - sj));
-            const double w = (wa + wb) + wc;
-            const double sg = ((rh[0] + rh[1 * NW]) + (rh[2 * NW] + rh[3 * NW])) + (rh[4 * NW] + rh[5 * NW]);
+            const Real sj = sh0[1 - P];
+            const Real wa = fma(rh[1 * NW], sn[c0 + 1] - sj, rh[0] * (sn[c0 - 1] - sj));
+            const Real wb = fma(rh[3 * NW], sn[c0 + SX] - sj, rh[2 * NW] * (sn[c0 - SX] - sj));
+            const Real wc = fma(rh[5 * NW], s0 - sj, rh[4 * NW] * (sh0[P] - sj));
+            const Real w = (wa + wb) + wc;
+            const Real sg = ((rh[0] + rh[1 * NW]) + (rh[2 * NW] + rh[3 * NW])) + (rh[4 * NW] + rh[5 * NW]);
             // x fluxes stay in the warp (one tile row): from lane-1 (+x) and lane+1 (-x)
-            const double fpx = __shfl_up_sync(0xffffffffu, rh[1 * NW] * w, 1);
-            const double fmx = __shfl_down_sync(0xffffffffu, rh[0] * w, 1);
-            gx_new = (tx > 0 ? fpx : 0.0) + (tx + 1 < TX ? fmx : 0.0);
+            const Real fpx = __shfl_up_sync(0xffffffffu, rh[1 * NW] * w, 1);
+            const Real fmx = __shfl_down_sync(0xffffffffu, rh[0] * w, 1);
+            gx_new = (tx > 0 ? fpx : Real(0)) + (tx + 1 < TX ? fmx : Real(0));
             if (ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;       // +y flux -> (tx, ty+1)
             if (ty > 0) Fj[NT + tid - TX] = rh[2 * NW] * w;       // -y flux -> (tx, ty-1)
             fzm = rh[4 * NW] * w;
@@ -374,27 +389,27 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             sw_new = sg * w;
         }
         if (w1) {  // ring-1 edge column: only the flux toward the tile
-            const double* rg = st + SLOT_DT + w1i;
-            const double sj = sh1[1 - P];
-            const double wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
-            const double wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
-            const double wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
-            const double w = (wa + wb) + wc;
-            const double cf = dir1 == 0 ? rg[1 * NW] : (dir1 == 1 ? rg[0] : (dir1 == 2 ? rg[3 * NW] : rg[2 * NW]));
+            const Real* rg = st + SLOT_DT + w1i;
+            const Real sj = sh1[1 - P];
+            const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
+            const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
+            const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
+            const Real w = (wa + wb) + wc;
+            const Real cf = dir1 == 0 ? rg[1 * NW] : (dir1 == 1 ? rg[0] : (dir1 == 2 ? rg[3 * NW] : rg[2 * NW]));
             if (xedge) sE[(1 - P) * 2 * TY + f1] = cf * w;
             else Fj[f1] = cf * w;
         }
         // ---- Z: plane i = k-2 (tile columns)
         const int i = k - 2;
         if (i >= ilo && i < ihi) {  // uniform
-            const double* Fi = sF + P * 2 * NT;
-            const double* Ei = sE + P * 2 * TY + ty;
-            const double ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : 0.0);  // ring-1 x edge fluxes
-            const double z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
-            const double sz = scale * z;  // dT (TMA zero fill) makes q vanish outside the volume
-            const double q0 = sz * dq[P][0], q1 = sz * dq[P][1], q2 = sz * dq[P][2];
+            const Real* Fi = sF + P * 2 * NT;
+            const Real* Ei = sE + P * 2 * TY + ty;
+            const Real ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : Real(0));  // ring-1 x edge fluxes
+            const Real z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
+            const Real sz = scale * z;  // dT (TMA zero fill) makes q vanish outside the volume
+            const Real q0 = sz * dq[P][0], q1 = sz * dq[P][1], q2 = sz * dq[P][2];
             const int bz = zbase(i);
-            const double rz = zrem(i);
+            const Real rz = zrem(i);
             if (bz > cur) {  // nodal plane `cur` complete: x collapse now, y collapse after the barrier
                 xcollapse(acc00, acc01, acc02);
                 ypend = cur;
@@ -404,11 +419,11 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
                 acc10 = acc11 = acc12 = 0.0;
                 cur = bz;
             }
-            acc00 = fma(1.0 - rz, q0, acc00);
+            acc00 = fma(Real(1) - rz, q0, acc00);
             acc10 = fma(rz, q0, acc10);
-            acc01 = fma(1.0 - rz, q1, acc01);
+            acc01 = fma(Real(1) - rz, q1, acc01);
             acc11 = fma(rz, q1, acc11);
-            acc02 = fma(1.0 - rz, q2, acc02);
+            acc02 = fma(Real(1) - rz, q2, acc02);
             acc12 = fma(rz, q2, acc12);
         }
         // ---- histories
@@ -447,22 +462,36 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
 }  // namespace
 
-std::size_t hv2_smem_bytes(int nlx, int nsl, int zc) {
-    const std::size_t d = static_cast<std::size_t>(RING) * SLOT + 2 * NS + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P + 3 * TY * nlx +
-                          static_cast<std::size_t>(NSL) * nsl + TY;
-    return (d + 4 + zc + 8) * sizeof(double) + (TY + zc + 8) * sizeof(int);
+namespace {
+template <typename Real>
+std::size_t smem_bytes(int nlx, int nsl, int zc) {
+    using G = Geo<Real>;
+    const std::size_t ring = static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 32;
+    const std::size_t dbl = (static_cast<std::size_t>(NSL) * nsl + TY + zc + 8) * sizeof(double);
+    const std::size_t real = (2 * static_cast<std::size_t>(G::NS) + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P +
+                              3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real);
+    return ring + dbl + real + (TY + zc + 8) * sizeof(int);
+}
+}  // namespace
+
+// fp32 = true: the Hv state (dT, rho-hat) and the arithmetic in single precision (FAST32 mode)
+std::size_t hv2_smem_bytes(int nlx, int nsl, int zc, bool fp32) {
+    return fp32 ? smem_bytes<float>(nlx, nsl, zc) : smem_bytes<double>(nlx, nsl, zc);
 }
 
 int hv2_nsl_max() { return 2 * NT; }
 int hv2_ring_planes() { return NSL; }
 int hv2_threads() { return NT; }
+int hv2_box_origin(bool fp32) { return fp32 ? Geo<float>::XO : Geo<double>::XO; }
 
 void hv2_set_smem_cap(int bytes) {
-    MFREG_CUDA(cudaFuncSetAttribute(k_hv2, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-void hv2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s) {
-    k_hv2<<<grid, NT, smem, s>>>(a, maps);
+void hv2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
+    if (fp32) k_hv2<float><<<grid, NT, smem, s>>>(a, maps);
+    else k_hv2<double><<<grid, NT, smem, s>>>(a, maps);
 }
 
 }  // namespace mfreg_b200

@@ -156,9 +156,11 @@ __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __
 // on a tie, and the one-sided gradient there depends on that choice), then the
 // trilinear value / gradient with fused arithmetic (continuous in the cell
 // fraction, so contraction only moves the last bits).
+// (OutT = float: the FAST32 state; the cell choice and P y stay exact fp64)
+template <typename OutT>
 __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __restrict__ y,
-                                                   const double* __restrict__ T, double* __restrict__ Tw,
-                                                   double* __restrict__ dT, int zoff) {
+                                                   const double* __restrict__ T, OutT* __restrict__ Tw,
+                                                   OutT* __restrict__ dT, int zoff) {
     const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
     const int x = blockIdx.x * 32 + threadIdx.x, yy = blockIdx.y * 8 + threadIdx.y;
     const int z = blockIdx.z + zoff;
@@ -243,10 +245,10 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
     const double gzv = cy[1] - cy[0];
     const long long i = x + static_cast<long long>(yy) * mx + static_cast<long long>(z) * plane,
                     n = static_cast<long long>(plane) * mz;
-    Tw[i] = fma(fz, gzv, cy[0]);
-    dT[i] = fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0];
-    dT[n + i] = fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1];
-    dT[2 * n + i] = gzv * P.tgt.ih[2];
+    Tw[i] = static_cast<OutT>(fma(fz, gzv, cy[0]));
+    dT[i] = static_cast<OutT>(fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0]);
+    dT[n + i] = static_cast<OutT>(fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1]);
+    dT[2 * n + i] = static_cast<OutT>(gzv * P.tgt.ih[2]);
 }
 
 __global__ void k_sample(Grid g, const double* __restrict__ T, const double* __restrict__ pts, idx_t n,
@@ -859,15 +861,34 @@ void launch_warp(const DevPlan& P0, const double* y, const double* T, double* Tw
     if (gr.z == 0) return;
     note_launch(), k_warp<<<gr, block3(), 0, s>>>(P, y, T, Tw, dT, zlo);
 }
-void launch_warp_fast(const DevPlan& P0, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
-                      int zlo, int zhi) {
+template <typename OutT>
+void warp_fast_impl(const DevPlan& P0, const double* y, const double* T, OutT* Tw, OutT* dT, cudaStream_t s, int zlo,
+                    int zhi) {
     DevPlan P = P0;
     P.tgt.set_inv();
     if (zhi < 0) zhi = static_cast<int>(P.tgt.m[2]);
     if (zhi <= zlo) return;
     const dim3 gr(static_cast<unsigned>((P.tgt.m[0] + 31) / 32), static_cast<unsigned>((P.tgt.m[1] + 7) / 8),
                   static_cast<unsigned>(zhi - zlo));
-    note_launch(), k_warp_fast<<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo);
+    note_launch(), k_warp_fast<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo);
+}
+__global__ void k_to_float(idx_t n, const double* __restrict__ a, float* __restrict__ o) {
+    for (idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+         i += static_cast<idx_t>(gridDim.x) * blockDim.x)
+        o[i] = static_cast<float>(a[i]);
+}
+void launch_to_float(idx_t n, const double* a, float* o, cudaStream_t s) {
+    if (n <= 0) return;
+    note_launch();
+    k_to_float<<<static_cast<unsigned>(std::min<idx_t>((n + 255) / 256, 148 * 16)), 256, 0, s>>>(n, a, o);
+}
+void launch_warp_fast(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
+                      int zlo, int zhi) {
+    warp_fast_impl(P, y, T, Tw, dT, s, zlo, zhi);
+}
+void launch_warp_fast(const DevPlan& P, const double* y, const double* T, float* Tw, float* dT, cudaStream_t s,
+                      int zlo, int zhi) {
+    warp_fast_impl(P, y, T, Tw, dT, s, zlo, zhi);
 }
 void launch_ngf_ws(const Grid& img0, const double* R, const double* Tw, double tau, double rho, double* r,
                    double* inv1, double* inv2, double* rh, cudaStream_t s) {

@@ -31,6 +31,10 @@ void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n,
 // image planes [zlo, zhi) (zhi < 0: all)
 void launch_warp_fast(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
                       int zlo = 0, int zhi = -1);
+// FAST32 state: single-precision copies / T_w, dT
+void launch_to_float(idx_t n, const double* a, float* o, cudaStream_t s);
+void launch_warp_fast(const DevPlan& P, const double* y, const double* T, float* Tw, float* dT, cudaStream_t s,
+                      int zlo = 0, int zhi = -1);
 void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw, double* dT, cudaStream_t s,
                  int zlo = 0, int zhi = -1);
 

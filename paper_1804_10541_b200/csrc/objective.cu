@@ -158,10 +158,18 @@ DeviceNgf::DeviceNgf(const Grid& img, const double* R_dev, double tau, double rh
     : g_(img), tau_(tau), rho_(rho), mode_(mode), s_(s), R_(R_dev), red_(mode, img.count()) {
     if (!(rho > 0.0)) throw std::invalid_argument("NGF: rho must be > 0");  // ngf.cpp:168-170
     const std::size_t n = static_cast<std::size_t>(img.count());
-    Tw.resize(n);
-    dT.resize(3 * n);
-    if (mode == Mode::Parity) ensure_ws();
-    else frh.resize(6 * n);
+    if (mode == Mode::Fast32) {  // single-precision state; R converted once per level
+        R32.resize(n);
+        Tw32.resize(n);
+        dT32.resize(3 * n);
+        frh32.resize(6 * n);
+        launch_to_float(static_cast<idx_t>(n), R_dev, R32.get(), s);
+    } else {
+        Tw.resize(n);
+        dT.resize(3 * n);
+        if (mode == Mode::Parity) ensure_ws();
+        else frh.resize(6 * n);
+    }
     tab_ = make_hv_table(img);
 }
 
@@ -175,7 +183,7 @@ void DeviceNgf::ensure_ws() {
     inv2.resize(n);
     rh.resize(7 * n);
     sv.resize(n);
-    if (mode_ == Mode::Fast) wbuf.resize(n);
+    if (mode_ != Mode::Parity) wbuf.resize(n);
 }
 
 void DeviceNgf::populate_points(const double* T_dev, const double* pts_dev) {
@@ -244,7 +252,7 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     check_launch("identity");
     sliced_ = !slab.full(static_cast<int>(img_.m[2]), static_cast<int>(dg_.m[2]));
     if (sliced_) {
-        if (mode != Mode::Fast) throw std::invalid_argument("z slabs require fast mode");
+        if (mode == Mode::Parity) throw std::invalid_argument("z slabs require fast mode");
         const auto parts = slab_partition(img_, dg_, 1);  // validates the grids
         (void)parts;
         const int mz = static_cast<int>(img_.m[2]), msz = static_cast<int>(dg_.m[2]);
@@ -252,8 +260,9 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
               slab.own_lo < slab.own_hi && slab.own_hi <= msz))
             throw std::invalid_argument("slab: invalid z window");
     }
-    if (mode == Mode::Fast) {
-        fused_ = std::make_unique<FusedPlan>(plan_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.frh.get(), slab_);
+    if (mode != Mode::Parity) {
+        fused_ = std::make_unique<FusedPlan>(plan_, ngf_.state_R(), ngf_.state_Tw(), ngf_.state_dT(), ngf_.state_frh(),
+                                             slab_, mode == Mode::Fast32);
         MFREG_CUDA(cudaStreamCreateWithFlags(&s2_, cudaStreamNonBlocking));
         MFREG_CUDA(cudaEventCreateWithFlags(&ev_fork_, cudaEventDisableTiming));
         MFREG_CUDA(cudaEventCreateWithFlags(&ev_join_, cudaEventDisableTiming));
@@ -271,15 +280,21 @@ DeviceObjective::~DeviceObjective() {
 
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
 
+// fast-mode warp into the state arrays of the objective's precision
+void DeviceObjective::warp_state(const double* y, cudaStream_t s, int zlo, int zhi) {
+    if (ngf_.fp32())
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw32.get(), ngf_.dT32.get(), s, zlo, zhi);
+    else
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, zlo, zhi);
+}
+
 // fast mode: the launch sequence of eval (captured once per (y, grad) into a CUDA graph)
 void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStream_t s) {
     const idx_t ny = dg_.count();
     const int mz = static_cast<int>(img_.m[2]);
-    if (sliced_)  // the slab's planes + 3 halo planes (state of the 2 halo planes the Hv reads)
-        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, std::max(0, slab_.zlo - 3),
-                         std::min(mz, slab_.zhi + 3));
-    else
-        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s);
+    // (sliced: the slab's planes + 3 halo planes, the state of the 2 halo planes the Hv reads)
+    const int wlo = sliced_ ? std::max(0, slab_.zlo - 3) : 0, whi = sliced_ ? std::min(mz, slab_.zhi + 3) : -1;
+    warp_state(y, s, wlo, whi);
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s);
     // curvature value / gradient on the side stream, overlapping the image pass
     MFREG_CUDA(cudaEventRecord(ev_fork_, s));
@@ -295,8 +310,8 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     if (grad && alpha_ != 0.0)
         launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
-    launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, ngf_.frh.get(),
-                      grad != nullptr, s);
+    launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
+                      static_cast<double*>(ngf_.state_frh()), grad != nullptr, s);
     MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     FinalizeSpec f;
     f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
@@ -347,9 +362,9 @@ double DeviceObjective::profile_kernel(int which, const double* p, int reps, std
             launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
         else if (which == 1)
             launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                              ngf_.frh.get(), true, s_);
+                              static_cast<double*>(ngf_.state_frh()), true, s_);
         else
-            launch_warp_fast(plan_.view(), p, T_, ngf_.Tw.get(), ngf_.dT.get(), s_);
+            warp_state(p, s_, 0, -1);
         MFREG_CUDA(cudaEventRecord(e1, s_));
         MFREG_CUDA(cudaEventSynchronize(e1));
         float ms = 0.0f;

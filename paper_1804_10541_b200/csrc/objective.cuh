@@ -32,7 +32,10 @@ struct CudaError : std::runtime_error {
 
 void check_launch(const char* what);
 
-enum class Mode : int { Parity = 0, Fast = 1 };
+// Parity: bitwise = reference; Fast: fused kernels, fp64; Fast32: fused kernels with the
+// image-grid state (T_w, dT, rho-hat) and the fused arithmetic in fp32 (north star's optional
+// fp32 mode, tolerance 1e-4); nodal vectors, reductions and solvers stay fp64.
+enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 
 // RAII device array of doubles (or raw bytes).
 template <typename T>
@@ -261,6 +264,12 @@ public:
     const double* R_;  // borrowed
     DVec Tw, dT, r, inv1, inv2, rh, sv, wbuf;
     DVec frh;  // fast mode: rho-hat [6][n] (-x,+x,-y,+y,-z,+z), the Hv state
+    DevArray<float> R32, Tw32, dT32, frh32;  // Fast32 state
+    bool fp32() const { return mode_ == Mode::Fast32; }
+    const void* state_R() const { return fp32() ? static_cast<const void*>(R32.get()) : R_; }
+    void* state_Tw() { return fp32() ? static_cast<void*>(Tw32.get()) : Tw.get(); }
+    void* state_dT() { return fp32() ? static_cast<void*>(dT32.get()) : dT.get(); }
+    void* state_frh() { return fp32() ? static_cast<void*>(frh32.get()) : frh.get(); }
     HvTable tab_;
     Reducer red_;
 };
@@ -301,6 +310,7 @@ public:
 
 private:
     void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s);
+    void warp_state(const double* y, cudaStream_t s, int zlo, int zhi);
     void enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip, cudaStream_t s);
     Grid img_, dg_;
     SlabSpec slab_;

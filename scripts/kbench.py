@@ -25,7 +25,7 @@ def main():
     ap.add_argument("--h", type=float, nargs=3, default=(1.0, 1.0, 1.0))
     ap.add_argument("--no-flush", action="store_true")
     a = ap.parse_args()
-    mode = P.Mode.FAST if a.mode == "fast" else P.Mode.PARITY
+    mode = {"fast": P.Mode.FAST, "fast32": P.Mode.FAST32, "parity": P.Mode.PARITY}[a.mode]
     img = P.make_image_grid(a.m, a.h)
     dg = P.deformation_grid_for(img, 4)
     R = P.make_phantom(img, device=True)
