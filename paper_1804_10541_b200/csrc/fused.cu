@@ -899,10 +899,12 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     // Hv kernel (2 CTAs/SM; the eval kernel then runs two waves of half the height)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
     const int mz = t.zhi - t.zlo;
-    int best = (mz + 255) / 256;
+    // (chunks of <= zmax planes: the two-CTA kernels keep per-chunk z tables in shared memory)
+    const char* zenv = std::getenv("MFREG_ZC_MAX");
+    const int zmax = zenv ? std::max(4, std::atoi(zenv)) : 128;  // measured: longer chunks stream slower
+    int best = (mz + zmax - 1) / zmax;
     double best_cost = 1e300;
-    // (chunks of <= 256 planes: the two-CTA kernels keep per-chunk z tables in shared memory)
-    for (int ntz = (mz + 255) / 256; ntz <= std::max((mz + 255) / 256, mz / 4); ++ntz) {
+    for (int ntz = (mz + zmax - 1) / zmax; ntz <= std::max((mz + zmax - 1) / zmax, mz / 4); ++ntz) {
         const int zc = (mz + ntz - 1) / ntz;
         const int real_ntz = (mz + zc - 1) / zc;
         const double waves = std::ceil(static_cast<double>(nxy * real_ntz) / (2 * kSMs));

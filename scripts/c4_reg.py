@@ -5,7 +5,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1804_10541_b200 as P
 
-m = tuple(int(v) for v in sys.argv[1:4]) if len(sys.argv) > 3 else (512, 512, 900)
+args = [a for a in sys.argv[1:] if not a.startswith("--")]
+m = tuple(int(v) for v in args[:3]) if len(args) >= 3 else (512, 512, 900)
+mode = P.Mode.FAST32 if "--fast32" in sys.argv else P.Mode.FAST
 img = P.make_image_grid(m, (1.0, 1.0, 1.0))
 t0 = time.perf_counter()
 R = P.make_phantom(img, device=True)
@@ -13,7 +15,8 @@ R.mul_(1000.0)
 T = P.warp_sinusoid(R, img, 3.0, 42)
 torch.cuda.synchronize()
 print(f"inputs {m}: {time.perf_counter() - t0:.2f} s, {torch.cuda.memory_allocated() / 1e9:.1f} GB")
-cfg = P.MultilevelConfig(levels=3, deform_ratio=4, method=P.Method.GAUSS_NEWTON, mode=P.Mode.FAST)
+cfg = P.MultilevelConfig(levels=3, deform_ratio=4, method=P.Method.GAUSS_NEWTON, mode=mode)
+print("mode", "FAST32" if mode == P.Mode.FAST32 else "FAST")
 for rep in range(2):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
