@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
     ap.add_argument("--no-gn", action="store_true", help="skip the full GN registration timing")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-c4", action="store_true", help="skip the 512x512x900 (C4) registrations")
     return ap.parse_args()
 
 
@@ -313,6 +314,52 @@ def run_ours(args, rank, world, local):
               "final_J": levels[-1][0][-1].j if levels[-1][0] else None,
               "reference_cpu_s_8thr_container": 519.0}
 
+    # the optional fp32 mode (FAST32) on the same workload: operator rate and kernel times
+    fast32 = None
+    if mode == P.Mode.FAST and world == 1:
+        o32 = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.Mode.FAST32)
+        for _ in range(3):
+            o32.eval(y, grad)
+            o32.gn_hessian_vec(p, q)
+        torch.cuda.synchronize()
+        ev32 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for a_, b_ in ev32:
+            flush.zero_()
+            a_.record()
+            o32.eval(y, grad)
+            o32.gn_hessian_vec(p, q)
+            b_.record()
+        torch.cuda.synchronize()
+        ms32 = statistics.mean(a_.elapsed_time(b_) for a_, b_ in ev32)
+        reps = max(5, args.steps)
+        k32 = {"hv_pass": o32.profile_kernel(0, p, reps), "eval_pass": o32.profile_kernel(1, p, reps),
+               "warp": o32.profile_kernel(2, y, reps)}
+        fast32 = {"value": 2.0 * n / (ms32 * 1e-3) / 1e9, "unit": "Gvoxel/s", "ms_per_step": ms32,
+                  "kernels_ms": k32, "tolerance": "max-rel 1e-4 vs reference (tests/test_gpu_fast32.py)",
+                  "algorithmic_bytes_per_voxel_hv": 20.0,
+                  "hv_frac": 20.0 * n / (k32["hv_pass"] * 1e-3) / 1e9 / peak}
+        del o32
+
+    # north-star case C4: full 3-level GN registration of a 512x512x900 pair on this GPU,
+    # fp64 (FAST) and the optional fp32 mode (FAST32); wall clock from the host
+    gn_c4 = None
+    if not args.no_c4 and world == 1 and mode == P.Mode.FAST:
+        gn_c4 = {"image": [512, 512, 900], "levels": LEVELS, "method": "gauss-newton"}
+        img4 = P.make_image_grid((512, 512, 900), H)
+        R4 = P.make_phantom(img4, device=True)
+        R4.mul_(1000.0)
+        T4 = P.warp_sinusoid(R4, img4, 3.0, 42)
+        for name, md in (("fast", P.Mode.FAST), ("fast32", P.Mode.FAST32)):
+            cfg4 = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, _, lv4 = P.register_multilevel(R4, T4, img4, cfg4)
+            torch.cuda.synchronize()
+            gn_c4[name] = {"wall_s": time.perf_counter() - t0, "outer_iters": [len(t) for t, _ in lv4],
+                           "cg_iters": int(sum(r.cg_iters for t, _ in lv4 for r in t)),
+                           "final_J": lv4[-1][0][-1].j if lv4[-1][0] else None}
+        del R4, T4
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
@@ -331,7 +378,8 @@ def run_ours(args, rank, world, local):
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv,
                 "gvox_s_grad_eval": n / (ms_eval * 1e-3) / 1e9, "gvox_s_gn_hv": n / (ms_hv * 1e-3) / 1e9,
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "gn_registration": gn}
+                "clocks": clocks, "gn_registration": gn, "gn_registration_c4": gn_c4,
+                "fast32": fast32}
         print(json.dumps(line), flush=True)
 
 
