@@ -100,7 +100,7 @@ __device__ __forceinline__ Coef<Real> ngf_coef(const FArgs& a, Real dR0, Real dR
 }
 
 template <typename Real>
-__global__ void __launch_bounds__(NT, 2) k_ev2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
+__global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
     using G = Geo<Real>;
     constexpr int XO = G::XO, SX = G::SX, NS = G::NS, SLOT_R = G::SLOT_R, SLOT_T = G::SLOT_T, SLOT_D = G::SLOT_D,
                   SLOT = G::SLOT;

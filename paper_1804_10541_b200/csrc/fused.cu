@@ -896,7 +896,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     fin_lo_ = full ? 0 : std::min(own_lo_, bz[out_lo_]);
     fin_hi_ = full ? msz : std::max(own_hi_, bz[out_hi_ - 1] + 2);
     // z chunking: minimise waves x (planes per chunk + 4 halo planes), waves of the
-    // Hv kernel (2 CTAs/SM; the eval kernel then runs two waves of half the height)
+    // two-CTA Hv kernel (the eval kernel runs 2 CTAs/SM in fp64, 3 in FAST32)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
     const int mz = t.zhi - t.zlo;
     // (chunks of <= zmax planes: the two-CTA kernels keep per-chunk z tables in shared memory)
