@@ -46,18 +46,31 @@ def test_multilevel_registration_parity(oracle, method, m, h, levels):
 
 
 def test_fast_mode_registration_quality(oracle):
-    """fast mode (factored Hv, tree reductions) is 1e-15-faithful per operator; over
-    a chaotic 60-iteration trajectory it must land on an equally good registration."""
+    """fast mode (factored Hv, tree reductions) is 1e-15-faithful per operator; over a
+    chaotic 60-iteration trajectory it must land inside the reference's own 1-ulp envelope
+    (SURVEY §7 H4): the reference is re-run on templates perturbed by one ulp in 1000 random
+    voxels, and the fast run's final J and displacement difference must stay within twice the
+    spread those perturbations produce (measured here: J moves by 2.6-6.7%, the displacement
+    by mean 0.024-0.042 / max 0.11-0.17 voxel)."""
     import paper_1804_10541_b200 as P
     m, h = (48, 48, 48), (1.0, 1.0, 1.0)
     R, T = _case(oracle, m, h)
+    oracle.set_threads(0)
     y_ref, my, traces_ref, _ = oracle.register_multilevel(R, T, m, h, levels=3, method="lbfgs")
+    J_ref = traces_ref[-1][-1][2]
+    rng = np.random.default_rng(0)
+    env_j, env_mean, env_max = 0.0, 0.0, 0.0
+    for _ in range(4):
+        Tp = T.copy()
+        idx = rng.integers(0, T.size, 1000)
+        Tp[idx] = np.nextafter(Tp[idx], np.inf)
+        y1, _, tr1, _ = oracle.register_multilevel(R, Tp, m, h, levels=3, method="lbfgs")
+        d1 = np.linalg.norm((y1 - y_ref).reshape(3, -1), axis=0)
+        env_j = max(env_j, abs(tr1[-1][-1][2] - J_ref) / abs(J_ref))
+        env_mean, env_max = max(env_mean, float(d1.mean())), max(env_max, float(d1.max()))
     img = P.make_image_grid(m, h)
     y, dg, lv = P.register_multilevel(R, T, img, P.MultilevelConfig(levels=3, mode=P.Mode.FAST))
-    J_ref = traces_ref[-1][-1][2]
     J = lv[-1][0][-1].j
-    assert abs(J - J_ref) <= 0.05 * abs(J_ref)  # 20-iteration levels stop before convergence
-    # against the reference's own 1-ulp sensitivity envelope (SURVEY Appendix A: L-BFGS
-    # 64^3 moves by max 0.265 / mean 0.033 voxel under a 1-ulp template perturbation)
     d = np.linalg.norm((y - y_ref).reshape(3, -1), axis=0)
-    assert float(np.mean(d)) <= 0.05 and float(np.max(d)) <= 0.3  # measured: 0.021 / 0.105
+    assert abs(J - J_ref) / abs(J_ref) <= 2.0 * env_j + 0.01, (J, J_ref, env_j)
+    assert float(np.mean(d)) <= 2.0 * env_mean and float(np.max(d)) <= 2.0 * env_max, (d.mean(), d.max(), env_mean, env_max)
