@@ -106,6 +106,56 @@ def config_case(o: Oracle, name, m, h, ratio, method, max_iters):
     print(f"cfg_{name}: {method} iters={len(trace)} lsf={lsf} J={trace[-1][2] if trace else None}")
 
 
+def sinusoid_displacement(terms, extent, pts):
+    """synthetic.cpp:91-107 SinusoidWarp::displacement at (N, 3) points (numpy restatement)."""
+    amp, freq, phase = terms
+    x = pts / np.asarray(extent)[None, :]
+    u = np.zeros_like(pts)
+    for t in range(amp.shape[0]):
+        w = np.ones(len(pts))
+        for a in range(3):
+            w = w * np.sin(np.pi * freq[t][a] * x[:, a] + phase[t][a] * x[:, a] * (1.0 - x[:, a]))
+        for d in range(3):
+            u[:, d] += amp[t][d] * w
+    return u
+
+
+def c3_landmarks(o: Oracle, m, h, count=300, seed=3):
+    """300 seeded landmark voxels; moving = phi^-1(fixed) by the fixed-point inversion of
+    tests/acceptance.cpp:476-487 (40 iterations of q = p - u(q))."""
+    extent = [m[a] * h[a] for a in range(3)]
+    terms = o.sinusoid_terms(extent, 3.0, 42)
+    rng = np.random.default_rng(seed)
+    idx = rng.integers(0, m, (count, 3))
+    fixed = (idx + 0.5) * np.asarray(h)
+    q = fixed.copy()
+    for _ in range(40):
+        q = fixed - sinusoid_displacement(terms, extent, q)
+    return fixed, q
+
+
+def c3_case(o: Oracle):
+    """BASELINE configs[2] (C3): DIR-Lab-shaped 256x256x100, h = (0.97, 0.97, 2.5), 4-level
+    L-BFGS, landmark-style check: trace, y hash and the landmark errors
+    (io::landmark_error before / after) of the unmodified reference."""
+    import hashlib
+    m, h = (256, 256, 100), (0.97, 0.97, 2.5)
+    ref = o.make_phantom(m, h) * 1000.0
+    tpl = o.warp_sinusoid(ref, m, h, 3.0, 42)
+    y, my, traces, lsf = o.register_multilevel(ref, tpl, m, h, levels=4, method="lbfgs")
+    hy = o.make_deform_grid(m, h, my)
+    fixed, moving = c3_landmarks(o, m, h)
+    before = o.io_landmark_error(fixed, moving, nodal_coords(my, hy), my, hy)
+    after = o.io_landmark_error(fixed, moving, y, my, hy)
+    flat = np.array([r for t in traces for r in t], dtype=np.float64)
+    np.savez_compressed(os.path.join(OUT, "c3_lbfgs.npz"), m=np.array(m), h=np.array(h), my=np.array(my), levels=4,
+                        trace=flat, level_iters=np.array([len(t) for t in traces]), lsf=np.array(lsf),
+                        y_sha=hashlib.sha256(y.tobytes()).hexdigest(), ref_sha=hashlib.sha256(ref.tobytes()).hexdigest(),
+                        tpl_sha=hashlib.sha256(tpl.tobytes()).hexdigest(), lm_before=np.array(before[:2]),
+                        lm_after=np.array(after[:2]), fixed=fixed, moving=moving)
+    print(f"c3_lbfgs: iters={[len(t) for t in traces]} landmark error {before[0]:.4f} -> {after[0]:.4f}")
+
+
 def multilevel_case(o: Oracle, name, m, h, levels, method, max_iters):
     m, h = tuple(m), tuple(h)
     ref = o.make_phantom(m, h) * 1000.0
@@ -126,6 +176,7 @@ def main():
         o.set_threads(os.cpu_count() or 1)
         config_case(o, "c1", (256, 256, 1), (1.0, 1.0, 1.0), 4, "gn", 20)
         config_case(o, "c1p", (256, 256, 8), (1.0, 1.0, 1.0), 4, "gn", 3)
+        c3_case(o)
         return
     o = Oracle("ref")
     o.set_threads(1)
@@ -144,6 +195,7 @@ def main():
     o.set_threads(os.cpu_count() or 1)  # the reference's results are thread-count invariant
     config_case(o, "c1", (256, 256, 1), (1.0, 1.0, 1.0), 4, "gn", 20)
     config_case(o, "c1p", (256, 256, 8), (1.0, 1.0, 1.0), 4, "gn", 3)
+    c3_case(o)
 
 
 if __name__ == "__main__":
