@@ -27,3 +27,16 @@ for name, mode in (("fast", P.Mode.FAST), ("fast32", P.Mode.FAST32)):
     kh = obj.profile_kernel(0, p, 5, 0); ke = obj.profile_kernel(1, p, 5, 0); kw = obj.profile_kernel(2, y, 5, 0)
     print(f"{name}: create {tc*1e3:.0f} ms, eval {te*1e3:.2f} ms, hv {th*1e3:.3f} ms | kernels hv {kh:.3f} ev {ke:.3f} warp {kw:.3f} ms", flush=True)
     del obj
+
+# one CG solve (50 iterations) at the finest level, and the Armijo value-only eval
+obj = P.Objective(R, T, img, dg, P.NgfParams(), 1.0, P.Mode.FAST)
+g = torch.empty_like(y)
+obj.eval(y, g)
+b = -g
+torch.cuda.synchronize(); t0 = time.perf_counter()
+x, it, rr, br = P.cg_solve(obj, b, 50, 1e-2)
+torch.cuda.synchronize(); tcg = time.perf_counter() - t0
+torch.cuda.synchronize(); t0 = time.perf_counter()
+for _ in range(5): obj.eval(y)
+torch.cuda.synchronize(); tv = (time.perf_counter() - t0) / 5
+print(f"cg: {it} iterations {tcg*1e3:.1f} ms ({tcg/max(it,1)*1e3:.3f} ms/iter); value-only eval {tv*1e3:.2f} ms", flush=True)
