@@ -294,11 +294,11 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     const int mz = static_cast<int>(img_.m[2]);
     // (sliced: the slab's planes + 3 halo planes, the state of the 2 halo planes the Hv reads)
     const int wlo = sliced_ ? std::max(0, slab_.zlo - 3) : 0, whi = sliced_ ? std::min(mz, slab_.zhi + 3) : -1;
-    warp_state(y, s, wlo, whi);
-    launch_sub(3 * ny, y, xid_.get(), u_.get(), s);
-    // curvature value / gradient on the side stream, overlapping the image pass
+    // curvature value / gradient on the side stream (it needs only y), overlapping the
+    // warp and the image pass
     MFREG_CUDA(cudaEventRecord(ev_fork_, s));
     MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
+    launch_sub(3 * ny, y, xid_.get(), u_.get(), s2_);
     launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
     const idx_t pn = dg_.m[0] * dg_.m[1];
     if (sliced_)  // owned nodal planes only, per component
@@ -310,6 +310,7 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     if (grad && alpha_ != 0.0)
         launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
+    warp_state(y, s, wlo, whi);
     launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
                       static_cast<double*>(ngf_.state_frh()), grad != nullptr, s);
     MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
