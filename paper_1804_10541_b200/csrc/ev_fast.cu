@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         if (grad && i >= ilo && i < ihi) {  // uniform
             const Real* Fi = sF + P * 2 * NT;
             const Real* Ei = sE + P * 2 * TY + ty;
-            const Real ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : 0.0);
+            const Real ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : Real(0));
             const Real z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
             const Real sz = scale * z;  // dT vanishes outside the volume (TMA zero fill)
             const Real* dq = st + SLOT_D + tid;
