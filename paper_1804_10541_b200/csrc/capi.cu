@@ -469,8 +469,12 @@ int mfreg_cu_objective_eval(mfreg_cu_objective* obj, const double* y, double* gr
         if (!y) throw std::invalid_argument("Objective::eval: y length mismatch");
         In yi(y, nd, where, kStream, &obj->stage[0]);
         Out g(grad, nd, where, &obj->stage[1]);
-        const double v = obj->obj->eval(yi.ptr, g.ptr);
-        g.finish(kStream);
+        // one synchronisation: the gradient copy-out rides behind the scalar copy-out
+        obj->obj->eval_begin(yi.ptr, g.ptr);
+        if (where == MFREG_CU_HOST && grad)
+            MFREG_CUDA(cudaMemcpyAsync(grad, g.ptr, nd * sizeof(double), cudaMemcpyDeviceToHost, kStream));
+        MFREG_CUDA(cudaStreamSynchronize(kStream));
+        const double v = obj->obj->eval_end();
         if (j) *j = v;
     });
 }

@@ -147,6 +147,10 @@ Scalars::Scalars(int n) : d_(static_cast<std::size_t>(n)) {
 Scalars::~Scalars() {
     if (h_) cudaFreeHost(h_);
 }
+void Scalars::fetch_async(int n, cudaStream_t s) {
+    MFREG_CUDA(cudaMemcpyAsync(h_, d_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
+}
+
 const double* Scalars::fetch(int n, cudaStream_t s) {
     MFREG_CUDA(cudaMemcpyAsync(h_, d_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
     MFREG_CUDA(cudaStreamSynchronize(s));
@@ -380,15 +384,19 @@ double DeviceObjective::profile_kernel(int which, const double* p, int reps, std
 
 // optimizer.cpp:64-92
 double DeviceObjective::eval(const double* y, double* grad) {
+    eval_begin(y, grad);
+    MFREG_CUDA(cudaStreamSynchronize(s_));
+    return eval_end();
+}
+
+void DeviceObjective::eval_begin(const double* y, double* grad) {
     const idx_t ny = dg_.count();
     if (fused_) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
         graphs_.run({y, grad, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(1)}, s_,
                     [&](cudaStream_t cs) { enqueue_eval_fast(y, grad, cs); });
-        const double* h = sc_.fetch(2, s_);
-        last_distance_ = h[0];
-        last_regularizer_ = h[1];
-        return last_distance_ + last_regularizer_;
+        sc_.fetch_async(2, s_);
+        return;
     }
     ngf_.populate_warp(plan_.view(), y, T_);
     ngf_.value_async(sc_.dev(0));
@@ -402,7 +410,11 @@ double DeviceObjective::eval(const double* y, double* grad) {
         if (alpha_ != 0.0) launch_bilap(dg_, lapu_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, grad, s_);
     }
     check_launch("Objective::eval");
-    const double* h = sc_.fetch(2, s_);
+    sc_.fetch_async(2, s_);
+}
+
+double DeviceObjective::eval_end() {
+    const double* h = sc_.host();
     last_distance_ = h[0];
     last_regularizer_ = h[1];
     return last_distance_ + last_regularizer_;

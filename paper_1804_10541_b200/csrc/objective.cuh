@@ -195,6 +195,9 @@ public:
     double* dev(int i) { return d_.get() + i; }
     // copies [0, n) to host and synchronises the stream
     const double* fetch(int n, cudaStream_t s);
+    // enqueues the copy of [0, n) only; host() is valid after the stream is synchronised
+    void fetch_async(int n, cudaStream_t s);
+    const double* host() const { return h_; }
 
 private:
     DVec d_;
@@ -284,6 +287,10 @@ public:
     ~DeviceObjective() override;
     idx_t dof() const override { return 3 * dg_.count(); }
     double eval(const double* y, double* grad) override;
+    // eval split for host-buffer callers: enqueue everything (incl. the scalar copy-out),
+    // let the caller enqueue its own copies, synchronise once, then read J
+    void eval_begin(const double* y, double* grad);
+    double eval_end();
     void gn_hessian_vec(const double* p, double* q) override;
     void seed_hessian_vec(const double* p, double gamma, double* q) override;
     double min_spacing() const override;
