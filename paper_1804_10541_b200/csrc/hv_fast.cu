@@ -114,8 +114,8 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     // item-1 interpolants, x-collapsed rows (Real) | int tables
     Real* const stg = reinterpret_cast<Real*>(smem_raw);
     unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (32 B)
-    double* const slab = reinterpret_cast<double*>(bars + 4);  // [NSL][nsl] nodal p
-    double* const sry = slab + NSL * nsl;       // [TY]
+    Real* const slab = reinterpret_cast<Real*>(bars + 4);  // [NSL][nsl] nodal p (NSL * nsl is a multiple of 4)
+    double* const sry = reinterpret_cast<double*>(slab + NSL * nsl);  // [TY]
     double* const sZr = sry + TY;               // [zc + 8] rem_z of the planes kfirst ..
     Real* const sS = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [2][NS] by plane parity
     Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
@@ -154,7 +154,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = sm0 * a.P.src.m[1];
     // (offsets within one component plane; component d adds d * ns)
     int slab_off[2], slab_d[2];
-    double slab_v[2] = {0.0, 0.0};
+    Real slab_v[2] = {Real(0), Real(0)};
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
         const int t = tid + u * NT;
@@ -170,16 +170,16 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 #pragma unroll
         for (int u = 0; u < 2; ++u)
             if (slab_off[u] >= 0)
-                slab_v[u] = __ldg(a.p + slab_d[u] * ns + static_cast<long long>(nz) * sm01 + slab_off[u]);
+                slab_v[u] = static_cast<Real>(__ldg(a.p + slab_d[u] * ns + static_cast<long long>(nz) * sm01 + slab_off[u]));
     };
     auto slab_store = [&](int nz) {
-        double* dst = slab + (nz & (NSL - 1)) * nsl;
+        Real* dst = slab + (nz & (NSL - 1)) * nsl;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
             if (slab_off[u] >= 0) dst[tid + u * NT] = slab_v[u];
     };
     auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
-        const double* q = slab + (nz & (NSL - 1)) * nsl + off;
+        const Real* q = slab + (nz & (NSL - 1)) * nsl + off;
         const int pl = nxf * nyf;
         auto v = [&](int i) { return static_cast<Real>(q[i]); };
         o0 = lerp(ry, lerp(rx, v(0), v(1)), lerp(rx, v(nxf), v(nxf + 1)));
@@ -467,7 +467,7 @@ template <typename Real>
 std::size_t smem_bytes(int nlx, int nsl, int zc) {
     using G = Geo<Real>;
     const std::size_t ring = static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 32;
-    const std::size_t dbl = (static_cast<std::size_t>(NSL) * nsl + TY + zc + 8) * sizeof(double);
+    const std::size_t dbl = static_cast<std::size_t>(NSL) * nsl * sizeof(Real) + (TY + zc + 8) * sizeof(double);
     const std::size_t real = (2 * static_cast<std::size_t>(G::NS) + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P +
                               3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real);
     return ring + dbl + real + (TY + zc + 8) * sizeof(int);
