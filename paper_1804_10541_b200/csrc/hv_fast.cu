@@ -119,8 +119,9 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     double* const sZr = sry + TY;               // [zc + 8] rem_z of the planes kfirst ..
     Real* const sS = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [2][NS] by plane parity
     Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
-    Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
-    Real* const sQ1 = sE + 2 * 2 * TY;          // [6][NX_P] item-1 P p at nodal planes bz, bz+1
+    Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
+                                                // then 2 zero entries (the edge-flux slot of inner lanes)
+    Real* const sQ1 = sE + 2 * 2 * TY + 2;      // [6][NX_P] item-1 P p at nodal planes bz, bz+1
     Real* const sQx = sQ1 + 6 * NX_P;           // [3][TY][nlx] (completions >= 2 steps apart)
     int* const sby = reinterpret_cast<int*>(sQx + 3 * TY * nlx);  // [TY]
     int* const sZb = sby + TY;                  // [zc + 8] base_z of the planes kfirst ..
@@ -149,6 +150,11 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         ry = __ldg(&a.P.rem[1][gyc]);
     };
     const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
+    // edge-flux slot of the tile column (lanes 0 / 31 read a ring-1 x edge, the others a zero
+    // slot past both parity halves) and the ring-1 item's coefficient offset toward the tile
+    const int eoff = tx == 0 ? ty : (tx == TX - 1 ? TY + ty : -1);
+    const int cfo = dir1 == 0 ? 1 * NW : (dir1 == 1 ? 0 : (dir1 == 2 ? 3 * NW : 2 * NW));
+    const Real mpx = tx > 0 ? Real(1) : Real(0), mmx = tx + 1 < TX ? Real(1) : Real(0);
 
     // nodal p elements this thread loads (<= 2 per thread; host guarantees nsl <= 2 * NT)
     const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = sm0 * a.P.src.m[1];
@@ -199,6 +205,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // first lane of my segment
     const bool send = lane == 31 || ((starts >> (lane + 1)) & 1u);
 
+    if (tid < 2) sE[4 * TY + tid] = Real(0);
     if (tid < TY) {
         const int gyc = min(y0 + tid, my - 1);
         sby[tid] = __ldg(&a.P.base[1][gyc]) - nyA;
@@ -381,7 +388,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             // x fluxes stay in the warp (one tile row): from lane-1 (+x) and lane+1 (-x)
             const Real fpx = __shfl_up_sync(0xffffffffu, rh[1 * NW] * w, 1);
             const Real fmx = __shfl_down_sync(0xffffffffu, rh[0] * w, 1);
-            gx_new = (tx > 0 ? fpx : Real(0)) + (tx + 1 < TX ? fmx : Real(0));
+            gx_new = fma(mpx, fpx, mmx * fmx);
             if (ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;       // +y flux -> (tx, ty+1)
             if (ty > 0) Fj[NT + tid - TX] = rh[2 * NW] * w;       // -y flux -> (tx, ty-1)
             fzm = rh[4 * NW] * w;
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
             const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
             const Real w = (wa + wb) + wc;
-            const Real cf = dir1 == 0 ? rg[1 * NW] : (dir1 == 1 ? rg[0] : (dir1 == 2 ? rg[3 * NW] : rg[2 * NW]));
+            const Real cf = rg[cfo];
             if (xedge) sE[(1 - P) * 2 * TY + f1] = cf * w;
             else Fj[f1] = cf * w;
         }
@@ -403,8 +410,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         const int i = k - 2;
         if (i >= ilo && i < ihi) {  // uniform
             const Real* Fi = sF + P * 2 * NT;
-            const Real* Ei = sE + P * 2 * TY + ty;
-            const Real ex = tx == 0 ? Ei[0] : (tx == TX - 1 ? Ei[TY] : Real(0));  // ring-1 x edge fluxes
+            const Real ex = sE[eoff >= 0 ? P * 2 * TY + eoff : 4 * TY];  // ring-1 x edge flux (or zero)
             const Real z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
             const Real sz = scale * z;  // dT (TMA zero fill) makes q vanish outside the volume
             const Real q0 = sz * dq[P][0], q1 = sz * dq[P][1], q2 = sz * dq[P][2];
@@ -468,7 +474,7 @@ std::size_t smem_bytes(int nlx, int nsl, int zc) {
     using G = Geo<Real>;
     const std::size_t ring = static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 32;
     const std::size_t dbl = static_cast<std::size_t>(NSL) * nsl * sizeof(Real) + (TY + zc + 8) * sizeof(double);
-    const std::size_t real = (2 * static_cast<std::size_t>(G::NS) + 2 * 2 * NT + 2 * 2 * TY + 6 * NX_P +
+    const std::size_t real = (2 * static_cast<std::size_t>(G::NS) + 2 * 2 * NT + 2 * 2 * TY + 2 + 6 * NX_P +
                               3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real);
     return ring + dbl + real + (TY + zc + 8) * sizeof(int);
 }
