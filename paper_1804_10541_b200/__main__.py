@@ -8,10 +8,16 @@
     python -m paper_1804_10541_b200 eval-landmarks --fixed-landmarks f.txt --moving-landmarks m.txt
                                          --deformation y.def [--spacing sx sy sz]
 
-Same options, defaults and printed keys as the reference (its `selftest` and
-`--threads` have no counterpart: the device path has no CPU worker pool). The
-extra `--mode` selects the execution mode; `parity` (default) reproduces the
-reference's numbers bit for bit.
+    python -m paper_1804_10541_b200 selftest [--seed 1234] [--quick]
+
+Same options, defaults and printed keys as the reference (`--threads` has no
+counterpart: the device path has no CPU worker pool). The extra `--mode`
+selects the execution mode; `parity` (default) reproduces the reference's
+numbers bit for bit. `selftest` runs the reference's self-consistency suites
+(mfreg_cli.cpp:171-296) on the device: the sparse-matrix oracle checks become
+fast-vs-parity checks (the parity objective is the bitwise replica of the
+reference), plus grid-transfer adjointness, GN symmetry / PSD and the
+finite-difference gradient check.
 """
 from __future__ import annotations
 
@@ -87,6 +93,74 @@ def _cmd_eval_landmarks(a) -> int:
     return 0
 
 
+def _cmd_selftest(a) -> int:
+    import paper_1804_10541_b200 as P
+    failures = 0
+
+    def check(name, ok):
+        nonlocal failures
+        sys.stdout.write(f"selftest.{name}: {'pass' if ok else 'FAIL'}\n")
+        failures += 0 if ok else 1
+
+    # 6^3 image, 4^3 nodes, smoothed random volumes, tau = rho = 1 (mfreg_cli.cpp:172-180)
+    rng = np.random.default_rng(a.seed)
+    m = (6, 6, 6)
+    img = P.make_image_grid(m)
+    dg = P.make_deform_grid(img, (4, 4, 4))
+
+    def smooth_random():
+        v = rng.uniform(0.0, 1.0, m[::-1])
+        p = np.pad(v, 1, mode="edge")
+        s_ = (p[1:-1, 1:-1, 1:-1] + p[:-2, 1:-1, 1:-1] + p[2:, 1:-1, 1:-1] + p[1:-1, :-2, 1:-1] + p[1:-1, 2:, 1:-1]
+              + p[1:-1, 1:-1, :-2] + p[1:-1, 1:-1, 2:]) / 7.0
+        return np.ascontiguousarray(s_.ravel())
+
+    R, T = smooth_random(), smooth_random()
+    objs = {md: P.Objective(R, T, img, dg, P.NgfParams(1.0, 1.0), 1.0, md) for md in (P.Mode.PARITY, P.Mode.FAST)}
+    y = objs[P.Mode.PARITY].identity() + rng.uniform(-0.3, 0.3, 3 * dg.count())
+    grads = {}
+    for md, o in objs.items():
+        g = np.empty(o.dof())
+        o.eval(y, g)
+        grads[md] = g
+    scale = max(1.0, float(np.max(np.abs(grads[P.Mode.PARITY]))))
+    check("parity-gradient", float(np.max(np.abs(grads[P.Mode.FAST] - grads[P.Mode.PARITY]))) <= 1e-12 * scale)
+    p = rng.uniform(-0.3, 0.3, y.size)
+    qp = objs[P.Mode.PARITY].gn_hessian_vec(p)
+    qf = objs[P.Mode.FAST].gn_hessian_vec(p)
+    scale = max(1.0, float(np.max(np.abs(qp))))
+    check("parity-hvp", float(np.max(np.abs(qf - qp))) <= 1e-12 * scale)
+    w = rng.uniform(-0.3, 0.3, 3 * img.count())
+    a_ = float(np.dot(P.transfer_apply(dg, img, y), w))
+    b_ = float(np.dot(y, P.transfer_apply_transpose(dg, img, w)))
+    check("transfer-adjoint", abs(a_ - b_) <= 1e-12 * max(1.0, abs(a_)))
+    obj = objs[P.Mode.PARITY]
+    sym = psd = True
+    for _ in range(3 if a.quick else 10):
+        p = rng.uniform(-0.3, 0.3, y.size)
+        r = rng.uniform(-0.3, 0.3, y.size)
+        q, hq = obj.gn_hessian_vec(p), obj.gn_hessian_vec(r)
+        sym = sym and abs(float(q @ r) - float(p @ hq)) <= 1e-12 * max(1.0, abs(float(q @ r)))
+        psd = psd and float(q @ p) >= -1e-10 * float(p @ p)
+    check("gn-symmetry", sym)
+    check("gn-psd", psd)
+    if not a.quick:
+        g = np.empty(obj.dof())
+        obj.eval(y, g)
+        ok = True
+        for _ in range(5):
+            v = rng.uniform(-0.3, 0.3, y.size)
+            gv = float(g @ v)
+            best = 1e9
+            for eps in (1e-4, 1e-5, 1e-6):
+                fp, fm = obj.eval(y + eps * v), obj.eval(y - eps * v)
+                best = min(best, abs((fp - fm) / (2.0 * eps) - gv) / max(1e-12, abs(gv)))
+            ok = ok and best <= 1e-6
+        check("gradient-fd", ok)
+    sys.stdout.write(f"selftest.failures: {failures}\n")
+    return 0 if failures == 0 else 1
+
+
 def main(argv=None) -> int:
     ap = argparse.ArgumentParser(prog="paper_1804_10541_b200",
                                  description="Deformable 3D image registration (NGF + curvature), B200 path")
@@ -113,9 +187,13 @@ def main(argv=None) -> int:
     e.add_argument("--moving-landmarks", required=True)
     e.add_argument("--deformation", required=True)
     e.add_argument("--spacing", type=float, nargs=3, default=[1.0, 1.0, 1.0])
+    st = sub.add_parser("selftest", help="run built-in derivative verification suites")
+    st.add_argument("--seed", type=int, default=1234)
+    st.add_argument("--quick", action="store_true")
     a = ap.parse_args(argv)
     try:
-        return {"register": _cmd_register, "warp": _cmd_warp, "eval-landmarks": _cmd_eval_landmarks}[a.cmd](a)
+        return {"register": _cmd_register, "warp": _cmd_warp, "eval-landmarks": _cmd_eval_landmarks,
+                "selftest": _cmd_selftest}[a.cmd](a)
     except Exception as ex:  # the reference CLI: "error: <what>" on stderr, exit 1
         sys.stderr.write(f"error: {ex}\n")
         return 1

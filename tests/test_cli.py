@@ -74,3 +74,12 @@ def test_cli_register_warp_landmarks_match_reference(oracle, tmp_path):
     a = oracle.io_landmark_error(fx, mv, y_ref, my, hy)
     assert r.stdout == (f"command: eval-landmarks\nlandmarks: 50\nerror-before: {b[0]:.6f} +- {b[1]:.6f}\n"
                         f"error-after: {a[0]:.6f} +- {a[1]:.6f}\n")
+
+
+@pytest.mark.gpu
+def test_cli_selftest():
+    r = run_cli("selftest")
+    assert r.returncode == 0, r.stdout + r.stderr
+    for name in ("parity-gradient", "parity-hvp", "transfer-adjoint", "gn-symmetry", "gn-psd", "gradient-fd"):
+        assert f"selftest.{name}: pass" in r.stdout
+    assert r.stdout.endswith("selftest.failures: 0\n")
