@@ -151,6 +151,17 @@ def lib() -> C.CDLL:
     return _lib
 
 
+_FNS: dict = {}
+
+
+def _lib_fn(name: str):
+    """Cached ctypes function object (hot-path calls skip the attribute lookup)."""
+    fn = _FNS.get(name)
+    if fn is None:
+        fn = _FNS[name] = getattr(lib(), name)
+    return fn
+
+
 def exported_symbols() -> list[str]:
     return list(_SIGS)
 
@@ -182,6 +193,8 @@ def _ptr(x):
     """(pointer, where) for a numpy array or a CUDA torch tensor (fp64, contiguous)."""
     if x is None:
         return None, HOST
+    if _F64 is not None and getattr(x, "dtype", None) is _F64 and x.is_cuda and x.is_contiguous():
+        return x.data_ptr(), DEVICE  # fast path
     if _is_torch(x):
         import torch
         if x.dtype != torch.float64 or not x.is_contiguous():
@@ -202,9 +215,18 @@ def _empty_like_kind(ref, n: int):
     return np.empty(n, dtype=np.float64)
 
 
+_F64 = None
+
+
 def _as_input(x, where: int):
     """Make `x` match the location `where` (numpy for host, CUDA tensor for device)."""
+    global _F64
     if where == DEVICE:
+        if _F64 is None:
+            import torch
+            _F64 = torch.float64
+        if x.dtype is _F64 and x.is_cuda and x.is_contiguous():  # fast path: already a CUDA fp64 tensor
+            return x
         import torch
         if _is_torch(x):
             return x.to(device="cuda", dtype=torch.float64).contiguous()
@@ -517,8 +539,10 @@ class Objective:
         if grad is not None and _where_of(grad) != w:
             raise ValueError("y and grad must live on the same side")
         j = C.c_double()
-        _check(lib().mfreg_cu_objective_eval(self._h, _ptr(yy)[0], _ptr(grad)[0] if grad is not None else None, w,
-                                             C.byref(j)))
+        rc = _lib_fn("mfreg_cu_objective_eval")(self._h, _ptr(yy)[0], _ptr(grad)[0] if grad is not None else None, w,
+                                                C.byref(j))
+        if rc:
+            _check(rc)
         return j.value
 
     def last_distance(self) -> float:
@@ -535,7 +559,9 @@ class Objective:
         w = _where_of(p)
         p = _as_input(p, w)
         q = _empty_like_kind(p, self._dof) if q is None else q
-        _check(lib().mfreg_cu_objective_gn_hessian_vec(self._h, _ptr(p)[0], _ptr(q)[0], w))
+        rc = _lib_fn("mfreg_cu_objective_gn_hessian_vec")(self._h, _ptr(p)[0], _ptr(q)[0], w)
+        if rc:
+            _check(rc)
         return q
 
     def profile_kernel(self, which: int, operand, reps: int = 10, flush_bytes: int = 256 << 20) -> float:
