@@ -716,8 +716,6 @@ struct FinArgs {
     int nS;                   // number of device scalars summed into S
     long long fin_lo, nwin;   // finalize nodes [fin_lo, fin_lo + nwin) (per component)
     long long add_lo, add_hi; // nodes where `add` applies and the dot counts (owned)
-    const int* flat;          // per-node partial offsets [node][flat_k] (-1 padded), or null
-    int flat_k;
 };
 
 __device__ __forceinline__ long long clampl(long long v, long long hi) { return v < 0 ? 0 : (v > hi ? hi : v); }
@@ -735,6 +733,7 @@ __device__ __forceinline__ double lapc(const double* __restrict__ u, const Grid&
 }
 
 constexpr int FIN_THREADS = 256;
+constexpr int kFinBlocks = 148 * 8;  // finalize grid cap (grid-stride beyond)
 
 __device__ double block_reduce(double v, double* sh) {
 #pragma unroll
@@ -758,53 +757,54 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     __shared__ bool last;
     if (a.skip && *a.skip) return;  // uniform
     const long long ny = a.gy.count();
-    // one thread per (component, node) of the window: component-major like the nodal vectors
-    const long long tw = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x;
     double r0 = 0.0, r1 = 0.0;
-    if (tw < 3 * a.nwin && a.out) {
-        const int d = static_cast<int>(tw / a.nwin);
-        const long long node = a.fin_lo + (tw - d * a.nwin);
-        const long long t = d * ny + node;
-        const bool owned = node >= a.add_lo && node < a.add_hi;
+    // one thread per node of the window, all three components: a node's per-tile partials are
+    // three adjacent values, so each gather entry is one contiguous 24-byte (12-byte) read and
+    // the per-axis gather tables (a few KB, L1-resident) are walked once per node. Grid-stride
+    // over a capped grid keeps the completion-counter atomics few.
+    if (a.out) {
         const int mx = static_cast<int>(a.gy.m[0]), pn = static_cast<int>(a.gy.m[0] * a.gy.m[1]);
-        const int nz = static_cast<int>(node / pn), rem = static_cast<int>(node - static_cast<long long>(nz) * pn);
-        const int nyy = rem / mx, nx = rem - nyy * mx;
         const TileMeta& tm = a.tm;
-        // operands issued first so their latency overlaps the gather
-        const double addv = (a.add && owned) ? __ldg(a.add + t) : 0.0;
-        const double dotv = (a.dot_a && owned) ? __ldg(a.dot_a + t) : 0.0;
-        double v = 0.0;
-        if (a.flat) {  // flat per-node offset list (one dependent load level)
-            const int4* fl = reinterpret_cast<const int4*>(a.flat + node * a.flat_k);
-            for (int q = 0; q < a.flat_k / 4; ++q) {
-                const int4 o = __ldg(fl + q);
-                if (o.x >= 0) v += static_cast<double>(__ldg(part + o.x + d));
-                if (o.y >= 0) v += static_cast<double>(__ldg(part + o.y + d));
-                if (o.z >= 0) v += static_cast<double>(__ldg(part + o.z + d));
-                if (o.w >= 0) v += static_cast<double>(__ldg(part + o.w + d));
-                if (o.w < 0) break;
+        for (long long tw = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x; tw < a.nwin;
+             tw += static_cast<long long>(gridDim.x) * FIN_THREADS) {
+            const long long node = a.fin_lo + tw;
+            const bool owned = node >= a.add_lo && node < a.add_hi;
+            const int nz = static_cast<int>(node / pn), rem = static_cast<int>(node - static_cast<long long>(nz) * pn);
+            const int nyy = rem / mx, nx = rem - nyy * mx;
+            // operands issued first so their latency overlaps the gather
+            double addv[3] = {0.0, 0.0, 0.0}, dotv[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                if (a.add && owned) addv[d] = __ldg(a.add + d * ny + node);
+                if (a.dot_a && owned) dotv[d] = __ldg(a.dot_a + d * ny + node);
             }
-        } else {
-        // gather lists (independent loads, no dependent index chains)
-        const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
-        const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
-        const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
-        for (int ez = zb; ez < ze; ++ez) {
-            const int2 Z = __ldg(&tm.g_ent[2][ez]);
-            for (int ey = yb; ey < ye; ++ey) {
-                const int2 Y = __ldg(&tm.g_ent[1][ey]);
-                const std::size_t tile_row = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx;
-                const std::size_t loc_row = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx;
-                for (int ex = xb; ex < xe; ++ex) {
-                    const int2 X = __ldg(&tm.g_ent[0][ex]);
-                    v += static_cast<double>(__ldg(part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3 + d));
+            double v[3] = {0.0, 0.0, 0.0};
+            const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
+            const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
+            const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
+            for (int ez = zb; ez < ze; ++ez) {  // CSR order: z tiles, then y, then x (fixed sum order)
+                const int2 Z = __ldg(&tm.g_ent[2][ez]);
+                for (int ey = yb; ey < ye; ++ey) {
+                    const int2 Y = __ldg(&tm.g_ent[1][ey]);
+                    const std::size_t tile_row = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx;
+                    const std::size_t loc_row = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx;
+                    for (int ex = xb; ex < xe; ++ex) {
+                        const int2 X = __ldg(&tm.g_ent[0][ex]);
+                        const PT* q = part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3;
+                        const PT q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+                        v[0] += static_cast<double>(q0);
+                        v[1] += static_cast<double>(q1);
+                        v[2] += static_cast<double>(q2);
+                    }
                 }
             }
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                if (a.add && owned) v[d] += addv[d];
+                a.out[d * ny + node] = v[d];
+                if (a.dot_a && owned) r0 += dotv[d] * v[d];
+            }
         }
-        }
-        if (a.add && owned) v += addv;
-        a.out[t] = v;
-        if (a.dot_a && owned) r0 = dotv * v;
     }
     if (a.sc == nullptr) return;
     r0 = block_reduce(r0, sh);
@@ -920,8 +920,6 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     const int ntl[3] = {t.ntx, t.nty, t.ntz};
     const int org[3] = {0, 0, t.zlo}, end[3] = {static_cast<int>(g.m[0]), static_cast<int>(g.m[1]), t.zhi};
     int nl[3];
-    std::vector<int> hoff[3];
-    std::vector<int2> hent[3];
     for (int a = 0; a < 3; ++a) {
         const auto& base = plan.host_base[a];
         const int ms = static_cast<int>(P.src.m[a]);
@@ -948,44 +946,12 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
             MFREG_CUDA(cudaMemcpy(gent_[a].get(), ent.data(), ent.size() * sizeof(int2), cudaMemcpyHostToDevice));
         t.g_off[a] = goff_[a].get();
         t.g_ent[a] = gent_[a].get();
-        hoff[a] = std::move(off);
-        hent[a] = std::move(ent);
     }
     t.nlx = nl[0];
     t.nly = nl[1];
     t.nlz = nl[2];
     t.part_stride = static_cast<std::size_t>(t.nlz) * t.nly * t.nlx * 3;
     part_.resize(t.part_stride * static_cast<std::size_t>(ntiles()));
-    // flat finalize gather lists: per node, the partial offsets in CSR order (z tiles,
-    // then y, then x), padded with -1 to a multiple of 4 entries (one dependent load
-    // level in the finalize instead of three nested CSR walks)
-    {
-        int kmax[3] = {0, 0, 0};
-        for (int a = 0; a < 3; ++a)
-            for (std::size_t nd = 0; nd + 1 < hoff[a].size(); ++nd) kmax[a] = std::max(kmax[a], hoff[a][nd + 1] - hoff[a][nd]);
-        const int K = ((kmax[0] * kmax[1] * kmax[2] + 3) / 4) * 4;
-        const long long msx = P.src.m[0], msy = P.src.m[1], msz = P.src.m[2], nn = msx * msy * msz;
-        if (part_.size() < (1ull << 31) && K > 0 && static_cast<double>(nn) * K < 4e9) {
-            std::vector<int> flat(static_cast<std::size_t>(nn) * K, -1);
-            for (long long nz = 0; nz < msz; ++nz)
-                for (long long nyy = 0; nyy < msy; ++nyy)
-                    for (long long nx = 0; nx < msx; ++nx) {
-                        int* dst = flat.data() + ((nz * msy + nyy) * msx + nx) * K;
-                        int c = 0;
-                        for (int ez = hoff[2][nz]; ez < hoff[2][nz + 1]; ++ez)
-                            for (int ey = hoff[1][nyy]; ey < hoff[1][nyy + 1]; ++ey)
-                                for (int ex = hoff[0][nx]; ex < hoff[0][nx + 1]; ++ex) {
-                                    const int2 Z = hent[2][ez], Y = hent[1][ey], X = hent[0][ex];
-                                    const std::size_t tile = (static_cast<std::size_t>(Z.x) * t.nty + Y.x) * t.ntx + X.x;
-                                    const std::size_t loc = (static_cast<std::size_t>(Z.y) * t.nly + Y.y) * t.nlx + X.y;
-                                    dst[c++] = static_cast<int>(tile * t.part_stride + loc * 3);
-                                }
-                    }
-            flat_.resize(flat.size());
-            MFREG_CUDA(cudaMemcpy(flat_.get(), flat.data(), flat.size() * sizeof(int), cudaMemcpyHostToDevice));
-            flat_k_ = K;
-        }
-    }
     MFREG_CUDA(cudaMemset(part_.get(), 0, part_.size() * sizeof(double)));
     vpart_.resize(static_cast<std::size_t>(ntiles()));
     const long long ny = P.src.count();
@@ -1185,10 +1151,10 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.nwin = (fp.fin_hi() - fp.fin_lo()) * pn;
     a.add_lo = fp.own_lo() * pn;
     a.add_hi = fp.own_hi() * pn;
-    a.flat = fp.flat();
-    a.flat_k = fp.flat_k();
     note_launch();
-    const unsigned blocks = static_cast<unsigned>(std::max(1LL, (3 * a.nwin + FIN_THREADS - 1) / FIN_THREADS));
+    // value-only calls (no gradient) need one block for the scalars
+    const long long want = spec.out ? (a.nwin + FIN_THREADS - 1) / FIN_THREADS : 1;
+    const unsigned blocks = static_cast<unsigned>(std::max(1LL, std::min(want, static_cast<long long>(kFinBlocks))));
     if (fp.fp32()) k_nodal_finalize<float><<<blocks, FIN_THREADS, 0, s>>>(a);
     else k_nodal_finalize<double><<<blocks, FIN_THREADS, 0, s>>>(a);
 }

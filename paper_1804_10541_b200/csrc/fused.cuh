@@ -54,8 +54,6 @@ public:
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
     int seg_width() const { return segw_; }
-    const int* flat() const { return flat_k_ ? flat_.get() : nullptr; }
-    int flat_k() const { return flat_k_; }
     bool ev2() const { return ev2_; }  // two-CTA/SM eval kernel (ev_fast.cu)
     std::size_t ev2_smem() const { return ev2_smem_; }
     const void* maps_ev2() const { return maps_ev2_; }
@@ -90,8 +88,6 @@ private:
     std::size_t hv2_smem_ = 0;
     int segw_ = 32;
     bool ev2_ = false;
-    DevArray<int> flat_;
-    int flat_k_ = 0;
     std::size_t ev2_smem_ = 0;
     alignas(64) unsigned char maps_ev2_[3 * 128];
     alignas(64) unsigned char maps_hv2_[3 * 128];

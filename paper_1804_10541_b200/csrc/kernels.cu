@@ -562,50 +562,67 @@ __global__ void k_inf_norm(idx_t n, const double* __restrict__ a, double scale, 
     if ((threadIdx.x & 31) == 0 && m > 0.0) atomicMax(out, static_cast<unsigned long long>(__double_as_longlong(m)));
 }
 
-// curvature.cpp:9-21 — ((u- - 2u) + u+) / (h*h) summed over x, y, z from 0.0
-__device__ __forceinline__ double lap_at(const double* __restrict__ u, const Grid& g, idx_t x, idx_t y, idx_t z) {
-    const double ui = u[g.lin(x, y, z)];
+// curvature.cpp:9-21 — ((u- - 2u) + u+) / (h*h) summed over x, y, z from 0.0.
+// The quotient by h*h is the IEEE division; when every h*h is a power of two (the usual
+// unit image spacing and power-of-two deformation ratios) the multiply by its exact
+// reciprocal is the same correctly rounded value and replaces the division (P2).
+struct LapGeo {
+    int mx, my, mz, pn;
+    double hh[3];   // RN(h*h) as the reference forms it
+    double ihh[3];  // 1 / hh, exact when P2
+};
+
+template <bool P2>
+__device__ __forceinline__ double lap_div(double v, double hh, double ihh) {
+    if constexpr (P2) return v * ihh;
+    else return v / hh;
+}
+
+template <bool P2>
+__device__ __forceinline__ double lap_at(const double* __restrict__ u, const LapGeo& g, int x, int y, int z, int i) {
+    const double ui = __ldg(&u[i]);
+    const int ox0 = x > 0 ? 1 : 0, ox1 = x < g.mx - 1 ? 1 : 0;
+    const int oy0 = y > 0 ? g.mx : 0, oy1 = y < g.my - 1 ? g.mx : 0;
+    const int oz0 = z > 0 ? g.pn : 0, oz1 = z < g.mz - 1 ? g.pn : 0;
     double s = 0.0;
-    {
-        const double h = g.h[0];
-        s += (u[g.lin(clampi(x - 1, g.m[0] - 1), y, z)] - 2.0 * ui + u[g.lin(clampi(x + 1, g.m[0] - 1), y, z)]) /
-             (h * h);
-    }
-    {
-        const double h = g.h[1];
-        s += (u[g.lin(x, clampi(y - 1, g.m[1] - 1), z)] - 2.0 * ui + u[g.lin(x, clampi(y + 1, g.m[1] - 1), z)]) /
-             (h * h);
-    }
-    {
-        const double h = g.h[2];
-        s += (u[g.lin(x, y, clampi(z - 1, g.m[2] - 1))] - 2.0 * ui + u[g.lin(x, y, clampi(z + 1, g.m[2] - 1))]) /
-             (h * h);
-    }
+    s += lap_div<P2>(__ldg(&u[i - ox0]) - 2.0 * ui + __ldg(&u[i + ox1]), g.hh[0], g.ihh[0]);
+    s += lap_div<P2>(__ldg(&u[i - oy0]) - 2.0 * ui + __ldg(&u[i + oy1]), g.hh[1], g.ihh[1]);
+    s += lap_div<P2>(__ldg(&u[i - oz0]) - 2.0 * ui + __ldg(&u[i + oz1]), g.hh[2], g.ihh[2]);
     return s;
 }
 
-__global__ void k_lap3(Grid g, const double* __restrict__ u, double* __restrict__ out) {
-    idx_t x, y, z;
-    if (!coords(g, x, y, z)) return;
-    const idx_t n = g.count(), i = g.lin(x, y, z);
+__device__ __forceinline__ bool lap_coords(const LapGeo& g, int& x, int& y, int& z, int& i) {
+    x = static_cast<int>(blockIdx.x) * BX + threadIdx.x;
+    y = static_cast<int>(blockIdx.y) * BY + threadIdx.y;
+    z = blockIdx.z;
+    i = x + y * g.mx + z * g.pn;
+    return x < g.mx && y < g.my;
+}
+
+template <bool P2>
+__global__ void __launch_bounds__(BX * BY) k_lap3(LapGeo g, const double* __restrict__ u, double* __restrict__ out) {
+    int x, y, z, i;
+    if (!lap_coords(g, x, y, z, i)) return;
+    const long long n = static_cast<long long>(g.pn) * g.mz;
 #pragma unroll
-    for (int d = 0; d < 3; ++d) out[d * n + i] = lap_at(u + d * n, g, x, y, z);
+    for (int d = 0; d < 3; ++d) out[d * n + i] = lap_at<P2>(u + d * n, g, x, y, z, i);
 }
 
 // curvature.cpp:53-72 second pass (+ the alpha axpy of optimizer.cpp:84-89/98-103,
 // or the gamma shift of optimizer.cpp:106-111)
-__global__ void k_bilap(Grid g, const double* __restrict__ lu, double scale, int mode, double alpha, double gamma,
-                        const double* __restrict__ p, double* __restrict__ out) {
-    idx_t x, y, z;
-    if (!coords(g, x, y, z)) return;
-    const idx_t n = g.count(), i = g.lin(x, y, z);
+template <bool P2, int MODE>
+__global__ void __launch_bounds__(BX * BY) k_bilap(LapGeo g, const double* __restrict__ lu, double scale, double alpha,
+                                                   double gamma, const double* __restrict__ p, double* __restrict__ out) {
+    int x, y, z, i;
+    if (!lap_coords(g, x, y, z, i)) return;
+    const long long n = static_cast<long long>(g.pn) * g.mz;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
-        const double v = scale * lap_at(lu + d * n, g, x, y, z);
-        const idx_t o = d * n + i;
-        if (mode == 0) out[o] = v;
-        else if (mode == 1) out[o] += alpha * v;
-        else out[o] = v + gamma * p[o];
+        const double v = scale * lap_at<P2>(lu + d * n, g, x, y, z, i);
+        const long long o = d * n + i;
+        if constexpr (MODE == 0) out[o] = v;
+        else if constexpr (MODE == 1) out[o] += alpha * v;
+        else out[o] = v + gamma * __ldg(&p[o]);
     }
 }
 
@@ -937,12 +954,41 @@ void launch_inf_norm(idx_t n, const double* a, double scale, double* out, cudaSt
     note_launch(), k_inf_norm<<<nb, 256, 0, s>>>(n, a, scale, reinterpret_cast<unsigned long long*>(out));
 }
 
-void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s) {
-    note_launch(), k_lap3<<<grid3(g), block3(), 0, s>>>(g, u, out);
+static bool lap_geo(const Grid& g, LapGeo& o) {
+    o.mx = static_cast<int>(g.m[0]);
+    o.my = static_cast<int>(g.m[1]);
+    o.mz = static_cast<int>(g.m[2]);
+    o.pn = o.mx * o.my;
+    bool p2 = true;
+    for (int a = 0; a < 3; ++a) {
+        o.hh[a] = g.h[a] * g.h[a];
+        int e = 0;
+        p2 = p2 && std::frexp(o.hh[a], &e) == 0.5 && e > -1000 && e < 1000;
+        o.ihh[a] = 1.0 / o.hh[a];
+    }
+    return p2;
 }
+
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s) {
+    LapGeo lg;
+    if (lap_geo(g, lg)) note_launch(), k_lap3<true><<<grid3(g), block3(), 0, s>>>(lg, u, out);
+    else note_launch(), k_lap3<false><<<grid3(g), block3(), 0, s>>>(lg, u, out);
+}
+
+template <bool P2>
+static void launch_bilap_t(const Grid& g, const LapGeo& lg, const double* lap_u, double scale, int mode, double alpha,
+                           double gamma, const double* p, double* out, cudaStream_t s) {
+    if (mode == 0) k_bilap<P2, 0><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
+    else if (mode == 1) k_bilap<P2, 1><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
+    else k_bilap<P2, 2><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
+}
+
 void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
                   const double* p, double* out, cudaStream_t s) {
-    note_launch(), k_bilap<<<grid3(g), block3(), 0, s>>>(g, lap_u, scale, mode, alpha, gamma, p, out);
+    LapGeo lg;
+    note_launch();
+    if (lap_geo(g, lg)) launch_bilap_t<true>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
+    else launch_bilap_t<false>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
 }
 void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s) {
     note_launch(), k_curv_finalize<<<1, 1, 0, s>>>(S3, cellvol, alpha, out);
