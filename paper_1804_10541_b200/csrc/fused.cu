@@ -732,8 +732,8 @@ __device__ __forceinline__ double lapc(const double* __restrict__ u, const Grid&
     return s;
 }
 
-constexpr int FIN_THREADS = 256;
-constexpr int kFinBlocks = 148 * 8;  // finalize grid cap (grid-stride beyond)
+constexpr int FIN_THREADS = 128;
+constexpr int kFinBlocks = 148 * 16;  // finalize grid cap (grid-stride beyond)
 
 __device__ double block_reduce(double v, double* sh) {
 #pragma unroll
@@ -750,7 +750,10 @@ __device__ double block_reduce(double v, double* sh) {
     return v;
 }
 
-template <typename PT>  // partial element type (fp32 partials in FAST32 mode)
+// PT: partial element type (fp32 partials in FAST32 mode); K: compile-time bound on the
+// gather entries per node per axis (fully unrolled, predicated: every load of a node is in
+// flight at once), 0 = dynamic loops
+template <typename PT, int K>
 __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     const PT* const part = reinterpret_cast<const PT*>(a.part);
     __shared__ double sh[32];
@@ -782,21 +785,36 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
             const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
             const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
             const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
-            for (int ez = zb; ez < ze; ++ez) {  // CSR order: z tiles, then y, then x (fixed sum order)
-                const int2 Z = __ldg(&tm.g_ent[2][ez]);
-                for (int ey = yb; ey < ye; ++ey) {
-                    const int2 Y = __ldg(&tm.g_ent[1][ey]);
-                    const std::size_t tile_row = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx;
-                    const std::size_t loc_row = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx;
-                    for (int ex = xb; ex < xe; ++ex) {
-                        const int2 X = __ldg(&tm.g_ent[0][ex]);
-                        const PT* q = part + (tile_row + X.x) * tm.part_stride + (loc_row + X.y) * 3;
-                        const PT q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
-                        v[0] += static_cast<double>(q0);
-                        v[1] += static_cast<double>(q1);
-                        v[2] += static_cast<double>(q2);
-                    }
+            auto entry = [&](int2 Z, int2 Y, int2 X) {
+                const std::size_t tile = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx + X.x;
+                const std::size_t loc = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx + X.y;
+                const PT* q = part + tile * tm.part_stride + loc * 3;
+                const PT q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
+                v[0] += static_cast<double>(q0);
+                v[1] += static_cast<double>(q1);
+                v[2] += static_cast<double>(q2);
+            };
+            // CSR order: z tiles, then y, then x (fixed sum order)
+            if constexpr (K > 0) {
+                int2 Z[K], Y[K], X[K];
+#pragma unroll
+                for (int k = 0; k < K; ++k) {
+                    Z[k] = zb + k < ze ? __ldg(&tm.g_ent[2][zb + k]) : make_int2(0, 0);
+                    Y[k] = yb + k < ye ? __ldg(&tm.g_ent[1][yb + k]) : make_int2(0, 0);
+                    X[k] = xb + k < xe ? __ldg(&tm.g_ent[0][xb + k]) : make_int2(0, 0);
                 }
+#pragma unroll
+                for (int kz = 0; kz < K; ++kz)
+#pragma unroll
+                    for (int ky = 0; ky < K; ++ky)
+#pragma unroll
+                        for (int kx = 0; kx < K; ++kx)
+                            if (zb + kz < ze && yb + ky < ye && xb + kx < xe) entry(Z[kz], Y[ky], X[kx]);
+            } else {
+                for (int ez = zb; ez < ze; ++ez)
+                    for (int ey = yb; ey < ye; ++ey)
+                        for (int ex = xb; ex < xe; ++ex)
+                            entry(__ldg(&tm.g_ent[2][ez]), __ldg(&tm.g_ent[1][ey]), __ldg(&tm.g_ent[0][ex]));
             }
 #pragma unroll
             for (int d = 0; d < 3; ++d) {
@@ -938,6 +956,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
             for (int k = 0; k < ntl[a]; ++k)
                 if (n0[k] <= nd && nd <= n1[k]) ent.push_back(make_int2(k, nd - n0[k]));
             off[nd + 1] = static_cast<int>(ent.size());
+            gmax_ = std::max(gmax_, off[nd + 1] - off[nd]);
         }
         goff_[a].resize(ms + 1);
         gent_[a].resize(std::max<std::size_t>(1, ent.size()));
@@ -1155,8 +1174,14 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     // value-only calls (no gradient) need one block for the scalars
     const long long want = spec.out ? (a.nwin + FIN_THREADS - 1) / FIN_THREADS : 1;
     const unsigned blocks = static_cast<unsigned>(std::max(1LL, std::min(want, static_cast<long long>(kFinBlocks))));
-    if (fp.fp32()) k_nodal_finalize<float><<<blocks, FIN_THREADS, 0, s>>>(a);
-    else k_nodal_finalize<double><<<blocks, FIN_THREADS, 0, s>>>(a);
+    const bool k2 = fp.gather_max() <= 2;
+    if (fp.fp32()) {
+        if (k2) k_nodal_finalize<float, 2><<<blocks, FIN_THREADS, 0, s>>>(a);
+        else k_nodal_finalize<float, 0><<<blocks, FIN_THREADS, 0, s>>>(a);
+    } else {
+        if (k2) k_nodal_finalize<double, 2><<<blocks, FIN_THREADS, 0, s>>>(a);
+        else k_nodal_finalize<double, 0><<<blocks, FIN_THREADS, 0, s>>>(a);
+    }
 }
 
 }  // namespace mfreg_b200

@@ -54,6 +54,7 @@ public:
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
     int seg_width() const { return segw_; }
+    int gather_max() const { return gmax_; }  // max finalize gather entries per node per axis
     bool ev2() const { return ev2_; }  // two-CTA/SM eval kernel (ev_fast.cu)
     std::size_t ev2_smem() const { return ev2_smem_; }
     const void* maps_ev2() const { return maps_ev2_; }
@@ -87,6 +88,7 @@ private:
     bool hv2_ = false;
     std::size_t hv2_smem_ = 0;
     int segw_ = 32;
+    int gmax_ = 0;
     bool ev2_ = false;
     std::size_t ev2_smem_ = 0;
     alignas(64) unsigned char maps_ev2_[3 * 128];
