@@ -5,6 +5,10 @@
 #include <cmath>
 #include <deque>
 
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+
 #include "cg.cuh"
 #include "objective.cuh"
 
@@ -22,6 +26,15 @@ bool should_stop(const OptimizerConfig& cfg, double g0, double min_hy, double j_
     if (std::abs(j_prev - j_cur) <= cfg.tol_rel_j * std::max(1.0, std::abs(j_prev))) return true;
     if (step_inf <= cfg.tol_step * min_hy) return true;
     return false;
+}
+
+// MFREG_TRACE_TIME=1: per-iteration host wall split of the Gauss-Newton loop on stderr
+bool trace_time() {
+    static const bool on = [] {
+        const char* e = std::getenv("MFREG_TRACE_TIME");
+        return e && *e && *e != '0';
+    }();
+    return on;
 }
 
 // optimizer.cpp:156-175 with phi(eta) = J(y + eta d), value-only evaluation
@@ -70,8 +83,10 @@ MinimizeResult gauss_newton_minimize(DeviceProblem& P, const double* y0, double*
             out.trace.push_back(rec);
             break;
         }
+        const auto t_cg = std::chrono::steady_clock::now();
         launch_neg(n, grad.get(), b.get(), s);
         const CgResult sol = cg_solve(P, 0, 0.0, b.get(), dir.get(), cfg.cg);
+        const auto t_ls = std::chrono::steady_clock::now();
         rec.cg_iters = sol.iters;
         const double gdotd = P.dot(grad.get(), dir.get());
         const double dinf = P.inf_norm(dir.get(), 1.0);
@@ -86,8 +101,15 @@ MinimizeResult gauss_newton_minimize(DeviceProblem& P, const double* y0, double*
         const double j_prev = j;
         launch_axpy_to(n, y, eta, dir.get(), y, s);
         const double step_inf = P.inf_norm(dir.get(), eta);
+        const auto t_ev = std::chrono::steady_clock::now();
         j = P.eval(y, grad.get());
         out.trace.push_back(rec);
+        if (trace_time()) {
+            const auto t_end = std::chrono::steady_clock::now();
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            std::fprintf(stderr, "gn it %d: cg %d iters %.2f ms, line search eta %.3g %.2f ms, eval %.2f ms\n", it,
+                         sol.iters, ms(t_cg, t_ls), eta, ms(t_ls, t_ev), ms(t_ev, t_end));
+        }
         if (should_stop(cfg, g0, min_hy, j_prev, j, P.norm(grad.get()), step_inf)) break;
     }
     return out;
