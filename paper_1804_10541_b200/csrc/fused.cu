@@ -752,8 +752,9 @@ __device__ double block_reduce(double v, double* sh) {
 
 // PT: partial element type (fp32 partials in FAST32 mode); K: compile-time bound on the
 // gather entries per node per axis (fully unrolled, predicated: every load of a node is in
-// flight at once), 0 = dynamic loops
-template <typename PT, int K>
+// flight at once), 0 = dynamic loops; C: components per thread (3: one thread per node; 1: one
+// thread per (node, component), for small windows where one thread per node leaves the SMs idle)
+template <typename PT, int K, int C>
 __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     const PT* const part = reinterpret_cast<const PT*>(a.part);
     __shared__ double sh[32];
@@ -761,38 +762,42 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
     if (a.skip && *a.skip) return;  // uniform
     const long long ny = a.gy.count();
     double r0 = 0.0, r1 = 0.0;
-    // one thread per node of the window, all three components: a node's per-tile partials are
-    // three adjacent values, so each gather entry is one contiguous 24-byte (12-byte) read and
-    // the per-axis gather tables (a few KB, L1-resident) are walked once per node. Grid-stride
-    // over a capped grid keeps the completion-counter atomics few.
+    // C = 3: one thread per node of the window, all three components: a node's per-tile partials
+    // are three adjacent values, so each gather entry is one contiguous 24-byte (12-byte) read
+    // and the per-axis gather tables (a few KB, L1-resident) are walked once per node. C = 1:
+    // consecutive threads take the components of one node (same tables, adjacent partials).
+    // Grid-stride over a capped grid keeps the completion-counter atomics few.
     if (a.out) {
         const int mx = static_cast<int>(a.gy.m[0]), pn = static_cast<int>(a.gy.m[0] * a.gy.m[1]);
         const TileMeta& tm = a.tm;
-        for (long long tw = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x; tw < a.nwin;
+        const long long nthr = a.nwin * (3 / C);
+        for (long long tw = static_cast<long long>(blockIdx.x) * FIN_THREADS + threadIdx.x; tw < nthr;
              tw += static_cast<long long>(gridDim.x) * FIN_THREADS) {
-            const long long node = a.fin_lo + tw;
+            const long long node = a.fin_lo + (C == 3 ? tw : tw / 3);
+            const int d0 = C == 3 ? 0 : static_cast<int>(tw - (tw / 3) * 3);
             const bool owned = node >= a.add_lo && node < a.add_hi;
             const int nz = static_cast<int>(node / pn), rem = static_cast<int>(node - static_cast<long long>(nz) * pn);
             const int nyy = rem / mx, nx = rem - nyy * mx;
             // operands issued first so their latency overlaps the gather
-            double addv[3] = {0.0, 0.0, 0.0}, dotv[3] = {0.0, 0.0, 0.0};
+            double addv[C], dotv[C], v[C];
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                if (a.add && owned) addv[d] = __ldg(a.add + d * ny + node);
-                if (a.dot_a && owned) dotv[d] = __ldg(a.dot_a + d * ny + node);
+            for (int c = 0; c < C; ++c) {
+                addv[c] = (a.add && owned) ? __ldg(a.add + (d0 + c) * ny + node) : 0.0;
+                dotv[c] = (a.dot_a && owned) ? __ldg(a.dot_a + (d0 + c) * ny + node) : 0.0;
+                v[c] = 0.0;
             }
-            double v[3] = {0.0, 0.0, 0.0};
             const int zb = __ldg(&tm.g_off[2][nz]), ze = __ldg(&tm.g_off[2][nz + 1]);
             const int yb = __ldg(&tm.g_off[1][nyy]), ye = __ldg(&tm.g_off[1][nyy + 1]);
             const int xb = __ldg(&tm.g_off[0][nx]), xe = __ldg(&tm.g_off[0][nx + 1]);
             auto entry = [&](int2 Z, int2 Y, int2 X) {
                 const std::size_t tile = (static_cast<std::size_t>(Z.x) * tm.nty + Y.x) * tm.ntx + X.x;
                 const std::size_t loc = (static_cast<std::size_t>(Z.y) * tm.nly + Y.y) * tm.nlx + X.y;
-                const PT* q = part + tile * tm.part_stride + loc * 3;
-                const PT q0 = __ldg(q), q1 = __ldg(q + 1), q2 = __ldg(q + 2);
-                v[0] += static_cast<double>(q0);
-                v[1] += static_cast<double>(q1);
-                v[2] += static_cast<double>(q2);
+                const PT* q = part + tile * tm.part_stride + loc * 3 + d0;
+                PT qv[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) qv[c] = __ldg(q + c);
+#pragma unroll
+                for (int c = 0; c < C; ++c) v[c] += static_cast<double>(qv[c]);
             };
             // CSR order: z tiles, then y, then x (fixed sum order)
             if constexpr (K > 0) {
@@ -817,10 +822,10 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
                             entry(__ldg(&tm.g_ent[2][ez]), __ldg(&tm.g_ent[1][ey]), __ldg(&tm.g_ent[0][ex]));
             }
 #pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                if (a.add && owned) v[d] += addv[d];
-                a.out[d * ny + node] = v[d];
-                if (a.dot_a && owned) r0 += dotv[d] * v[d];
+            for (int c = 0; c < C; ++c) {
+                if (a.add && owned) v[c] += addv[c];
+                a.out[(d0 + c) * ny + node] = v[c];
+                if (a.dot_a && owned) r0 += dotv[c] * v[c];
             }
         }
     }
@@ -1172,15 +1177,20 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.add_hi = fp.own_hi() * pn;
     note_launch();
     // value-only calls (no gradient) need one block for the scalars
-    const long long want = spec.out ? (a.nwin + FIN_THREADS - 1) / FIN_THREADS : 1;
+    // one thread per node once that fills the GPU (about 16 resident warps per SM), else one
+    // thread per (node, component)
+    const bool per_node = a.nwin >= static_cast<long long>(kSMs) * 16 * 32;
+    const long long nthr = per_node ? a.nwin : 3 * a.nwin;
+    const long long want = spec.out ? (nthr + FIN_THREADS - 1) / FIN_THREADS : 1;
     const unsigned blocks = static_cast<unsigned>(std::max(1LL, std::min(want, static_cast<long long>(kFinBlocks))));
     const bool k2 = fp.gather_max() <= 2;
+    auto go = [&](auto kern) { kern<<<blocks, FIN_THREADS, 0, s>>>(a); };
     if (fp.fp32()) {
-        if (k2) k_nodal_finalize<float, 2><<<blocks, FIN_THREADS, 0, s>>>(a);
-        else k_nodal_finalize<float, 0><<<blocks, FIN_THREADS, 0, s>>>(a);
+        if (k2) per_node ? go(k_nodal_finalize<float, 2, 3>) : go(k_nodal_finalize<float, 2, 1>);
+        else per_node ? go(k_nodal_finalize<float, 0, 3>) : go(k_nodal_finalize<float, 0, 1>);
     } else {
-        if (k2) k_nodal_finalize<double, 2><<<blocks, FIN_THREADS, 0, s>>>(a);
-        else k_nodal_finalize<double, 0><<<blocks, FIN_THREADS, 0, s>>>(a);
+        if (k2) per_node ? go(k_nodal_finalize<double, 2, 3>) : go(k_nodal_finalize<double, 2, 1>);
+        else per_node ? go(k_nodal_finalize<double, 0, 3>) : go(k_nodal_finalize<double, 0, 1>);
     }
 }
 
