@@ -40,7 +40,7 @@ B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # capture of the same workload (profiles/), or None when not captured for this build
-TRAFFIC = {"hv_pass": 171.57e6, "eval_pass": 145.73e6, "warp": 29.35e6}  # bytes/launch, profiles/r1b_ncu_full.md
+TRAFFIC = {"hv_pass": 171.50e6, "eval_pass": 146.09e6, "warp": 28.23e6}  # bytes/launch, profiles/r1c_ncu_full.md
 METRIC = "NGF+curvature derivative eval Gvoxel/s (%HBM roofline); full GN registration wall s"
 
 
