@@ -710,6 +710,7 @@ struct FinArgs {
     const double* dot_a;
     int value;
     double* sc;
+    double* sc_host;
     double* red;
     unsigned int* counter;
     const int* skip;
@@ -857,6 +858,11 @@ __global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
             double S = 0.0;
             for (int k = 0; a.S && k < a.nS; ++k) S += a.S[k];
             a.sc[1] = a.S ? a.alpha * (a.cell_y * S) : 0.0;  // alpha S
+            if (a.sc_host) {
+                a.sc_host[0] = a.sc[0];
+                a.sc_host[1] = a.sc[1];
+                __threadfence_system();
+            }
         } else {
             a.sc[0] = s0;                             // <dot_a, out>
         }
@@ -1166,6 +1172,7 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     a.dot_a = spec.dot_a;
     a.value = spec.value ? 1 : 0;
     a.sc = spec.sc;
+    a.sc_host = spec.sc_host;
     a.red = fp.red();
     a.counter = fp.counter();
     a.skip = spec.skip;

@@ -126,6 +126,7 @@ struct FinalizeSpec {
     const double* dot_a = nullptr;
     bool value = false;           // eval: D and alpha S into sc[0], sc[1]
     double* sc = nullptr;         // device scalars
+    double* sc_host = nullptr;    // device view of mapped host scalars: value mode also writes D, alpha S there
     const int* skip = nullptr;    // device flag: skip the launch when set
 };
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s);

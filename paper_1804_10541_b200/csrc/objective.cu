@@ -141,7 +141,8 @@ void Reducer::sum(int kind, idx_t n, const double* a, const double* b, double* o
 }
 
 Scalars::Scalars(int n) : d_(static_cast<std::size_t>(n)) {
-    MFREG_CUDA(cudaMallocHost(&h_, n * sizeof(double)));
+    MFREG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_), n * sizeof(double), cudaHostAllocMapped));
+    MFREG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd_), h_, 0));
     MFREG_CUDA(cudaMemset(d_.get(), 0, n * sizeof(double)));
 }
 Scalars::~Scalars() {
@@ -326,6 +327,7 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     f.out = grad;
     f.value = true;
     f.sc = sc_.dev(0);
+    f.sc_host = sc_.host_dev();  // D, alpha S straight to the host (eval_end reads them)
     launch_nodal_finalize(plan_, *fused_, f, s);
     check_launch("Objective::eval (fused)");
 }
@@ -395,8 +397,7 @@ void DeviceObjective::eval_begin(const double* y, double* grad) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
         graphs_.run({y, grad, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(1)}, s_,
                     [&](cudaStream_t cs) { enqueue_eval_fast(y, grad, cs); });
-        sc_.fetch_async(2, s_);
-        return;
+        return;  // the finalize wrote D and alpha S to the mapped host scalars
     }
     ngf_.populate_warp(plan_.view(), y, T_);
     ngf_.value_async(sc_.dev(0));

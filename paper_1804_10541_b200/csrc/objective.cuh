@@ -198,10 +198,14 @@ public:
     // enqueues the copy of [0, n) only; host() is valid after the stream is synchronised
     void fetch_async(int n, cudaStream_t s);
     const double* host() const { return h_; }
+    // device view of the (mapped, pinned) host buffer: a kernel that writes a scalar here
+    // makes it readable by the host after the stream synchronises, with no copy
+    double* host_dev() { return hd_; }
 
 private:
     DVec d_;
     double* h_ = nullptr;
+    double* hd_ = nullptr;
 };
 
 // Abstract problem the device-resident solvers drive (reference Problem,
