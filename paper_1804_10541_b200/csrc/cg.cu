@@ -130,7 +130,33 @@ DeviceCg::DeviceCg(idx_t n) : n_(n), r_(n), p_(n), ap_(n), st_(1), red_(1024), c
 }
 
 DeviceCg::~DeviceCg() {
+    for (auto& g : graphs_)
+        if (g.exec) cudaGraphExecDestroy(g.exec);
+    if (cs_) cudaStreamDestroy(cs_);
     if (host_) cudaFreeHost(host_);
+}
+
+void DeviceCg::window(DeviceProblem& P, int op, double gamma, double* x, const CgConfig& cfg, int w,
+                      bool fused_update) {
+    const idx_t n = n_;
+    cudaStream_t s = P.stream();
+    CgState* st = st_.get();
+    double* scal = reinterpret_cast<double*>(&st->scratch);
+    const unsigned ub = static_cast<unsigned>(std::min<long long>(blocks_for(n, UPD_THREADS), 1024));
+    for (int j = 0; j < w; ++j) {
+        P.apply_dot(op, gamma, p_.get(), ap_.get(), &st->pap, &st->done);
+        note_launch(), k_cg_alpha<<<1, 1, 0, s>>>(st);
+        if (fused_update) {
+            note_launch(), k_cg_update_fused<<<ub, UPD_THREADS, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st,
+                                                                        red_.get(), counter_.get(), cfg.rel_tol);
+        } else {
+            note_launch(), k_cg_update_xr<<<blocks_for(n), 256, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st);
+            P.dot_async(r_.get(), r_.get(), scal);
+            note_launch(), k_cg_beta<<<1, 1, 0, s>>>(st, scal, cfg.rel_tol);
+        }
+        note_launch(), k_cg_update_p<<<blocks_for(n), 256, 0, s>>>(n, r_.get(), p_.get(), st);
+    }
+    MFREG_CUDA(cudaMemcpyAsync(host_, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
 }
 
 CgResult DeviceCg::solve(DeviceProblem& P, int op, double gamma, const double* b, double* x, const CgConfig& cfg,
@@ -146,27 +172,63 @@ CgResult DeviceCg::solve(DeviceProblem& P, int op, double gamma, const double* b
     P.dot_async(b, b, scal);
     note_launch(), k_cg_init<<<1, 1, 0, s>>>(st, scal);
     const bool fused_update = P.fast_reductions();
-    const unsigned ub = static_cast<unsigned>(std::min<long long>(blocks_for(n, UPD_THREADS), 1024));
-    for (int it = 0; it < cfg.max_iters; ++it) {
-        if (it > 0 && it % poll == 0) {
-            MFREG_CUDA(cudaMemcpyAsync(host_, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    // Windows of `poll` iterations between host checks of `done`. When the problem allows it
+    // each window replays one CUDA graph (captured on first use per operator / x / window
+    // length): the small per-iteration kernels then cost no host launch time, which is what
+    // bounds CG on the coarse pyramid levels.
+    const bool graphs = P.cg_graphable();
+    if (cfg.max_iters <= 0) MFREG_CUDA(cudaMemcpyAsync(host_, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
+    for (int it = 0; it < cfg.max_iters;) {
+        const int w = std::min(poll, cfg.max_iters - it);
+        if (it > 0) {
             MFREG_CUDA(cudaStreamSynchronize(s));
             if (host_->done) break;
         }
-        P.apply_dot(op, gamma, p_.get(), ap_.get(), &st->pap, &st->done);
-        note_launch(), k_cg_alpha<<<1, 1, 0, s>>>(st);
-        if (fused_update) {
-            note_launch(), k_cg_update_fused<<<ub, UPD_THREADS, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st,
-                                                                        red_.get(), counter_.get(), cfg.rel_tol);
+        if (!graphs) {
+            window(P, op, gamma, x, cfg, w, fused_update);
         } else {
-            note_launch(), k_cg_update_xr<<<blocks_for(n), 256, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st);
-            P.dot_async(r_.get(), r_.get(), scal);
-            note_launch(), k_cg_beta<<<1, 1, 0, s>>>(st, scal, cfg.rel_tol);
+            GraphEntry* e = nullptr;
+            for (auto& g : graphs_)
+                if (g.P == &P && g.op == op && g.w == w && g.gamma == gamma && g.tol == cfg.rel_tol && g.x == x &&
+                    g.fused == fused_update)
+                    e = &g;
+            if (!e) {
+                if (!cs_) MFREG_CUDA(cudaStreamCreateWithFlags(&cs_, cudaStreamNonBlocking));
+                const long long l0 = launch_counter();
+                MFREG_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
+                P.redirect_stream(cs_);
+                try {
+                    window(P, op, gamma, x, cfg, w, fused_update);
+                } catch (...) {
+                    P.redirect_stream(s);
+                    cudaGraph_t g = nullptr;
+                    cudaStreamEndCapture(cs_, &g);
+                    if (g) cudaGraphDestroy(g);
+                    cudaGetLastError();
+                    throw;
+                }
+                P.redirect_stream(s);
+                cudaGraph_t g = nullptr;
+                MFREG_CUDA(cudaStreamEndCapture(cs_, &g));
+                cudaGraphExec_t ex = nullptr;
+                const cudaError_t err = cudaGraphInstantiate(&ex, g, 0);
+                cudaGraphDestroy(g);
+                MFREG_CUDA(err);
+                const long long nl = launch_counter() - l0;
+                note_launches(-nl);  // counted on every replay instead
+                if (graphs_.size() >= 8) {
+                    cudaGraphExecDestroy(graphs_.front().exec);
+                    graphs_.erase(graphs_.begin());
+                }
+                graphs_.push_back(GraphEntry{&P, op, w, gamma, cfg.rel_tol, x, fused_update, ex, nl});
+                e = &graphs_.back();
+            }
+            MFREG_CUDA(cudaGraphLaunch(e->exec, s));
+            note_launches(e->launches);
         }
-        note_launch(), k_cg_update_p<<<blocks_for(n), 256, 0, s>>>(n, r_.get(), p_.get(), st);
+        it += w;
     }
     check_launch("cg_solve (device)");
-    MFREG_CUDA(cudaMemcpyAsync(host_, st, sizeof(CgState), cudaMemcpyDeviceToHost, s));
     MFREG_CUDA(cudaStreamSynchronize(s));
     CgResult res;
     res.iters = host_->iters;

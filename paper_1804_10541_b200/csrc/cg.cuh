@@ -1,6 +1,8 @@
 // Device-resident CG (see cg.cu).
 #pragma once
 
+#include <vector>
+
 #include "objective.cuh"
 
 namespace mfreg_b200 {
@@ -22,6 +24,19 @@ public:
                    int poll = 8);
 
 private:
+    // `w` CG iterations (device-side early exit once done), then the state copy to host_
+    void window(DeviceProblem& P, int op, double gamma, double* x, const CgConfig& cfg, int w, bool fused_update);
+    struct GraphEntry {
+        const void* P;
+        int op, w;
+        double gamma, tol;
+        double* x;
+        bool fused;
+        cudaGraphExec_t exec;
+        long long launches;
+    };
+    std::vector<GraphEntry> graphs_;
+    cudaStream_t cs_ = nullptr;  // capture stream (the problem's own stream may be the legacy one)
     idx_t n_;
     DVec r_, p_, ap_;
     DevArray<CgState> st_;

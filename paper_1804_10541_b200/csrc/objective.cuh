@@ -127,10 +127,12 @@ public:
     ~GraphCache();
     GraphCache(const GraphCache&) = delete;
     GraphCache& operator=(const GraphCache&) = delete;
+    bool enabled() const { return enabled_; }
     template <class F>
     void run(const Key& k, cudaStream_t s, F&& enqueue) {
-        if (!enabled_) {
-            enqueue(s);
+        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+        if (!enabled_ || (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)) {
+            enqueue(s);  // graphs off, or `s` is being captured by an enclosing graph (CG window)
             return;
         }
         Entry* e = find(k);
@@ -238,6 +240,11 @@ public:
         else gn_hessian_vec(p, q);
         dot_async(p, q, pq_dev);
     }
+    // the CG loop may be captured into CUDA graphs (everything apply_dot / dot_async enqueue
+    // is device work on stream(), no host synchronisation or allocation)
+    virtual bool cg_graphable() const { return false; }
+    // route the problem's work to `s` (the CG graph capture stream) until redirected back
+    virtual void redirect_stream(cudaStream_t s) { (void)s; }
     // device-resident CG workspace (created on first use)
     class DeviceCg& cg_workspace();
 
@@ -306,6 +313,8 @@ public:
     cudaStream_t stream() const override { return s_; }
     void dot_async(const double* a, const double* b, double* out_dev) override;
     bool fast_reductions() const override { return fused_ != nullptr; }
+    bool cg_graphable() const override { return fused_ != nullptr && !sliced_ && graphs_.enabled(); }
+    void redirect_stream(cudaStream_t s) override { s_ = s; }
     void apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) override;
     const double* identity_dev() const { return xid_.get(); }
     const Grid& image_grid() const { return img_; }
