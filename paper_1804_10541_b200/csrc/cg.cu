@@ -84,7 +84,17 @@ __global__ void __launch_bounds__(UPD_THREADS) k_cg_update_fused(long long n, co
     __shared__ double sh[32];
     __shared__ bool last;
     if (st->done) return;  // uniform: every block sees the same flag (set only by a previous launch)
-    const double alpha = st->alpha;
+    // k_cg_alpha folded in: every block applies the same test to the same <p, Ap>
+    const double pap = st->pap;
+    if (!isfinite(pap) || pap <= 0.0) {  // optimizer.cpp:127-131
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            st->breakdown = !isfinite(pap) ? 1 : 0;
+            st->done = 1;
+        }
+        return;
+    }
+    const double alpha = st->rr / pap;
+    if (blockIdx.x == 0 && threadIdx.x == 0) st->alpha = alpha;
     double acc = 0.0;
     for (long long i = static_cast<long long>(blockIdx.x) * UPD_THREADS + threadIdx.x; i < n;
          i += static_cast<long long>(gridDim.x) * UPD_THREADS) {
@@ -120,6 +130,53 @@ __global__ void __launch_bounds__(UPD_THREADS) k_cg_update_fused(long long n, co
     }
 }
 
+// small systems (coarse pyramid levels): the whole CG update in one block — alpha test,
+// x += alpha p, r -= alpha Ap, <r, r> (fixed-order block tree), the beta logic and
+// p = r + beta p — one launch instead of three
+constexpr int SMALL_THREADS = 1024;
+constexpr long long kSmallN = 4 * 1024;
+__global__ void __launch_bounds__(SMALL_THREADS) k_cg_step_small(long long n, double* __restrict__ p,
+                                                                 const double* __restrict__ ap, double* __restrict__ x,
+                                                                 double* __restrict__ r, CgState* st, double tol) {
+    __shared__ double sh[32];
+    __shared__ int go;
+    if (st->done) return;
+    const double pap = st->pap;
+    if (!isfinite(pap) || pap <= 0.0) {
+        if (threadIdx.x == 0) {
+            st->breakdown = !isfinite(pap) ? 1 : 0;
+            st->done = 1;
+        }
+        return;
+    }
+    const double alpha = st->rr / pap;
+    double acc = 0.0;
+    for (long long i = threadIdx.x; i < n; i += SMALL_THREADS) {
+        x[i] += alpha * p[i];
+        const double ri = r[i] - alpha * ap[i];
+        r[i] = ri;
+        acc = fma(ri, ri, acc);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = sh[threadIdx.x];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) {
+            st->alpha = alpha;
+            cg_beta_logic(st, v, tol);
+            go = st->done ? 0 : 1;
+        }
+    }
+    __syncthreads();
+    if (!go) return;
+    const double beta = st->beta;
+    for (long long i = threadIdx.x; i < n; i += SMALL_THREADS) p[i] = r[i] + beta * p[i];
+}
+
 inline unsigned blocks_for(long long n, int t = 256) { return static_cast<unsigned>((n + t - 1) / t); }
 
 }  // namespace
@@ -145,11 +202,16 @@ void DeviceCg::window(DeviceProblem& P, int op, double gamma, double* x, const C
     const unsigned ub = static_cast<unsigned>(std::min<long long>(blocks_for(n, UPD_THREADS), 1024));
     for (int j = 0; j < w; ++j) {
         P.apply_dot(op, gamma, p_.get(), ap_.get(), &st->pap, &st->done);
-        note_launch(), k_cg_alpha<<<1, 1, 0, s>>>(st);
+        if (fused_update && n <= kSmallN) {
+            note_launch(), k_cg_step_small<<<1, SMALL_THREADS, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st,
+                                                                       cfg.rel_tol);
+            continue;
+        }
         if (fused_update) {
             note_launch(), k_cg_update_fused<<<ub, UPD_THREADS, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st,
                                                                         red_.get(), counter_.get(), cfg.rel_tol);
         } else {
+            note_launch(), k_cg_alpha<<<1, 1, 0, s>>>(st);
             note_launch(), k_cg_update_xr<<<blocks_for(n), 256, 0, s>>>(n, p_.get(), ap_.get(), x, r_.get(), st);
             P.dot_async(r_.get(), r_.get(), scal);
             note_launch(), k_cg_beta<<<1, 1, 0, s>>>(st, scal, cfg.rel_tol);
