@@ -226,6 +226,7 @@ CgResult DeviceCg::solve(DeviceProblem& P, int op, double gamma, const double* b
     const idx_t n = n_;
     cudaStream_t s = P.stream();
     CgState* st = st_.get();
+    P.prepare_operator();  // outside any capture: the window graphs replay the operator as is
     MFREG_CUDA(cudaMemsetAsync(x, 0, n * sizeof(double), s));
     MFREG_CUDA(cudaMemcpyAsync(r_.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     MFREG_CUDA(cudaMemcpyAsync(p_.get(), b, n * sizeof(double), cudaMemcpyDeviceToDevice, s));

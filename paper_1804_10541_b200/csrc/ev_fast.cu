@@ -278,10 +278,11 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
                                      in0 && jin);
             Rm0 = Rj;
             Tm0 = Tj;
-            if (in0 && j >= z0 && j < z1) {  // Hv state of the tile voxel
+            if (in0 && j >= z0 && j < z1) {  // Hv state of the tile voxel (none when value-only lazy)
                 const long long gi = col0 + static_cast<long long>(j) * plane;
+                if (frh_out)
 #pragma unroll
-                for (int d = 0; d < 6; ++d) frh_out[d * n + gi] = cf.e[d];
+                    for (int d = 0; d < 6; ++d) frh_out[d * n + gi] = cf.e[d];
                 if (j >= ilo && j < ihi) dsum += fma(-static_cast<double>(cf.r), static_cast<double>(cf.r), 1.0);
             }
             const Real r = cf.r;

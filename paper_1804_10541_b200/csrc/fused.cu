@@ -468,12 +468,14 @@ __global__ void __launch_bounds__(NTH, 1) k_fused(const __grid_constant__ FArgs 
                 bR_new[3 * NB] = e3;
                 if (tile && j >= z0 && j < z1) {
                     const long long gi = col + static_cast<long long>(j) * plane;
-                    a.frh_out[gi] = e0;
-                    a.frh_out[n + gi] = e1;
-                    a.frh_out[2 * n + gi] = e2;
-                    a.frh_out[3 * n + gi] = e3;
-                    a.frh_out[4 * n + gi] = e4;
-                    a.frh_out[5 * n + gi] = e5;
+                    if (a.frh_out) {  // none when value-only lazy
+                        a.frh_out[gi] = e0;
+                        a.frh_out[n + gi] = e1;
+                        a.frh_out[2 * n + gi] = e2;
+                        a.frh_out[3 * n + gi] = e3;
+                        a.frh_out[4 * n + gi] = e4;
+                        a.frh_out[5 * n + gi] = e5;
+                    }
                     if (j >= ilo && j < ihi) dsum += fma(-r, r, 1.0);
                 }
             }

@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __re
     const long long i = x + static_cast<long long>(yy) * mx + static_cast<long long>(z) * plane,
                     n = static_cast<long long>(plane) * mz;
     Tw[i] = static_cast<OutT>(fma(fz, gzv, cy[0]));
+    if (dT == nullptr) return;  // value-only evaluation: the Hv state is refreshed lazily
     dT[i] = static_cast<OutT>(fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0]);
     dT[n + i] = static_cast<OutT>(fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1]);
     dT[2 * n + i] = static_cast<OutT>(gzv * P.tgt.ih[2]);

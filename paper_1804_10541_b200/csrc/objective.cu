@@ -10,6 +10,8 @@
 
 namespace mfreg_b200 {
 
+bool no_lazy_state();
+
 void check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
@@ -286,16 +288,28 @@ DeviceObjective::~DeviceObjective() {
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
 
 // fast-mode warp into the state arrays of the objective's precision
-void DeviceObjective::warp_state(const double* y, cudaStream_t s, int zlo, int zhi) {
+void DeviceObjective::warp_state(const double* y, cudaStream_t s, int zlo, int zhi, bool state) {
     if (ngf_.fp32())
-        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw32.get(), ngf_.dT32.get(), s, zlo, zhi);
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw32.get(), state ? ngf_.dT32.get() : nullptr, s, zlo, zhi);
     else
-        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), ngf_.dT.get(), s, zlo, zhi);
+        launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), state ? ngf_.dT.get() : nullptr, s, zlo, zhi);
+}
+
+// a14: Hv uses the state of the last eval, value-only included. A lazy value-only
+// eval skipped writing that state (dT, rho-hat); rebuild it at the recorded point.
+void DeviceObjective::refresh_state() {
+    if (!stale_) return;
+    warp_state(ylazy_.get(), s_, 0, -1, true);
+    launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
+                      static_cast<double*>(ngf_.state_frh()), false, s_);
+    check_launch("Objective: Hv state refresh");
+    stale_ = false;
 }
 
 // fast mode: the launch sequence of eval (captured once per (y, grad) into a CUDA graph)
-void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStream_t s) {
+void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStream_t s, bool state) {
     const idx_t ny = dg_.count();
+    if (!state) MFREG_CUDA(cudaMemcpyAsync(ylazy_.get(), y, 3 * ny * sizeof(double), cudaMemcpyDeviceToDevice, s));
     const int mz = static_cast<int>(img_.m[2]);
     // (sliced: the slab's planes + 3 halo planes, the state of the 2 halo planes the Hv reads)
     const int wlo = sliced_ ? std::max(0, slab_.zlo - 3) : 0, whi = sliced_ ? std::min(mz, slab_.zhi + 3) : -1;
@@ -315,9 +329,9 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     if (grad && alpha_ != 0.0)
         launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
-    warp_state(y, s, wlo, whi);
+    warp_state(y, s, wlo, whi, state);
     launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                      static_cast<double*>(ngf_.state_frh()), grad != nullptr, s);
+                      state ? static_cast<double*>(ngf_.state_frh()) : nullptr, grad != nullptr, s);
     MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     FinalizeSpec f;
     f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
@@ -357,6 +371,7 @@ void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* 
 
 double DeviceObjective::profile_kernel(int which, const double* p, int reps, std::size_t flush_bytes) {
     if (!fused_) throw std::logic_error("profile_kernel: fast mode only");
+    refresh_state();
     DevArray<unsigned char> scratch(flush_bytes);
     cudaEvent_t e0, e1;
     MFREG_CUDA(cudaEventCreate(&e0));
@@ -395,8 +410,13 @@ void DeviceObjective::eval_begin(const double* y, double* grad) {
     const idx_t ny = dg_.count();
     if (fused_) {
         if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
-        graphs_.run({y, grad, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(1)}, s_,
-                    [&](cudaStream_t cs) { enqueue_eval_fast(y, grad, cs); });
+        // value-only calls (Armijo trials) skip the Hv state; refresh_state() rebuilds it if an
+        // Hv follows without a gradient evaluation in between
+        const bool lazy = grad == nullptr && !sliced_ && !no_lazy_state();
+        if (lazy && ylazy_.size() < static_cast<std::size_t>(3 * ny)) ylazy_.resize(static_cast<std::size_t>(3 * ny));
+        graphs_.run({y, grad, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(lazy ? 4 : 1)}, s_,
+                    [&](cudaStream_t cs) { enqueue_eval_fast(y, grad, cs, !lazy); });
+        stale_ = lazy;
         return;  // the finalize wrote D and alpha S to the mapped host scalars
     }
     ngf_.populate_warp(plan_.view(), y, T_);
@@ -424,6 +444,7 @@ double DeviceObjective::eval_end() {
 // optimizer.cpp:94-104
 void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
     if (fused_) {
+        refresh_state();
         graphs_.run({p, q, nullptr, nullptr, nullptr, reinterpret_cast<const void*>(2)}, s_,
                     [&](cudaStream_t cs) { enqueue_hv_fast(p, q, nullptr, nullptr, nullptr, cs); });
         return;
@@ -468,8 +489,18 @@ void DeviceObjective::apply_dot(int op, double gamma, const double* p, double* q
         return;
     }
     // fused GN Hv with <p, q> folded into the nodal finalize
+    refresh_state();
     graphs_.run({p, q, pq_dev, skip, nullptr, reinterpret_cast<const void*>(3)}, s_,
                 [&](cudaStream_t cs) { enqueue_hv_fast(p, q, p, pq_dev, skip, cs); });
+}
+
+// MFREG_NO_LAZY_STATE=1: value-only evaluations write the Hv state eagerly (A/B switch)
+bool no_lazy_state() {
+    static const bool off = [] {
+        const char* e = std::getenv("MFREG_NO_LAZY_STATE");
+        return e && e[0] == '1';
+    }();
+    return off;
 }
 
 // ------------------------------------------------------------------ GraphCache

@@ -245,6 +245,8 @@ public:
     virtual bool cg_graphable() const { return false; }
     // route the problem's work to `s` (the CG graph capture stream) until redirected back
     virtual void redirect_stream(cudaStream_t s) { (void)s; }
+    // make the operator's cached state current (called before a CG loop is captured)
+    virtual void prepare_operator() {}
     // device-resident CG workspace (created on first use)
     class DeviceCg& cg_workspace();
 
@@ -315,6 +317,7 @@ public:
     bool fast_reductions() const override { return fused_ != nullptr; }
     bool cg_graphable() const override { return fused_ != nullptr && !sliced_ && graphs_.enabled(); }
     void redirect_stream(cudaStream_t s) override { s_ = s; }
+    void prepare_operator() override { refresh_state(); }
     void apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) override;
     const double* identity_dev() const { return xid_.get(); }
     const Grid& image_grid() const { return img_; }
@@ -329,12 +332,17 @@ public:
     double profile_kernel(int which, const double* p, int reps, std::size_t flush_bytes);
 
 private:
-    void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s);
-    void warp_state(const double* y, cudaStream_t s, int zlo, int zhi);
+    // state=false: value-only evaluation that leaves the Hv state (dT, rho-hat) unwritten and
+    // records y in ylazy_; refresh_state() rebuilds that state before the next Hv needs it
+    void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s, bool state = true);
+    void warp_state(const double* y, cudaStream_t s, int zlo, int zhi, bool state = true);
+    void refresh_state();
     void enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip, cudaStream_t s);
     Grid img_, dg_;
     SlabSpec slab_;
     bool sliced_ = false;
+    bool stale_ = false;  // Hv state belongs to ylazy_, not yet rebuilt (lazy value-only eval)
+    DVec ylazy_;
     double alpha_;
     cudaStream_t s_;
     const double* T_;
