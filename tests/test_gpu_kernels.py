@@ -66,3 +66,38 @@ def test_hv_kernel_variants(P, oracle, case):
     for a_, b_ in zip(res[1], res[0]):
         assert max_rel(a_, b_) <= 1e-12
 
+
+
+@pytest.mark.parametrize("mode", ["FAST", "FAST32"])
+def test_value_only_eval_state_rule(P, oracle, mode):
+    """Hv uses the state of the LAST eval call, value-only included. The fast
+    path skips the state writes on value-only calls and rebuilds the state before the next
+    Hv / CG loop: the result must equal an objective whose last eval at y2 took a gradient."""
+    m, h = (48, 40, 36), (1.0, 1.0, 1.0)
+    R = oracle.make_phantom(m, h) * 1000.0
+    T = oracle.warp_sinusoid(R, m, h, 3.0, 42)
+    img = P.make_image_grid(m, h)
+    dg = P.deformation_grid_for(img, 4)
+    md = getattr(P.Mode, mode)
+    a = P.Objective(R, T, img, dg, P.NgfParams(), 1.0, md)
+    b = P.Objective(R, T, img, dg, P.NgfParams(), 1.0, md)
+    rng = np.random.default_rng(5)
+    y1 = a.identity() + rng.uniform(-0.4, 0.4, a.dof())
+    y2 = a.identity() + rng.uniform(-0.4, 0.4, a.dof())
+    p = rng.uniform(-1, 1, a.dof())
+    g = np.empty(a.dof())
+    a.eval(y1, g)
+    for _ in range(4):  # also through the captured (graph) value-only path
+        j_lazy = a.eval(y2)
+    q_lazy = a.gn_hessian_vec(p)
+    j_full = b.eval(y2, g)
+    q_full = b.gn_hessian_vec(p)
+    assert j_lazy == j_full
+    assert np.array_equal(q_lazy, q_full)
+    # CG after a value-only eval (the state is rebuilt before the window graphs are captured)
+    a.eval(y1, g)
+    a.eval(y2)
+    b.eval(y2, g)
+    xa = P.cg_solve(a, -g, 12, 1e-12)[0]
+    xb = P.cg_solve(b, -g, 12, 1e-12)[0]
+    assert np.array_equal(np.asarray(xa), np.asarray(xb))
