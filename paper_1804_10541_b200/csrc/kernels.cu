@@ -157,8 +157,15 @@ __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __
 // trilinear value / gradient with fused arithmetic (continuous in the cell
 // fraction, so contraction only moves the last bits).
 // (OutT = float: the FAST32 state; the cell choice and P y stay exact fp64)
+// 6 resident blocks (48 warps) per SM: the kernel is global-load latency bound (two levels
+// of dependent gathers, nodal y then the template), so occupancy beats registers — measured
+// 40 regs / 6 blocks: -18% at 128^3, -25% at 512x512x256 against 48 regs / 5 blocks; 7 blocks
+// spill (slower)
+#ifndef MFREG_WARP_MINB
+#define MFREG_WARP_MINB 6
+#endif
 template <typename OutT>
-__global__ void __launch_bounds__(256) k_warp_fast(DevPlan P, const double* __restrict__ y,
+__global__ void __launch_bounds__(256, MFREG_WARP_MINB) k_warp_fast(DevPlan P, const double* __restrict__ y,
                                                    const double* __restrict__ T, OutT* __restrict__ Tw,
                                                    OutT* __restrict__ dT, int zoff) {
     const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
