@@ -758,7 +758,10 @@ __device__ double block_reduce(double v, double* sh) {
 // flight at once), 0 = dynamic loops; C: components per thread (3: one thread per node; 1: one
 // thread per (node, component), for small windows where one thread per node leaves the SMs idle)
 template <typename PT, int K, int C>
-__global__ void __launch_bounds__(FIN_THREADS) k_nodal_finalize(FinArgs a) {
+#ifndef MFREG_FIN_MINB
+#define MFREG_FIN_MINB 8  // 64 registers, 32 warps/SM: the gather is latency bound (C4: -30%)
+#endif
+__global__ void __launch_bounds__(FIN_THREADS, MFREG_FIN_MINB) k_nodal_finalize(FinArgs a) {
     const PT* const part = reinterpret_cast<const PT*>(a.part);
     __shared__ double sh[32];
     __shared__ bool last;
