@@ -77,6 +77,7 @@ __global__ void k_cg_update_p(long long n, const double* __restrict__ r, double*
 // fast mode: x += alpha p, r -= alpha Ap and <r, r> in one pass (fixed-order tree,
 // last block applies the beta logic)
 constexpr int UPD_THREADS = 256;
+constexpr int kTicketGroups = 32;
 __global__ void __launch_bounds__(UPD_THREADS) k_cg_update_fused(long long n, const double* __restrict__ p,
                                                                  const double* __restrict__ ap, double* __restrict__ x,
                                                                  double* __restrict__ r, CgState* st, double* red,
@@ -114,7 +115,17 @@ __global__ void __launch_bounds__(UPD_THREADS) k_cg_update_fused(long long n, co
         if (threadIdx.x == 0) {
             red[blockIdx.x] = v;
             __threadfence();
-            last = atomicAdd(counter, 1u) == gridDim.x - 1;
+            // two-level completion ticket (group counters, then the top one): avoids ~10^3
+            // same-address atomics per launch
+            const unsigned g = blockIdx.x % kTicketGroups, ng = min(gridDim.x, static_cast<unsigned>(kTicketGroups));
+            const unsigned gsize = (gridDim.x - g + kTicketGroups - 1) / kTicketGroups;
+            bool lst = false;
+            if (atomicAdd(counter + 1 + g, 1u) == gsize - 1) {
+                counter[1 + g] = 0u;
+                __threadfence();
+                lst = atomicAdd(counter, 1u) == ng - 1;
+            }
+            last = lst;
         }
     }
     __syncthreads();
@@ -181,9 +192,9 @@ inline unsigned blocks_for(long long n, int t = 256) { return static_cast<unsign
 
 }  // namespace
 
-DeviceCg::DeviceCg(idx_t n) : n_(n), r_(n), p_(n), ap_(n), st_(1), red_(1024), counter_(1) {
+DeviceCg::DeviceCg(idx_t n) : n_(n), r_(n), p_(n), ap_(n), st_(1), red_(1024), counter_(1 + kTicketGroups) {
     MFREG_CUDA(cudaMallocHost(&host_, sizeof(CgState)));
-    MFREG_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
+    MFREG_CUDA(cudaMemset(counter_.get(), 0, (1 + kTicketGroups) * sizeof(unsigned int)));
 }
 
 DeviceCg::~DeviceCg() {

@@ -737,6 +737,7 @@ __device__ __forceinline__ double lapc(const double* __restrict__ u, const Grid&
 
 constexpr int FIN_THREADS = 128;
 constexpr int kFinBlocks = 148 * 16;  // finalize grid cap (grid-stride beyond)
+constexpr int kFinGroups = 32;        // completion-ticket groups (counter_ holds 1 + kFinGroups)
 
 __device__ double block_reduce(double v, double* sh) {
 #pragma unroll
@@ -841,8 +842,17 @@ __global__ void __launch_bounds__(FIN_THREADS, MFREG_FIN_MINB) k_nodal_finalize(
         a.red[2 * blockIdx.x] = r0;
         a.red[2 * blockIdx.x + 1] = r1;
         __threadfence();
-        const unsigned int t = atomicAdd(a.counter, 1u);
-        last = (t == gridDim.x - 1);
+        // two-level completion ticket (kFinGroups group counters, then one top counter): a
+        // single counter serialised ~10^3 same-address atomics per launch (several us)
+        const unsigned g = blockIdx.x % kFinGroups, ng = min(gridDim.x, static_cast<unsigned>(kFinGroups));
+        const unsigned gsize = (gridDim.x - g + kFinGroups - 1) / kFinGroups;
+        bool lst = false;
+        if (atomicAdd(a.counter + 1 + g, 1u) == gsize - 1) {
+            a.counter[1 + g] = 0u;
+            __threadfence();
+            lst = atomicAdd(a.counter, 1u) == ng - 1;
+        }
+        last = lst;
     }
     __syncthreads();
     if (!last) return;
@@ -991,8 +1001,8 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     vpart_.resize(static_cast<std::size_t>(ntiles()));
     const long long ny = P.src.count();
     red_.resize(static_cast<std::size_t>(2 * ((3 * ny + FIN_THREADS - 1) / FIN_THREADS) + 2));
-    counter_.resize(1);
-    MFREG_CUDA(cudaMemset(counter_.get(), 0, sizeof(unsigned int)));
+    counter_.resize(1 + kFinGroups);
+    MFREG_CUDA(cudaMemset(counter_.get(), 0, (1 + kFinGroups) * sizeof(unsigned int)));
     // nodal slab footprint of a tile's halo-2 columns (max over tiles), per axis
     for (int a2 = 0; a2 < 2; ++a2) {
         const auto& base = plan.host_base[a2];

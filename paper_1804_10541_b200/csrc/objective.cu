@@ -4,6 +4,9 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <cstdint>
+#include <string>
+
 #include "objective.cuh"
 #include "cg.cuh"
 #include "fused.cuh"
@@ -11,6 +14,44 @@
 namespace mfreg_b200 {
 
 bool no_lazy_state();
+
+namespace {
+constexpr std::uint64_t kPoolKeepBytes = 16ull << 30;
+cudaMemPool_t default_pool() {
+    int dev = 0;
+    MFREG_CUDA(cudaGetDevice(&dev));
+    cudaMemPool_t pool = nullptr;
+    MFREG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    static thread_local int configured = -1;
+    if (configured != dev) {
+        std::uint64_t keep = kPoolKeepBytes;
+        MFREG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        configured = dev;
+    }
+    return pool;
+}
+}  // namespace
+
+void* device_alloc(std::size_t bytes) {
+    cudaMemPool_t pool = default_pool();
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, 0);
+    if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+        cudaGetLastError();
+        MFREG_CUDA(cudaDeviceSynchronize());
+        MFREG_CUDA(cudaMemPoolTrimTo(pool, 0));
+        e = cudaMallocAsync(&p, bytes, 0);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw CudaError(std::string("cudaMallocAsync(") + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+    }
+    return p;
+}
+
+void device_free(void* p) {
+    if (p) cudaFreeAsync(p, 0);
+}
 
 void check_launch(const char* what) {
     const cudaError_t e = cudaGetLastError();

@@ -37,6 +37,13 @@ void check_launch(const char* what);
 // fp32 mode, tolerance 1e-4); nodal vectors, reductions and solvers stay fp64.
 enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 
+// Device allocations come from the device's default stream-ordered pool (allocated and
+// freed on the legacy stream, which all library work is ordered with) with up to
+// kPoolKeepBytes kept cached: objectives are created per pyramid level and per call, and
+// cudaMalloc/cudaFree of their state cost tens of milliseconds with a wide spread.
+void* device_alloc(std::size_t bytes);
+void device_free(void* p);
+
 // RAII device array of doubles (or raw bytes).
 template <typename T>
 class DevArray {
@@ -63,11 +70,11 @@ public:
     void resize(std::size_t n) {
         if (n == n_) return;
         release();
-        if (n) MFREG_CUDA(cudaMalloc(&p_, n * sizeof(T)));
+        if (n) p_ = static_cast<T*>(device_alloc(n * sizeof(T)));
         n_ = n;
     }
     void release() {
-        if (p_) cudaFree(p_);
+        if (p_) device_free(p_);
         p_ = nullptr;
         n_ = 0;
     }

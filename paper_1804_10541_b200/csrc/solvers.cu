@@ -243,11 +243,19 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
     DVec y, y0;
     Grid prev{};
     bool have_prev = false;
+    auto ms_since = [](std::chrono::steady_clock::time_point t) {
+        return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+    };
     for (int l = cfg.levels - 1; l >= 0; --l) {
+        const auto t_level = std::chrono::steady_clock::now();
         const Grid dg = deformation_grid_for(G[l], cfg.deform_ratio);
         const double* rp = l == 0 ? R_dev : R[l].get();
         const double* tp = l == 0 ? T_dev : T[l].get();
         DeviceObjective obj(rp, tp, G[l], dg, cfg.tau, cfg.rho, cfg.alpha, cfg.mode, s);
+        if (trace_time()) {
+            MFREG_CUDA(cudaStreamSynchronize(s));
+            std::fprintf(stderr, "level %d: objective %.2f ms\n", l, ms_since(t_level));
+        }
         y0.resize(static_cast<std::size_t>(obj.dof()));
         if (have_prev) launch_prolong(prev, dg, y.get(), y0.get(), s);
         else MFREG_CUDA(cudaMemcpyAsync(y0.get(), obj.identity_dev(), obj.dof() * sizeof(double),
@@ -257,6 +265,7 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
         MinimizeResult res = cfg.method == Method::Lbfgs ? lbfgs_minimize(obj, y0.get(), yl.get(), cfg.opt)
                                                          : gauss_newton_minimize(obj, y0.get(), yl.get(), cfg.opt);
         MFREG_CUDA(cudaStreamSynchronize(s));
+        if (trace_time()) std::fprintf(stderr, "level %d: total %.2f ms\n", l, ms_since(t_level));
         y = std::move(yl);
         out.levels.push_back({G[l], dg, std::move(res)});
         prev = dg;

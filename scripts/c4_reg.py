@@ -17,7 +17,7 @@ torch.cuda.synchronize()
 print(f"inputs {m}: {time.perf_counter() - t0:.2f} s, {torch.cuda.memory_allocated() / 1e9:.1f} GB")
 cfg = P.MultilevelConfig(levels=3, deform_ratio=4, method=P.Method.GAUSS_NEWTON, mode=mode)
 print("mode", "FAST32" if mode == P.Mode.FAST32 else "FAST")
-for rep in range(2):
+for rep in range(int(os.environ.get("REPS", "2"))):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     y, dg, levels = P.register_multilevel(R, T, img, cfg)
