@@ -494,15 +494,24 @@ __device__ __forceinline__ double sum_term(int kind, const double* __restrict__ 
     return x * x;
 }
 
-// parallel.cpp:51-73: one thread per 4096-element chunk, sequential partial sum
-__global__ void k_chunks(int kind, idx_t n, const double* __restrict__ a, const double* __restrict__ b,
-                         double* __restrict__ partials) {
-    const idx_t c = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-    const idx_t nch = (n + kChunk - 1) / kChunk;
-    if (c >= nch) return;
+// parallel.cpp:51-73: per 4096-element chunk, the sequential partial sum. One warp per chunk:
+// the lanes evaluate the chunk's terms with coalesced loads into shared memory, then lane 0
+// adds them in index order (bitwise the reference's loop: the terms do not depend on the
+// order, the additions are sequential). One thread per chunk left all but a few SMs idle and
+// read 32 scattered lines per warp load (0.59 ms at 128^3).
+__global__ void __launch_bounds__(32) k_chunks_warp(int kind, idx_t n, const double* __restrict__ a,
+                                                    const double* __restrict__ b, double* __restrict__ partials) {
+    extern __shared__ double terms[];  // [kChunk]
+    const idx_t c = blockIdx.x;
     const idx_t lo = c * kChunk, hi = min(n, lo + kChunk);
+    const int cnt = static_cast<int>(hi - lo), lane = threadIdx.x;
+#pragma unroll 8
+    for (int i = lane; i < cnt; i += 32) terms[i] = sum_term(kind, a, b, lo + i);
+    __syncwarp();
+    if (lane != 0) return;
     double s = 0.0;
-    for (idx_t i = lo; i < hi; ++i) s += sum_term(kind, a, b, i);
+#pragma unroll 16
+    for (int i = 0; i < cnt; ++i) s += terms[i];
     partials[c] = s;
 }
 
@@ -947,7 +956,9 @@ idx_t tree_blocks(idx_t n) { return std::max<idx_t>(1, (n + kTreeSpan - 1) / kTr
 void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                         double scale, cudaStream_t s) {
     const idx_t nch = chunk_count(n);
-    if (nch > 0) note_launch(), k_chunks<<<blocks1(nch, 128), 128, 0, s>>>(kind, n, a, b, partials);
+    if (nch > 0)
+        note_launch(), k_chunks_warp<<<static_cast<unsigned>(nch), 32, kChunk * sizeof(double), s>>>(kind, n, a, b,
+                                                                                                     partials);
     note_launch(), k_serial<<<1, 32, 0, s>>>(partials, nch, scale, out);
 }
 void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
