@@ -236,6 +236,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     auto zbase = [&](int k) { return __ldg(&a.P.base[2][min(max(k, 0), mz - 1)]); };
     auto zrem = [&](int k) { return __ldg(&a.P.rem[2][min(max(k, 0), mz - 1)]); };
 
+    pdl_wait();       // T_w, dT (the warp kernel before this launch) from here on
     __syncthreads();  // tables, barriers
     for (int m = 0; m < RING - 2; ++m)
         if (kfirst + m <= klast) EV2_ISSUE(kfirst + m, m);
@@ -355,6 +356,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         if (k + 1 <= klast) step(Par<1>{}, k + 1);
     }
 #undef EV2_ISSUE
+    pdl_trigger();  // the finalize may be scheduled while the tiles flush
     if (grad) {  // flush: pending y collapse, then the last two nodal planes
         if (ypend >= 0) ycollapse(ypend);
         __syncthreads();
@@ -397,8 +399,8 @@ void ev2_set_smem_cap(int bytes) {
 }
 
 void ev2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
-    if (fp32) k_ev2<float><<<grid, NT, smem, s>>>(a, maps);
-    else k_ev2<double><<<grid, NT, smem, s>>>(a, maps);
+    if (fp32) launch_pdl(k_ev2<float>, grid, dim3(NT), smem, s, a, maps);
+    else launch_pdl(k_ev2<double>, grid, dim3(NT), smem, s, a, maps);
 }
 
 }  // namespace mfreg_b200

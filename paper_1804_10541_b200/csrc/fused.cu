@@ -766,9 +766,10 @@ __global__ void __launch_bounds__(FIN_THREADS, MFREG_FIN_MINB) k_nodal_finalize(
     const PT* const part = reinterpret_cast<const PT*>(a.part);
     __shared__ double sh[32];
     __shared__ bool last;
-    if (a.skip && *a.skip) return;  // uniform
+    if (a.skip && *a.skip) return;  // uniform (set two launches earlier)
     const long long ny = a.gy.count();
     double r0 = 0.0, r1 = 0.0;
+    pdl_wait();  // partials of the image pass, the side-stream curvature term
     // C = 3: one thread per node of the window, all three components: a node's per-tile partials
     // are three adjacent values, so each gather entry is one contiguous 24-byte (12-byte) read
     // and the per-axis gather tables (a few KB, L1-resident) are walked once per node. C = 1:
@@ -1170,6 +1171,14 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     else k_fused<true, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MFREG_NO_PDL");
+        return !(e && e[0] == '1');
+    }();
+    return on;
+}
+
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s) {
     FinArgs a{};
     a.gy = plan.view().src;
@@ -1206,7 +1215,7 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     const long long want = spec.out ? (nthr + FIN_THREADS - 1) / FIN_THREADS : 1;
     const unsigned blocks = static_cast<unsigned>(std::max(1LL, std::min(want, static_cast<long long>(kFinBlocks))));
     const bool k2 = fp.gather_max() <= 2;
-    auto go = [&](auto kern) { kern<<<blocks, FIN_THREADS, 0, s>>>(a); };
+    auto go = [&](auto kern) { launch_pdl(kern, dim3(blocks), dim3(FIN_THREADS), 0, s, a); };
     if (fp.fp32()) {
         if (k2) per_node ? go(k_nodal_finalize<float, 2, 3>) : go(k_nodal_finalize<float, 2, 1>);
         else per_node ? go(k_nodal_finalize<float, 0, 3>) : go(k_nodal_finalize<float, 0, 1>);

@@ -23,6 +23,8 @@
 // per node in a fixed order by the finalize kernel (deterministic, no atomics).
 #pragma once
 
+#include <utility>
+
 #include "objective.cuh"
 
 namespace mfreg_b200 {
@@ -129,6 +131,23 @@ struct FinalizeSpec {
     double* sc_host = nullptr;    // device view of mapped host scalars: value mode also writes D, alpha S there
     const int* skip = nullptr;    // device flag: skip the launch when set
 };
+// cudaLaunchKernelEx with programmatic stream serialisation (MFREG_NO_PDL=1: plain launch)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    MFREG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s);
 
 }  // namespace mfreg_b200

@@ -43,6 +43,13 @@ __device__ __forceinline__ float lerp(float t, float a, float b) { return fmaf(t
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
 
+// Programmatic dependent launch: kernels launched with launch_pdl() may start while the
+// previous kernel in the stream drains; everything that reads that kernel's output must
+// follow pdl_wait() (a no-op for an ordinary launch).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// lets the next (PDL) launch in the stream be scheduled once every CTA of this grid got here
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }

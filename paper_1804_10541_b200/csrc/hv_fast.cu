@@ -283,6 +283,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         }
     };
 
+    pdl_wait();       // p (the CG update before this launch) from here on
     __syncthreads();  // tables, barriers
     // first two nodal planes, synchronously; first two staged planes
     // (the planes steps kfirst .. kfirst+2 read; later steps prefetch one plane each,
@@ -453,6 +454,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         step(Par<0>{}, k);
         if (k + 1 <= klast) step(Par<1>{}, k + 1);
     }
+    pdl_trigger();  // the finalize may be scheduled while the tiles flush
     // ---- flush: pending y collapse, then the last two nodal planes
     if (ypend >= 0) ycollapse(ypend);
     __syncthreads();
@@ -496,8 +498,8 @@ void hv2_set_smem_cap(int bytes) {
 }
 
 void hv2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
-    if (fp32) k_hv2<float><<<grid, NT, smem, s>>>(a, maps);
-    else k_hv2<double><<<grid, NT, smem, s>>>(a, maps);
+    if (fp32) launch_pdl(k_hv2<float>, grid, dim3(NT), smem, s, a, maps);
+    else launch_pdl(k_hv2<double>, grid, dim3(NT), smem, s, a, maps);
 }
 
 }  // namespace mfreg_b200

@@ -168,6 +168,7 @@ template <typename OutT>
 __global__ void __launch_bounds__(256, MFREG_WARP_MINB) k_warp_fast(DevPlan P, const double* __restrict__ y,
                                                    const double* __restrict__ T, OutT* __restrict__ Tw,
                                                    OutT* __restrict__ dT, int zoff) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the eval pass (PDL) may queue behind
     const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
     const int x = blockIdx.x * 32 + threadIdx.x, yy = blockIdx.y * 8 + threadIdx.y;
     const int z = blockIdx.z + zoff;
