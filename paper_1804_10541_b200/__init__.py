@@ -236,6 +236,11 @@ def _as_input(x, where: int):
     return np.ascontiguousarray(x, dtype=np.float64)
 
 
+def _dev_f64(x) -> bool:
+    """x is a contiguous CUDA float64 torch tensor (checked without importing torch)."""
+    return _F64 is not None and getattr(x, "dtype", None) is _F64 and x.is_cuda and x.is_contiguous()
+
+
 def _where_of(*xs) -> int:
     for x in xs:
         if x is not None and _is_torch(x) and x.is_cuda:
@@ -534,6 +539,13 @@ class Objective:
 
     def eval(self, y, grad=None) -> float:
         """J(y); fills `grad` (same kind as y, length dof) when given."""
+        if _dev_f64(y) and (grad is None or _dev_f64(grad)):  # direct path: CUDA fp64 contiguous tensors
+            j = C.c_double()
+            rc = _lib_fn("mfreg_cu_objective_eval")(self._h, y.data_ptr(), grad.data_ptr() if grad is not None else None,
+                                                    DEVICE, C.byref(j))
+            if rc:
+                _check(rc)
+            return j.value
         w = _where_of(y)
         yy = _as_input(y, w)
         if grad is not None and _where_of(grad) != w:
@@ -556,6 +568,11 @@ class Objective:
         return r.value
 
     def gn_hessian_vec(self, p, q=None):
+        if q is not None and _dev_f64(p) and _dev_f64(q):  # direct path: CUDA fp64 contiguous tensors
+            rc = _lib_fn("mfreg_cu_objective_gn_hessian_vec")(self._h, p.data_ptr(), q.data_ptr(), DEVICE)
+            if rc:
+                _check(rc)
+            return q
         w = _where_of(p)
         p = _as_input(p, w)
         q = _empty_like_kind(p, self._dof) if q is None else q
