@@ -16,7 +16,13 @@ namespace mfreg_b200 {
 bool no_lazy_state();
 
 namespace {
-constexpr std::uint64_t kPoolKeepBytes = 16ull << 30;
+// bytes of freed device memory the pool keeps for reuse (MFREG_POOL_KEEP_GB, default 32: one
+// C4 registration's state fits, so a second registration in the process allocates nothing)
+std::uint64_t pool_keep_bytes() {
+    const char* e = std::getenv("MFREG_POOL_KEEP_GB");
+    const double gb = e ? std::atof(e) : 32.0;
+    return static_cast<std::uint64_t>(std::max(0.0, gb) * static_cast<double>(1ull << 30));
+}
 cudaMemPool_t default_pool() {
     int dev = 0;
     MFREG_CUDA(cudaGetDevice(&dev));
@@ -24,7 +30,7 @@ cudaMemPool_t default_pool() {
     MFREG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
     static thread_local int configured = -1;
     if (configured != dev) {
-        std::uint64_t keep = kPoolKeepBytes;
+        std::uint64_t keep = pool_keep_bytes();
         MFREG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
         configured = dev;
     }

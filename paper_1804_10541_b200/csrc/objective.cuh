@@ -39,7 +39,7 @@ enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 
 // Device allocations come from the device's default stream-ordered pool (allocated and
 // freed on the legacy stream, which all library work is ordered with) with up to
-// kPoolKeepBytes kept cached: objectives are created per pyramid level and per call, and
+// MFREG_POOL_KEEP_GB (default 32) kept cached: objectives are created per pyramid level and per call, and
 // cudaMalloc/cudaFree of their state cost tens of milliseconds with a wide spread.
 void* device_alloc(std::size_t bytes);
 void device_free(void* p);
