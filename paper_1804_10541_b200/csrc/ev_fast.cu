@@ -373,10 +373,47 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     for (int o = 16; o > 0; o >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, o);
     if (lane == 0) sred[row] = dsum;
     __syncthreads();
+    // (the last-CTA flag goes to sred[0] once thread 0 has read sred: no static shared memory,
+    // which would push two CTAs past an SM's shared memory at the dynamic-size cap)
+    unsigned int* const s_last = reinterpret_cast<unsigned int*>(sred);
     if (tid == 0) {
         double s = 0.0;
         for (int w = 0; w < NT / 32; ++w) s += sred[w];
         a.vpart[tile_id] = s;
+        if (a.vticket) {  // two-level completion ticket over the CTAs (32 group counters, then one)
+            __threadfence();
+            const unsigned nct = gridDim.x * gridDim.y * gridDim.z, id = static_cast<unsigned>(tile_id);
+            const unsigned g = id % 32u, ng = min(nct, 32u), gsize = (nct - g + 31u) / 32u;
+            unsigned lst = 0;
+            if (atomicAdd(a.vticket + 1 + g, 1u) == gsize - 1) {
+                a.vticket[1 + g] = 0u;
+                __threadfence();
+                lst = atomicAdd(a.vticket, 1u) == ng - 1 ? 1u : 0u;
+            }
+            *s_last = lst;
+        }
+    }
+    if (!a.vticket) return;
+    __syncthreads();
+    if (!*s_last) return;
+    // last CTA: D = h_bar * sum over tiles in tile order per thread, then a fixed tree
+    __threadfence();
+    const unsigned nct = gridDim.x * gridDim.y * gridDim.z;
+    double v = 0.0;
+    for (unsigned t = tid; t < nct; t += NT) v += a.vpart[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();  // sred reuse
+    if (lane == 0) sred[row] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += sred[w];
+        const double d = a.dscale * t;
+        a.dsc[0] = d;
+        a.dsc_host[0] = d;
+        __threadfence_system();
+        a.vticket[0] = 0u;
     }
 }
 

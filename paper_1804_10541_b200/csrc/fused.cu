@@ -1000,6 +1000,8 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     part_.resize(t.part_stride * static_cast<std::size_t>(ntiles()));
     MFREG_CUDA(cudaMemset(part_.get(), 0, part_.size() * sizeof(double)));
     vpart_.resize(static_cast<std::size_t>(ntiles()));
+    vticket_.resize(33);
+    MFREG_CUDA(cudaMemset(vticket_.get(), 0, 33 * sizeof(unsigned int)));
     const long long ny = P.src.count();
     red_.resize(static_cast<std::size_t>(2 * ((3 * ny + FIN_THREADS - 1) / FIN_THREADS) + 2));
     counter_.resize(1 + kFinGroups);
@@ -1147,8 +1149,8 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     else k_fused<false, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
 }
 
-void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
-                       double tau, double rho, double* frh, bool grad, cudaStream_t s) {
+bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
+                       double tau, double rho, double* frh, bool grad, cudaStream_t s, double* d_dev, double* d_host) {
     FArgs a = make_args(plan, fp);
     a.scale = -2.0 * a.g.cell_volume();
     a.tau = tau;
@@ -1162,13 +1164,20 @@ void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, true);
     if (fp.ev2()) {
+        if (d_dev && d_host) {
+            a.vticket = fp.vticket();
+            a.dsc = d_dev;
+            a.dsc_host = d_host;
+            a.dscale = plan.view().tgt.cell_volume();  // h_bar (ngf.cpp:227)
+        }
         ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s,
                    fp.fp32());
-        return;
+        return a.vticket != nullptr;
     }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_ev());
     if (fp.tma()) k_fused<true, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
     else k_fused<true, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
+    return false;
 }
 
 bool pdl_enabled() {

@@ -56,7 +56,8 @@ public:
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
     int seg_width() const { return segw_; }
-    int gather_max() const { return gmax_; }  // max finalize gather entries per node per axis
+    int gather_max() const { return gmax_; }
+    unsigned int* vticket() { return vticket_.get(); }  // max finalize gather entries per node per axis
     bool ev2() const { return ev2_; }  // two-CTA/SM eval kernel (ev_fast.cu)
     std::size_t ev2_smem() const { return ev2_smem_; }
     const void* maps_ev2() const { return maps_ev2_; }
@@ -91,6 +92,7 @@ private:
     std::size_t hv2_smem_ = 0;
     int segw_ = 32;
     int gmax_ = 0;
+    DevArray<unsigned int> vticket_;
     bool ev2_ = false;
     std::size_t ev2_smem_ = 0;
     alignas(64) unsigned char maps_ev2_[3 * 128];
@@ -111,8 +113,11 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
 // Eval image pass on the warped state (T_w, dT from launch_warp): rho-hat (6 per
 // voxel, stored as Hv state), per-tile sums of (1 - r^2) and, when `grad`, the
 // NGF gradient -2h dT (dr^T r) spread by P^T into per-tile partials.
-void launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
-                       double tau, double rho, double* frh, bool grad, cudaStream_t s);
+// d_dev / d_host (optional): with the two-CTA kernel, its last CTA writes D there (returns
+// true); otherwise (legacy kernel) D is left to the finalize (returns false)
+bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
+                       double tau, double rho, double* frh, bool grad, cudaStream_t s, double* d_dev = nullptr,
+                       double* d_host = nullptr);
 
 // Nodal finalize (one launch):
 //   out != null: out = gather(P^T partials) [+ add];

@@ -32,6 +32,12 @@ struct FArgs {
     int dbg;            // profiling switches (0 in production)
     int segw;           // max image columns per nodal x cell (segmented-scan length)
     const int* skip;    // device flag: return immediately when set (CG already converged)
+    // eval (two-CTA kernel): when set, the last CTA to finish sums the per-tile (1 - r^2) in tile
+    // order and writes D = dscale * sum to dsc[0] and the mapped host scalar dsc_host[0]
+    unsigned int* vticket;  // [1 + 32] completion counters
+    double* dsc;
+    double* dsc_host;
+    double dscale;
 };
 
 struct TmaMaps {

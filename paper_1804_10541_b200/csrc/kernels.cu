@@ -644,6 +644,15 @@ __global__ void __launch_bounds__(BX * BY) k_bilap(LapGeo g, const double* __res
     }
 }
 
+// alpha S = alpha (h^y sum (Lap u)^2) into a device scalar and a mapped host scalar (fast eval)
+__global__ void k_curv_value(const double* __restrict__ S, double cellvol, double alpha, double* out_dev,
+                             double* out_host) {
+    const double v = alpha * (cellvol * S[0]);
+    *out_dev = v;
+    *out_host = v;
+    __threadfence_system();
+}
+
 __global__ void k_curv_finalize(const double* __restrict__ S3, double cellvol, double alpha, double* out) {
     double total = 0.0;
     total += S3[0];
@@ -1009,6 +1018,10 @@ void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, do
     note_launch();
     if (lap_geo(g, lg)) launch_bilap_t<true>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
     else launch_bilap_t<false>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
+}
+void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,
+                       cudaStream_t s) {
+    note_launch(), k_curv_value<<<1, 1, 0, s>>>(S, cellvol, alpha, out_dev, out_host);
 }
 void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s) {
     note_launch(), k_curv_finalize<<<1, 1, 0, s>>>(S3, cellvol, alpha, out);

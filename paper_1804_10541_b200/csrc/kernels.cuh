@@ -72,6 +72,8 @@ void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, do
                   const double* p, double* out, cudaStream_t s);
 // curvature value finalize: out = alpha * (cellvol * ((S0 + S1) + S2))
 void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s);
+void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,
+                       cudaStream_t s);
 void launch_add_scalars(const double* a, const double* b, double* out, cudaStream_t s);
 
 // ---- BLAS-1 (exact, element-parallel)

@@ -373,13 +373,28 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
                        sc2_.get() + d, 1.0, s2_);
     else
         red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, s2_);
+    // two-CTA eval kernel (whole domain): D comes from its last CTA and alpha S from the side
+    // stream, both straight into the host scalars; the finalize is then a pure gather
+    const bool scalars_direct = !sliced_ && fused_->ev2();
+    if (scalars_direct) launch_curv_value(sc2_.get(), dg_.cell_volume(), alpha_, sc_.dev(1), sc_.host_dev() + 1, s2_);
     if (grad && alpha_ != 0.0)
         launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
     warp_state(y, s, wlo, whi, state);
     launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                      state ? static_cast<double*>(ngf_.state_frh()) : nullptr, grad != nullptr, s);
+                      state ? static_cast<double*>(ngf_.state_frh()) : nullptr, grad != nullptr, s,
+                      scalars_direct ? sc_.dev(0) : nullptr, scalars_direct ? sc_.host_dev() : nullptr);
     MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
+    if (scalars_direct) {
+        if (grad) {
+            FinalizeSpec f;
+            f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
+            f.out = grad;
+            launch_nodal_finalize(plan_, *fused_, f, s);
+        }
+        check_launch("Objective::eval (fused)");
+        return;
+    }
     FinalizeSpec f;
     f.add = (grad && alpha_ != 0.0) ? curv_.get() : nullptr;
     f.S = sc2_.get();
