@@ -1,0 +1,64 @@
+"""The launch machinery must not change a single bit: CUDA graphs (per-call and CG windows),
+programmatic dependent launches and the lazy Hv state are switched off one at a time
+(MFREG_NO_GRAPHS / MFREG_NO_PDL / MFREG_NO_LAZY_STATE, read once per process, hence the
+subprocesses) and J, the gradient, Hv, a value-only eval followed by Hv, and a CG solve are
+compared bitwise with the default configuration, in fast and fast32 modes."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys
+import numpy as np
+sys.path.insert(0, {root!r})
+import paper_1804_10541_b200 as P
+mode = getattr(P.Mode, {mode!r})
+img = P.make_image_grid((72, 56, 48))
+dg = P.deformation_grid_for(img, 4)
+R = P.make_phantom(img) * 1000.0
+T = P.warp_sinusoid(R, img, 3.0, 42)
+o = P.Objective(R, T, img, dg, P.NgfParams(), 1.0, mode)
+rng = np.random.default_rng(3)
+y = o.identity() + rng.uniform(-0.4, 0.4, o.dof())
+y2 = o.identity() + rng.uniform(-0.4, 0.4, o.dof())
+p = rng.uniform(-1.0, 1.0, o.dof())
+out = []
+for rep in range(4):  # repeats reach the graph-replay paths
+    g = np.empty(o.dof())
+    j = o.eval(y, g)
+    q = o.gn_hessian_vec(p)
+    j2 = o.eval(y2)
+    q2 = o.gn_hessian_vec(p)
+    x = np.asarray(P.cg_solve(o, -g, 20, 1e-12)[0])
+    out.append(np.concatenate([[j, j2], g, q, q2, x]))
+np.save({path!r}, np.stack(out))
+"""
+
+
+def _run(tmp_path, mode, env_extra, tag):
+    path = str(tmp_path / f"{mode}_{tag}.npy")
+    env = dict(os.environ)
+    for k in ("MFREG_NO_GRAPHS", "MFREG_NO_PDL", "MFREG_NO_LAZY_STATE"):
+        env.pop(k, None)
+    env.update(env_extra)
+    code = SCRIPT.format(root=ROOT, mode=mode, path=path)
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    return np.load(path)
+
+
+@pytest.mark.parametrize("mode", ["FAST", "FAST32"])
+def test_launch_modes_bitwise(tmp_path, mode):
+    base = _run(tmp_path, mode, {}, "default")
+    for rep in range(1, base.shape[0]):
+        assert np.array_equal(base[rep], base[0]), f"replay {rep} differs from the first call"
+    for var in ("MFREG_NO_GRAPHS", "MFREG_NO_PDL", "MFREG_NO_LAZY_STATE"):
+        other = _run(tmp_path, mode, {var: "1"}, var)
+        assert np.array_equal(other, base), f"{var}=1 changes the results"
