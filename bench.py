@@ -40,7 +40,7 @@ B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
 # dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
 # capture of the same workload (profiles/), or None when not captured for this build
-TRAFFIC = {"hv_pass": 171.50e6, "eval_pass": 146.09e6, "warp": 28.23e6}  # bytes/launch, profiles/r1c_ncu_full.md
+TRAFFIC = {"hv_pass": 171.05e6, "eval_pass": 147.62e6, "warp": 29.42e6}  # bytes/launch, profiles/r1c_ncu_full.md
 METRIC = "NGF+curvature derivative eval Gvoxel/s (%HBM roofline); full GN registration wall s"
 
 
@@ -123,7 +123,7 @@ class Clocks:
     def summary(self):
         self.f.flush()
         self.f.seek(0)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw = [], None, set(), []
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.f.read().strip().splitlines():
             parts = [x.strip() for x in line.split(",")]
@@ -134,12 +134,16 @@ class Clocks:
                 mx = float(parts[1])
             except ValueError:
                 continue
+            try:
+                pw.append(float(parts[2]))
+            except ValueError:
+                pass
             for nm, v in zip(names, parts[3:7]):
                 if v.lower() == "active":
                     reasons.add(nm)
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+                "samples": len(sm), "sm_mhz_min": min(sm) if sm else None, "power_w_max": max(pw) if pw else None}
 
 
 def measured_hbm_peak():
@@ -353,6 +357,7 @@ def run_ours(args, rank, world, local):
         R4 = P.make_phantom(img4, device=True)
         R4.mul_(1000.0)
         T4 = P.warp_sinusoid(R4, img4, 3.0, 42)
+        ck4 = Clocks(local).__enter__()  # clocks over the C4 runs (sustained load: power cap shows here)
         for name, md in (("fast", P.Mode.FAST), ("fast32", P.Mode.FAST32)):
             cfg4 = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
             walls = []
@@ -365,6 +370,8 @@ def run_ours(args, rank, world, local):
             gn_c4[name] = {"wall_s": walls[0], "wall_s_warm": walls[1], "outer_iters": [len(t) for t, _ in lv4],
                            "cg_iters": int(sum(r.cg_iters for t, _ in lv4 for r in t)),
                            "final_J": lv4[-1][0][-1].j if lv4[-1][0] else None}
+        ck4.__exit__(None, None, None)
+        gn_c4["clocks"] = ck4.summary()
         del R4, T4
 
     cpu = None
