@@ -452,6 +452,139 @@ __global__ void k_hv_closed(Grid g, HvTable tab, double scale, const double* __r
     out[2 * n + i] = scale * qz;
 }
 
+// The offset table of every grid with m_x, m_y >= 5 (kappa order = lexicographic (dz, dy, dx)
+// order of the 25 3-D offsets), built at compile time so the closed-form Hv below runs with
+// immediate offsets and fully unrolled group / pair loops; make_hv_table() output is compared
+// with it on the host and the generic kernel serves every other grid.
+struct CanonHvTable {
+    int ngroups;
+    int dx[25], dy[25], dz[25], npairs[25], pa[25][7], pb[25][7];
+};
+constexpr int cdx(int d) { return d == NEGX ? -1 : (d == POSX ? 1 : 0); }
+constexpr int cdy(int d) { return d == NEGY ? -1 : (d == POSY ? 1 : 0); }
+constexpr int cdz(int d) { return d == NEGZ ? -1 : (d == POSZ ? 1 : 0); }
+constexpr CanonHvTable make_canon_hv_table() {
+    CanonHvTable t{};
+    long long kap[25] = {};
+    int ng = 0;
+    for (int da = 0; da < 7; ++da)
+        for (int db = 0; db < 7; ++db) {
+            const int dx = cdx(db) - cdx(da), dy = cdy(db) - cdy(da), dz = cdz(db) - cdz(da);
+            int e = 0;
+            while (e < ng && !(t.dx[e] == dx && t.dy[e] == dy && t.dz[e] == dz)) ++e;
+            if (e == ng) {
+                t.dx[e] = dx;
+                t.dy[e] = dy;
+                t.dz[e] = dz;
+                kap[e] = dx + 1000LL * dy + 1000000LL * dz;
+                ++ng;
+            }
+            t.pa[e][t.npairs[e]] = da;
+            t.pb[e][t.npairs[e]] = db;
+            ++t.npairs[e];
+        }
+    t.ngroups = ng;
+    for (int i = 1; i < ng; ++i)  // stable insertion sort by kappa (std::stable_sort in make_hv_table)
+        for (int j = i; j > 0 && kap[j] < kap[j - 1]; --j) {
+            const long long tk = kap[j]; kap[j] = kap[j - 1]; kap[j - 1] = tk;
+            int v = t.dx[j]; t.dx[j] = t.dx[j - 1]; t.dx[j - 1] = v;
+            v = t.dy[j]; t.dy[j] = t.dy[j - 1]; t.dy[j - 1] = v;
+            v = t.dz[j]; t.dz[j] = t.dz[j - 1]; t.dz[j - 1] = v;
+            v = t.npairs[j]; t.npairs[j] = t.npairs[j - 1]; t.npairs[j - 1] = v;
+            for (int q = 0; q < 7; ++q) {
+                v = t.pa[j][q]; t.pa[j][q] = t.pa[j - 1][q]; t.pa[j - 1][q] = v;
+                v = t.pb[j][q]; t.pb[j][q] = t.pb[j - 1][q]; t.pb[j - 1][q] = v;
+            }
+        }
+    return t;
+}
+constexpr CanonHvTable kCanonHv = make_canon_hv_table();
+
+bool is_canon_hv_table(const HvTable& t) {
+    if (t.ngroups != kCanonHv.ngroups) return false;
+    for (int e = 0; e < t.ngroups; ++e) {
+        if (t.dx[e] != kCanonHv.dx[e] || t.dy[e] != kCanonHv.dy[e] || t.dz[e] != kCanonHv.dz[e] ||
+            t.npairs[e] != kCanonHv.npairs[e])
+            return false;
+        for (int q = 0; q < t.npairs[e]; ++q)
+            if (t.pa[e][q] != kCanonHv.pa[e][q] || t.pb[e][q] != kCanonHv.pb[e][q]) return false;
+    }
+    return true;
+}
+
+// k_hv_closed with the compile-time table: same groups, pairs, bounds tests and operation
+// order per voxel (bitwise the generic kernel); the group and pair loops are unrolled by
+// template recursion so every table entry is an immediate
+struct CanonCtx {
+    long long i, n, pl;
+    int x, y, z, mx, my, mz;
+    bool ok[7];
+    long long off[7];
+    const double* __restrict__ rh;
+    const double* __restrict__ sv;
+};
+
+template <int E, int Q>
+__device__ __forceinline__ void canon_pairs(const CanonCtx& c, double& drdr) {
+    if constexpr (Q < kCanonHv.npairs[E]) {
+        constexpr int da = kCanonHv.pa[E][Q], db = kCanonHv.pb[E][Q];
+        if (c.ok[db]) {
+            const long long t = c.i + c.off[db];
+            drdr += __ldg(&c.rh[(6 - da) * c.n + t]) * __ldg(&c.rh[(6 - db) * c.n + t]);
+        }
+        canon_pairs<E, Q + 1>(c, drdr);
+    }
+}
+
+template <int E>
+__device__ __forceinline__ void canon_group(const CanonCtx& c, double d0, double d1, double d2, double& qx, double& qy,
+                                            double& qz) {
+    if constexpr (E < kCanonHv.ngroups) {
+        constexpr int DX = kCanonHv.dx[E], DY = kCanonHv.dy[E], DZ = kCanonHv.dz[E];
+        const int tx = c.x + DX, ty = c.y + DY, tz = c.z + DZ;
+        if (!(tx < 0 || ty < 0 || tz < 0 || tx >= c.mx || ty >= c.my || tz >= c.mz)) {
+            double drdr = 0.0;
+            canon_pairs<E, 0>(c, drdr);
+            const double cc = drdr * __ldg(&c.sv[c.i + DX + static_cast<long long>(DY) * c.mx + DZ * c.pl]);
+            qx += cc * d0;
+            qy += cc * d1;
+            qz += cc * d2;
+        }
+        canon_group<E + 1>(c, d0, d1, d2, qx, qy, qz);
+    }
+}
+
+__global__ void __launch_bounds__(BX * BY) k_hv_closed_canon(Grid g, double scale, const double* __restrict__ rh,
+                                                             const double* __restrict__ sv,
+                                                             const double* __restrict__ dT, double* __restrict__ out) {
+    CanonCtx c;
+    c.x = static_cast<int>(blockIdx.x) * BX + threadIdx.x;
+    c.y = static_cast<int>(blockIdx.y) * BY + threadIdx.y;
+    c.z = blockIdx.z;
+    c.mx = static_cast<int>(g.m[0]);
+    c.my = static_cast<int>(g.m[1]);
+    c.mz = static_cast<int>(g.m[2]);
+    if (c.x >= c.mx || c.y >= c.my) return;
+    c.pl = static_cast<long long>(c.mx) * c.my;
+    c.n = c.pl * c.mz;
+    c.i = c.x + static_cast<long long>(c.y) * c.mx + c.z * c.pl;
+    c.rh = rh;
+    c.sv = sv;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+        const int ux = c.x + cdx(d), uy = c.y + cdy(d), uz = c.z + cdz(d);
+        c.ok[d] = ux >= 0 && uy >= 0 && uz >= 0 && ux < c.mx && uy < c.my && uz < c.mz;
+        c.off[d] = cdx(d) + static_cast<long long>(cdy(d)) * c.mx + cdz(d) * c.pl;
+    }
+    const long long i = c.i, n = c.n;
+    double qx = 0.0, qy = 0.0, qz = 0.0;
+    const double d0 = dT[i], d1 = dT[n + i], d2 = dT[2 * n + i];
+    canon_group<0>(c, d0, d1, d2, qx, qy, qz);
+    out[i] = scale * qx;
+    out[n + i] = scale * qy;
+    out[2 * n + i] = scale * qz;
+}
+
 // fast mode, pass 1: w_t = (dr s)_t = sum_k rho-hat_t(k) s_{t+k}
 __global__ void k_hv_w(Grid g, const double* __restrict__ rh, const double* __restrict__ sv, double* __restrict__ w) {
     idx_t x, y, z;
@@ -951,7 +1084,10 @@ void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv
 void launch_hv_closed(const Grid& img, const HvTable& tab, const double* rh, const double* sv, const double* dT,
                       double* out, cudaStream_t s) {
     const double scale = 2.0 * img.cell_volume();
-    note_launch(), k_hv_closed<<<grid3(img), block3(), 0, s>>>(img, tab, scale, rh, sv, dT, out);
+    if (is_canon_hv_table(tab))
+        note_launch(), k_hv_closed_canon<<<grid3(img), block3(), 0, s>>>(img, scale, rh, sv, dT, out);
+    else
+        note_launch(), k_hv_closed<<<grid3(img), block3(), 0, s>>>(img, tab, scale, rh, sv, dT, out);
 }
 void launch_hv_factored(const Grid& img, const double* rh, const double* sv, const double* dT, double* wbuf,
                         double* out, cudaStream_t s) {
