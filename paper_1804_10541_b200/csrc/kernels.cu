@@ -633,14 +633,15 @@ __device__ __forceinline__ double sum_term(int kind, const double* __restrict__ 
 // adds them in index order (bitwise the reference's loop: the terms do not depend on the
 // order, the additions are sequential). One thread per chunk left all but a few SMs idle and
 // read 32 scattered lines per warp load (0.59 ms at 128^3).
-__global__ void __launch_bounds__(32) k_chunks_warp(int kind, idx_t n, const double* __restrict__ a,
+template <int KIND>  // the term kind as a template parameter: branch-free batched term loads
+__global__ void __launch_bounds__(32) k_chunks_warp(idx_t n, const double* __restrict__ a,
                                                     const double* __restrict__ b, double* __restrict__ partials) {
     extern __shared__ double terms[];  // [kChunk]
     const idx_t c = blockIdx.x;
     const idx_t lo = c * kChunk, hi = min(n, lo + kChunk);
     const int cnt = static_cast<int>(hi - lo), lane = threadIdx.x;
-#pragma unroll 8
-    for (int i = lane; i < cnt; i += 32) terms[i] = sum_term(kind, a, b, lo + i);
+#pragma unroll 16
+    for (int i = lane; i < cnt; i += 32) terms[i] = sum_term(KIND, a, b, lo + i);
     __syncwarp();
     if (lane != 0) return;
     double s = 0.0;
@@ -1102,9 +1103,14 @@ idx_t tree_blocks(idx_t n) { return std::max<idx_t>(1, (n + kTreeSpan - 1) / kTr
 void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                         double scale, cudaStream_t s) {
     const idx_t nch = chunk_count(n);
-    if (nch > 0)
-        note_launch(), k_chunks_warp<<<static_cast<unsigned>(nch), 32, kChunk * sizeof(double), s>>>(kind, n, a, b,
-                                                                                                     partials);
+    if (nch > 0) {
+        const unsigned g = static_cast<unsigned>(nch);
+        const std::size_t sm = kChunk * sizeof(double);
+        note_launch();
+        if (kind == SUM_ONE_MINUS_SQ) k_chunks_warp<SUM_ONE_MINUS_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
+        else if (kind == SUM_DOT) k_chunks_warp<SUM_DOT><<<g, 32, sm, s>>>(n, a, b, partials);
+        else k_chunks_warp<SUM_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
+    }
     note_launch(), k_serial<<<1, 32, 0, s>>>(partials, nch, scale, out);
 }
 void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
