@@ -635,9 +635,17 @@ __device__ __forceinline__ double sum_term(int kind, const double* __restrict__ 
 // read 32 scattered lines per warp load (0.59 ms at 128^3).
 template <int KIND>  // the term kind as a template parameter: branch-free batched term loads
 __global__ void __launch_bounds__(32) k_chunks_warp(idx_t n, const double* __restrict__ a,
-                                                    const double* __restrict__ b, double* __restrict__ partials) {
+                                                    const double* __restrict__ b, double* __restrict__ partials,
+                                                    idx_t nseg_chunks = 0) {
     extern __shared__ double terms[];  // [kChunk]
-    const idx_t c = blockIdx.x;
+    idx_t c = blockIdx.x;
+    if (nseg_chunks) {  // segmented: block -> (segment d, chunk c) over arrays a + d n (3 components at once)
+        const idx_t d = c / nseg_chunks;
+        c -= d * nseg_chunks;
+        a += d * n;
+        if (b) b += d * n;
+        partials += d * nseg_chunks;
+    }
     const idx_t lo = c * kChunk, hi = min(n, lo + kChunk);
     const int cnt = static_cast<int>(hi - lo), lane = threadIdx.x;
 #pragma unroll 16
@@ -648,6 +656,15 @@ __global__ void __launch_bounds__(32) k_chunks_warp(idx_t n, const double* __res
 #pragma unroll 16
     for (int i = 0; i < cnt; ++i) s += terms[i];
     partials[c] = s;
+}
+
+// three segments' partials, each combined in chunk order by its own thread
+__global__ void k_serial3(const double* __restrict__ partials, idx_t nch, double scale, double* __restrict__ out) {
+    const int d = threadIdx.x;
+    if (d >= 3) return;
+    double t = 0.0;
+    for (idx_t c = 0; c < nch; ++c) t += partials[d * nch + c];
+    out[d] = scale * t;
 }
 
 // partials combined in chunk order (parallel.cpp:69-72), times `scale` (ngf.cpp:227)
@@ -1112,6 +1129,19 @@ void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, dou
         else k_chunks_warp<SUM_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
     }
     note_launch(), k_serial<<<1, 32, 0, s>>>(partials, nch, scale, out);
+}
+void launch_chunked_sum3(int kind, idx_t n, const double* a, const double* b, double* partials, double* out3,
+                         double scale, cudaStream_t s) {
+    const idx_t nch = chunk_count(n);
+    if (nch > 0) {
+        const unsigned g = static_cast<unsigned>(3 * nch);
+        const std::size_t sm = kChunk * sizeof(double);
+        note_launch();
+        if (kind == SUM_ONE_MINUS_SQ) k_chunks_warp<SUM_ONE_MINUS_SQ><<<g, 32, sm, s>>>(n, a, b, partials, nch);
+        else if (kind == SUM_DOT) k_chunks_warp<SUM_DOT><<<g, 32, sm, s>>>(n, a, b, partials, nch);
+        else k_chunks_warp<SUM_SQ><<<g, 32, sm, s>>>(n, a, b, partials, nch);
+    }
+    note_launch(), k_serial3<<<1, 32, 0, s>>>(partials, nch, scale, out3);
 }
 void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                      double scale, cudaStream_t s) {

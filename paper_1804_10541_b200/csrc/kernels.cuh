@@ -58,6 +58,9 @@ enum SumKind { SUM_ONE_MINUS_SQ = 0, SUM_DOT = 1, SUM_SQ = 2 };
 void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                         double scale, cudaStream_t s);
 // fast: deterministic two-level tree sum (fixed block partition, fixed order)
+// three equal-length segments (a + d n, d = 0..2), each summed as launch_chunked_sum into out3[d]
+void launch_chunked_sum3(int kind, idx_t n, const double* a, const double* b, double* partials, double* out3,
+                         double scale, cudaStream_t s);
 void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                      double scale, cudaStream_t s);
 idx_t chunk_count(idx_t n);

@@ -189,6 +189,18 @@ void Reducer::sum(int kind, idx_t n, const double* a, const double* b, double* o
     check_launch("reduction");
 }
 
+void Reducer::sum3(int kind, idx_t n, const double* a, const double* b, double* out_dev, double scale,
+                   cudaStream_t s) {
+    if (mode_ != Mode::Parity) {
+        for (int d = 0; d < 3; ++d) sum(kind, n, a + d * n, b ? b + d * n : nullptr, out_dev + d, scale, s);
+        return;
+    }
+    const idx_t need = 3 * chunk_count(n);
+    if (static_cast<std::size_t>(need) > partials_.size()) partials_.resize(static_cast<std::size_t>(need));
+    launch_chunked_sum3(kind, n, a, b, partials_.get(), out_dev, scale, s);
+    check_launch("reduction (3 segments)");
+}
+
 Scalars::Scalars(int n) : d_(static_cast<std::size_t>(n)) {
     MFREG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_), n * sizeof(double), cudaHostAllocMapped));
     MFREG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd_), h_, 0));
@@ -485,7 +497,7 @@ void DeviceObjective::eval_begin(const double* y, double* grad) {
     ngf_.value_async(sc_.dev(0));
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
     launch_lap3(dg_, u_.get(), lapu_.get(), s_);
-    for (int d = 0; d < 3; ++d) ngf_.reducer().sum(SUM_SQ, ny, lapu_.get() + d * ny, nullptr, sc_.dev(4 + d), 1.0, s_);
+    ngf_.reducer().sum3(SUM_SQ, ny, lapu_.get(), nullptr, sc_.dev(4), 1.0, s_);
     launch_curv_finalize(sc_.dev(4), dg_.cell_volume(), alpha_, sc_.dev(1), s_);
     if (grad) {
         ngf_.gradient(img3_.get());

@@ -189,6 +189,8 @@ public:
     Reducer(Mode mode, idx_t max_n);
     // device result into out_dev (scaled)
     void sum(int kind, idx_t n, const double* a, const double* b, double* out_dev, double scale, cudaStream_t s);
+    // three segments a + d n (d = 0..2) into out_dev[0..2], each exactly as sum(); one launch pair
+    void sum3(int kind, idx_t n, const double* a, const double* b, double* out_dev, double scale, cudaStream_t s);
     Mode mode() const { return mode_; }
 
 private:
