@@ -16,11 +16,11 @@ namespace mfreg_b200 {
 bool no_lazy_state();
 
 namespace {
-// bytes of freed device memory the pool keeps for reuse (MFREG_POOL_KEEP_GB, default 32: one
-// C4 registration's state fits, so a second registration in the process allocates nothing)
+// bytes of freed device memory the pool keeps for reuse (MFREG_POOL_KEEP_GB, default 8; only
+// blocks below kBigAllocBytes come from the pool)
 std::uint64_t pool_keep_bytes() {
     const char* e = std::getenv("MFREG_POOL_KEEP_GB");
-    const double gb = e ? std::atof(e) : 32.0;
+    const double gb = e ? std::atof(e) : 8.0;
     return static_cast<std::uint64_t>(std::max(0.0, gb) * static_cast<double>(1ull << 30));
 }
 cudaMemPool_t default_pool() {
@@ -39,8 +39,22 @@ cudaMemPool_t default_pool() {
 }  // namespace
 
 void* device_alloc(std::size_t bytes) {
-    cudaMemPool_t pool = default_pool();
     void* p = nullptr;
+    if (bytes >= kBigAllocBytes) {
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaErrorMemoryAllocation) {  // cached pool blocks may hold the memory: release, retry
+            cudaGetLastError();
+            MFREG_CUDA(cudaDeviceSynchronize());
+            MFREG_CUDA(cudaMemPoolTrimTo(default_pool(), 0));
+            e = cudaMalloc(&p, bytes);
+        }
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            throw CudaError(std::string("cudaMalloc(") + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
+        }
+        return p;
+    }
+    cudaMemPool_t pool = default_pool();
     cudaError_t e = cudaMallocAsync(&p, bytes, 0);
     if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
         cudaGetLastError();
@@ -55,8 +69,10 @@ void* device_alloc(std::size_t bytes) {
     return p;
 }
 
-void device_free(void* p) {
-    if (p) cudaFreeAsync(p, 0);
+void device_free(void* p, std::size_t bytes) {
+    if (!p) return;
+    if (bytes >= kBigAllocBytes) cudaFree(p);
+    else cudaFreeAsync(p, 0);
 }
 
 void check_launch(const char* what) {

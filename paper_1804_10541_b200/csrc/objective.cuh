@@ -39,10 +39,13 @@ enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 
 // Device allocations come from the device's default stream-ordered pool (allocated and
 // freed on the legacy stream, which all library work is ordered with) with up to
-// MFREG_POOL_KEEP_GB (default 32) kept cached: objectives are created per pyramid level and per call, and
+// MFREG_POOL_KEEP_GB (default 8) kept cached: objectives are created per pyramid level and per call, and
 // cudaMalloc/cudaFree of their state cost tens of milliseconds with a wide spread.
+// (blocks of kBigAllocBytes and more use plain cudaMalloc / cudaFree: growing the pool by tens of
+// GB on first use measured 0.6-4 s against 0.05 s for cudaMalloc)
+constexpr std::size_t kBigAllocBytes = std::size_t(256) << 20;
 void* device_alloc(std::size_t bytes);
-void device_free(void* p);
+void device_free(void* p, std::size_t bytes);
 
 // RAII device array of doubles (or raw bytes).
 template <typename T>
@@ -74,7 +77,7 @@ public:
         n_ = n;
     }
     void release() {
-        if (p_) device_free(p_);
+        if (p_) device_free(p_, n_ * sizeof(T));
         p_ = nullptr;
         n_ = 0;
     }
