@@ -271,9 +271,11 @@ CgResult DeviceCg::solve(DeviceProblem& P, int op, double gamma, const double* b
                 const long long l0 = launch_counter();
                 MFREG_CUDA(cudaStreamBeginCapture(cs_, cudaStreamCaptureModeRelaxed));
                 P.redirect_stream(cs_);
+                GraphCache::capturing() = true;
                 try {
                     window(P, op, gamma, x, cfg, w, fused_update);
                 } catch (...) {
+                    GraphCache::capturing() = false;
                     P.redirect_stream(s);
                     cudaGraph_t g = nullptr;
                     cudaStreamEndCapture(cs_, &g);
@@ -281,6 +283,7 @@ CgResult DeviceCg::solve(DeviceProblem& P, int op, double gamma, const double* b
                     cudaGetLastError();
                     throw;
                 }
+                GraphCache::capturing() = false;
                 P.redirect_stream(s);
                 cudaGraph_t g = nullptr;
                 MFREG_CUDA(cudaStreamEndCapture(cs_, &g));

@@ -132,6 +132,12 @@ std::vector<SlabInfo> slab_partition(const Grid& image, const Grid& deform, int 
 // (replayed on the caller's stream; LRU-bounded). MFREG_NO_GRAPHS=1 disables.
 class GraphCache {
 public:
+    // set while this thread captures an enclosing graph (DeviceCg windows): nested calls enqueue
+    // their work inline instead of launching their own graphs
+    static bool& capturing() {
+        static thread_local bool flag = false;
+        return flag;
+    }
     using Key = std::array<const void*, 6>;
     explicit GraphCache(std::size_t cap = 8);
     ~GraphCache();
@@ -140,9 +146,8 @@ public:
     bool enabled() const { return enabled_; }
     template <class F>
     void run(const Key& k, cudaStream_t s, F&& enqueue) {
-        cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
-        if (!enabled_ || (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone)) {
-            enqueue(s);  // graphs off, or `s` is being captured by an enclosing graph (CG window)
+        if (!enabled_ || capturing()) {
+            enqueue(s);  // graphs off, or an enclosing graph (CG window) is being captured
             return;
         }
         Entry* e = find(k);
