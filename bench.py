@@ -1,24 +1,27 @@
 """Benchmark: NGF + curvature derivative evaluation on B200 (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1], "C2"): 128^3 synthetic CT-like phantom (x1000)
-warped by a sinusoid (amp 3 voxels, seed 42), nodal grid 33^3 (ratio 4), tau =
-rho = 10, alpha = 1; y = identity + U(-0.3, 0.3), p ~ U(-1, 1).
+Headline workload (BASELINE.json configs[3], "C4", the largest configuration that fits one
+GPU): the finest level of the 512x512x900 thorax-abdomen-shaped pair, spacing h = 0.7 (the
+interpolation-tie hazard of SURVEY H1), nodal grid 129x129x226 (ratio 4); R = the
+reference's phantom x1000, T = R warped by its sinusoid (amp 3 voxels, seed 42), tau = rho
+= 10, alpha = 1; y = identity + U(-0.3, 0.3), p ~ U(-1, 1).
 
 One step = one gradient evaluation Objective::eval(y, grad) + one Gauss-Newton
-Hessian-vector product Objective::gn_hessian_vec(p) — the two derivative
-operators the GN/CG solver is made of. `value` counts
-image voxels processed by derivative evaluations per second (2 m per step),
-inputs resident in HBM, L2 flushed between steps, device time from CUDA events.
-`e2e` is the same step through the C ABI with HOST buffers (y, p in; grad, q
-out), so H2D/D2H copies are inside the timed region. The full 3-level
-Gauss-Newton registration of the same pair (the metric's second half) is timed
-once and reported under `gn_registration`.
+Hessian-vector product Objective::gn_hessian_vec(p) — the two derivative operators the
+GN/CG solver is made of. `value` counts image voxels processed by
+derivative evaluations per second (2 m per step), inputs resident in HBM (per-step state
+> 20 GB, far larger than L2; L2 also flushed between steps), device time from CUDA events.
+`e2e` is the same step through the C ABI with HOST buffers (y, p in; grad, q out), so the
+H2D/D2H copies are inside the timed region. The full 3-level Gauss-Newton registration of
+the C4 pair (the metric's second half) is timed under `gn_registration_c4`.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--mode fast|parity]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c4|c2] [--mode fast|parity]
 """
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -32,16 +35,45 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-M = (128, 128, 128)
-H = (1.0, 1.0, 1.0)
 RATIO = 4
 LEVELS = 3
+# (image size, spacing, CPU-baseline sample of the same workload)
+WORKLOADS = {
+    "c4": {"m": (512, 512, 900), "h": (0.7, 0.7, 0.7), "sample_m": (512, 512, 24),
+           "name": "C4 finest level: 512x512x900 image (h=0.7) / 129x129x226 nodal, eval(grad) + gn_hessian_vec"},
+    "c2": {"m": (128, 128, 128), "h": (1.0, 1.0, 1.0), "sample_m": (128, 128, 128),
+           "name": "C2 finest level: 128^3 image / 33^3 nodal, eval(grad) + gn_hessian_vec"},
+}
 B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
-# dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu --set full
-# capture of the same workload (profiles/), or None when not captured for this build
-TRAFFIC = {"hv_pass": 171.05e6, "eval_pass": 147.62e6, "warp": 29.42e6}  # bytes/launch, profiles/r1c_ncu_full.md
+TRAFFIC_FILE = os.path.join(ROOT, "profiles", "traffic.json")  # written by scripts/ncu_traffic.py
 METRIC = "NGF+curvature derivative eval Gvoxel/s (%HBM roofline); full GN registration wall s"
+DATA = "synthetic (reference phantom x1000, sinusoid warp amp 3 seed 42)"
+
+
+def csrc_sha() -> str:
+    """Hash of the CUDA sources: an ncu traffic capture is only quoted for the build it measured."""
+    d = os.path.join(ROOT, "paper_1804_10541_b200", "csrc")
+    h = hashlib.sha256()
+    for f in sorted(os.listdir(d)):
+        if f.endswith((".cu", ".cuh")):
+            with open(os.path.join(d, f), "rb") as fh:
+                h.update(f.encode() + fh.read())
+    return h.hexdigest()[:16]
+
+
+def traffic_for(workload: str, kernel: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
+    of this workload and source hash (profiles/traffic.json), else None."""
+    try:
+        with open(TRAFFIC_FILE) as f:
+            t = json.load(f)
+        e = t[workload][kernel]
+        if e.get("csrc_sha") != csrc_sha():
+            return None, f"capture {e.get('csrc_sha')} is for other sources"
+        return float(e["bytes"]), e.get("source", "profiles/traffic.json")
+    except Exception as exc:  # noqa: BLE001
+        return None, f"no capture ({type(exc).__name__})"
 
 
 def parse():
@@ -50,10 +82,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c4")
     ap.add_argument("--mode", choices=["fast", "parity"], default="fast")
-    ap.add_argument("--no-gn", action="store_true", help="skip the full GN registration timing")
+    ap.add_argument("--no-gn", action="store_true", help="skip the full GN registration timings")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
-    ap.add_argument("--no-c4", action="store_true", help="skip the 512x512x900 (C4) registrations")
+    ap.add_argument("--no-fast32", action="store_true", help="skip the optional fp32 mode lines")
     return ap.parse_args()
 
 
@@ -154,8 +187,13 @@ def measured_hbm_peak():
         return 6650.0, "fallback"
 
 
-def make_inputs_gpu(P, torch):
-    img = P.make_image_grid(M, H)
+
+
+def make_inputs_gpu(P, torch, wl: str):
+    """The workload on the GPU: the reference's phantom and sinusoid warp re-implemented as
+    device generators (bitwise equal to synthetic.cpp, tests/test_capi_host.py)."""
+    m, h = WORKLOADS[wl]["m"], WORKLOADS[wl]["h"]
+    img = P.make_image_grid(m, h)
     dg = P.deformation_grid_for(img, RATIO)
     R = P.make_phantom(img, device=True)
     R.mul_(1000.0)
@@ -165,50 +203,96 @@ def make_inputs_gpu(P, torch):
     xid = torch.from_numpy(dg.point_coords()).cuda()
     y = xid + (torch.rand(nd, generator=gen, device="cuda", dtype=torch.float64) * 0.6 - 0.3)
     p = torch.rand(nd, generator=gen, device="cuda", dtype=torch.float64) * 2.0 - 1.0
+    del xid
     return img, dg, R, T, y, p
 
 
-def cpu_reference_rate(R, T, y, p, steps: int, threads: int):
-    """Reference CPU implementation (oracle/_ref, else the C port) timed on host cores."""
+def cpu_reference_sample(wl: str, steps: int, threads: int):
+    """The reference CPU implementation (oracle/_ref = the unmodified reference library, else
+    the C port) on a bounded sample of the workload: the same spacing, ratio and inputs
+    generated by the reference's own synthetic.cpp, on a z sub-slab (C4: 512x512x24). Only
+    the checker library is loaded — never libmfreg_cuda.so. Returns per-voxel timings."""
     from oracle.oracle import Oracle, available
     kind = "reference" if available("ref") else "port"
     o = Oracle("ref" if kind == "reference" else "port")
     o.set_threads(threads)
-    my = [((M[a] + RATIO - 1) // RATIO + 1) for a in range(3)]
-    obj = o.objective(R, T, M, H, my, 10.0, 10.0, 1.0)
+    m, h = WORKLOADS[wl]["sample_m"], WORKLOADS[wl]["h"]
+    R = o.make_phantom(m, h) * 1000.0
+    T = o.warp_sinusoid(R, m, h, 3.0, 42)
+    my, _ = o.deformation_grid_for(m, h, RATIO)
+    obj = o.objective(R, T, m, h, my, 10.0, 10.0, 1.0)
+    rng = np.random.default_rng(8)
+    y = obj.identity() + rng.uniform(-0.3, 0.3, obj.dof)
+    p = rng.uniform(-1.0, 1.0, obj.dof)
     obj.eval(y)  # warm
-    ts = []
+    te, th, tv = [], [], []
     for _ in range(steps):
         t0 = time.perf_counter()
         obj.eval(y)
+        t1 = time.perf_counter()
         obj.gn_hessian_vec(p)
-        ts.append(time.perf_counter() - t0)
-    n = int(np.prod(M))
-    t = statistics.median(ts)
-    return 2.0 * n / t / 1e9, kind, (threads if kind == "reference" else 1), t
+        t2 = time.perf_counter()
+        obj.eval(y, want_grad=False)
+        t3 = time.perf_counter()
+        te.append(t1 - t0)
+        th.append(t2 - t1)
+        tv.append(t3 - t2)
+    n = int(np.prod(m))
+    step = statistics.median(a + b for a, b in zip(te, th))
+    return {"kind": kind, "cores": threads if kind == "reference" else 1, "n": n, "m": list(m),
+            "value": 2.0 * n / step / 1e9, "s_per_step": step,
+            "s_per_vox_eval": statistics.median(te) / n, "s_per_vox_hv": statistics.median(th) / n,
+            "s_per_vox_value": statistics.median(tv) / n,
+            "sample": f"{steps} steps of eval(y,grad)+gn_hessian_vec(p) on a {m[0]}x{m[1]}x{m[2]} z sub-slab "
+                      f"(h={h[0]}, inputs from the reference's synthetic.cpp), median; Gvoxel/s per voxel "
+                      f"is size-independent (the reference kernels are linear in the voxel count)"}
+
+
+def cpu_gn_model(cpu: dict, levels_gpu, img_counts):
+    """CPU reference wall time of the same multilevel GN run, extrapolated from the measured
+    per-voxel costs: per level, (outer iterations) gradient evals + (CG iterations) GN Hv +
+    (line-search trials) value-only evals, with the iteration counts of the GPU run."""
+    t = 0.0
+    for (trace, _), n in zip(levels_gpu, img_counts):
+        outer = len(trace)
+        cg = sum(r.cg_iters for r in trace)
+        t += n * (outer * cpu["s_per_vox_eval"] + cg * cpu["s_per_vox_hv"] + 2 * outer * cpu["s_per_vox_value"])
+    return t
 
 
 def run_reference_arm(args, rank, world):
+    """--impl reference: the reference's CPU implementation of the path on the host cores, on a
+    bounded sample of the same workload (rank 0 only). Loads oracle/_ref only."""
     if rank != 0:
         return
-    import torch
-    import paper_1804_10541_b200 as P
-    torch.cuda.set_device(0)
-    img, dg, R, T, y, p = make_inputs_gpu(P, torch)
-    R, T, y, p = (x.cpu().numpy() for x in (R, T, y, p))
     threads = os.cpu_count() or 1
     steps = max(1, min(args.steps, 5))
-    rate, kind, cores, t = cpu_reference_rate(R, T, y, p, steps, threads)
-    line = {"metric": METRIC, "value": rate, "unit": "Gvoxel/s", "n_gpus": world, "steps": steps,
-            "warmup": 1, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic (phantom x1000, sinusoid warp amp 3 seed 42)",
-            "config": {"workload": "C2 finest level: 128^3 image / 33^3 nodal, eval(grad) + gn_hessian_vec",
-                       "image": list(M), "nodal": list(dg.m), "threads": threads},
+    cpu = cpu_reference_sample(args.workload, steps, threads)
+    wl = WORKLOADS[args.workload]
+    line = {"metric": METRIC, "value": cpu["value"], "unit": "Gvoxel/s", "n_gpus": world, "steps": steps,
+            "warmup": 1, "ms_per_step": cpu["s_per_step"] * 1e3, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]), "threads": threads},
             "impl": "reference",
-            "cpu_baseline": {"value": rate, "unit": "Gvoxel/s", "cores": cores, "kind": kind,
-                             "sample": f"{steps} steps of eval(y,grad)+gn_hessian_vec(p) at 128^3, median"},
-            "e2e": {"value": rate, "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {"value": cpu["value"], "unit": "Gvoxel/s", "cores": cpu["cores"], "kind": cpu["kind"],
+                             "sample": cpu["sample"]},
+            "e2e": {"value": cpu["value"], "unit": "Gvoxel/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def time_steps(obj, y, grad, p, q, steps, flush, torch):
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    for k in range(steps):
+        flush.zero_()
+        a, b, c = ev[k]
+        a.record()
+        obj.eval(y, grad)
+        b.record()
+        obj.gn_hessian_vec(p, q)
+        c.record()
+    torch.cuda.synchronize()
+    return [e[0].elapsed_time(e[1]) for e in ev], [e[1].elapsed_time(e[2]) for e in ev]
 
 
 def run_ours(args, rank, world, local):
@@ -216,7 +300,8 @@ def run_ours(args, rank, world, local):
     import paper_1804_10541_b200 as P
     torch.cuda.set_device(local)
     mode = P.Mode.FAST if args.mode == "fast" else P.Mode.PARITY
-    img, dg, R, T, y, p = make_inputs_gpu(P, torch)
+    wl = WORKLOADS[args.workload]
+    img, dg, R, T, y, p = make_inputs_gpu(P, torch, args.workload)
     n = img.count()
     nd = 3 * dg.count()
     obj = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, mode)
@@ -224,32 +309,17 @@ def run_ours(args, rank, world, local):
     q = torch.empty_like(y)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")  # > 126 MB L2
 
-    def step():
+    for _ in range(args.warmup):
         obj.eval(y, grad)
         obj.gn_hessian_vec(p, q)
-
-    for _ in range(args.warmup):
-        step()
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     l0 = P.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     with Clocks(local) as ck:
-        for k in range(args.steps):
-            flush.zero_()
-            a, b, c = ev[k]
-            a.record()
-            obj.eval(y, grad)
-            b.record()
-            obj.gn_hessian_vec(p, q)
-            c.record()
-        torch.cuda.synchronize()
+        t_eval, t_hv = time_steps(obj, y, grad, p, q, args.steps, flush, torch)
     barrier(world)
     launches = P.launch_count() - l0
-    t_eval = [e[0].elapsed_time(e[1]) for e in ev]
-    t_hv = [e[1].elapsed_time(e[2]) for e in ev]
     ms_step = max_over_ranks(sum(t_eval) / args.steps + sum(t_hv) / args.steps, world)
     ms_eval = statistics.mean(t_eval)
     ms_hv = statistics.mean(t_hv)
@@ -266,14 +336,15 @@ def run_ours(args, rank, world, local):
         obj.eval(yh, gh)
         obj.gn_hessian_vec(ph, qh)
     barrier(world)
-    t0 = time.perf_counter()
     k_e2e = max(3, args.steps // 2)
+    t0 = time.perf_counter()
     for _ in range(k_e2e):
         obj.eval(yh, gh)
         obj.gn_hessian_vec(ph, qh)
     e2e_s = max_over_ranks((time.perf_counter() - t0) / k_e2e, world)
     e2e = {"value": 2.0 * n * world / e2e_s / 1e9, "unit": "Gvoxel/s", "h2d_bytes_per_step": 2 * nd * 8,
-           "d2h_bytes_per_step": 2 * nd * 8 + 16, "ms_per_step": e2e_s * 1e3}
+           "d2h_bytes_per_step": 2 * nd * 8 + 16, "ms_per_step": e2e_s * 1e3,
+           "path": "Objective.eval / gn_hessian_vec with pinned numpy buffers through the C ABI"}
 
     peak, peak_kind = measured_hbm_peak()
     roofline = None
@@ -289,56 +360,36 @@ def run_ours(args, rank, world, local):
         # canonical state R, T_w, dT (40 B); eval pass reads R, T_w, dT (40 B); warp reads T
         # and writes T_w, dT (8 + 32 B)
         b_alg = {"hv_pass": B_CANON_HV, "eval_pass": 40.0, "warp": 40.0}
-        kern = {k: {"ms": v, "achieved_gbs": b_alg[k] * n / (v * 1e-3) / 1e9, "algorithmic_bytes_per_voxel": b_alg[k],
-                    "frac": b_alg[k] * n / (v * 1e-3) / 1e9 / peak} for k, v in k_ms.items()}
+        kern = {}
+        for k, v in k_ms.items():
+            tr, src = traffic_for(args.workload, k)
+            kern[k] = {"ms": v, "achieved_gbs": b_alg[k] * n / (v * 1e-3) / 1e9, "algorithmic_bytes_per_voxel": b_alg[k],
+                       "frac": b_alg[k] * n / (v * 1e-3) / 1e9 / peak, "traffic": tr, "traffic_source": src,
+                       "share_of_step": v / ms_step}
         dom = max(k_ms, key=k_ms.get)
         names = {"hv_pass": "k_hv2 (GN Hv image pass: P p, dr, dr^T, dT, P^T partials)",
                  "eval_pass": "k_ev2 (NGF eval pass: rho-hat, r, D partials, gradient dr^T r, P^T partials)",
                  "warp": "k_warp_fast (P y, trilinear T, dT/dP)"}
         roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
-                    "frac": kern[dom]["frac"], "traffic": TRAFFIC.get(dom), "traffic_unit": "bytes/launch (ncu dram read+write)",
+                    "frac": kern[dom]["frac"], "traffic": kern[dom]["traffic"],
+                    "traffic_unit": "bytes/launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+                    "traffic_source": kern[dom]["traffic_source"],
                     "algorithmic_bytes_per_launch": b_alg[dom] * n, "kernel": names[dom],
                     "algorithmic_bytes_per_voxel": b_alg[dom], "units_per_launch": n, "peak_source": peak_kind,
                     "kernels": kern,
                     "operators": {"gn_hessian_vec": {"ms": ms_hv, "frac": B_CANON_HV * n / (ms_hv * 1e-3) / 1e9 / peak},
                                   "eval_grad": {"ms": ms_eval, "frac": B_CANON_GRAD * n / (ms_eval * 1e-3) / 1e9 / peak}}}
 
-    gn = None
-    if not args.no_gn:
-        cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=mode)
-        P.register_multilevel(R, T, img, P.MultilevelConfig(levels=LEVELS, method=P.Method.GAUSS_NEWTON, mode=mode,
-                                                              opt=P.OptimizerConfig(max_iters=1)))
-        walls = []
-        for _ in range(3):  # host-driven solver loops: median of 3 runs (single runs vary 2x on a busy host)
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            yy, dgf, levels = P.register_multilevel(R, T, img, cfg)
-            torch.cuda.synchronize()
-            walls.append(time.perf_counter() - t0)
-        wall = max_over_ranks(statistics.median(walls), world)
-        gn = {"wall_s": wall, "wall_s_runs": walls, "mode": args.mode, "levels": LEVELS,
-              "outer_iters": [len(t) for t, _ in levels],
-              "cg_iters": int(sum(r.cg_iters for t, _ in levels for r in t)),
-              "final_J": levels[-1][0][-1].j if levels[-1][0] else None,
-              "reference_cpu_s_8thr_container": 519.0}
-
-    # the optional fp32 mode (FAST32) on the same workload: operator rate and kernel times
+    # the optional fp32 mode (FAST32) on the same workload: operator rate and Hv kernel time
     fast32 = None
-    if mode == P.Mode.FAST and world == 1:
+    if mode == P.Mode.FAST and world == 1 and not args.no_fast32:
         o32 = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.Mode.FAST32)
         for _ in range(3):
             o32.eval(y, grad)
             o32.gn_hessian_vec(p, q)
         torch.cuda.synchronize()
-        ev32 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-        for a_, b_ in ev32:
-            flush.zero_()
-            a_.record()
-            o32.eval(y, grad)
-            o32.gn_hessian_vec(p, q)
-            b_.record()
-        torch.cuda.synchronize()
-        ms32 = statistics.mean(a_.elapsed_time(b_) for a_, b_ in ev32)
+        te32, th32 = time_steps(o32, y, grad, p, q, args.steps, flush, torch)
+        ms32 = statistics.mean(te32) + statistics.mean(th32)
         reps = max(5, args.steps)
         k32 = {"hv_pass": o32.profile_kernel(0, p, reps), "eval_pass": o32.profile_kernel(1, p, reps),
                "warp": o32.profile_kernel(2, y, reps)}
@@ -347,80 +398,85 @@ def run_ours(args, rank, world, local):
                   "algorithmic_bytes_per_voxel_hv": 20.0,
                   "hv_frac": 20.0 * n / (k32["hv_pass"] * 1e-3) / 1e9 / peak}
         del o32
-
-    # north-star case C4: full 3-level GN registration of a 512x512x900 pair on this GPU,
-    # fp64 (FAST) and the optional fp32 mode (FAST32); wall clock from the host
-    gn_c4 = None
-    if not args.no_c4 and world == 1 and mode == P.Mode.FAST:
-        gn_c4 = {"image": [512, 512, 900], "levels": LEVELS, "method": "gauss-newton"}
-        img4 = P.make_image_grid((512, 512, 900), H)
-        R4 = P.make_phantom(img4, device=True)
-        R4.mul_(1000.0)
-        T4 = P.warp_sinusoid(R4, img4, 3.0, 42)
-        ck4 = Clocks(local).__enter__()  # clocks over the C4 runs (sustained load: power cap shows here)
-        for name, md in (("fast", P.Mode.FAST), ("fast32", P.Mode.FAST32)):
-            cfg4 = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
-            walls = []
-            for _ in range(2):  # cold (first registration in the process), then warm (pooled memory)
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                _, _, lv4 = P.register_multilevel(R4, T4, img4, cfg4)
-                torch.cuda.synchronize()
-                walls.append(time.perf_counter() - t0)
-            gn_c4[name] = {"wall_s": walls[0], "wall_s_warm": walls[1], "outer_iters": [len(t) for t, _ in lv4],
-                           "cg_iters": int(sum(r.cg_iters for t, _ in lv4 for r in t)),
-                           "final_J": lv4[-1][0][-1].j if lv4[-1][0] else None}
-        ck4.__exit__(None, None, None)
-        gn_c4["clocks"] = ck4.summary()
-        del R4, T4
+    del obj
+    torch.cuda.synchronize()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        rate, kind, cores, t = cpu_reference_rate(R.cpu().numpy(), T.cpu().numpy(), yh, ph, 3, threads)
-        cpu = {"value": rate, "unit": "Gvoxel/s", "cores": cores, "kind": kind,
-               "sample": f"3 steps of eval(y,grad)+gn_hessian_vec(p) at 128^3 ({t:.2f} s/step median)"}
+        cpu = cpu_reference_sample(args.workload, 3, threads)
+
+    # the metric's second half: the full 3-level GN registration of this pair on this GPU,
+    # wall clock from the host (cold = first registration in the process, then warm); the
+    # same run in FAST32; the CPU reference's wall time for the same iteration counts,
+    # extrapolated from its measured per-voxel costs
+    gn = None
+    if not args.no_gn and world == 1 and mode == P.Mode.FAST:
+        gn = {"workload": f"{wl['m'][0]}x{wl['m'][1]}x{wl['m'][2]} h={wl['h'][0]}, {LEVELS} levels, ratio {RATIO}",
+              "method": "gauss-newton"}
+        sizes, mm = [], list(wl["m"])
+        for _ in range(LEVELS):
+            sizes.append(int(np.prod(mm)))
+            mm = [(v + 1) // 2 for v in mm]
+        sizes = sizes[::-1]  # coarsest first, as the level traces
+        ckg = Clocks(local).__enter__()
+        for name, md in (("fast", P.Mode.FAST), ("fast32", P.Mode.FAST32)):
+            if name == "fast32" and args.no_fast32:
+                continue
+            cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
+            walls = []
+            for _ in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, _, lv = P.register_multilevel(R, T, img, cfg)
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t0)
+            gn[name] = {"wall_s": walls[0], "wall_s_warm": walls[1], "outer_iters": [len(t) for t, _ in lv],
+                        "cg_iters": int(sum(r.cg_iters for t, _ in lv for r in t)),
+                        "final_J": lv[-1][0][-1].j if lv[-1][0] else None}
+            if name == "fast" and cpu is not None:
+                gn["reference_cpu_wall_s_extrapolated"] = cpu_gn_model(cpu, lv, sizes)
+                gn["reference_cpu_model"] = ("per level: outer x eval(grad) + CG x gn_hessian_vec + 2 x outer value-only "
+                                             "evals, iteration counts of this run, per-voxel costs of cpu_baseline "
+                                             f"({cpu['cores']} threads)")
+        ckg.__exit__(None, None, None)
+        gn["clocks"] = ckg.summary()
 
     if rank == 0:
+        cpu_line = None
+        if cpu is not None:
+            cpu_line = {"value": cpu["value"], "unit": "Gvoxel/s", "cores": cpu["cores"], "kind": cpu["kind"],
+                        "sample": cpu["sample"]}
         line = {"metric": METRIC, "value": value, "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (phantom x1000, sinusoid warp amp 3 seed 42)",
-                "config": {"workload": "C2 finest level: 128^3 image / 33^3 nodal, eval(grad) + gn_hessian_vec",
-                           "image": list(M), "nodal": list(dg.m), "mode": args.mode,
-                           "l2": "flushed between steps (256 MB write); per-step state 350 MB > L2",
+                "vs_baseline": None, "dtype": "f64", "data": DATA,
+                "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]),
+                           "nodal": list(dg.m), "mode": args.mode,
+                           "l2": "inputs larger than L2 (per-step state > 20 GB at C4) and L2 flushed between steps "
+                                 "(256 MB write)",
                            "parallelism": "single GPU"},
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv,
                 "gvox_s_grad_eval": n / (ms_eval * 1e-3) / 1e9, "gvox_s_gn_hv": n / (ms_hv * 1e-3) / 1e9,
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-                "clocks": clocks, "gn_registration": gn, "gn_registration_c4": gn_c4,
-                "fast32": fast32}
+                "roofline": roofline, "cpu_baseline": cpu_line, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clocks, "gn_registration": gn, "fast32": fast32}
         print(json.dumps(line), flush=True)
 
 
 def run_slabs(args, rank, world, local):
-    """N > 1: weak scaling over z slabs. The global volume is
-    128 x 128 x (128 N) (nodal 33 x 33 x (32 N + 1)); rank r evaluates its
-    128-plane slab. Every step performs the real halo exchanges, shared-plane
-    sums and scalar all-gathers over NCCL (slab.py)."""
+    """N > 1: strong scaling of the same workload over z slabs: rank r evaluates
+    its slab of the global volume; every step performs the real halo exchanges, shared-plane
+    sums and scalar reductions."""
     import torch
     import paper_1804_10541_b200 as P
     torch.cuda.set_device(local)
     if args.mode != "fast":
         raise SystemExit("z slabs run in fast mode")
-    gm = (M[0], M[1], M[2] * world)
-    img = P.make_image_grid(gm, H)
-    dg = P.deformation_grid_for(img, RATIO)
-    R = P.make_phantom(img, device=True)
-    R.mul_(1000.0)
-    T = P.warp_sinusoid(R, img, 3.0, 42)
-    gen = torch.Generator(device="cuda").manual_seed(8)
+    wl = WORKLOADS[args.workload]
+    img, dg, R, T, y, p = make_inputs_gpu(P, torch, args.workload)
     nd = 3 * dg.count()
-    y = torch.from_numpy(dg.point_coords()).cuda() + (torch.rand(nd, generator=gen, device="cuda",
-                                                                 dtype=torch.float64) * 0.6 - 0.3)
-    p = torch.rand(nd, generator=gen, device="cuda", dtype=torch.float64) * 2.0 - 1.0
     so = P.slab.SlabObjective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.slab.TorchComm())
     s = so.info
-    n_loc = (s.zhi - s.zlo) * gm[0] * gm[1]
+    n_loc = (s.zhi - s.zlo) * wl["m"][0] * wl["m"][1]
     n_glob = img.count()
     grad = torch.zeros_like(y)
     q = torch.zeros_like(y)
@@ -429,25 +485,13 @@ def run_slabs(args, rank, world, local):
         so.eval(y, grad)
         so.gn_hessian_vec(p, q)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
-           torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     l0 = P.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     with Clocks(local) as ck:
-        for k in range(args.steps):
-            flush.zero_()
-            a, b, c = ev[k]
-            a.record()
-            so.eval(y, grad)
-            b.record()
-            so.gn_hessian_vec(p, q)
-            c.record()
-        torch.cuda.synchronize()
+        t_eval, t_hv = time_steps(so, y, grad, p, q, args.steps, flush, torch)
     barrier(world)
     launches = P.launch_count() - l0
-    t_eval = [e[0].elapsed_time(e[1]) for e in ev]
-    t_hv = [e[1].elapsed_time(e[2]) for e in ev]
     ms_step = max_over_ranks(sum(t_eval) / args.steps + sum(t_hv) / args.steps, world)
     ms_eval = max_over_ranks(statistics.mean(t_eval), world)
     ms_hv = max_over_ranks(statistics.mean(t_hv), world)
@@ -483,16 +527,13 @@ def run_slabs(args, rank, world, local):
                 "algorithmic_bytes_per_voxel": B_CANON_HV, "peak_source": peak_kind}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f64", "data": "synthetic (phantom x1000, sinusoid warp amp 3 seed 42)",
-                "config": {"workload": f"C2 finest level per GPU: 128^3 image slab of {list(gm)} / nodal {list(dg.m)}, "
-                                       "eval(grad) + gn_hessian_vec",
-                           "image": list(gm), "nodal": list(dg.m), "mode": args.mode,
-                           "l2": "flushed between steps (256 MB write)",
-                           "parallelism": f"z slabs x{world} (halo exchange + shared-plane sums over NCCL)"},
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+                "vs_baseline": None, "dtype": "f64", "data": DATA,
+                "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]),
+                           "nodal": list(dg.m), "mode": args.mode, "l2": "inputs larger than L2; flushed between steps",
+                           "parallelism": f"z slabs x{world} (halo exchange + shared-plane sums)"},
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv, "roofline": roofline, "cpu_baseline": None,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
-                "gn_registration": None}
+                "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "gn_registration": None}
         print(json.dumps(line), flush=True)
 
 

@@ -18,6 +18,10 @@ from typing import Sequence
 import numpy as np
 
 from ._build import LIB as _LIB_PATH
+from ._build import variant_lib as _variant_lib
+
+if os.environ.get("MFREG_LIB_VARIANT"):  # A/B experiment builds (scripts/variants.py)
+    _LIB_PATH = _variant_lib(os.environ["MFREG_LIB_VARIANT"])
 
 __all__ = [
     "GridDesc", "NgfParams", "OptimizerConfig", "IterationRecord", "MultilevelConfig", "Method", "Mode",
@@ -241,6 +245,25 @@ def _dev_f64(x) -> bool:
     return _F64 is not None and getattr(x, "dtype", None) is _F64 and x.is_cuda and x.is_contiguous()
 
 
+def _numel(x) -> int:
+    return int(x.numel()) if _is_torch(x) else int(np.asarray(x).size)
+
+
+def _need(x, n: int, msg: str) -> None:
+    """Length check with the reference's std::invalid_argument text (raised as ValueError)."""
+    if x is not None and _numel(x) != n:
+        raise ValueError(msg)
+
+
+def _same_side(*xs) -> int:
+    """All operands host, or all CUDA tensors: a mixed call would hand a host pointer to a
+    device kernel (or the reverse)."""
+    ws = {_where_of(x) for x in xs if x is not None}
+    if len(ws) > 1:
+        raise ValueError("operands must all be host arrays or all CUDA tensors")
+    return ws.pop() if ws else HOST
+
+
 def _where_of(*xs) -> int:
     for x in xs:
         if x is not None and _is_torch(x) and x.is_cuda:
@@ -306,6 +329,7 @@ def _nodal(g: GridDesc) -> GridDesc:
 # ------------------------------------------------------------------ kernel API
 def transfer_apply(nodal: GridDesc, image: GridDesc, y):
     """P y (transfer.cpp:49-86)."""
+    _need(y, 3 * nodal.count(), "transfer_apply: length mismatch")
     w = _where_of(y)
     y = _as_input(y, w)
     out = _empty_like_kind(y, 3 * image.count())
@@ -315,6 +339,7 @@ def transfer_apply(nodal: GridDesc, image: GridDesc, y):
 
 def transfer_apply_transpose(nodal: GridDesc, image: GridDesc, w_img):
     """P^T w (transfer.cpp:131-150), deterministic gather in the reference's order."""
+    _need(w_img, 3 * image.count(), "transfer_apply_transpose: length mismatch")
     w = _where_of(w_img)
     w_img = _as_input(w_img, w)
     out = _empty_like_kind(w_img, 3 * nodal.count())
@@ -325,9 +350,12 @@ def transfer_apply_transpose(nodal: GridDesc, image: GridDesc, w_img):
 
 def sample_deformed(tpl, image: GridDesc, points):
     """T(points) and dT/dP (volume.cpp:76-94). Returns (values, partials[3n])."""
+    if _numel(points) % 3:
+        raise ValueError("sample_deformed: points length must be a multiple of 3")
+    _need(tpl, image.count(), "sample_deformed: template length mismatch")
     w = _where_of(tpl, points)
     tpl, points = _as_input(tpl, w), _as_input(points, w)
-    n = (points.numel() if _is_torch(points) else points.size) // 3
+    n = _numel(points) // 3
     vals, parts = _empty_like_kind(points, n), _empty_like_kind(points, 3 * n)
     _check(lib().mfreg_cu_sample_deformed(C.byref(image.c()), _ptr(tpl)[0], _ptr(points)[0], n, _ptr(vals)[0],
                                           _ptr(parts)[0], w))
@@ -336,6 +364,7 @@ def sample_deformed(tpl, image: GridDesc, points):
 
 def downsample(v, image: GridDesc):
     """Block-mean halving (volume.cpp:123-160). Returns (data, coarse grid)."""
+    _need(v, image.count(), "downsample: volume length mismatch")
     w = _where_of(v)
     v = _as_input(v, w)
     og = _Grid()
@@ -348,6 +377,7 @@ def downsample(v, image: GridDesc):
 
 def prolong(y_coarse, coarse: GridDesc, fine: GridDesc):
     """Displacement prolongation (multilevel.cpp:78-115)."""
+    _need(y_coarse, 3 * coarse.count(), "prolong: field length mismatch")
     w = _where_of(y_coarse)
     y_coarse = _as_input(y_coarse, w)
     out = _empty_like_kind(y_coarse, 3 * fine.count())
@@ -356,6 +386,7 @@ def prolong(y_coarse, coarse: GridDesc, fine: GridDesc):
 
 
 def laplacian_apply(u_comp, g: GridDesc):
+    _need(u_comp, g.count(), "laplacian_apply: length mismatch")
     w = _where_of(u_comp)
     u_comp = _as_input(u_comp, w)
     out = _empty_like_kind(u_comp, g.count())
@@ -364,6 +395,7 @@ def laplacian_apply(u_comp, g: GridDesc):
 
 
 def curvature_value(u, g: GridDesc, mode: int = PARITY) -> float:
+    _need(u, 3 * g.count(), "curvature_value: length must be 3*m^y")
     w = _where_of(u)
     u = _as_input(u, w)
     v = C.c_double()
@@ -372,6 +404,7 @@ def curvature_value(u, g: GridDesc, mode: int = PARITY) -> float:
 
 
 def curvature_gradient(u, g: GridDesc):
+    _need(u, 3 * g.count(), "curvature: buffer length mismatch")
     w = _where_of(u)
     u = _as_input(u, w)
     out = _empty_like_kind(u, 3 * g.count())
@@ -380,6 +413,7 @@ def curvature_gradient(u, g: GridDesc):
 
 
 def curvature_hessian_vec(p, g: GridDesc):
+    _need(p, 3 * g.count(), "curvature: buffer length mismatch")
     w = _where_of(p)
     p = _as_input(p, w)
     out = _empty_like_kind(p, 3 * g.count())
@@ -401,6 +435,9 @@ class NgfContext:
     def __init__(self, reference, image: GridDesc, params: NgfParams = NgfParams(), mode: int = PARITY):
         self.image = image
         self.n = image.count()
+        if mode == Mode.FAST32:
+            raise ValueError("NGF kernel API: FAST32 is an Objective mode (the kernel-level NGF API is fp64)")
+        _need(reference, self.n, "NGF: reference length mismatch")
         w = _where_of(reference)
         reference = _as_input(reference, w)
         h = _vp()
@@ -415,7 +452,9 @@ class NgfContext:
 
     def populate(self, tpl, points) -> None:
         """populate_ngf_workspace (ngf.cpp:185-214)."""
-        w = _where_of(tpl, points)
+        _need(tpl, self.n, "NGF: template length mismatch")
+        _need(points, 3 * self.n, "transfer_apply: length mismatch")
+        w = _same_side(tpl, points)
         tpl, points = _as_input(tpl, w), _as_input(points, w)
         _check(lib().mfreg_cu_ngf_populate(self._h, _ptr(tpl)[0], _ptr(points)[0], w))
 
@@ -431,6 +470,7 @@ class NgfContext:
         return out
 
     def hessian_vec(self, p):
+        _need(p, 3 * self.n, "ngf_hessian_vec: vector length must be 3*m")
         w = _where_of(p)
         p = _as_input(p, w)
         out = _empty_like_kind(p, 3 * self.n)
@@ -500,7 +540,9 @@ class Objective:
     def __init__(self, reference, tpl, image: GridDesc, deform: GridDesc, params: NgfParams = NgfParams(),
                  alpha: float = 1.0, mode: int = PARITY):
         self.image, self.deform, self.params, self._alpha, self.mode = image, _nodal(deform), params, alpha, mode
-        w = _where_of(reference, tpl)
+        _need(reference, image.count(), "Objective: reference length mismatch")
+        _need(tpl, image.count(), "Objective: template length mismatch")
+        w = _same_side(reference, tpl)
         reference, tpl = _as_input(reference, w), _as_input(tpl, w)
         h = _vp()
         _check(lib().mfreg_cu_objective_create(_ptr(reference)[0], _ptr(tpl)[0], C.byref(image.c()),
@@ -539,6 +581,8 @@ class Objective:
 
     def eval(self, y, grad=None) -> float:
         """J(y); fills `grad` (same kind as y, length dof) when given."""
+        _need(y, self._dof, "Objective::eval: y length mismatch")
+        _need(grad, self._dof, "Objective::eval: grad length mismatch")
         if _dev_f64(y) and (grad is None or _dev_f64(grad)):  # direct path: CUDA fp64 contiguous tensors
             j = C.c_double()
             rc = _lib_fn("mfreg_cu_objective_eval")(self._h, y.data_ptr(), grad.data_ptr() if grad is not None else None,
@@ -546,10 +590,8 @@ class Objective:
             if rc:
                 _check(rc)
             return j.value
-        w = _where_of(y)
+        w = _same_side(y, grad)
         yy = _as_input(y, w)
-        if grad is not None and _where_of(grad) != w:
-            raise ValueError("y and grad must live on the same side")
         j = C.c_double()
         rc = _lib_fn("mfreg_cu_objective_eval")(self._h, _ptr(yy)[0], _ptr(grad)[0] if grad is not None else None, w,
                                                 C.byref(j))
@@ -568,12 +610,14 @@ class Objective:
         return r.value
 
     def gn_hessian_vec(self, p, q=None):
+        _need(p, self._dof, "transfer_apply: length mismatch")
+        _need(q, self._dof, "transfer_apply_transpose: length mismatch")
         if q is not None and _dev_f64(p) and _dev_f64(q):  # direct path: CUDA fp64 contiguous tensors
             rc = _lib_fn("mfreg_cu_objective_gn_hessian_vec")(self._h, p.data_ptr(), q.data_ptr(), DEVICE)
             if rc:
                 _check(rc)
             return q
-        w = _where_of(p)
+        w = _same_side(p, q)
         p = _as_input(p, w)
         q = _empty_like_kind(p, self._dof) if q is None else q
         rc = _lib_fn("mfreg_cu_objective_gn_hessian_vec")(self._h, _ptr(p)[0], _ptr(q)[0], w)
@@ -590,7 +634,9 @@ class Objective:
         return ms.value
 
     def seed_hessian_vec(self, p, gamma: float, q=None):
-        w = _where_of(p)
+        _need(p, self._dof, "curvature: buffer length mismatch")
+        _need(q, self._dof, "curvature: buffer length mismatch")
+        w = _same_side(p, q)
         p = _as_input(p, w)
         q = _empty_like_kind(p, self._dof) if q is None else q
         _check(lib().mfreg_cu_objective_seed_hessian_vec(self._h, _ptr(p)[0], float(gamma), _ptr(q)[0], w))
@@ -598,7 +644,9 @@ class Objective:
 
     def dot(self, a, b) -> float:
         """vec_dot (optimizer.cpp:12-19) over the dof this objective owns."""
-        w = _where_of(a, b)
+        _need(a, self._dof, "vec_dot: length mismatch")
+        _need(b, self._dof, "vec_dot: length mismatch")
+        w = _same_side(a, b)
         a, b = _as_input(a, w), _as_input(b, w)
         v = C.c_double()
         _check(lib().mfreg_cu_objective_dot(self._h, _ptr(a)[0], _ptr(b)[0], w, C.byref(v)))
@@ -607,6 +655,7 @@ class Objective:
 
 def cg_solve(obj: Objective, b, max_iters: int = 50, rel_tol: float = 1e-2, seed: bool = False, gamma: float = 0.0):
     """cg_solve (optimizer.cpp:113-154) on obj's GN operator (or the seed operator). Returns (x, iters, relres, breakdown)."""
+    _need(b, obj.dof(), "cg_solve: length mismatch")
     w = _where_of(b)
     b = _as_input(b, w)
     x = _empty_like_kind(b, obj.dof())
@@ -618,6 +667,7 @@ def cg_solve(obj: Objective, b, max_iters: int = 50, rel_tol: float = 1e-2, seed
 
 def _minimize(obj: Objective, y0, cfg: OptimizerConfig | None, method: int):
     cfg = cfg or OptimizerConfig()
+    _need(y0, obj.dof(), "Objective::eval: y length mismatch")
     w = _where_of(y0)
     y0 = _as_input(y0, w)
     y = _empty_like_kind(y0, obj.dof())
@@ -656,7 +706,9 @@ class MultilevelConfig:
 def register_multilevel(reference, tpl, image: GridDesc, cfg: MultilevelConfig | None = None):
     """register_multilevel (multilevel.cpp:117-145). Returns (y, deform_grid, per-level (traces, line_search_failed))."""
     cfg = cfg or MultilevelConfig()
-    w = _where_of(reference, tpl)
+    _need(reference, image.count(), "build_pyramid: image sizes differ")
+    _need(tpl, image.count(), "build_pyramid: image sizes differ")
+    w = _same_side(reference, tpl)
     reference, tpl = _as_input(reference, w), _as_input(tpl, w)
     dg = deformation_grid_for(image, cfg.deform_ratio)
     y = _empty_like_kind(reference, 3 * dg.count())

@@ -34,8 +34,19 @@ def _stale(obj: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def variant_lib(variant: str) -> str:
+    """Path of an experiment build (scripts/variants.py): libmfreg_cuda_<variant>.so."""
+    return os.path.join(HERE, "variants", f"libmfreg_cuda_{variant}.so")  # travels to the GPU box
+
+
+def build(verbose: bool = False, force: bool = False, variant: str = "", defines: tuple = ()) -> str:
+    """Compile the library; `variant`/`defines`: an A/B experiment build with extra -D flags
+    (loaded by the package when MFREG_LIB_VARIANT=<variant>)."""
+    obj_dir = os.path.join(OBJ, variant) if variant else OBJ
+    lib_path = variant_lib(variant) if variant else LIB
+    flags = NVCC_FLAGS + [f"-D{d}" for d in defines]
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
     headers.append(os.path.join(HERE, "..", "include", "mfreg_cuda.h"))
     jobs = []
@@ -43,9 +54,9 @@ def build(verbose: bool = False, force: bool = False) -> str:
         s = os.path.join(CSRC, src)
         if not os.path.exists(s):
             continue
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
-        if force or _stale(o, [s, *headers, __file__]):
-            jobs.append([_nvcc(), *NVCC_FLAGS, "-c", s, "-o", o])
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
+        if force or variant or _stale(o, [s, *headers, __file__]):
+            jobs.append([_nvcc(), *flags, "-c", s, "-o", o])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -56,10 +67,10 @@ def build(verbose: bool = False, force: bool = False) -> str:
 
     with cf.ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 4))) as ex:
         list(ex.map(run, jobs))
-    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
-    if jobs or not os.path.exists(LIB) or _stale(LIB, objs):
-        run([_nvcc(), *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"])
-    return LIB
+    objs = [os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    if jobs or not os.path.exists(lib_path) or _stale(lib_path, objs):
+        run([_nvcc(), *ARCH, "-shared", "-o", lib_path, *objs, "-lcudart"])
+    return lib_path
 
 
 if __name__ == "__main__":

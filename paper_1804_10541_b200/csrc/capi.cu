@@ -312,6 +312,8 @@ int mfreg_cu_curvature_hessian_vec(const mfreg_cu_grid* nodal, const double* p, 
 int mfreg_cu_ngf_create(const double* ref, const mfreg_cu_grid* image, double tau, double rho, int mode, int where,
                         mfreg_cu_ngf** out) {
     return guard([&] {
+        if (mode == MFREG_CU_FAST32)  // DeviceNgf's unfused kernels need the fp64 state
+            throw std::invalid_argument("NGF kernel API: FAST32 is an Objective mode (the kernel-level NGF API is fp64)");
         auto h = std::make_unique<mfreg_cu_ngf>();
         h->g = to_grid(image);
         validate_grid(h->g, false);

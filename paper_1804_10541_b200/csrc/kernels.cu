@@ -164,46 +164,12 @@ __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __
 #ifndef MFREG_WARP_MINB
 #define MFREG_WARP_MINB 6
 #endif
+// trilinear T at the sample point pt (the reference's cell choice) and its analytic
+// gradient, stored at image index (x, yy, z); shared by the two fast warp kernels
 template <typename OutT>
-__global__ void __launch_bounds__(256, MFREG_WARP_MINB) k_warp_fast(DevPlan P, const double* __restrict__ y,
-                                                   const double* __restrict__ T, OutT* __restrict__ Tw,
-                                                   OutT* __restrict__ dT, int zoff) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the eval pass (PDL) may queue behind
-    const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
-    const int x = blockIdx.x * 32 + threadIdx.x, yy = blockIdx.y * 8 + threadIdx.y;
-    const int z = blockIdx.z + zoff;
-    if (x >= mx || yy >= my) return;
-    const int bx = __ldg(&P.base[0][x]), by = __ldg(&P.base[1][yy]), bz = __ldg(&P.base[2][z]);
-    const double rx = __ldg(&P.rem[0][x]), ry = __ldg(&P.rem[1][yy]), rz = __ldg(&P.rem[2][z]);
-    const double wx[2] = {1.0 - rx, rx}, wy[2] = {1.0 - ry, ry}, wz[2] = {1.0 - rz, rz};
-    double w[8];
-#pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-            for (int a = 0; a < 2; ++a) w[(g * 2 + b) * 2 + a] = wx[a] * wy[b] * wz[g];
-    // 32-bit element offsets (nodal arrays and image volumes are < 2^31 elements)
-    const int ns = static_cast<int>(P.src.count());
-    const int sm0 = static_cast<int>(P.src.m[0]), sm01 = static_cast<int>(P.src.m[0] * P.src.m[1]);
-    // four corner-row pointers (b, g); the a = 1 corner is an immediate offset
-    const double* yr[2][2];
-    yr[0][0] = y + (bx + by * sm0 + bz * sm01);
-    yr[0][1] = yr[0][0] + sm0;
-    yr[1][0] = yr[0][0] + sm01;
-    yr[1][1] = yr[1][0] + sm0;
-    double pt[3];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-        double acc = 0.0;
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-#pragma unroll
-            for (int b = 0; b < 2; ++b)
-#pragma unroll
-                for (int a = 0; a < 2; ++a) acc += w[(g * 2 + b) * 2 + a] * __ldg(yr[g][b] + d * ns + a);
-        pt[d] = acc;
-    }
+__device__ __forceinline__ void warp_sample_store(const DevPlan& P, const double* __restrict__ T, const double pt[3],
+                                                  int x, int yy, int z, int mx, int my, int mz,
+                                                  OutT* __restrict__ Tw, OutT* __restrict__ dT) {
     const int m3[3] = {mx, my, mz};
     int i0[3];
     double f[3];
@@ -1037,6 +1003,131 @@ HvTable make_hv_table(const Grid& g) {
 void launch_transfer_apply(const DevPlan& P, const double* y, double* out, cudaStream_t s) {
     note_launch(), k_transfer_apply<<<grid3(P.tgt), block3(), 0, s>>>(P, y, out);
 }
+
+template <typename OutT>
+__global__ void __launch_bounds__(256, MFREG_WARP_MINB) k_warp_fast(DevPlan P, const double* __restrict__ y,
+                                                   const double* __restrict__ T, OutT* __restrict__ Tw,
+                                                   OutT* __restrict__ dT, int zoff) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the eval pass (PDL) may queue behind
+    const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
+    const int x = blockIdx.x * 32 + threadIdx.x, yy = blockIdx.y * 8 + threadIdx.y;
+    const int z = blockIdx.z + zoff;
+    if (x >= mx || yy >= my) return;
+    const int bx = __ldg(&P.base[0][x]), by = __ldg(&P.base[1][yy]), bz = __ldg(&P.base[2][z]);
+    const double rx = __ldg(&P.rem[0][x]), ry = __ldg(&P.rem[1][yy]), rz = __ldg(&P.rem[2][z]);
+    const double wx[2] = {1.0 - rx, rx}, wy[2] = {1.0 - ry, ry}, wz[2] = {1.0 - rz, rz};
+    double w[8];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int a = 0; a < 2; ++a) w[(g * 2 + b) * 2 + a] = wx[a] * wy[b] * wz[g];
+    // 32-bit element offsets (nodal arrays and image volumes are < 2^31 elements)
+    const int ns = static_cast<int>(P.src.count());
+    const int sm0 = static_cast<int>(P.src.m[0]), sm01 = static_cast<int>(P.src.m[0] * P.src.m[1]);
+    // four corner-row pointers (b, g); the a = 1 corner is an immediate offset
+    const double* yr[2][2];
+    yr[0][0] = y + (bx + by * sm0 + bz * sm01);
+    yr[0][1] = yr[0][0] + sm0;
+    yr[1][0] = yr[0][0] + sm01;
+    yr[1][1] = yr[1][0] + sm0;
+    double pt[3];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+        double acc = 0.0;
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) acc += w[(g * 2 + b) * 2 + a] * __ldg(yr[g][b] + d * ns + a);
+        pt[d] = acc;
+    }
+    warp_sample_store(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+}
+
+// z-marching fast warp: one thread per image column (x, y) over a chunk of planes. The
+// column's x-y corner weights wx*wy are formed once; the nodal values of the current nodal z
+// cell (two nodal planes over the block's x-y footprint, 3 components) are staged in shared
+// memory once per cell (every ~ratio planes) instead of 24 global loads per voxel. Per plane,
+// P y is 8 + 24 multiplies and 24 adds in the reference's operation order
+// (transfer.cpp:66-81: acc += ((wx*wy)*wz)*y, (g,b,a) order from 0.0), bitwise the same as
+// transfer_point / k_warp_fast.
+constexpr int WZ_NXF = 34, WZ_NYF = 10;
+#ifndef MFREG_WARPZ_MINB
+#define MFREG_WARPZ_MINB 5  // measured at C4: 5 blocks (48 regs) 3.01 ms, 6 (40, spills) 2.96, 4 (64) 3.16; nodal values in registers, 2 blocks: 3.90; per-voxel kernel 3.52
+#endif  // nodal footprint bound of a 32x8 column block (ratio >= 1)
+template <typename OutT>
+__global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, const double* __restrict__ y,
+                                                   const double* __restrict__ T, OutT* __restrict__ Tw,
+                                                   OutT* __restrict__ dT, int zlo, int zhi, int zc) {
+    __shared__ double sy[3][2][WZ_NYF][WZ_NXF];
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the eval pass (PDL) may queue behind
+    const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+    const int x = x0 + threadIdx.x, yy = y0 + threadIdx.y;
+    const bool in = x < mx && yy < my;
+    const int xc = min(x, mx - 1), yc = min(yy, my - 1);
+    const int zb = zlo + static_cast<int>(blockIdx.z) * zc, ze = min(zhi, zb + zc);
+    const int fx0 = __ldg(&P.base[0][x0]), fy0 = __ldg(&P.base[1][y0]);
+    const int nxf = __ldg(&P.base[0][min(x0 + 31, mx - 1)]) - fx0 + 2;
+    const int nyf = __ldg(&P.base[1][min(y0 + 7, my - 1)]) - fy0 + 2;
+    const int lx = __ldg(&P.base[0][xc]) - fx0, ly = __ldg(&P.base[1][yc]) - fy0;
+    const double rx = __ldg(&P.rem[0][xc]), ry = __ldg(&P.rem[1][yc]);
+    const double wx[2] = {1.0 - rx, rx}, wy[2] = {1.0 - ry, ry};
+    double wxy[2][2];
+#pragma unroll
+    for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) wxy[b][a] = wx[a] * wy[b];
+    const int ns = static_cast<int>(P.src.count());
+    const int sm0 = static_cast<int>(P.src.m[0]), sm01 = static_cast<int>(P.src.m[0] * P.src.m[1]);
+    const int tid = threadIdx.x + 32 * threadIdx.y, nfill = 3 * 2 * nyf * nxf;
+    auto ptof = [&](double rz, double pt[3]) {
+        const double wz[2] = {1.0 - rz, rz};
+        double w[2][2][2];
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int b = 0; b < 2; ++b)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) w[g][b][a] = wxy[b][a] * wz[g];
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            double acc = 0.0;
+#pragma unroll
+            for (int g = 0; g < 2; ++g)
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int a = 0; a < 2; ++a) acc += w[g][b][a] * sy[d][g][ly + b][lx + a];
+            pt[d] = acc;
+        }
+    };
+    int cur = -1;
+#pragma unroll 1
+    for (int z = zb; z < ze;) {
+        const int bz = __ldg(&P.base[2][z]);
+        if (bz != cur) {  // uniform across the block (same plane): restage the cell's nodal values
+            cur = bz;
+            __syncthreads();
+            for (int t = tid; t < nfill; t += 256) {
+                const int ix = t % nxf, r = t / nxf, iy = r % nyf, gd = r / nyf;  // gd = d * 2 + g
+                (&sy[0][0][0][0])[(gd * WZ_NYF + iy) * WZ_NXF + ix] =
+                    __ldg(y + (gd >> 1) * ns + (bz + (gd & 1)) * sm01 + (fy0 + iy) * sm0 + fx0 + ix);
+            }
+            __syncthreads();
+        }
+        if (in) {
+            double pt[3];
+            ptof(__ldg(&P.rem[2][z]), pt);
+            warp_sample_store(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+        }
+        ++z;
+    }
+}
+
 void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s) {
     note_launch(), k_transfer_T<<<grid3(P.src), block3(), 0, s>>>(P, w, out);
 }
@@ -1063,8 +1154,22 @@ void warp_fast_impl(const DevPlan& P0, const double* y, const double* T, OutT* T
     P.tgt.set_inv();
     if (zhi < 0) zhi = static_cast<int>(P.tgt.m[2]);
     if (zhi <= zlo) return;
-    const dim3 gr(static_cast<unsigned>((P.tgt.m[0] + 31) / 32), static_cast<unsigned>((P.tgt.m[1] + 7) / 8),
-                  static_cast<unsigned>(zhi - zlo));
+    const unsigned gx = static_cast<unsigned>((P.tgt.m[0] + 31) / 32), gy = static_cast<unsigned>((P.tgt.m[1] + 7) / 8);
+    static const bool zmarch = [] {
+        const char* e = std::getenv("MFREG_WARP_Z");
+        return !(e && e[0] == '0');
+    }();
+    if (zmarch) {
+        // z chunks: enough blocks for ~8 per SM, each chunk <= 64 planes
+        const int nz = zhi - zlo;
+        const long long cols = static_cast<long long>(gx) * gy;
+        const int nch = std::max<int>((nz + 63) / 64, static_cast<int>(std::min<long long>(nz, (148LL * 8 + cols - 1) / cols)));
+        const int zc = (nz + nch - 1) / nch;
+        const dim3 gr(gx, gy, static_cast<unsigned>((nz + zc - 1) / zc));
+        note_launch(), k_warp_z<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo, zhi, zc);
+        return;
+    }
+    const dim3 gr(gx, gy, static_cast<unsigned>(zhi - zlo));
     note_launch(), k_warp_fast<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo);
 }
 __global__ void k_to_float(idx_t n, const double* __restrict__ a, float* __restrict__ o) {
