@@ -4,7 +4,7 @@
  *
  * Drop-in boundary for the reference C++ library mfreg (/root/reference/proj).
  * The reference has no FFI; its public surface is the C++ API in
- * include/mfreg/*.hpp. Each entry point below names the reference declaration
+ * include/mfreg/<name>.hpp. Each entry point below names the reference declaration
  * it replaces (file:line under /root/reference/proj/include/mfreg/). Plain
  * pointers and sizes only; no C++ or torch types cross this boundary.
  *
@@ -210,6 +210,79 @@ int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfr
                                  const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
                                  mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
                                  int where);
+
+/* register_multilevel with the per-level results of multilevel.hpp:47-51: level_image_grids /
+ * level_deform_grids [levels] (coarsest first) and, when level_y is non-NULL, every level's
+ * final deformation concatenated coarsest first (3 * count(level deform grid) each; at most
+ * level_y_cap doubles, else MFREG_CU_EINVAL). */
+int mfreg_cu_register_multilevel_ex(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                    const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
+                                    mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
+                                    mfreg_cu_grid* level_image_grids, mfreg_cu_grid* level_deform_grids,
+                                    double* level_y, int64_t level_y_cap, int where);
+
+/* ---- drop-in API: the rest of the reference's public surface (csrc/api.cu) ----------
+ * All computed on the GPU in the reference's operation order (bitwise in parity). */
+
+/* vec_dot / vec_inf_norm (optimizer.hpp:18-20; optimizer.cpp:12-29): the exact
+ * 4096-element chunked sum of the reference; vec_norm = sqrt(vec_dot(a, a)) */
+int mfreg_cu_vec_dot(const double* a, const double* b, int64_t n, int where, double* out);
+int mfreg_cu_vec_inf_norm(const double* a, int64_t n, int where, double* out);
+/* make_transfer_plan (transfer.hpp:22; transfer.cpp:11-47): base[k], rem[k] over the image
+ * axes concatenated (m_x, then m_y, then m_z entries); either may be NULL */
+int mfreg_cu_transfer_plan(const mfreg_cu_grid* nodal, const mfreg_cu_grid* image, int64_t* base, double* rem);
+/* discrete_gradient (volume.hpp:50-51; volume.cpp:96-109) at the voxels idx[0..n) (host
+ * array; NULL = every voxel in order) -> out6[6k..6k+5] (backward x,y,z, forward x,y,z) */
+int mfreg_cu_discrete_gradient(const mfreg_cu_grid* image, const double* v, const int64_t* idx, int64_t n,
+                               double* out6, int where);
+/* eps_norm (volume.hpp:53; volume.cpp:115-121) of n 6-vectors */
+int mfreg_cu_eps_norm(const double* g6, int64_t n, double eps, double* out, int where);
+/* laplacian(u_comp, g, i) (curvature.hpp:13; curvature.cpp:9-21) at the nodes idx[0..n) (host array) */
+int mfreg_cu_laplacian_at(const mfreg_cu_grid* nodal, const double* u_comp, const int64_t* idx, int64_t n, double* out,
+                          int where);
+/* nodal_interpolate(comp, g, p) (multilevel.hpp:28-29; multilevel.cpp:51-76) at n points
+ * (x, y, z interleaved) */
+int mfreg_cu_nodal_interpolate(const mfreg_cu_grid* nodal, const double* comp, const double* pts, int64_t n,
+                               double* out, int where);
+/* make_ngf_precomp (ngf.hpp:26; ngf.cpp:167-183): ref_grads [m][6], ref_norms [m] */
+int mfreg_cu_ngf_precomp(const double* ref, const mfreg_cu_grid* image, double rho, double* ref_grads,
+                         double* ref_norms, int where);
+/* NgfWorkspace::tpl_grads [m][6] of the last mfreg_cu_ngf_populate (ngf.cpp:195-201) */
+int mfreg_cu_ngf_tpl_grads(mfreg_cu_ngf* ngf, double* tpl_grads, int where);
+/* make_offset_table (ngf.hpp:67-85; ngf.cpp:267-300): entries grouped by linear kappa,
+ * ascending; pairs (a, b) as Dir values, flattened entry by entry (<= 25 entries, 49 pairs);
+ * MFREG_CU_ELOGIC on the closed-form mismatch, as the reference */
+int mfreg_cu_offset_table(const mfreg_cu_grid* image, int* nentries, int64_t* kappa, int* npairs, int* pairs);
+/* armijo_search (optimizer.hpp:138-139; optimizer.cpp:156-175) on a host phi(eta); phi sets
+ * *err != 0 to abort (MFREG_CU_EOTHER) */
+int mfreg_cu_armijo_search(double (*phi)(void* ctx, double eta, int* err), void* ctx, double f0, double gdotd,
+                           double c1, double beta, int max_backtracks, double eta0, double* eta, int* accepted,
+                           int* descent, double* f_new);
+
+/* A host-defined mfreg::Problem (optimizer.hpp:36-48) as C callbacks. Vectors passed to the
+ * callbacks are host memory of length n; a callback returns 0 on success. alpha,
+ * last_distance and last_regularizer may be NULL (0.0, the Problem defaults). */
+typedef struct {
+    void* ctx;
+    int (*eval)(void* ctx, const double* y, double* grad /* NULL: value only */, double* j);
+    int (*gn_hessian_vec)(void* ctx, const double* p, double* q);
+    int (*seed_hessian_vec)(void* ctx, const double* p, double gamma, double* q);
+    double (*min_spacing)(void* ctx);
+    double (*alpha)(void* ctx);
+    double (*last_distance)(void* ctx);
+    double (*last_regularizer)(void* ctx);
+} mfreg_cu_problem_ops;
+/* lbfgs_minimize / gauss_newton_minimize (optimizer.hpp:162-165) on a host Problem: the
+ * solver loops run device-resident (vectors in HBM, exact chunked reductions), the
+ * problem's operators are called back on host copies */
+int mfreg_cu_problem_minimize(const mfreg_cu_problem_ops* ops, int64_t n, int method, const double* y0,
+                              const mfreg_cu_opt_config* cfg, double* y_out, mfreg_cu_iter_record* trace, int cap,
+                              int* ntrace, int* line_search_failed, int where);
+/* cg_solve(apply, b, cfg) (optimizer.hpp:123; optimizer.cpp:113-154): apply =
+ * ops->gn_hessian_vec (op 0) or ops->seed_hessian_vec with gamma (op 1) */
+int mfreg_cu_problem_cg_solve(const mfreg_cu_problem_ops* ops, int64_t n, int op, double gamma, const double* b,
+                              int max_iters, double rel_tol, double* x, int* iters, double* relres, int* breakdown,
+                              int where);
 
 /* ---- synthetic inputs (synthetic.hpp:13-44) --------------------------------- */
 int mfreg_cu_make_phantom(const mfreg_cu_grid* image, double* out, int where);

@@ -135,6 +135,27 @@ _SIGS = {
     "mfreg_cu_make_phantom": ([_gp, _dp, C.c_int], C.c_int),
     "mfreg_cu_warp_sinusoid": ([_gp, _dp, C.c_double, C.c_uint64, _dp, C.c_int], C.c_int),
     "mfreg_cu_scale": ([C.c_int64, C.c_double, _dp, C.c_int], C.c_int),
+    "mfreg_cu_register_multilevel_ex": ([_dp, _dp, _gp, C.POINTER(_MlConfig), _dp, _gp, C.POINTER(_IterRecord),
+                                         C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), _gp, _gp, _dp, C.c_int64,
+                                         C.c_int], C.c_int),
+    "mfreg_cu_vec_dot": ([_dp, _dp, C.c_int64, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_vec_inf_norm": ([_dp, C.c_int64, C.c_int, C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_transfer_plan": ([_gp, _gp, _dp, _dp], C.c_int),
+    "mfreg_cu_discrete_gradient": ([_gp, _dp, _dp, C.c_int64, _dp, C.c_int], C.c_int),
+    "mfreg_cu_eps_norm": ([_dp, C.c_int64, C.c_double, _dp, C.c_int], C.c_int),
+    "mfreg_cu_laplacian_at": ([_gp, _dp, _dp, C.c_int64, _dp, C.c_int], C.c_int),
+    "mfreg_cu_nodal_interpolate": ([_gp, _dp, _dp, C.c_int64, _dp, C.c_int], C.c_int),
+    "mfreg_cu_ngf_precomp": ([_dp, _gp, C.c_double, _dp, _dp, C.c_int], C.c_int),
+    "mfreg_cu_ngf_tpl_grads": ([_vp, _dp, C.c_int], C.c_int),
+    "mfreg_cu_offset_table": ([_gp, C.POINTER(C.c_int), _dp, _dp, _dp], C.c_int),
+    "mfreg_cu_armijo_search": ([C.c_void_p, C.c_void_p, C.c_double, C.c_double, C.c_double, C.c_double, C.c_int,
+                                C.c_double, C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_problem_minimize": ([C.c_void_p, C.c_int64, C.c_int, _dp, C.POINTER(_OptConfig), _dp,
+                                   C.POINTER(_IterRecord), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int],
+                                  C.c_int),
+    "mfreg_cu_problem_cg_solve": ([C.c_void_p, C.c_int64, C.c_int, C.c_double, _dp, C.c_int, C.c_double, _dp,
+                                   C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int], C.c_int),
 }
 
 _lib = None

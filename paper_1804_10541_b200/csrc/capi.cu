@@ -7,130 +7,19 @@
 #include <string>
 
 #include "../../include/mfreg_cuda.h"
+#include "capi_util.cuh"
 #include "io.cuh"
 #include "objective.cuh"
 
 using namespace mfreg_b200;
+using namespace mfreg_b200::capi;
+
+std::string& mfreg_b200::capi::last_error() {
+    static thread_local std::string e;
+    return e;
+}
 
 namespace {
-
-thread_local std::string g_err;
-
-template <typename Fn>
-int guard(Fn&& fn) {
-    try {
-        fn();
-        return MFREG_CU_OK;
-    } catch (const std::invalid_argument& e) {
-        g_err = e.what();
-        return MFREG_CU_EINVAL;
-    } catch (const CudaError& e) {
-        g_err = e.what();
-        return MFREG_CU_ECUDA;
-    } catch (const std::logic_error& e) {
-        g_err = e.what();
-        return MFREG_CU_ELOGIC;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return MFREG_CU_EOTHER;
-    }
-}
-
-Grid to_grid(const mfreg_cu_grid* g) {
-    if (!g) throw std::invalid_argument("null grid");
-    Grid r{};
-    for (int a = 0; a < 3; ++a) {
-        r.m[a] = g->m[a];
-        r.h[a] = g->h[a];
-    }
-    return r;
-}
-void from_grid(const Grid& g, mfreg_cu_grid* o) {
-    for (int a = 0; a < 3; ++a) {
-        o->m[a] = g.m[a];
-        o->h[a] = g.h[a];
-    }
-}
-
-void check_where(int where) {
-    if (where != MFREG_CU_HOST && where != MFREG_CU_DEVICE) throw std::invalid_argument("where must be HOST or DEVICE");
-}
-
-// Read-only input: device view of a host or device array of n doubles.
-// `cache`: a per-handle staging buffer reused across calls (no cudaMalloc/cudaFree
-// on the per-iteration path); null = a temporary.
-struct In {
-    In(const double* p, std::size_t n, int where, cudaStream_t s, DVec* cache = nullptr) {
-        check_where(where);
-        if (where == MFREG_CU_DEVICE || !p) {
-            ptr = p;
-        } else {
-            DVec& b = cache ? *cache : buf;
-            if (b.size() < n) b.resize(n);
-            MFREG_CUDA(cudaMemcpyAsync(b.get(), p, n * sizeof(double), cudaMemcpyHostToDevice, s));
-            ptr = b.get();
-        }
-    }
-    DVec buf;
-    const double* ptr = nullptr;
-};
-
-// Output: device buffer written by kernels, copied back on finish() for host.
-struct Out {
-    Out(double* p, std::size_t n, int where, DVec* cache = nullptr) : host(p), n(n), where(where) {
-        check_where(where);
-        if (where == MFREG_CU_DEVICE || !p) {
-            ptr = p;
-        } else {
-            DVec& b = cache ? *cache : buf;
-            if (b.size() < n) b.resize(n);
-            ptr = b.get();
-        }
-    }
-    void finish(cudaStream_t s) {
-        if (where == MFREG_CU_HOST && host) {
-            MFREG_CUDA(cudaMemcpyAsync(host, ptr, n * sizeof(double), cudaMemcpyDeviceToHost, s));
-            MFREG_CUDA(cudaStreamSynchronize(s));
-        }
-    }
-    double* host;
-    std::size_t n;
-    int where;
-    DVec buf;
-    double* ptr = nullptr;
-};
-
-Mode to_mode(int mode) {
-    if (mode != MFREG_CU_PARITY && mode != MFREG_CU_FAST && mode != MFREG_CU_FAST32)
-        throw std::invalid_argument("mode must be PARITY, FAST or FAST32");
-    return static_cast<Mode>(mode);
-}
-
-OptimizerConfig to_cfg(const mfreg_cu_opt_config* k) {
-    OptimizerConfig c;
-    if (!k) return c;
-    c.max_iters = k->max_iters;
-    c.armijo = {k->c1, k->beta, k->max_backtracks};
-    c.cg = {k->cg_max_iters, k->cg_rel_tol};
-    c.h0_cg = {k->h0_max_iters, k->h0_rel_tol};
-    c.lbfgs_history = k->lbfgs_history;
-    c.gamma = k->gamma;
-    c.tol_rel_j = k->tol_rel_j;
-    c.tol_grad = k->tol_grad;
-    c.tol_step = k->tol_step;
-    return c;
-}
-
-int copy_trace(const std::vector<IterationRecord>& t, mfreg_cu_iter_record* out, int cap) {
-    int n = 0;
-    for (const auto& r : t) {
-        if (out && n < cap) out[n] = {r.iter, r.cg_iters, r.j, r.distance, r.regularizer, r.grad_norm, r.step};
-        ++n;
-    }
-    return n;
-}
-
-constexpr cudaStream_t kStream = 0;  // legacy default stream: ordered with torch's default stream
 
 // synthetic.cpp:110-143, computed with the same libstdc++ engine/distributions
 WarpTerms sinusoid_terms(const double extent[3], double max_amp, std::uint64_t seed) {
@@ -160,22 +49,9 @@ WarpTerms sinusoid_terms(const double extent[3], double max_amp, std::uint64_t s
 
 }  // namespace
 
-struct mfreg_cu_ngf {
-    Grid g;
-    DVec R;
-    std::unique_ptr<DeviceNgf> ngf;
-};
-
-struct mfreg_cu_objective {
-    Grid img, dg;
-    DVec R, T;
-    std::unique_ptr<DeviceObjective> obj;
-    DVec stage[4];  // host-call staging (y / p in, grad / q out), reused
-};
-
 extern "C" {
 
-const char* mfreg_cu_last_error(void) { return g_err.c_str(); }
+const char* mfreg_cu_last_error(void) { return last_error().c_str(); }
 int mfreg_cu_version(void) { return 1; }
 int mfreg_cu_device_count(int* n) { return guard([&] { MFREG_CUDA(cudaGetDeviceCount(n)); }); }
 int mfreg_cu_set_device(int device) { return guard([&] { MFREG_CUDA(cudaSetDevice(device)); }); }
@@ -575,10 +451,11 @@ int mfreg_cu_prolong(const mfreg_cu_grid* coarse, const mfreg_cu_grid* fine, con
     });
 }
 
-int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfreg_cu_grid* image,
-                                 const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
-                                 mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
-                                 int where) {
+static int register_multilevel_impl(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                    const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
+                                    mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
+                                    mfreg_cu_grid* level_image, mfreg_cu_grid* level_deform, double* level_y,
+                                    int64_t level_y_cap, int where) {
     return guard([&] {
         const Grid g = to_grid(image);
         validate_grid(g, false);
@@ -593,13 +470,24 @@ int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfr
         mc.method = cfg->method == MFREG_CU_GAUSS_NEWTON ? Method::GaussNewton : Method::Lbfgs;
         mc.mode = to_mode(cfg->mode);
         mc.opt = to_cfg(&cfg->opt);
+        mc.keep_level_y = level_y != nullptr;
         MultilevelResult res = register_multilevel(r.ptr, t.ptr, g, mc, kStream);
         if (deform_out) from_grid(res.deform_grid, deform_out);
         check_where(where);
-        if (y_out)
-            MFREG_CUDA(cudaMemcpyAsync(y_out, res.y.get(), res.y.size() * sizeof(double),
-                                       where == MFREG_CU_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
-                                       kStream));
+        const cudaMemcpyKind kind = where == MFREG_CU_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (y_out) MFREG_CUDA(cudaMemcpyAsync(y_out, res.y.get(), res.y.size() * sizeof(double), kind, kStream));
+        int64_t yoff = 0;
+        for (std::size_t l = 0; l < res.levels.size(); ++l) {
+            if (level_image) from_grid(res.levels[l].image_grid, level_image + l);
+            if (level_deform) from_grid(res.levels[l].deform_grid, level_deform + l);
+            if (level_y) {
+                const auto& yl = res.levels[l].y;
+                if (yoff + static_cast<int64_t>(yl.size()) > level_y_cap)
+                    throw std::invalid_argument("register_multilevel: level_y buffer too small");
+                MFREG_CUDA(cudaMemcpyAsync(level_y + yoff, yl.get(), yl.size() * sizeof(double), kind, kStream));
+                yoff += static_cast<int64_t>(yl.size());
+            }
+        }
         MFREG_CUDA(cudaStreamSynchronize(kStream));
         int off = 0;
         for (std::size_t l = 0; l < res.levels.size(); ++l) {
@@ -610,6 +498,24 @@ int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfr
             off += k;
         }
     });
+}
+
+int mfreg_cu_register_multilevel(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                 const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
+                                 mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
+                                 int where) {
+    return register_multilevel_impl(ref, tpl, image, cfg, y_out, deform_out, trace, cap, level_iters,
+                                    line_search_failed, nullptr, nullptr, nullptr, 0, where);
+}
+
+int mfreg_cu_register_multilevel_ex(const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                                    const mfreg_cu_ml_config* cfg, double* y_out, mfreg_cu_grid* deform_out,
+                                    mfreg_cu_iter_record* trace, int cap, int* level_iters, int* line_search_failed,
+                                    mfreg_cu_grid* level_image_grids, mfreg_cu_grid* level_deform_grids,
+                                    double* level_y, int64_t level_y_cap, int where) {
+    return register_multilevel_impl(ref, tpl, image, cfg, y_out, deform_out, trace, cap, level_iters,
+                                    line_search_failed, level_image_grids, level_deform_grids, level_y, level_y_cap,
+                                    where);
 }
 
 int mfreg_cu_make_phantom(const mfreg_cu_grid* image, double* out, int where) {

@@ -426,10 +426,12 @@ struct MultilevelConfig {
     Method method = Method::Lbfgs;
     Mode mode = Mode::Parity;
     OptimizerConfig opt{};
+    bool keep_level_y = false;  // LevelResult::y (multilevel.hpp:47-51 result.y) for every level
 };
 struct LevelResult {
     Grid image_grid, deform_grid;
     MinimizeResult result;
+    DVec y;  // the level's final deformation (when MultilevelConfig::keep_level_y)
 };
 struct MultilevelResult {
     DVec y;

@@ -266,8 +266,13 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
                                                          : gauss_newton_minimize(obj, y0.get(), yl.get(), cfg.opt);
         MFREG_CUDA(cudaStreamSynchronize(s));
         if (trace_time()) std::fprintf(stderr, "level %d: total %.2f ms\n", l, ms_since(t_level));
+        LevelResult lr{G[l], dg, std::move(res), DVec()};
+        if (cfg.keep_level_y) {
+            lr.y.resize(static_cast<std::size_t>(obj.dof()));
+            MFREG_CUDA(cudaMemcpyAsync(lr.y.get(), yl.get(), obj.dof() * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        }
         y = std::move(yl);
-        out.levels.push_back({G[l], dg, std::move(res)});
+        out.levels.push_back(std::move(lr));
         prev = dg;
         have_prev = true;
     }

@@ -51,3 +51,33 @@ def test_drop_in_matches_reference(tmp_path, oracle):
     assert len(its) == len(trace)
     for row, ref in zip(its, trace):
         assert float(row[3]) == ref[2] and int(row[5]) == ref[1] and float(row[7]) == ref[6]
+
+
+def _build_client(tmp_path):
+    import paper_1804_10541_b200 as P
+    if not os.path.exists(P._LIB_PATH):
+        P.build()
+    exe = str(tmp_path / "api_client")
+    libdir = os.path.dirname(P._LIB_PATH)
+    subprocess.run(["g++", "-std=c++20", "-O2", "-Wall", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "api_client.cpp"), "-L", libdir, "-lmfreg_cuda",
+                    f"-Wl,-rpath,{libdir}", "-o", exe], check=True)
+    return exe
+
+
+def test_api_client_compiles_unchanged(tmp_path):
+    """The reference-style client (a user Problem, cg_solve / armijo_search with lambdas, the
+    kernel-level ngf / volume / transfer / curvature / multilevel calls, LevelResult fields)
+    compiles against the drop-in header exactly as it does against the reference headers."""
+    assert os.path.exists(_build_client(tmp_path))
+
+
+@pytest.mark.gpu
+def test_api_client_matches_reference(tmp_path):
+    """Every printed result (bit patterns and byte hashes) equals the unmodified reference's
+    output on the same inputs (tests/golden/api_client_ref.txt, gen_api_client.py)."""
+    out = subprocess.run([_build_client(tmp_path)], capture_output=True, text=True, check=True).stdout.splitlines()
+    ref = open(os.path.join(ROOT, "tests", "golden", "api_client_ref.txt")).read().splitlines()
+    assert len(out) == len(ref)
+    bad = [(o, r) for o, r in zip(out, ref) if o != r]
+    assert not bad, bad[:10]
