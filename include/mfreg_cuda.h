@@ -191,6 +191,52 @@ int mfreg_cu_objective_create_slab(const double* ref, const double* tpl, const m
                                    const mfreg_cu_grid* deform, double tau, double rho, double alpha,
                                    const int32_t slab[4], int where, mfreg_cu_objective** out);
 
+/* ---- z slabs in the library (csrc/slab.cu): one rank per GPU --------
+ * A communicator carries the plane exchanges (ncclSend/ncclRecv) and the scalar
+ * all-gathers (ncclAllGather); scalars are summed in rank order, so every rank holds
+ * identical J / dot products and takes identical solver branches. */
+typedef struct mfreg_cu_comm mfreg_cu_comm;
+typedef struct mfreg_cu_slab mfreg_cu_slab;
+/* ncclGetUniqueId on one rank; every rank passes the same 128 bytes to create_nccl */
+int mfreg_cu_comm_nccl_unique_id(unsigned char out[128]);
+/* NCCL communicator of `nranks` on the calling thread's current device (libnccl.so.2 is
+ * loaded at run time) */
+int mfreg_cu_comm_create_nccl(const unsigned char id[128], int nranks, int rank, mfreg_cu_comm** out);
+/* `nranks` in-process communicators (out[0..nranks)) for ranks running as threads of one
+ * process, on one or several devices (device copies + host barriers) */
+int mfreg_cu_comm_create_local(int nranks, mfreg_cu_comm** out);
+int mfreg_cu_comm_destroy(mfreg_cu_comm* comm);
+int mfreg_cu_comm_rank(mfreg_cu_comm* comm, int* rank, int* size);
+/* this rank's share of Objective (optimizer.hpp:53-106), fast mode: ref / tpl are the whole
+ * volume (replicated), the slab is slab_partition(image, deform, size)[rank] */
+int mfreg_cu_slab_create(mfreg_cu_comm* comm, const double* ref, const double* tpl, const mfreg_cu_grid* image,
+                         const mfreg_cu_grid* deform, double tau, double rho, double alpha, int where,
+                         mfreg_cu_slab** out);
+int mfreg_cu_slab_destroy(mfreg_cu_slab* slab);
+/* zlo, zhi, own_lo, own_hi, need_lo, need_hi, bnd of this rank */
+int mfreg_cu_slab_info(mfreg_cu_slab* slab, int32_t info[7]);
+int mfreg_cu_slab_identity(mfreg_cu_slab* slab, double* out_dev);
+/* Objective::eval on device vectors (full length 3 m^y, owned planes valid; the halo planes
+ * of y are overwritten): the global J on every rank; grad valid on the owned planes */
+int mfreg_cu_slab_eval(mfreg_cu_slab* slab, double* y_dev, double* grad_dev, double* j);
+int mfreg_cu_slab_last(mfreg_cu_slab* slab, double* distance, double* regularizer);
+/* Objective::gn_hessian_vec, q valid on the owned planes (p's halo planes overwritten) */
+int mfreg_cu_slab_gn_hessian_vec(mfreg_cu_slab* slab, double* p_dev, double* q_dev);
+/* vec_dot over the whole (sharded) vector, identical on every rank */
+int mfreg_cu_slab_dot(mfreg_cu_slab* slab, const double* a_dev, const double* b_dev, double* out);
+/* every rank's owned planes into v (the whole vector on every rank) */
+int mfreg_cu_slab_gather(mfreg_cu_slab* slab, double* v_dev);
+/* gauss_newton_minimize / lbfgs_minimize, sharded and device-resident; y_out gathered */
+int mfreg_cu_slab_minimize(mfreg_cu_slab* slab, int method, const double* y0_dev, const mfreg_cu_opt_config* cfg,
+                           double* y_out_dev, mfreg_cu_iter_record* trace, int cap, int* ntrace,
+                           int* line_search_failed);
+/* register_multilevel over z slabs (fast mode): every level sharded over the communicator
+ * (levels too thin for the slab halo run replicated); result on every rank */
+int mfreg_cu_slab_register_multilevel(mfreg_cu_comm* comm, const double* ref, const double* tpl,
+                                      const mfreg_cu_grid* image, const mfreg_cu_ml_config* cfg, double* y_out,
+                                      mfreg_cu_grid* deform_out, mfreg_cu_iter_record* trace, int cap, int* level_iters,
+                                      int* line_search_failed, int where);
+
 /* ---- solvers (optimizer.hpp:123-166) ---------------------------------------- */
 /* cg_solve on the objective's GN operator (op = 0) or seed operator (op = 1, gamma) */
 int mfreg_cu_cg_solve(mfreg_cu_objective* obj, int op, double gamma, const double* b, int max_iters, double rel_tol,

@@ -154,6 +154,25 @@ _SIGS = {
     "mfreg_cu_problem_minimize": ([C.c_void_p, C.c_int64, C.c_int, _dp, C.POINTER(_OptConfig), _dp,
                                    C.POINTER(_IterRecord), C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int],
                                   C.c_int),
+    "mfreg_cu_comm_nccl_unique_id": ([C.c_void_p], C.c_int),
+    "mfreg_cu_comm_create_nccl": ([C.c_void_p, C.c_int, C.c_int, C.POINTER(_vp)], C.c_int),
+    "mfreg_cu_comm_create_local": ([C.c_int, C.POINTER(_vp)], C.c_int),
+    "mfreg_cu_comm_destroy": ([_vp], C.c_int),
+    "mfreg_cu_comm_rank": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "mfreg_cu_slab_create": ([_vp, _dp, _dp, _gp, _gp, C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)],
+                             C.c_int),
+    "mfreg_cu_slab_destroy": ([_vp], C.c_int),
+    "mfreg_cu_slab_info": ([_vp, C.POINTER(C.c_int32)], C.c_int),
+    "mfreg_cu_slab_identity": ([_vp, _dp], C.c_int),
+    "mfreg_cu_slab_eval": ([_vp, _dp, _dp, C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_slab_last": ([_vp, C.POINTER(C.c_double), C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_slab_gn_hessian_vec": ([_vp, _dp, _dp], C.c_int),
+    "mfreg_cu_slab_dot": ([_vp, _dp, _dp, C.POINTER(C.c_double)], C.c_int),
+    "mfreg_cu_slab_gather": ([_vp, _dp], C.c_int),
+    "mfreg_cu_slab_minimize": ([_vp, C.c_int, _dp, C.POINTER(_OptConfig), _dp, C.POINTER(_IterRecord), C.c_int,
+                                C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "mfreg_cu_slab_register_multilevel": ([_vp, _dp, _dp, _gp, C.POINTER(_MlConfig), _dp, _gp, C.POINTER(_IterRecord),
+                                           C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.c_int], C.c_int),
     "mfreg_cu_problem_cg_solve": ([C.c_void_p, C.c_int64, C.c_int, C.c_double, _dp, C.c_int, C.c_double, _dp,
                                    C.POINTER(C.c_int), C.POINTER(C.c_double), C.POINTER(C.c_int), C.c_int], C.c_int),
 }

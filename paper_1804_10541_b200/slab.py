@@ -396,3 +396,149 @@ def torch_axpy_to(y, eta: float, d, out) -> None:
     """out = y + eta * d (optimizer.cpp:170, elementwise)."""
     import torch
     torch.add(y, d, alpha=eta, out=out)
+
+
+# ------------------------------------------------------------------ native (C++) slabs
+# The library's own z-slab path (csrc/slab.cu): the exchanges run over NCCL (or the
+# in-process communicator) inside the C++ SlabProblem, and the device-resident solvers and
+# the multilevel driver run sharded on it — no per-iteration Python or eager torch.
+class NativeComm:
+    """A C++ communicator handle: `nccl(rank, size)` (one process per GPU; the unique id is
+    broadcast over torch.distributed) or `local(n)` (n ranks as threads of one process)."""
+
+    def __init__(self, handle):
+        self._h = handle
+        r, s = C.c_int(), C.c_int()
+        _check(lib().mfreg_cu_comm_rank(self._h, C.byref(r), C.byref(s)))
+        self.rank, self.size = r.value, s.value
+
+    @classmethod
+    def nccl(cls, group=None) -> "NativeComm":
+        import torch.distributed as dist
+        rank = dist.get_rank(group) if dist.is_initialized() else 0
+        size = dist.get_world_size(group) if dist.is_initialized() else 1
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            _check(lib().mfreg_cu_comm_nccl_unique_id(uid))
+        if size > 1:
+            box = [bytes(uid)]
+            dist.broadcast_object_list(box, src=0 if group is None else dist.get_global_rank(group, 0), group=group)
+            uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        h = _vp()
+        _check(lib().mfreg_cu_comm_create_nccl(uid, size, rank, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def local(cls, n: int) -> list["NativeComm"]:
+        hs = (_vp * n)()
+        _check(lib().mfreg_cu_comm_create_local(int(n), hs))
+        return [cls(_vp(h)) for h in hs]
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().mfreg_cu_comm_destroy(self._h)
+                self._h = None
+        except Exception:  # interpreter shutdown
+            pass
+
+
+class NativeSlab:
+    """One rank's share of the objective in the library (mfreg_cu_slab_*): CUDA fp64 tensors of
+    length 3 m^y; eval / gn_hessian_vec / dot return global values identical on every rank."""
+
+    def __init__(self, comm: NativeComm, reference, tpl, image: GridDesc, deform: GridDesc,
+                 params: NgfParams = NgfParams(), alpha: float = 1.0):
+        self.comm, self.image, self.deform = comm, image, _nodal(deform)
+        w = _where_of(reference, tpl)
+        reference, tpl = _as_input(reference, w), _as_input(tpl, w)
+        h = _vp()
+        _check(lib().mfreg_cu_slab_create(comm._h, _ptr(reference)[0], _ptr(tpl)[0], C.byref(image.c()),
+                                          C.byref(self.deform.c()), float(params.tau), float(params.rho), float(alpha),
+                                          w, C.byref(h)))
+        self._h = h
+        tab = (C.c_int32 * 7)()
+        _check(lib().mfreg_cu_slab_info(self._h, tab))
+        self.info = SlabInfo(*tab)
+        self._dof = 3 * self.deform.count()
+
+    def __del__(self):
+        try:
+            if getattr(self, "_h", None):
+                lib().mfreg_cu_slab_destroy(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    def dof(self) -> int:
+        return self._dof
+
+    def identity(self, like):
+        import torch
+        out = torch.empty(self._dof, dtype=torch.float64, device=like.device)
+        _check(lib().mfreg_cu_slab_identity(self._h, out.data_ptr()))
+        return out
+
+    def eval(self, y, grad=None) -> float:
+        j = C.c_double()
+        _check(lib().mfreg_cu_slab_eval(self._h, y.data_ptr(), grad.data_ptr() if grad is not None else None,
+                                        C.byref(j)))
+        return j.value
+
+    def last(self):
+        d, r = C.c_double(), C.c_double()
+        _check(lib().mfreg_cu_slab_last(self._h, C.byref(d), C.byref(r)))
+        return d.value, r.value
+
+    def gn_hessian_vec(self, p, q):
+        _check(lib().mfreg_cu_slab_gn_hessian_vec(self._h, p.data_ptr(), q.data_ptr()))
+        return q
+
+    def dot(self, a, b) -> float:
+        v = C.c_double()
+        _check(lib().mfreg_cu_slab_dot(self._h, a.data_ptr(), b.data_ptr(), C.byref(v)))
+        return v.value
+
+    def gather(self, v):
+        _check(lib().mfreg_cu_slab_gather(self._h, v.data_ptr()))
+        return v
+
+    def minimize(self, y0, method: int, cfg=None):
+        """gauss_newton_minimize / lbfgs_minimize, sharded; (y gathered on every rank, trace, lsf)."""
+        import torch
+
+        from . import OptimizerConfig, _IterRecord, _records
+        cfg = cfg or OptimizerConfig()
+        y = torch.empty_like(y0)
+        cap = max(64, 4 * cfg.max_iters + 8)
+        tr = (_IterRecord * cap)()
+        nt, lsf = C.c_int(), C.c_int()
+        oc = cfg.c()
+        _check(lib().mfreg_cu_slab_minimize(self._h, int(method), y0.data_ptr(), C.byref(oc), y.data_ptr(), tr, cap,
+                                            C.byref(nt), C.byref(lsf)))
+        return y, _records(tr, min(nt.value, cap)), bool(lsf.value)
+
+
+def register_multilevel_native(comm: NativeComm, reference, tpl, image: GridDesc, cfg=None):
+    """register_multilevel (multilevel.cpp:117-145) over the communicator's z slabs, fast mode.
+    Returns (y, deform_grid, per-level (trace, line_search_failed)), identical on every rank."""
+    from . import FAST, MultilevelConfig, _empty_like_kind, _Grid, _IterRecord, _MlConfig, _records, deformation_grid_for
+    cfg = cfg or MultilevelConfig(mode=FAST)
+    w = _where_of(reference, tpl)
+    reference, tpl = _as_input(reference, w), _as_input(tpl, w)
+    dg = deformation_grid_for(image, cfg.deform_ratio)
+    y = _empty_like_kind(reference, 3 * dg.count())
+    mc = _MlConfig(int(cfg.levels), int(cfg.deform_ratio), float(cfg.ngf.tau), float(cfg.ngf.rho), float(cfg.alpha),
+                   int(cfg.method), int(cfg.mode), cfg.opt.c())
+    cap = max(64, cfg.levels * (cfg.opt.max_iters + 2))
+    tr = (_IterRecord * cap)()
+    li = (C.c_int * cfg.levels)()
+    lsf = (C.c_int * cfg.levels)()
+    og = _Grid()
+    _check(lib().mfreg_cu_slab_register_multilevel(comm._h, _ptr(reference)[0], _ptr(tpl)[0], C.byref(image.c()),
+                                                   C.byref(mc), _ptr(y)[0], C.byref(og), tr, cap, li, lsf, w))
+    levels, off = [], 0
+    for l in range(cfg.levels):
+        levels.append((_records(tr[off:off + li[l]], li[l]), bool(lsf[l])))
+        off += li[l]
+    return y, GridDesc(tuple(og.m), tuple(og.h), True), levels
