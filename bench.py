@@ -87,6 +87,7 @@ def parse():
     ap.add_argument("--no-gn", action="store_true", help="skip the full GN registration timings")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-fast32", action="store_true", help="skip the optional fp32 mode lines")
+    ap.add_argument("--slabs", action="store_true", help="run the z-slab path even at N=1 (checks that code path)")
     return ap.parse_args()
 
 
@@ -463,33 +464,44 @@ def run_ours(args, rank, world, local):
 
 
 def run_slabs(args, rank, world, local):
-    """N > 1: strong scaling of the same workload over z slabs: rank r evaluates
-    its slab of the global volume; every step performs the real halo exchanges, shared-plane
-    sums and scalar reductions."""
+    """N > 1: strong scaling of the same workload over z slabs in the library (csrc/slab.cu,
+    DESIGN.md §8): rank r evaluates its slab of the global volume; every step performs the
+    real NCCL plane exchanges, shared-plane sums and rank-ordered scalar all-gathers inside the
+    C++ SlabProblem. The sharded multilevel GN registration is timed under gn_registration."""
     import torch
     import paper_1804_10541_b200 as P
+    from paper_1804_10541_b200 import slab as S
     torch.cuda.set_device(local)
     if args.mode != "fast":
         raise SystemExit("z slabs run in fast mode")
     wl = WORKLOADS[args.workload]
     img, dg, R, T, y, p = make_inputs_gpu(P, torch, args.workload)
     nd = 3 * dg.count()
-    so = P.slab.SlabObjective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.slab.TorchComm())
-    s = so.info
+    comm = S.NativeComm.nccl()
+    sl = S.NativeSlab(comm, R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0)
+    s = sl.info
     n_loc = (s.zhi - s.zlo) * wl["m"][0] * wl["m"][1]
     n_glob = img.count()
     grad = torch.zeros_like(y)
     q = torch.zeros_like(y)
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device="cuda")
+
+    class _Step:  # time_steps() drives eval / gn_hessian_vec
+        def eval(self, yy, gg):
+            return sl.eval(yy, gg)
+
+        def gn_hessian_vec(self, pp, qq):
+            return sl.gn_hessian_vec(pp, qq)
+
     for _ in range(args.warmup):
-        so.eval(y, grad)
-        so.gn_hessian_vec(p, q)
+        sl.eval(y, grad)
+        sl.gn_hessian_vec(p, q)
     torch.cuda.synchronize()
     l0 = P.launch_count()
     barrier(world)
     torch.cuda.synchronize()
     with Clocks(local) as ck:
-        t_eval, t_hv = time_steps(so, y, grad, p, q, args.steps, flush, torch)
+        t_eval, t_hv = time_steps(_Step(), y, grad, p, q, args.steps, flush, torch)
     barrier(world)
     launches = P.launch_count() - l0
     ms_step = max_over_ranks(sum(t_eval) / args.steps + sum(t_hv) / args.steps, world)
@@ -505,8 +517,8 @@ def run_slabs(args, rank, world, local):
     def e2e_step():
         yd.copy_(yh, non_blocking=True)
         pd.copy_(ph, non_blocking=True)
-        so.eval(yd, grad)
-        so.gn_hessian_vec(pd, q)
+        sl.eval(yd, grad)
+        sl.gn_hessian_vec(pd, q)
         gh.copy_(grad, non_blocking=True)
         qh.copy_(q, non_blocking=True)
         torch.cuda.synchronize()
@@ -519,21 +531,39 @@ def run_slabs(args, rank, world, local):
         e2e_step()
     e2e_s = max_over_ranks((time.perf_counter() - t0) / k_e2e, world)
     e2e = {"value": 2.0 * n_glob / e2e_s / 1e9, "unit": "Gvoxel/s", "h2d_bytes_per_step": 2 * nd * 8 * world,
-           "d2h_bytes_per_step": 2 * nd * 8 * world, "ms_per_step": e2e_s * 1e3}
+           "d2h_bytes_per_step": 2 * nd * 8 * world, "ms_per_step": e2e_s * 1e3,
+           "path": "NativeSlab eval / gn_hessian_vec (C ABI mfreg_cu_slab_*) with pinned host copies"}
     peak, peak_kind = measured_hbm_peak()
     achieved = B_CANON_HV * n_loc / (ms_hv * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "gn_hessian_vec per rank (slab incl. halo exchange)",
-                "algorithmic_bytes_per_voxel": B_CANON_HV, "peak_source": peak_kind}
+                "traffic": None, "kernel": "gn_hessian_vec per rank (slab incl. NCCL halo exchange)",
+                "algorithmic_bytes_per_voxel": B_CANON_HV, "units_per_launch": n_loc, "peak_source": peak_kind}
+    gn = None
+    if not args.no_gn:
+        cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=P.FAST)
+        walls = []
+        for _ in range(2):  # cold, then warm
+            barrier(world)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, _, lv = S.register_multilevel_native(comm, R, T, img, cfg)
+            torch.cuda.synchronize()
+            walls.append(max_over_ranks(time.perf_counter() - t0, world))
+        gn = {"workload": f"{wl['m'][0]}x{wl['m'][1]}x{wl['m'][2]} h={wl['h'][0]}, {LEVELS} levels, ratio {RATIO}",
+              "method": "gauss-newton", "fast": {"wall_s": walls[0], "wall_s_warm": walls[1],
+                                                 "outer_iters": [len(t) for t, _ in lv],
+                                                 "cg_iters": int(sum(r.cg_iters for t, _ in lv for r in t)),
+                                                 "final_J": lv[-1][0][-1].j if lv[-1][0] else None},
+              "parallelism": f"z slabs x{world} (C++ SlabProblem, NCCL)"}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": DATA,
                 "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]),
                            "nodal": list(dg.m), "mode": args.mode, "l2": "inputs larger than L2; flushed between steps",
-                           "parallelism": f"z slabs x{world} (halo exchange + shared-plane sums)"},
+                           "parallelism": f"z slabs x{world} (C++ SlabProblem; NCCL plane exchanges)"},
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv, "roofline": roofline, "cpu_baseline": None,
-                "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "gn_registration": None}
+                "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "gn_registration": gn}
         print(json.dumps(line), flush=True)
 
 
@@ -542,7 +572,7 @@ def main():
     rank, world, local = dist_init(args.gpus)
     if args.impl == "reference":
         run_reference_arm(args, rank, world)
-    elif world > 1:
+    elif world > 1 or args.slabs:
         run_slabs(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
