@@ -156,6 +156,23 @@ def c3_case(o: Oracle):
     print(f"c3_lbfgs: iters={[len(t) for t in traces]} landmark error {before[0]:.4f} -> {after[0]:.4f}")
 
 
+def c2_case(o: Oracle):
+    """BASELINE configs[1] (C2): 128^3 phantom pair, 3-level Gauss-Newton with the reference's
+    default OptimizerConfig (multilevel.cpp:117-145): per-level traces, final y (about 9 min
+    on 8 threads in the build container)."""
+    import hashlib
+    m, h = (128, 128, 128), (1.0, 1.0, 1.0)
+    ref = o.make_phantom(m, h) * 1000.0
+    tpl = o.warp_sinusoid(ref, m, h, 3.0, 42)
+    y, my, traces, lsf = o.register_multilevel(ref, tpl, m, h, levels=3, method="gn")
+    flat = np.array([r for t in traces for r in t], dtype=np.float64)
+    np.savez_compressed(os.path.join(OUT, "c2_gn.npz"), m=np.array(m), h=np.array(h), my=np.array(my), levels=3,
+                        trace=flat, level_iters=np.array([len(t) for t in traces]), lsf=np.array(lsf), y=y,
+                        ref_sha=hashlib.sha256(ref.tobytes()).hexdigest(),
+                        tpl_sha=hashlib.sha256(tpl.tobytes()).hexdigest())
+    print(f"c2_gn: iters={[len(t) for t in traces]} cg={int(flat[:, 1].sum())} J={flat[-1, 2]:.6f}")
+
+
 def multilevel_case(o: Oracle, name, m, h, levels, method, max_iters):
     m, h = tuple(m), tuple(h)
     ref = o.make_phantom(m, h) * 1000.0
@@ -171,12 +188,18 @@ def multilevel_case(o: Oracle, name, m, h, levels, method, max_iters):
 
 def main():
     os.makedirs(OUT, exist_ok=True)
+    if len(sys.argv) > 1 and sys.argv[1] == "c2":  # only the C2 registration
+        o = Oracle("ref")
+        o.set_threads(os.cpu_count() or 1)
+        c2_case(o)
+        return
     if len(sys.argv) > 1 and sys.argv[1] == "configs":  # only the config cases
         o = Oracle("ref")
         o.set_threads(os.cpu_count() or 1)
         config_case(o, "c1", (256, 256, 1), (1.0, 1.0, 1.0), 4, "gn", 20)
         config_case(o, "c1p", (256, 256, 8), (1.0, 1.0, 1.0), 4, "gn", 3)
         c3_case(o)
+        c2_case(o)
         return
     o = Oracle("ref")
     o.set_threads(1)

@@ -24,6 +24,10 @@
 
 #include "fused_dev.cuh"
 
+#ifndef MFREG_REVMAP
+#define MFREG_REVMAP 1
+#endif
+
 namespace mfreg_b200 {
 
 namespace {
@@ -218,9 +222,12 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         }
     };
     const int nyi = 3 * nly_t * nlx_t;
+    // the y collapse (and the nodal-plane loads) run on the highest threads: the halo items sit on
+    // the lowest ones, so this evens out the warps' work between barriers
+    const int rtid = MFREG_REVMAP ? NT - 1 - tid : tid;
     auto ycollapse = [&](int nzp) {
-        if (tid < nyi) {
-            const int lxn = tid % nlx_t, lyn = (tid / nlx_t) % nly_t, d = tid / (nlx_t * nly_t);
+        if (rtid < nyi) {
+            const int lxn = rtid % nlx_t, lyn = (rtid / nlx_t) % nly_t, d = rtid / (nlx_t * nly_t);
             const Real* q = sQx + d * TY * nlx + lxn;
             Real v = 0.0;
 #pragma unroll

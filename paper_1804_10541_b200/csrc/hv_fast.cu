@@ -31,6 +31,10 @@
 
 #include "fused_dev.cuh"
 
+#ifndef MFREG_REVMAP
+#define MFREG_REVMAP 1
+#endif
+
 namespace mfreg_b200 {
 
 namespace {
@@ -163,7 +167,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     Real slab_v[2] = {Real(0), Real(0)};
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-        const int t = tid + u * NT;
+        const int t = (MFREG_REVMAP ? NT - 1 - tid : tid) + u * NT;
         slab_off[u] = -1;
         slab_d[u] = 0;
         if (t < nsl) {
@@ -182,7 +186,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         Real* dst = slab + (nz & (NSL - 1)) * nsl;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-            if (slab_off[u] >= 0) dst[tid + u * NT] = slab_v[u];
+            if (slab_off[u] >= 0) dst[(MFREG_REVMAP ? NT - 1 - tid : tid) + u * NT] = slab_v[u];
     };
     auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
         const Real* q = slab + (nz & (NSL - 1)) * nsl + off;
@@ -267,9 +271,12 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     };
     // y collapse of sQx into the tile partial of nodal plane nzp
     const int nyi = 3 * nly_t * nlx_t;
+    // the y collapse (and the nodal-plane loads) run on the highest threads: the halo items sit on
+    // the lowest ones, so this evens out the warps' work between barriers
+    const int rtid = MFREG_REVMAP ? NT - 1 - tid : tid;
     auto ycollapse = [&](int nzp) {
-        if (tid < nyi) {
-            const int lxn = tid % nlx_t, lyn = (tid / nlx_t) % nly_t, d = tid / (nlx_t * nly_t);
+        if (rtid < nyi) {
+            const int lxn = rtid % nlx_t, lyn = (rtid / nlx_t) % nly_t, d = rtid / (nlx_t * nly_t);
             const Real* q = sQx + d * TY * nlx + lxn;
             Real v = 0.0;
 #pragma unroll
