@@ -104,6 +104,10 @@ int mfreg_cu_version(void);
 int mfreg_cu_device_count(int* n);
 int mfreg_cu_set_device(int device);
 int mfreg_cu_synchronize(void);
+/* high-water mark of the library's live device allocations (bytes) since load or the last
+ * reset (reset != 0 restarts it at the current level); the CLI's peak-derivative-buffer-bytes
+ * (the reference reports its host scratch peak, counters.hpp:30-47) */
+int mfreg_cu_device_memory_peak(int reset, int64_t* bytes);
 /* kernel launches issued by this library since load (for launch accounting) */
 int64_t mfreg_cu_launch_count(void);
 

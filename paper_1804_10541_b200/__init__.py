@@ -83,6 +83,7 @@ _SIGS = {
     "mfreg_cu_device_count": ([C.POINTER(C.c_int)], C.c_int),
     "mfreg_cu_set_device": ([C.c_int], C.c_int),
     "mfreg_cu_synchronize": ([], C.c_int),
+    "mfreg_cu_device_memory_peak": ([C.c_int, C.POINTER(C.c_int64)], C.c_int),
     "mfreg_cu_launch_count": ([], C.c_int64),
     "mfreg_cu_make_deform_grid": ([_gp, C.POINTER(C.c_int64), _gp], C.c_int),
     "mfreg_cu_deformation_grid_for": ([_gp, C.c_int64, _gp], C.c_int),
@@ -208,6 +209,13 @@ def _lib_fn(name: str):
 
 def exported_symbols() -> list[str]:
     return list(_SIGS)
+
+
+def device_memory_peak(reset: bool = False) -> int:
+    """High-water mark (bytes) of the library's device allocations since load / the last reset."""
+    v = C.c_int64()
+    _check(lib().mfreg_cu_device_memory_peak(1 if reset else 0, C.byref(v)))
+    return v.value
 
 
 def launch_count() -> int:

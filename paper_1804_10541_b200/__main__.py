@@ -38,6 +38,7 @@ def _cmd_register(a) -> int:
     cfg = P.MultilevelConfig(levels=a.levels, deform_ratio=a.deform_ratio, ngf=P.NgfParams(a.tau, a.edge_rho),
                              alpha=a.alpha, method=P.Method.GAUSS_NEWTON if a.optimizer == "gn" else P.Method.LBFGS,
                              opt=P.OptimizerConfig(max_iters=a.max_iters), mode=mode)
+    P.device_memory_peak(reset=True)
     t0 = time.perf_counter()
     y, dg, levels = P.register_multilevel(fixed, moving, img, cfg)
     elapsed = time.perf_counter() - t0
@@ -65,6 +66,9 @@ def _cmd_register(a) -> int:
     disp = np.sqrt((u * u).sum(axis=0))
     out(f"final.max-displacement: {disp.max():.6e}\nfinal.mean-displacement: {disp.mean():.6e}\n")
     out(f"runtime-seconds: {elapsed:.3f}\n")
+    # the reference reports its host scratch peak (counters.hpp:30-47); here: the device high-water
+    # mark of the library's allocations during the registration
+    out(f"peak-derivative-buffer-bytes: {P.device_memory_peak()}\n")
     P.io.write_deformation(a.out_deformation, y, dg)
     out(f"wrote-deformation: {a.out_deformation}\n")
     if a.out_warped:

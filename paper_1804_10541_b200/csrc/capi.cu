@@ -56,6 +56,9 @@ int mfreg_cu_version(void) { return 1; }
 int mfreg_cu_device_count(int* n) { return guard([&] { MFREG_CUDA(cudaGetDeviceCount(n)); }); }
 int mfreg_cu_set_device(int device) { return guard([&] { MFREG_CUDA(cudaSetDevice(device)); }); }
 int mfreg_cu_synchronize(void) { return guard([&] { MFREG_CUDA(cudaDeviceSynchronize()); }); }
+int mfreg_cu_device_memory_peak(int reset, int64_t* bytes) {
+    return guard([&] { *bytes = device_memory_peak(reset != 0); });
+}
 
 int mfreg_cu_make_deform_grid(const mfreg_cu_grid* image, const int64_t points[3], mfreg_cu_grid* out) {
     return guard([&] {

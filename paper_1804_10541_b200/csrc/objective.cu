@@ -1,5 +1,6 @@
 // DeviceObjective and its building blocks (see objective.cuh).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -38,7 +39,24 @@ cudaMemPool_t default_pool() {
 }
 }  // namespace
 
+namespace {
+std::atomic<long long> g_mem_cur{0}, g_mem_peak{0};  // library device allocations (live bytes, high-water mark)
+void mem_note(long long delta) {
+    const long long now = g_mem_cur.fetch_add(delta) + delta;
+    long long peak = g_mem_peak.load();
+    while (now > peak && !g_mem_peak.compare_exchange_weak(peak, now)) {
+    }
+}
+}  // namespace
+
+long long device_memory_peak(bool reset) {
+    const long long p = g_mem_peak.load();
+    if (reset) g_mem_peak.store(g_mem_cur.load());
+    return p;
+}
+
 void* device_alloc(std::size_t bytes) {
+    mem_note(static_cast<long long>(bytes));
     void* p = nullptr;
     if (bytes >= kBigAllocBytes) {
         cudaError_t e = cudaMalloc(&p, bytes);
@@ -71,6 +89,7 @@ void* device_alloc(std::size_t bytes) {
 
 void device_free(void* p, std::size_t bytes) {
     if (!p) return;
+    mem_note(-static_cast<long long>(bytes));
     if (bytes >= kBigAllocBytes) cudaFree(p);
     else cudaFreeAsync(p, 0);
 }

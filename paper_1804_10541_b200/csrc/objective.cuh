@@ -45,6 +45,8 @@ enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 // GB on first use measured 0.6-4 s against 0.05 s for cudaMalloc)
 constexpr std::size_t kBigAllocBytes = std::size_t(256) << 20;
 void* device_alloc(std::size_t bytes);
+// high-water mark of the library's live device allocations since load (or the last reset)
+long long device_memory_peak(bool reset);
 void device_free(void* p, std::size_t bytes);
 
 // RAII device array of doubles (or raw bytes).

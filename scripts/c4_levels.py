@@ -7,7 +7,7 @@ import paper_1804_10541_b200 as P
 
 mode = P.Mode.FAST32 if "--fast32" in sys.argv else P.Mode.FAST
 for m in ((128, 128, 225), (256, 256, 450), (512, 512, 900)):
-    img = P.make_image_grid(m, (1.0, 1.0, 1.0))
+    img = P.make_image_grid(m, (0.7, 0.7, 0.7))  # C4 spacing (exercises the tie hazard H1)
     R = P.make_phantom(img, device=True)
     R.mul_(1000.0)
     T = P.warp_sinusoid(R, img, 3.0, 42)

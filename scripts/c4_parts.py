@@ -4,7 +4,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import paper_1804_10541_b200 as P
 m = (512, 512, 900)
-img = P.make_image_grid(m)
+img = P.make_image_grid(m, (0.7, 0.7, 0.7))  # C4 spacing
 R = P.make_phantom(img, device=True); R.mul_(1000.0)
 T = P.warp_sinusoid(R, img, 3.0, 42)
 dg = P.deformation_grid_for(img, 4)

@@ -8,7 +8,7 @@ import paper_1804_10541_b200 as P
 args = [a for a in sys.argv[1:] if not a.startswith("--")]
 m = tuple(int(v) for v in args[:3]) if len(args) >= 3 else (512, 512, 900)
 mode = P.Mode.FAST32 if "--fast32" in sys.argv else P.Mode.FAST
-img = P.make_image_grid(m, (1.0, 1.0, 1.0))
+img = P.make_image_grid(m, (0.7, 0.7, 0.7))  # C4 spacing (exercises the tie hazard H1)
 t0 = time.perf_counter()
 R = P.make_phantom(img, device=True)
 R.mul_(1000.0)

@@ -38,6 +38,7 @@ def test_cli_register_warp_landmarks_match_reference(oracle, tmp_path):
                 "--max-iters", 4)
     assert r.returncode == 0, r.stderr
     lines = dict(l.split(": ", 1) for l in r.stdout.splitlines())
+    assert int(lines["peak-derivative-buffer-bytes"]) > 0  # the reference's key (mfreg_cli.cpp:88-89)
     from oracle.gen_golden import nodal_coords
     from oracle.oracle import OptConfig
     y_ref, my, traces, _ = oracle.register_multilevel(R, T, m, h, levels=2, method="gn",
