@@ -424,6 +424,97 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     }
 }
 
+// Value-only NGF pass (the Armijo trial evaluations): D = h_bar sum (1 - r^2) with r computed
+// exactly as k_ev2 computes it (same clamped differences with the TMA zero fill, ngf_coef) and
+// summed in k_ev2's order (per column over its planes, per tile by the same warp and row tree,
+// over tiles in the same last-CTA order), so D is bitwise the gradient evaluation's D. It reads
+// R and T_w only (16 B/voxel at fp64) and writes nothing per voxel: no TMA ring, no P^T, no
+// coefficient stores. One thread per tile column marching z; neighbours from L1.
+template <typename Real>
+__global__ void __launch_bounds__(NT) k_ev_value(const __grid_constant__ FArgs a, const Real* __restrict__ R,
+                                                 const Real* __restrict__ Tw) {
+    __shared__ double sred[NT / 32];
+    __shared__ unsigned int s_last;
+    const TileMeta& tm = a.tm;
+    const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
+    const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
+    const long long plane = static_cast<long long>(mx) * my;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);
+    const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
+    const int gx0 = x0 + lane, gy0 = y0 + row;
+    const bool in0 = gx0 < mx && gy0 < my;
+    const Real m0xm = gx0 > 0 ? Real(1) : Real(0), m0xp = gx0 + 1 < mx ? Real(1) : Real(0);
+    const Real m0ym = gy0 > 0 ? Real(1) : Real(0), m0yp = gy0 + 1 < my ? Real(1) : Real(0);
+    const bool hxm = gx0 > 0, hxp = gx0 + 1 < mx, hym = gy0 > 0, hyp = gy0 + 1 < my;
+    const long long col = static_cast<long long>(min(gx0, mx - 1)) + static_cast<long long>(min(gy0, my - 1)) * mx;
+    // a neighbour outside the volume reads 0 (the TMA zero fill k_ev2 sees)
+    auto ld = [&](const Real* f, long long i, bool ok) { return ok ? __ldg(f + i) : Real(0); };
+    double dsum = 0.0;
+    if (in0 && ilo < ihi) {
+        Real Rm = ld(R, col + (ilo - 1) * plane, ilo > 0), Tm = ld(Tw, col + (ilo - 1) * plane, ilo > 0);
+        Real Rj = __ldg(R + col + ilo * plane), Tj = __ldg(Tw + col + ilo * plane);
+#pragma unroll 1
+        for (int j = ilo; j < ihi; ++j) {
+            const long long o = col + j * plane;
+            const bool hzp = j + 1 < mz;
+            const Real Rp = ld(R, o + plane, hzp), Tp = ld(Tw, o + plane, hzp);
+            const Real mzm = j > 0 ? Real(1) : Real(0), mzp = hzp ? Real(1) : Real(0);
+            const Coef<Real> cf = ngf_coef(
+                a, m0xm * (ld(R, o - 1, hxm) - Rj), m0xp * (ld(R, o + 1, hxp) - Rj), m0ym * (ld(R, o - mx, hym) - Rj),
+                m0yp * (ld(R, o + mx, hyp) - Rj), mzm * (Rm - Rj), mzp * (Rp - Rj), m0xm * (ld(Tw, o - 1, hxm) - Tj),
+                m0xp * (ld(Tw, o + 1, hxp) - Tj), m0ym * (ld(Tw, o - mx, hym) - Tj), m0yp * (ld(Tw, o + mx, hyp) - Tj),
+                mzm * (Tm - Tj), mzp * (Tp - Tj), true);
+            dsum += fma(-static_cast<double>(cf.r), static_cast<double>(cf.r), 1.0);
+            Rm = Rj;
+            Tm = Tj;
+            Rj = Rp;
+            Tj = Tp;
+        }
+    }
+    // per-tile sum, then the last CTA: k_ev2's reduction order exactly
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) dsum += __shfl_down_sync(0xffffffffu, dsum, o);
+    if (lane == 0) sred[row] = dsum;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += sred[w];
+        a.vpart[tile_id] = t;
+        __threadfence();
+        const unsigned nct = gridDim.x * gridDim.y * gridDim.z, id = static_cast<unsigned>(tile_id);
+        const unsigned g = id % 32u, ng = min(nct, 32u), gsize = (nct - g + 31u) / 32u;
+        unsigned lst = 0;
+        if (atomicAdd(a.vticket + 1 + g, 1u) == gsize - 1) {
+            a.vticket[1 + g] = 0u;
+            __threadfence();
+            lst = atomicAdd(a.vticket, 1u) == ng - 1 ? 1u : 0u;
+        }
+        s_last = lst;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const unsigned nct = gridDim.x * gridDim.y * gridDim.z;
+    double v = 0.0;
+    for (unsigned t = tid; t < nct; t += NT) v += a.vpart[t];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    __syncthreads();
+    if (lane == 0) sred[row] = v;
+    __syncthreads();
+    if (tid == 0) {
+        double t = 0.0;
+        for (int w = 0; w < NT / 32; ++w) t += sred[w];
+        const double d = a.dscale * t;
+        a.dsc[0] = d;
+        a.dsc_host[0] = d;
+        __threadfence_system();
+        a.vticket[0] = 0u;
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -440,6 +531,11 @@ std::size_t ev2_smem_bytes(int nlx, bool fp32) { return fp32 ? smem_bytes<float>
 void ev2_set_smem_cap(int bytes) {
     MFREG_CUDA(cudaFuncSetAttribute(k_ev2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     MFREG_CUDA(cudaFuncSetAttribute(k_ev2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void ev_value_launch(const FArgs& a, const void* R, const void* Tw, dim3 grid, cudaStream_t s, bool fp32) {
+    if (fp32) k_ev_value<float><<<grid, NT, 0, s>>>(a, static_cast<const float*>(R), static_cast<const float*>(Tw));
+    else k_ev_value<double><<<grid, NT, 0, s>>>(a, static_cast<const double*>(R), static_cast<const double*>(Tw));
 }
 
 void ev2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {

@@ -24,6 +24,7 @@ void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std:
 // ev_fast.cu
 std::size_t ev2_smem_bytes(int nlx, bool fp32);
 void ev2_set_smem_cap(int bytes);
+void ev_value_launch(const fdev::FArgs& a, const void* R, const void* Tw, dim3 grid, cudaStream_t s, bool fp32);
 void ev2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
 
 namespace {
@@ -920,7 +921,7 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
 
 FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
                      const SlabSpec& slab, bool fp32)
-    : fp32_(fp32) {
+    : fp32_(fp32), state_R_(R), state_Tw_(Tw) {
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
     TileMeta& t = meta_;
@@ -1169,6 +1170,10 @@ bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
             a.dsc = d_dev;
             a.dsc_host = d_host;
             a.dscale = plan.view().tgt.cell_volume();  // h_bar (ngf.cpp:227)
+            if (!grad && !frh && value_pass_enabled()) {  // Armijo trial: D only, bitwise k_ev2's D
+                ev_value_launch(a, fp.state_R(), fp.state_Tw(), dim3(t.ntx, t.nty, t.ntz), s, fp.fp32());
+                return true;
+            }
         }
         ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s,
                    fp.fp32());
@@ -1178,6 +1183,15 @@ bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
     if (fp.tma()) k_fused<true, true><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
     else k_fused<true, false><<<dim3(t.ntx, t.nty, t.ntz), NTH, smem, s>>>(a, maps);
     return false;
+}
+
+// MFREG_NO_VALUE_PASS=1: value-only evaluations run the full eval pass (A/B switch)
+bool value_pass_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("MFREG_NO_VALUE_PASS");
+        return !(e && e[0] == '1');
+    }();
+    return on;
 }
 
 bool pdl_enabled() {

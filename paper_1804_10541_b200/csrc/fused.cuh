@@ -52,6 +52,8 @@ public:
     FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
               const SlabSpec& slab, bool fp32 = false);
     bool fp32() const { return fp32_; }
+    const void* state_R() const { return state_R_; }    // the arrays the passes read (fp64 or FAST32)
+    const void* state_Tw() const { return state_Tw_; }
     bool tma() const { return tma_; }
     bool hv2() const { return hv2_; }  // two-CTA/SM Hv kernel (hv_fast.cu)
     std::size_t hv2_smem() const { return hv2_smem_; }
@@ -100,6 +102,8 @@ private:
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
     bool fp32_ = false;
+    const void* state_R_ = nullptr;
+    const void* state_Tw_ = nullptr;
     bool make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh);
 };
 
@@ -138,6 +142,7 @@ struct FinalizeSpec {
 };
 // cudaLaunchKernelEx with programmatic stream serialisation (MFREG_NO_PDL=1: plain launch)
 bool pdl_enabled();
+bool value_pass_enabled();
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, Args&&... args) {
     cudaLaunchConfig_t cfg{};

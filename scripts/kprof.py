@@ -46,7 +46,19 @@ def main():
     for name, which, opnd in (("hv_pass", 0, p), ("eval_pass", 1, p), ("warp", 2, y)):
         ms = obj.profile_kernel(which, opnd, a.reps)
         out[name] = {"ms": round(ms, 4), "gvox_s": round(n / ms / 1e6, 2), "frac40": round(40 * n / ms / 1e6 / 6554.9, 4)}
-    obj.eval(y, g)
+    # operator times (events around the calls): gradient eval, value-only eval (Armijo trial), GN Hv
+    def ev_ms(fn, reps=a.reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) / reps, 4)
+    out["op_ms"] = {"eval_grad": ev_ms(lambda: obj.eval(y, g)), "eval_value": ev_ms(lambda: obj.eval(y)),
+                    "gn_hv": ev_ms(lambda: (obj.eval(y, g), obj.gn_hessian_vec(p, q)), 3)}
     print(json.dumps(out), flush=True)
 
 
