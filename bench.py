@@ -64,16 +64,18 @@ def csrc_sha() -> str:
 
 def traffic_for(workload: str, kernel: str):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch from the committed ncu capture
-    of this workload and source hash (profiles/traffic.json), else None."""
+    of this workload and source hash (profiles/traffic.json), else None; plus the capture's
+    fp64-pipe / issue-active / DRAM percentages of that kernel."""
     try:
         with open(TRAFFIC_FILE) as f:
             t = json.load(f)
         e = t[workload][kernel]
         if e.get("csrc_sha") != csrc_sha():
-            return None, f"capture {e.get('csrc_sha')} is for other sources"
-        return float(e["bytes"]), e.get("source", "profiles/traffic.json")
+            return None, f"capture {e.get('csrc_sha')} is for other sources", {}
+        extra = {k: e[k] for k in ("fp64_pipe_pct", "issue_active_pct", "dram_pct_of_peak") if k in e}
+        return float(e["bytes"]), e.get("source", "profiles/traffic.json"), extra
     except Exception as exc:  # noqa: BLE001
-        return None, f"no capture ({type(exc).__name__})"
+        return None, f"no capture ({type(exc).__name__})", {}
 
 
 def parse():
@@ -178,6 +180,16 @@ class Clocks:
         os.unlink(self.f.name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
                 "samples": len(sm), "sm_mhz_min": min(sm) if sm else None, "power_w_max": max(pw) if pw else None}
+
+
+def fp64_peak():
+    """Measured DFMA throughput of this GPU model (scripts/probe/fp64_peak.cu, profiles/), for the
+    fp64 ridge the kernels' fp64-pipe percentages refer to."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as f:
+            return float(json.load(f)["dfma_tflops"])
+    except Exception:  # noqa: BLE001
+        return None
 
 
 def measured_hbm_peak():
@@ -363,14 +375,14 @@ def run_ours(args, rank, world, local):
         b_alg = {"hv_pass": B_CANON_HV, "eval_pass": 40.0, "warp": 40.0}
         kern = {}
         for k, v in k_ms.items():
-            tr, src = traffic_for(args.workload, k)
+            tr, src, extra = traffic_for(args.workload, k)
             kern[k] = {"ms": v, "achieved_gbs": b_alg[k] * n / (v * 1e-3) / 1e9, "algorithmic_bytes_per_voxel": b_alg[k],
                        "frac": b_alg[k] * n / (v * 1e-3) / 1e9 / peak, "traffic": tr, "traffic_source": src,
-                       "share_of_step": v / ms_step}
+                       "share_of_step": v / ms_step, **{f"ncu_{x}": y for x, y in extra.items()}}
         dom = max(k_ms, key=k_ms.get)
         names = {"hv_pass": "k_hv2 (GN Hv image pass: P p, dr, dr^T, dT, P^T partials)",
                  "eval_pass": "k_ev2 (NGF eval pass: rho-hat, r, D partials, gradient dr^T r, P^T partials)",
-                 "warp": "k_warp_fast (P y, trilinear T, dT/dP)"}
+                 "warp": "k_warp_z (P y, trilinear T, dT/dP; z-marching)"}
         roofline = {"bound": "hbm", "achieved": kern[dom]["achieved_gbs"], "peak": peak, "unit": "GB/s",
                     "frac": kern[dom]["frac"], "traffic": kern[dom]["traffic"],
                     "traffic_unit": "bytes/launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
@@ -378,6 +390,7 @@ def run_ours(args, rank, world, local):
                     "algorithmic_bytes_per_launch": b_alg[dom] * n, "kernel": names[dom],
                     "algorithmic_bytes_per_voxel": b_alg[dom], "units_per_launch": n, "peak_source": peak_kind,
                     "kernels": kern,
+                    "fp64_peak_tflops": fp64_peak(),
                     "operators": {"gn_hessian_vec": {"ms": ms_hv, "frac": B_CANON_HV * n / (ms_hv * 1e-3) / 1e9 / peak},
                                   "eval_grad": {"ms": ms_eval, "frac": B_CANON_GRAD * n / (ms_eval * 1e-3) / 1e9 / peak}}}
 

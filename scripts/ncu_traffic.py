@@ -19,7 +19,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from bench import TRAFFIC_FILE, csrc_sha  # noqa: E402
 
-KERNELS = {"k_hv2": "hv_pass", "k_ev2": "eval_pass", "k_warp_fast": "warp"}
+KERNELS = {"k_hv2": "hv_pass", "k_ev2": "eval_pass", "k_warp_z": "warp", "k_warp_fast": "warp"}
+EXTRA = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+         "issue_active_pct": "smsp__issue_active.avg.pct_of_peak_sustained_active",
+         "dram_pct_of_peak": "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+         "warp_inst": "smsp__inst_executed.sum"}
 
 
 def main(workload: str, rep: str) -> None:
@@ -27,6 +31,7 @@ def main(workload: str, rep: str) -> None:
     rows = list(csv.reader(raw.splitlines()))
     hdr = rows[0]
     col = {k: hdr.index(k) for k in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum")}
+    col.update({k: hdr.index(v) for k, v in EXTRA.items() if v in hdr})
     per = {}
     for r in rows[2:]:
         name = r[col["Kernel Name"]]
@@ -34,7 +39,8 @@ def main(workload: str, rep: str) -> None:
         if key is None:
             continue
         f = lambda c: float(r[col[c]].replace(",", ""))  # noqa: E731
-        per.setdefault(key, []).append((f("dram__bytes_read.sum") + f("dram__bytes_write.sum"), f("gpu__time_duration.sum")))
+        per.setdefault(key, []).append((f("dram__bytes_read.sum") + f("dram__bytes_write.sum"), f("gpu__time_duration.sum"),
+                                        {k: f(k) for k in EXTRA if k in col}))
     try:
         with open(TRAFFIC_FILE) as fh:
             out = json.load(fh)
@@ -42,9 +48,13 @@ def main(workload: str, rep: str) -> None:
         out = {}
     sha = csrc_sha()
     for k, v in per.items():
-        out.setdefault(workload, {})[k] = {"bytes": statistics.median(b for b, _ in v), "launches": len(v),
-                                          "duration_us_ncu": statistics.median(t for _, t in v) / 1e3,
-                                          "csrc_sha": sha, "source": os.path.relpath(rep, ROOT)}
+        e = {"bytes": statistics.median(b for b, _, _ in v), "launches": len(v),
+             "duration_us_ncu": statistics.median(t for _, t, _ in v) / 1e3, "csrc_sha": sha,
+             "source": os.path.relpath(rep, ROOT)}
+        for x in EXTRA:
+            if x in v[0][2]:
+                e[x] = statistics.median(m[x] for _, _, m in v)
+        out.setdefault(workload, {})[k] = e
     with open(TRAFFIC_FILE, "w") as fh:
         json.dump(out, fh, indent=1)
     print(json.dumps(out[workload], indent=1))
