@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "libmfreg_cuda.so")
-SOURCES = ["kernels.cu", "fused.cu", "hv_fast.cu", "ev_fast.cu", "cg.cu", "objective.cu", "solvers.cu", "io.cu", "capi.cu", "api.cu", "slab.cu"]
+SOURCES = ["kernels.cu", "fused.cu", "hv_fast.cu", "hv3.cu", "ev_fast.cu", "cg.cu", "objective.cu", "solvers.cu", "io.cu", "capi.cu", "api.cu", "slab.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
                      "-Xptxas", "-O3", "--expt-relaxed-constexpr"]

@@ -21,6 +21,17 @@ int hv2_nsl_max();
 int hv2_threads();
 void hv2_set_smem_cap(int bytes);
 void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
+// hv3.cu
+std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32);
+int hv3_tile_x();
+int hv3_tile_y();
+int hv3_threads();
+int hv3_box_width(bool fp32);
+int hv3_box_rows();
+int hv3_box_origin(bool fp32);
+void hv3_set_smem_cap(int bytes);
+bool hv3_fp32_ok();
+void hv3_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
 // ev_fast.cu
 std::size_t ev2_smem_bytes(int nlx, bool fp32);
 void ev2_set_smem_cap(int bytes);
@@ -1070,11 +1081,143 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     const char* noe = std::getenv("MFREG_NO_EV2");
     ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
     if (ev2_) ev2_set_smem_cap(kSmem2Cta);
+    setup_hv3(plan, R, Tw, dT, zok, max_optin);
     // FAST32 runs only on the two-CTA kernels (the legacy fused kernels are fp64)
     if (fp32_ && !(hv2_ && ev2_))
         throw std::invalid_argument(
             "FAST32: the grid is not supported by the single-precision kernels (odd x size or nodal z cells "
             "spanning < 2 image planes)");
+}
+
+// Hv pass with recomputed coefficients (hv3.cu), opt-in (MFREG_HV3=1; MFREG_NO_HV3=1 wins): 28 x 12
+// output tiles over the same z window, one CTA per SM; per-axis finalize gather tables as for the
+// main tiling. Measured at C4: 8.1 ms fp64 / 5.7 ms FAST32 against k_hv2's 5.6 / 3.5 ms
+// -- the recomputation adds ~90 fp64 operations per voxel on B200's 60-per-clock fp64 pipe, and the
+// one-CTA-per-SM uniform-warp schedule issues at ~50%. Off when TMA cannot address the grid, nodal z
+// cells span < 2 image planes or a tile's nodal footprint exceeds one node per thread.
+void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, bool zok,
+                          int max_optin) {
+    const char* on = std::getenv("MFREG_HV3");
+    const char* off = std::getenv("MFREG_NO_HV3");
+    if (!(on && on[0] == '1') || (off && off[0] == '1') || !tma_ || !zok || (fp32_ && !hv3_fp32_ok())) return;
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    if (!encode) return;
+    const DevPlan& P = plan.view();
+    const Grid& g = P.tgt;
+    const int tsx = hv3_tile_x(), tsy = hv3_tile_y();
+    TileMeta t{};
+    t.ntx = static_cast<int>((g.m[0] + tsx - 1) / tsx);
+    t.nty = static_cast<int>((g.m[1] + tsy - 1) / tsy);
+    t.zlo = meta_.zlo;
+    t.zhi = meta_.zhi;
+    // z chunks: minimise waves x (planes + 4 halo planes), one CTA per SM
+    const long long nxy = static_cast<long long>(t.ntx) * t.nty;
+    const int mz = t.zhi - t.zlo;
+    const int zmax = 128;
+    int best = (mz + zmax - 1) / zmax;
+    double best_cost = 1e300;
+    for (int ntz = (mz + zmax - 1) / zmax; ntz <= std::max((mz + zmax - 1) / zmax, mz / 4); ++ntz) {
+        const int zc = (mz + ntz - 1) / ntz;
+        const int real_ntz = (mz + zc - 1) / zc;
+        const double cost = std::ceil(static_cast<double>(nxy * real_ntz) / kSMs) * (zc + 4);
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = ntz;
+        }
+    }
+    t.zc = (mz + best - 1) / best;
+    if (const char* zce = std::getenv("MFREG_HV3_ZC")) t.zc = std::max(4, std::min(mz, std::atoi(zce)));  // experiments
+    t.ntz = (mz + t.zc - 1) / t.zc;
+    const int tsz[3] = {tsx, tsy, t.zc};
+    const int ntl[3] = {t.ntx, t.nty, t.ntz};
+    const int org[3] = {0, 0, t.zlo}, end[3] = {static_cast<int>(g.m[0]), static_cast<int>(g.m[1]), t.zhi};
+    int nl[3];
+    int gmax = 0;
+    std::vector<int> off3[3];
+    std::vector<int2> ent3[3];
+    for (int a = 0; a < 3; ++a) {
+        const auto& base = plan.host_base[a];
+        const int ms = static_cast<int>(P.src.m[a]);
+        std::vector<int> n0(ntl[a]), n1(ntl[a]);
+        nl[a] = 0;
+        for (int k = 0; k < ntl[a]; ++k) {
+            const int x0 = org[a] + k * tsz[a], x1 = std::min(end[a], x0 + tsz[a]);
+            n0[k] = base[x0];
+            n1[k] = base[x1 - 1] + 1;
+            nl[a] = std::max(nl[a], n1[k] - n0[k] + 1);
+        }
+        off3[a].assign(ms + 1, 0);
+        for (int nd = 0; nd < ms; ++nd) {
+            for (int k = 0; k < ntl[a]; ++k)
+                if (n0[k] <= nd && nd <= n1[k]) ent3[a].push_back(make_int2(k, nd - n0[k]));
+            off3[a][nd + 1] = static_cast<int>(ent3[a].size());
+            gmax = std::max(gmax, off3[a][nd + 1] - off3[a][nd]);
+        }
+    }
+    t.nlx = nl[0];
+    t.nly = nl[1];
+    t.nlz = nl[2];
+    t.part_stride = static_cast<std::size_t>(t.nlz) * t.nly * t.nlx * 3;
+    // nodal footprint of the staged columns [x0 - 2, x0 + tsx + 1] and rows, max over tiles
+    int fp[2];
+    for (int a2 = 0; a2 < 2; ++a2) {
+        const auto& base = plan.host_base[a2];
+        const int m = static_cast<int>(g.m[a2]);
+        const int ts = a2 == 0 ? tsx : tsy;
+        int mxf = 0;
+        for (int k = 0; k < ntl[a2]; ++k) {
+            const int lo = std::max(k * ts - 2, 0), hi = std::min(m - 1, k * ts + ts + 1);
+            mxf = std::max(mxf, base[hi] - base[lo] + 2);
+        }
+        fp[a2] = mxf;
+    }
+    const std::size_t smem = hv3_smem_bytes(t.nlx, fp[0] * fp[1] * 3, t.zc, fp32_);
+    if (fp[0] * fp[1] * 3 > hv3_threads() || 3 * t.nlx * t.nly > hv3_threads() ||
+        smem > static_cast<std::size_t>(max_optin))
+        return;
+    // tensor maps: R, T_w (3-D boxes BX x 16), dT (4-D, 3 components); fp32 needs 16-byte rows
+    const int es = fp32_ ? 4 : 8;
+    if ((g.m[0] * es) % 16 != 0) return;
+    const cuuint64_t mx = g.m[0], my = g.m[1], mzz = g.m[2], n = g.count();
+    auto enc = [&](CUtensorMap* m, const void* base, int rank, cuuint64_t comps, cuuint32_t bc) {
+        const cuuint64_t e = static_cast<cuuint64_t>(es);
+        const cuuint64_t dims[4] = {mx, my, mzz, comps};
+        const cuuint64_t strides[3] = {mx * e, mx * my * e, n * e};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(hv3_box_width(fp32_)), static_cast<cuuint32_t>(hv3_box_rows()), 1, bc};
+        const cuuint32_t est[4] = {1, 1, 1, 1};
+        return encode(m, fp32_ ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
+                      const_cast<void*>(base), dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    TmaMaps maps{};
+    if (!(enc(&maps.a, R, 3, 1, 1) && enc(&maps.b, Tw, 3, 1, 1) && enc(&maps.c, dT, 4, 3, 3))) return;
+    std::memcpy(maps_hv3_, &maps, sizeof(TmaMaps));
+    for (int a = 0; a < 3; ++a) {
+        goff3_[a].resize(off3[a].size());
+        gent3_[a].resize(std::max<std::size_t>(1, ent3[a].size()));
+        MFREG_CUDA(cudaMemcpy(goff3_[a].get(), off3[a].data(), off3[a].size() * sizeof(int), cudaMemcpyHostToDevice));
+        if (!ent3[a].empty())
+            MFREG_CUDA(cudaMemcpy(gent3_[a].get(), ent3[a].data(), ent3[a].size() * sizeof(int2), cudaMemcpyHostToDevice));
+        t.g_off[a] = goff3_[a].get();
+        t.g_ent[a] = gent3_[a].get();
+    }
+    meta3_ = t;
+    part3_.resize(t.part_stride * static_cast<std::size_t>(ntiles3()));
+    MFREG_CUDA(cudaMemset(part3_.get(), 0, part3_.size() * sizeof(double)));
+    slab3_[0] = fp[0];
+    slab3_[1] = fp[1];
+    gmax3_ = gmax;
+    hv3_smem_ = smem;
+    hv3_set_smem_cap(max_optin);
+    hv3_ = true;
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh) {
@@ -1130,13 +1273,28 @@ bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, cons
 }
 
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     cudaStream_t s, const int* skip) {
+                     double tau, double rho, cudaStream_t s, const int* skip) {
     FArgs a = make_args(plan, fp);
+    a.tau = tau;
+    a.rho = rho;
     a.skip = skip;
     a.scale = 2.0 * a.g.cell_volume();
     a.frh = frh;
     a.dT = dT;
     a.p = p;
+    if (fp.hv3()) {
+        a.tm = fp.meta3();
+        a.part = fp.partials3();
+        a.nxf = fp.slab3_x();
+        a.nyf = fp.slab3_y();
+        a.R = static_cast<const double*>(fp.state_R());
+        a.Tw = static_cast<const double*>(fp.state_Tw());
+        note_launch();
+        const TileMeta& t3 = fp.meta3();
+        hv3_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv3()), dim3(t3.ntx, t3.nty, t3.ntz), fp.hv3_smem(), s,
+                   fp.fp32());
+        return;
+    }
     const TileMeta& t = fp.meta();
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
@@ -1205,10 +1363,11 @@ bool pdl_enabled() {
 void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const FinalizeSpec& spec, cudaStream_t s) {
     FinArgs a{};
     a.gy = plan.view().src;
-    a.tm = fp.meta();
-    a.part = fp.partials();
+    const bool p3 = spec.hv_pass && fp.hv3();
+    a.tm = p3 ? fp.meta3() : fp.meta();
+    a.part = p3 ? fp.partials3() : fp.partials();
     a.vpart = fp.value_partials();
-    a.ntiles = fp.ntiles();
+    a.ntiles = p3 ? fp.ntiles3() : fp.ntiles();
     a.hbar = plan.view().tgt.cell_volume();
     a.alpha = spec.alpha;
     a.scale_y = 2.0 * a.gy.cell_volume();
@@ -1237,7 +1396,7 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     const long long nthr = per_node ? a.nwin : 3 * a.nwin;
     const long long want = spec.out ? (nthr + FIN_THREADS - 1) / FIN_THREADS : 1;
     const unsigned blocks = static_cast<unsigned>(std::max(1LL, std::min(want, static_cast<long long>(kFinBlocks))));
-    const bool k2 = fp.gather_max() <= 2;
+    const bool k2 = (p3 ? fp.gather_max3() : fp.gather_max()) <= 2;
     auto go = [&](auto kern) { launch_pdl(kern, dim3(blocks), dim3(FIN_THREADS), 0, s, a); };
     if (fp.fp32()) {
         if (k2) per_node ? go(k_nodal_finalize<float, 2, 3>) : go(k_nodal_finalize<float, 2, 1>);

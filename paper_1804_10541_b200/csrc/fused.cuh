@@ -66,6 +66,17 @@ public:
     const void* maps_hv2() const { return maps_hv2_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
+    // Hv pass with recomputed coefficients (hv3.cu): own tiling (28 x 12 output tiles), own
+    // partials; when on, the Hv state is R, T_w, dT and the eval pass stores no rho-hat
+    bool hv3() const { return hv3_; }
+    const TileMeta& meta3() const { return meta3_; }
+    double* partials3() { return part3_.get(); }
+    int ntiles3() const { return meta3_.ntx * meta3_.nty * meta3_.ntz; }
+    int slab3_x() const { return slab3_[0]; }
+    int slab3_y() const { return slab3_[1]; }
+    int gather_max3() const { return gmax3_; }
+    std::size_t hv3_smem() const { return hv3_smem_; }
+    const void* maps_hv3() const { return maps_hv3_; }
     const TileMeta& meta() const { return meta_; }
     double* partials() { return part_.get(); }
     double* value_partials() { return vpart_.get(); }
@@ -101,6 +112,16 @@ private:
     alignas(64) unsigned char maps_hv2_[3 * 128];
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
+    bool hv3_ = false;
+    TileMeta meta3_{};
+    DevArray<int> goff3_[3];
+    DevArray<int2> gent3_[3];
+    DVec part3_;
+    int slab3_[2] = {0, 0};
+    int gmax3_ = 0;
+    std::size_t hv3_smem_ = 0;
+    alignas(64) unsigned char maps_hv3_[3 * 128];
+    void setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, bool zok, int max_optin);
     bool fp32_ = false;
     const void* state_R_ = nullptr;
     const void* state_Tw_ = nullptr;
@@ -111,8 +132,9 @@ private:
 constexpr int kRhoDirs = 6;
 
 // Gauss-Newton Hv image pass: s = dT . P p -> w -> z -> q^ = 2h z dT -> P^T partials.
+// (tau, rho: the NGF parameters, used when the pass recomputes the coefficients, hv3)
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     cudaStream_t s, const int* skip = nullptr);
+                     double tau, double rho, cudaStream_t s, const int* skip = nullptr);
 
 // Eval image pass on the warped state (T_w, dT from launch_warp): rho-hat (6 per
 // voxel, stored as Hv state), per-tile sums of (1 - r^2) and, when `grad`, the
@@ -139,6 +161,7 @@ struct FinalizeSpec {
     double* sc = nullptr;         // device scalars
     double* sc_host = nullptr;    // device view of mapped host scalars: value mode also writes D, alpha S there
     const int* skip = nullptr;    // device flag: skip the launch when set
+    bool hv_pass = false;         // the partials come from the Hv pass (hv3 tiling when on)
 };
 // cudaLaunchKernelEx with programmatic stream serialisation (MFREG_NO_PDL=1: plain launch)
 bool pdl_enabled();

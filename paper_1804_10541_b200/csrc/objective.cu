@@ -389,13 +389,16 @@ void DeviceObjective::warp_state(const double* y, cudaStream_t s, int zlo, int z
         launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), state ? ngf_.dT.get() : nullptr, s, zlo, zhi);
 }
 
+double* DeviceObjective::frh_out() { return fused_->hv3() ? nullptr : static_cast<double*>(ngf_.state_frh()); }
+
 // a14: Hv uses the state of the last eval, value-only included. A lazy value-only
 // eval skipped writing that state (dT, rho-hat); rebuild it at the recorded point.
 void DeviceObjective::refresh_state() {
     if (!stale_) return;
     warp_state(ylazy_.get(), s_, 0, -1, true);
-    launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                      static_cast<double*>(ngf_.state_frh()), false, s_);
+    if (!fused_->hv3())  // (hv3 recomputes the coefficients: T_w and dT are the whole state)
+        launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
+                          static_cast<double*>(ngf_.state_frh()), false, s_);
     check_launch("Objective: Hv state refresh");
     stale_ = false;
 }
@@ -429,7 +432,7 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
     warp_state(y, s, wlo, whi, state);
     launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                      state ? static_cast<double*>(ngf_.state_frh()) : nullptr, grad != nullptr, s,
+                      state ? frh_out() : nullptr, grad != nullptr, s,
                       scalars_direct ? sc_.dev(0) : nullptr, scalars_direct ? sc_.host_dev() : nullptr);
     MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     if (scalars_direct) {
@@ -466,7 +469,7 @@ void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* 
         launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
         MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
     }
-    launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s, skip);
+    launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s, skip);
     if (alpha_ != 0.0) MFREG_CUDA(cudaStreamWaitEvent(s, ev_join_, 0));
     FinalizeSpec f;
     f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
@@ -474,6 +477,7 @@ void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* 
     f.dot_a = dot_a;
     f.sc = sc;
     f.skip = skip;
+    f.hv_pass = true;
     launch_nodal_finalize(plan_, *fused_, f, s);
     check_launch("Objective::gn_hessian_vec (fused)");
 }
@@ -490,10 +494,10 @@ double DeviceObjective::profile_kernel(int which, const double* p, int reps, std
         if (flush_bytes) MFREG_CUDA(cudaMemsetAsync(scratch.get(), r & 0xff, flush_bytes, s_));
         MFREG_CUDA(cudaEventRecord(e0, s_));
         if (which == 0)
-            launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, s_);
+            launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s_);
         else if (which == 1)
             launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
-                              static_cast<double*>(ngf_.state_frh()), true, s_);
+                              frh_out(), true, s_);
         else
             warp_state(p, s_, 0, -1);
         MFREG_CUDA(cudaEventRecord(e1, s_));

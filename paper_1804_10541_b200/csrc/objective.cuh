@@ -356,6 +356,8 @@ private:
     void enqueue_eval_fast(const double* y, double* grad, cudaStream_t s, bool state = true);
     void warp_state(const double* y, cudaStream_t s, int zlo, int zhi, bool state = true);
     void refresh_state();
+    // where the eval pass stores rho-hat: nowhere when the Hv pass recomputes it (hv3)
+    double* frh_out();
     void enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip, cudaStream_t s);
     Grid img_, dg_;
     SlabSpec slab_;

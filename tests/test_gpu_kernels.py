@@ -1,5 +1,6 @@
-"""Kernel-variant parity: the two-CTA/SM fast kernels against the legacy fused
-kernels (MFREG_NO_HV2=1, MFREG_NO_EV2=1) and the CPU oracle, on shapes that exercise partial
+"""Kernel-variant parity: the two-CTA/SM kernels with stored coefficients (default), the Hv
+pass with recomputed coefficients (hv3, MFREG_HV3=1) and the legacy fused kernels
+(MFREG_NO_HV2=1, MFREG_NO_EV2=1) against each other and the CPU oracle, on shapes that exercise partial
 tiles, anisotropic spacing, thin volumes, coarse/fine deformation grids and z
 slabs. Fast-mode tolerance as DESIGN.md §3 (max-rel 1e-9)."""
 import os
@@ -20,11 +21,15 @@ def max_rel(a, b):
     return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300))
 
 
-def _objective(P, R, T, m, h, ratio, legacy):
-    keys = ("MFREG_NO_HV2", "MFREG_NO_EV2")
-    old = {k: os.environ.get(k) for k in keys}
-    for k in keys:
-        os.environ[k] = "1" if legacy else "0"
+VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0"},
+            "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0"},
+            "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1"}}
+
+
+def _objective(P, R, T, m, h, ratio, variant):
+    env = VARIANTS[variant]
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         img = P.make_image_grid(m, h)
         dg = P.deformation_grid_for(img, ratio)
@@ -50,7 +55,7 @@ def test_hv_kernel_variants(P, oracle, case):
     J, _, _, grad = o.eval(y)
     hv = o.gn_hessian_vec(p)
     res = []
-    for legacy in (True, False):
+    for legacy in VARIANTS:
         obj = _objective(P, R, T, m, h, ratio, legacy)
         g = np.empty(obj.dof())
         j = obj.eval(y, g)
@@ -63,8 +68,9 @@ def test_hv_kernel_variants(P, oracle, case):
         assert max_rel(j2, j) <= 1e-14
         assert np.array_equal(obj.gn_hessian_vec(p), q)
         res.append((j, g, q))
-    for a_, b_ in zip(res[1], res[0]):
-        assert max_rel(a_, b_) <= 1e-12
+    for other in res[1:]:
+        for a_, b_ in zip(other, res[0]):
+            assert max_rel(a_, b_) <= 1e-12
 
 
 
