@@ -29,7 +29,11 @@ EXTRA = {"fp64_pipe_pct": "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained
 def main(workload: str, rep: str) -> None:
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
-    hdr = rows[0]
+    hdr, units = rows[0], rows[1]
+    # the raw page scales each metric to a display unit (row 2): convert to bytes / ns
+    scale_of = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                "nsecond": 1.0, "usecond": 1e3, "msecond": 1e6, "second": 1e9,
+                "ns": 1.0, "us": 1e3, "ms": 1e6, "s": 1e9}
     col = {k: hdr.index(k) for k in ("Kernel Name", "dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum")}
     col.update({k: hdr.index(v) for k, v in EXTRA.items() if v in hdr})
     per = {}
@@ -38,7 +42,7 @@ def main(workload: str, rep: str) -> None:
         key = next((v for k, v in KERNELS.items() if k in name and "<float>" not in name), None)
         if key is None:
             continue
-        f = lambda c: float(r[col[c]].replace(",", ""))  # noqa: E731
+        f = lambda c: float(r[col[c]].replace(",", "")) * scale_of.get(units[col[c]], 1.0)  # noqa: E731
         per.setdefault(key, []).append((f("dram__bytes_read.sum") + f("dram__bytes_write.sum"), f("gpu__time_duration.sum"),
                                         {k: f(k) for k in EXTRA if k in col}))
     try:
