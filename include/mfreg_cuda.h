@@ -187,6 +187,11 @@ int mfreg_cu_objective_dot(mfreg_cu_objective* obj, const double* a, const doubl
  * comes from ranks r-1 / r+1), bnd (P^T planes [own_hi, own_hi + bnd) shared with
  * rank r+1, which adds them). Pure host computation. */
 int mfreg_cu_slab_partition(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int32_t* table);
+/* the same for parity-mode slabs (MFREG_CU_PARITY): their operand halo also covers the warp of
+ * the image planes of the nodal slab below own_lo, whose per-voxel terms the rank recomputes so
+ * that each owned node's P^T gather runs complete (bnd is then unused) */
+int mfreg_cu_slab_partition_mode(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int mode,
+                                 int32_t* table);
 /* Objective over one slab (fast mode): ref/tpl are the whole volume (replicated);
  * slab = {zlo, zhi, own_lo, own_hi} from the partition. eval / gn_hessian_vec
  * return this rank's contributions: D and alpha S of its planes (via
@@ -211,10 +216,13 @@ int mfreg_cu_comm_create_nccl(const unsigned char id[128], int nranks, int rank,
 int mfreg_cu_comm_create_local(int nranks, mfreg_cu_comm** out);
 int mfreg_cu_comm_destroy(mfreg_cu_comm* comm);
 int mfreg_cu_comm_rank(mfreg_cu_comm* comm, int* rank, int* size);
-/* this rank's share of Objective (optimizer.hpp:53-106), fast mode: ref / tpl are the whole
- * volume (replicated), the slab is slab_partition(image, deform, size)[rank] */
+/* this rank's share of Objective (optimizer.hpp:53-106): ref / tpl are the whole volume
+ * (replicated), the slab is slab_partition_mode(image, deform, size, mode)[rank].
+ * mode MFREG_CU_FAST: fused kernels, scalars within the fast-mode tolerance of one GPU;
+ * MFREG_CU_PARITY: J, gradient, GN Hv and every vec_dot bitwise equal to the one-GPU parity
+ * objective (the reference's 4096-chunk sums and red-black P^T order across ranks) */
 int mfreg_cu_slab_create(mfreg_cu_comm* comm, const double* ref, const double* tpl, const mfreg_cu_grid* image,
-                         const mfreg_cu_grid* deform, double tau, double rho, double alpha, int where,
+                         const mfreg_cu_grid* deform, double tau, double rho, double alpha, int mode, int where,
                          mfreg_cu_slab** out);
 int mfreg_cu_slab_destroy(mfreg_cu_slab* slab);
 /* zlo, zhi, own_lo, own_hi, need_lo, need_hi, bnd of this rank */
@@ -234,8 +242,8 @@ int mfreg_cu_slab_gather(mfreg_cu_slab* slab, double* v_dev);
 int mfreg_cu_slab_minimize(mfreg_cu_slab* slab, int method, const double* y0_dev, const mfreg_cu_opt_config* cfg,
                            double* y_out_dev, mfreg_cu_iter_record* trace, int cap, int* ntrace,
                            int* line_search_failed);
-/* register_multilevel over z slabs (fast mode): every level sharded over the communicator
- * (levels too thin for the slab halo run replicated); result on every rank */
+/* register_multilevel over z slabs (fast or parity mode, cfg->mode): every level sharded over
+ * the communicator (levels too thin for the slab halo run replicated); result on every rank */
 int mfreg_cu_slab_register_multilevel(mfreg_cu_comm* comm, const double* ref, const double* tpl,
                                       const mfreg_cu_grid* image, const mfreg_cu_ml_config* cfg, double* y_out,
                                       mfreg_cu_grid* deform_out, mfreg_cu_iter_record* trace, int cap, int* level_iters,

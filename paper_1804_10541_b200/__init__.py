@@ -124,6 +124,7 @@ _SIGS = {
     "mfreg_cu_objective_seed_hessian_vec": ([_vp, _dp, C.c_double, _dp, C.c_int], C.c_int),
     "mfreg_cu_objective_dot": ([_vp, _dp, _dp, C.c_int, C.POINTER(C.c_double)], C.c_int),
     "mfreg_cu_slab_partition": ([_gp, _gp, C.c_int, C.POINTER(C.c_int32)], C.c_int),
+    "mfreg_cu_slab_partition_mode": ([_gp, _gp, C.c_int, C.c_int, C.POINTER(C.c_int32)], C.c_int),
     "mfreg_cu_objective_create_slab": ([_dp, _dp, _gp, _gp, C.c_double, C.c_double, C.c_double,
                                         C.POINTER(C.c_int32), C.c_int, C.POINTER(_vp)], C.c_int),
     "mfreg_cu_cg_solve": ([_vp, C.c_int, C.c_double, _dp, C.c_int, C.c_double, _dp, C.POINTER(C.c_int),
@@ -160,8 +161,8 @@ _SIGS = {
     "mfreg_cu_comm_create_local": ([C.c_int, C.POINTER(_vp)], C.c_int),
     "mfreg_cu_comm_destroy": ([_vp], C.c_int),
     "mfreg_cu_comm_rank": ([_vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
-    "mfreg_cu_slab_create": ([_vp, _dp, _dp, _gp, _gp, C.c_double, C.c_double, C.c_double, C.c_int, C.POINTER(_vp)],
-                             C.c_int),
+    "mfreg_cu_slab_create": ([_vp, _dp, _dp, _gp, _gp, C.c_double, C.c_double, C.c_double, C.c_int, C.c_int,
+                              C.POINTER(_vp)], C.c_int),
     "mfreg_cu_slab_destroy": ([_vp], C.c_int),
     "mfreg_cu_slab_info": ([_vp, C.POINTER(C.c_int32)], C.c_int),
     "mfreg_cu_slab_identity": ([_vp, _dp], C.c_int),

@@ -309,8 +309,12 @@ int mfreg_cu_objective_create_slab(const double* ref, const double* tpl, const m
     });
 }
 int mfreg_cu_slab_partition(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int32_t* table) {
+    return mfreg_cu_slab_partition_mode(image, deform, nranks, MFREG_CU_FAST, table);
+}
+int mfreg_cu_slab_partition_mode(const mfreg_cu_grid* image, const mfreg_cu_grid* deform, int nranks, int mode,
+                                 int32_t* table) {
     return guard([&] {
-        const auto parts = slab_partition(to_grid(image), to_grid(deform), nranks);
+        const auto parts = slab_partition(to_grid(image), to_grid(deform), nranks, to_mode(mode) == Mode::Parity);
         for (int r = 0; r < nranks; ++r) {
             const SlabInfo& s = parts[r];
             const int32_t v[7] = {s.zlo, s.zhi, s.own_lo, s.own_hi, s.need_lo, s.need_hi, s.bnd};

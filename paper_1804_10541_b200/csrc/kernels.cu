@@ -25,10 +25,10 @@ inline dim3 block3() { return dim3(BX, BY, 1); }
 
 inline unsigned blocks1(idx_t n, int t = 256) { return static_cast<unsigned>(std::max<idx_t>(1, (n + t - 1) / t)); }
 
-__device__ __forceinline__ bool coords(const Grid& g, idx_t& x, idx_t& y, idx_t& z) {
+__device__ __forceinline__ bool coords(const Grid& g, idx_t& x, idx_t& y, idx_t& z, int zoff = 0) {
     x = static_cast<idx_t>(blockIdx.x) * BX + threadIdx.x;
     y = static_cast<idx_t>(blockIdx.y) * BY + threadIdx.y;
-    z = blockIdx.z;
+    z = static_cast<idx_t>(blockIdx.z) + zoff;  // z window [zoff, zoff + gridDim.z) (parity z slabs)
     return x < g.m[0] && y < g.m[1];
 }
 
@@ -241,9 +241,9 @@ __global__ void k_sample(Grid g, const double* __restrict__ T, const double* __r
 // transfer.cpp:92-150 as a per-node gather in the reference's exact accumulation
 // order: odd deformation z-slab first, then even; inside a slab image planes,
 // rows, columns ascending; each term ((wx*wy)*wz)*v. Deterministic, no atomics.
-__global__ void k_transfer_T(DevPlan P, const double* __restrict__ w, double* __restrict__ out) {
+__global__ void k_transfer_T(DevPlan P, const double* __restrict__ w, double* __restrict__ out, int zoff) {
     idx_t nx, ny, nz;
-    if (!coords(P.src, nx, ny, nz)) return;
+    if (!coords(P.src, nx, ny, nz, zoff)) return;
     const idx_t nt = P.tgt.count(), ns = P.src.count();
     const idx_t tm0 = P.tgt.m[0], tm01 = P.tgt.m[0] * P.tgt.m[1];
     const idx_t ncx = P.src.m[0] - 1, ncy = P.src.m[1] - 1, ncz = P.src.m[2] - 1;
@@ -320,9 +320,9 @@ __device__ __forceinline__ void dgrad6(const double* __restrict__ v, const Grid&
 // directions, stored direction-major rh[k*n+i]); rho-hat(0) summed over kAllDirs.
 __global__ void k_ngf_ws(Grid g, const double* __restrict__ R, const double* __restrict__ Tw, double tau, double rho,
                          double* __restrict__ r, double* __restrict__ inv1o, double* __restrict__ inv2o,
-                         double* __restrict__ rh) {
+                         double* __restrict__ rh, int zoff) {
     idx_t x, y, z;
-    if (!coords(g, x, y, z)) return;
+    if (!coords(g, x, y, z, zoff)) return;
     const idx_t n = g.count(), i = g.lin(x, y, z);
     double gt[6], gr[6];
     dgrad6(Tw, g, x, y, z, gt);
@@ -360,9 +360,9 @@ __global__ void k_ngf_ws(Grid g, const double* __restrict__ R, const double* __r
 // out_d = (-2 h_bar * acc) * dT_d. 3-D neighbours: wrapped linear neighbours of the
 // reference contribute exact zeros (clamped rho-hat), so skipping them is bitwise neutral.
 __global__ void k_ngf_gradient(Grid g, double scale, const double* __restrict__ r, const double* __restrict__ rh,
-                               const double* __restrict__ dT, double* __restrict__ out) {
+                               const double* __restrict__ dT, double* __restrict__ out, int zoff) {
     idx_t x, y, z;
-    if (!coords(g, x, y, z)) return;
+    if (!coords(g, x, y, z, zoff)) return;
     const idx_t n = g.count(), i = g.lin(x, y, z);
     double acc = 0.0;
 #pragma unroll
@@ -379,9 +379,9 @@ __global__ void k_ngf_gradient(Grid g, double scale, const double* __restrict__ 
 }
 
 __global__ void k_Pp_s(DevPlan P, const double* __restrict__ p, const double* __restrict__ dT,
-                       double* __restrict__ sv) {
+                       double* __restrict__ sv, int zoff) {
     idx_t x, yy, z;
-    if (!coords(P.tgt, x, yy, z)) return;
+    if (!coords(P.tgt, x, yy, z, zoff)) return;
     double v[3];
     transfer_point(P, p, x, yy, z, v);
     const idx_t n = P.tgt.count(), i = P.tgt.lin(x, yy, z);
@@ -391,9 +391,10 @@ __global__ void k_Pp_s(DevPlan P, const double* __restrict__ p, const double* __
 // ngf.cpp:105-163 (Alg. 4.2) bit-identical: entries by ascending kappa, pairs in
 // (da, db) insertion order, drdr accumulated from 0.0, c = drdr * s, q += c * dT_i.
 __global__ void k_hv_closed(Grid g, HvTable tab, double scale, const double* __restrict__ rh,
-                            const double* __restrict__ sv, const double* __restrict__ dT, double* __restrict__ out) {
+                            const double* __restrict__ sv, const double* __restrict__ dT, double* __restrict__ out,
+                            int zoff) {
     idx_t x, y, z;
-    if (!coords(g, x, y, z)) return;
+    if (!coords(g, x, y, z, zoff)) return;
     const idx_t n = g.count(), i = g.lin(x, y, z);
     double qx = 0.0, qy = 0.0, qz = 0.0;
     const double d0 = dT[i], d1 = dT[n + i], d2 = dT[2 * n + i];
@@ -522,11 +523,12 @@ __device__ __forceinline__ void canon_group(const CanonCtx& c, double d0, double
 
 __global__ void __launch_bounds__(BX * BY) k_hv_closed_canon(Grid g, double scale, const double* __restrict__ rh,
                                                              const double* __restrict__ sv,
-                                                             const double* __restrict__ dT, double* __restrict__ out) {
+                                                             const double* __restrict__ dT, double* __restrict__ out,
+                                                             int zoff) {
     CanonCtx c;
     c.x = static_cast<int>(blockIdx.x) * BX + threadIdx.x;
     c.y = static_cast<int>(blockIdx.y) * BY + threadIdx.y;
-    c.z = blockIdx.z;
+    c.z = static_cast<int>(blockIdx.z) + zoff;
     c.mx = static_cast<int>(g.m[0]);
     c.my = static_cast<int>(g.m[1]);
     c.mz = static_cast<int>(g.m[2]);
@@ -726,18 +728,19 @@ __device__ __forceinline__ double lap_at(const double* __restrict__ u, const Lap
     return s;
 }
 
-__device__ __forceinline__ bool lap_coords(const LapGeo& g, int& x, int& y, int& z, int& i) {
+__device__ __forceinline__ bool lap_coords(const LapGeo& g, int& x, int& y, int& z, int& i, int zoff) {
     x = static_cast<int>(blockIdx.x) * BX + threadIdx.x;
     y = static_cast<int>(blockIdx.y) * BY + threadIdx.y;
-    z = blockIdx.z;
+    z = static_cast<int>(blockIdx.z) + zoff;
     i = x + y * g.mx + z * g.pn;
     return x < g.mx && y < g.my;
 }
 
 template <bool P2>
-__global__ void __launch_bounds__(BX * BY) k_lap3(LapGeo g, const double* __restrict__ u, double* __restrict__ out) {
+__global__ void __launch_bounds__(BX * BY) k_lap3(LapGeo g, const double* __restrict__ u, double* __restrict__ out,
+                                                  int zoff) {
     int x, y, z, i;
-    if (!lap_coords(g, x, y, z, i)) return;
+    if (!lap_coords(g, x, y, z, i, zoff)) return;
     const long long n = static_cast<long long>(g.pn) * g.mz;
 #pragma unroll
     for (int d = 0; d < 3; ++d) out[d * n + i] = lap_at<P2>(u + d * n, g, x, y, z, i);
@@ -747,9 +750,10 @@ __global__ void __launch_bounds__(BX * BY) k_lap3(LapGeo g, const double* __rest
 // or the gamma shift of optimizer.cpp:106-111)
 template <bool P2, int MODE>
 __global__ void __launch_bounds__(BX * BY) k_bilap(LapGeo g, const double* __restrict__ lu, double scale, double alpha,
-                                                   double gamma, const double* __restrict__ p, double* __restrict__ out) {
+                                                   double gamma, const double* __restrict__ p, double* __restrict__ out,
+                                                   int zoff) {
     int x, y, z, i;
-    if (!lap_coords(g, x, y, z, i)) return;
+    if (!lap_coords(g, x, y, z, i, zoff)) return;
     const long long n = static_cast<long long>(g.pn) * g.mz;
 #pragma unroll
     for (int d = 0; d < 3; ++d) {
@@ -1128,8 +1132,20 @@ __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, con
     }
 }
 
-void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s) {
-    note_launch(), k_transfer_T<<<grid3(P.src), block3(), 0, s>>>(P, w, out);
+// z window helpers: [lo, hi) clipped to [0, m); hi < 0 means m
+static inline bool zwin(const Grid& g, dim3& gr, int& lo, int hi) {
+    gr = grid3(g);
+    const int m = static_cast<int>(g.m[2]);
+    lo = std::max(0, lo);
+    hi = hi < 0 ? m : std::min(hi, m);
+    if (hi <= lo) return false;
+    gr.z = static_cast<unsigned>(hi - lo);
+    return true;
+}
+void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s, int zlo, int zhi) {
+    dim3 gr;
+    if (!zwin(P.src, gr, zlo, zhi)) return;
+    note_launch(), k_transfer_T<<<gr, block3(), 0, s>>>(P, w, out, zlo);
 }
 void launch_sample(const Grid& img0, const double* T, const double* pts, idx_t n, double* vals, double* dT,
                    cudaStream_t s) {
@@ -1191,26 +1207,34 @@ void launch_warp_fast(const DevPlan& P, const double* y, const double* T, float*
     warp_fast_impl(P, y, T, Tw, dT, s, zlo, zhi);
 }
 void launch_ngf_ws(const Grid& img0, const double* R, const double* Tw, double tau, double rho, double* r,
-                   double* inv1, double* inv2, double* rh, cudaStream_t s) {
+                   double* inv1, double* inv2, double* rh, cudaStream_t s, int zlo, int zhi) {
     Grid img = img0;
     img.set_inv();
-    note_launch(), k_ngf_ws<<<grid3(img), block3(), 0, s>>>(img, R, Tw, tau, rho, r, inv1, inv2, rh);
+    dim3 gr;
+    if (!zwin(img, gr, zlo, zhi)) return;
+    note_launch(), k_ngf_ws<<<gr, block3(), 0, s>>>(img, R, Tw, tau, rho, r, inv1, inv2, rh, zlo);
 }
 void launch_ngf_gradient(const Grid& img, const double* r, const double* rh, const double* dT, double* out,
-                         cudaStream_t s) {
+                         cudaStream_t s, int zlo, int zhi) {
     const double scale = -2.0 * img.cell_volume();
-    note_launch(), k_ngf_gradient<<<grid3(img), block3(), 0, s>>>(img, scale, r, rh, dT, out);
+    dim3 gr;
+    if (!zwin(img, gr, zlo, zhi)) return;
+    note_launch(), k_ngf_gradient<<<gr, block3(), 0, s>>>(img, scale, r, rh, dT, out, zlo);
 }
-void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv, cudaStream_t s) {
-    note_launch(), k_Pp_s<<<grid3(P.tgt), block3(), 0, s>>>(P, p, dT, sv);
+void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv, cudaStream_t s, int zlo, int zhi) {
+    dim3 gr;
+    if (!zwin(P.tgt, gr, zlo, zhi)) return;
+    note_launch(), k_Pp_s<<<gr, block3(), 0, s>>>(P, p, dT, sv, zlo);
 }
 void launch_hv_closed(const Grid& img, const HvTable& tab, const double* rh, const double* sv, const double* dT,
-                      double* out, cudaStream_t s) {
+                      double* out, cudaStream_t s, int zlo, int zhi) {
     const double scale = 2.0 * img.cell_volume();
+    dim3 gr;
+    if (!zwin(img, gr, zlo, zhi)) return;
     if (is_canon_hv_table(tab))
-        note_launch(), k_hv_closed_canon<<<grid3(img), block3(), 0, s>>>(img, scale, rh, sv, dT, out);
+        note_launch(), k_hv_closed_canon<<<gr, block3(), 0, s>>>(img, scale, rh, sv, dT, out, zlo);
     else
-        note_launch(), k_hv_closed<<<grid3(img), block3(), 0, s>>>(img, tab, scale, rh, sv, dT, out);
+        note_launch(), k_hv_closed<<<gr, block3(), 0, s>>>(img, tab, scale, rh, sv, dT, out, zlo);
 }
 void launch_hv_factored(const Grid& img, const double* rh, const double* sv, const double* dT, double* wbuf,
                         double* out, cudaStream_t s) {
@@ -1234,6 +1258,51 @@ void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, dou
         else k_chunks_warp<SUM_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
     }
     note_launch(), k_serial<<<1, 32, 0, s>>>(partials, nch, scale, out);
+}
+// chunked_sum across ranks (z slabs, parity mode; DistSum in slab.cu): a rank's interior chunk
+// partials (k_chunks_warp on a chunk-aligned sub-range) and the raw terms of the chunks it only
+// partly owns; after the all-gather every rank rebuilds each chunk's sequential sum from the
+// pieces in index order and adds the chunks in order (parallel.cpp:51-73, bitwise).
+void launch_chunk_partials(int kind, idx_t n, const double* a, const double* b, double* partials, cudaStream_t s) {
+    const idx_t nch = chunk_count(n);
+    if (nch <= 0) return;
+    const unsigned g = static_cast<unsigned>(nch);
+    const std::size_t sm = kChunk * sizeof(double);
+    note_launch();
+    if (kind == SUM_ONE_MINUS_SQ) k_chunks_warp<SUM_ONE_MINUS_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
+    else if (kind == SUM_DOT) k_chunks_warp<SUM_DOT><<<g, 32, sm, s>>>(n, a, b, partials);
+    else k_chunks_warp<SUM_SQ><<<g, 32, sm, s>>>(n, a, b, partials);
+}
+__global__ void k_sum_terms(int kind, idx_t n, const double* __restrict__ a, const double* __restrict__ b,
+                            double* __restrict__ out) {
+    const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = sum_term(kind, a, b, i);
+}
+void launch_sum_terms(int kind, idx_t n, const double* a, const double* b, double* out, cudaStream_t s) {
+    if (n <= 0) return;
+    note_launch(), k_sum_terms<<<blocks1(n), 256, 0, s>>>(kind, n, a, b, out);
+}
+__global__ void k_chunk_assemble(idx_t nch, const long long* __restrict__ off, const int* __restrict__ cnt,
+                                 const ChunkPiece* __restrict__ pieces, const double* __restrict__ g,
+                                 double* __restrict__ vals) {
+    const idx_t c = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    if (c >= nch) return;
+    const int k = cnt[c];
+    if (k == 0) {
+        vals[c] = g[off[c]];
+        return;
+    }
+    double s = 0.0;  // the chunk's terms in index order, from 0.0, across the owners' pieces
+    for (int q = 0; q < k; ++q) {
+        const ChunkPiece pc = pieces[off[c] + q];
+        for (int t = 0; t < pc.len; ++t) s += g[pc.off + t];
+    }
+    vals[c] = s;
+}
+void launch_chunk_assemble(idx_t nch, const long long* off, const int* cnt, const ChunkPiece* pieces,
+                           const double* gathered, double* vals, double scale, double* out, cudaStream_t s) {
+    if (nch > 0) note_launch(), k_chunk_assemble<<<blocks1(nch, 128), 128, 0, s>>>(nch, off, cnt, pieces, gathered, vals);
+    note_launch(), k_serial<<<1, 32, 0, s>>>(vals, nch, scale, out);
 }
 void launch_chunked_sum3(int kind, idx_t n, const double* a, const double* b, double* partials, double* out3,
                          double scale, cudaStream_t s) {
@@ -1275,26 +1344,30 @@ static bool lap_geo(const Grid& g, LapGeo& o) {
     return p2;
 }
 
-void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s) {
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo, int zhi) {
     LapGeo lg;
-    if (lap_geo(g, lg)) note_launch(), k_lap3<true><<<grid3(g), block3(), 0, s>>>(lg, u, out);
-    else note_launch(), k_lap3<false><<<grid3(g), block3(), 0, s>>>(lg, u, out);
+    dim3 gr;
+    if (!zwin(g, gr, zlo, zhi)) return;
+    if (lap_geo(g, lg)) note_launch(), k_lap3<true><<<gr, block3(), 0, s>>>(lg, u, out, zlo);
+    else note_launch(), k_lap3<false><<<gr, block3(), 0, s>>>(lg, u, out, zlo);
 }
 
 template <bool P2>
-static void launch_bilap_t(const Grid& g, const LapGeo& lg, const double* lap_u, double scale, int mode, double alpha,
-                           double gamma, const double* p, double* out, cudaStream_t s) {
-    if (mode == 0) k_bilap<P2, 0><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
-    else if (mode == 1) k_bilap<P2, 1><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
-    else k_bilap<P2, 2><<<grid3(g), block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out);
+static void launch_bilap_t(dim3 gr, int zlo, const LapGeo& lg, const double* lap_u, double scale, int mode,
+                           double alpha, double gamma, const double* p, double* out, cudaStream_t s) {
+    if (mode == 0) k_bilap<P2, 0><<<gr, block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out, zlo);
+    else if (mode == 1) k_bilap<P2, 1><<<gr, block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out, zlo);
+    else k_bilap<P2, 2><<<gr, block3(), 0, s>>>(lg, lap_u, scale, alpha, gamma, p, out, zlo);
 }
 
 void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
-                  const double* p, double* out, cudaStream_t s) {
+                  const double* p, double* out, cudaStream_t s, int zlo, int zhi) {
     LapGeo lg;
+    dim3 gr;
+    if (!zwin(g, gr, zlo, zhi)) return;
     note_launch();
-    if (lap_geo(g, lg)) launch_bilap_t<true>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
-    else launch_bilap_t<false>(g, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
+    if (lap_geo(g, lg)) launch_bilap_t<true>(gr, zlo, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
+    else launch_bilap_t<false>(gr, zlo, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
 }
 void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,
                        cudaStream_t s) {

@@ -24,7 +24,9 @@ long long launch_counter();
 
 // ---- grid transfer and warp (transfer.cpp:49-150, volume.cpp:29-94)
 void launch_transfer_apply(const DevPlan& P, const double* y, double* out, cudaStream_t s);
-void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s);
+// (zlo, zhi): z window of the outputs (nodal planes for P^T / curvature, image planes otherwise);
+// the default is the whole grid
+void launch_transfer_T(const DevPlan& P, const double* w, double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
 void launch_sample(const Grid& img, const double* T, const double* pts, idx_t n, double* vals, double* dT,
                    cudaStream_t s);
 // Fused P*y + trilinear sample: T_w and dT/dP (32 B/voxel) without materialising P*y.
@@ -40,14 +42,15 @@ void launch_warp(const DevPlan& P, const double* y, const double* T, double* Tw,
 
 // ---- NGF workspace (ngf.cpp:185-214) + rho-hat table (ngf.cpp:39-64)
 void launch_ngf_ws(const Grid& img, const double* R, const double* Tw, double tau, double rho, double* r,
-                   double* inv1, double* inv2, double* rh, cudaStream_t s);
+                   double* inv1, double* inv2, double* rh, cudaStream_t s, int zlo = 0, int zhi = -1);
 void launch_ngf_gradient(const Grid& img, const double* r, const double* rh, const double* dT, double* out,
-                         cudaStream_t s);
+                         cudaStream_t s, int zlo = 0, int zhi = -1);
 // s_i = dT_i . (P p)_i  (the inner product inside ngf.cpp:145-148)
-void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv, cudaStream_t s);
+void launch_Pp_s(const DevPlan& P, const double* p, const double* dT, double* sv, cudaStream_t s, int zlo = 0,
+                 int zhi = -1);
 // parity: closed form (ngf.cpp:105-163), bit-identical
 void launch_hv_closed(const Grid& img, const HvTable& tab, const double* rh, const double* sv, const double* dT,
-                      double* out, cudaStream_t s);
+                      double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
 // fast: factored 2h dT^T dr^T (dr (dT p))
 void launch_hv_factored(const Grid& img, const double* rh, const double* sv, const double* dT, double* wbuf,
                         double* out, cudaStream_t s);
@@ -61,6 +64,15 @@ void launch_chunked_sum(int kind, idx_t n, const double* a, const double* b, dou
 // three equal-length segments (a + d n, d = 0..2), each summed as launch_chunked_sum into out3[d]
 void launch_chunked_sum3(int kind, idx_t n, const double* a, const double* b, double* partials, double* out3,
                          double scale, cudaStream_t s);
+// distributed chunked_sum pieces (slab.cu DistSum)
+struct ChunkPiece {
+    long long off;  // first term in the gathered blocks
+    int len;
+};
+void launch_chunk_partials(int kind, idx_t n, const double* a, const double* b, double* partials, cudaStream_t s);
+void launch_sum_terms(int kind, idx_t n, const double* a, const double* b, double* out, cudaStream_t s);
+void launch_chunk_assemble(idx_t nch, const long long* off, const int* cnt, const ChunkPiece* pieces,
+                           const double* gathered, double* vals, double scale, double* out, cudaStream_t s);
 void launch_tree_sum(int kind, idx_t n, const double* a, const double* b, double* partials, double* out,
                      double scale, cudaStream_t s);
 idx_t chunk_count(idx_t n);
@@ -69,10 +81,10 @@ idx_t tree_blocks(idx_t n);
 void launch_inf_norm(idx_t n, const double* a, double scale, double* out, cudaStream_t s);
 
 // ---- curvature (curvature.cpp:9-98), nodal grid, 3 components
-void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s);
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
 // mode 0: out = scale*Lap(in); 1: out += alpha*(scale*Lap(in)); 2: out = scale*Lap(in) + gamma*p
 void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
-                  const double* p, double* out, cudaStream_t s);
+                  const double* p, double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
 // curvature value finalize: out = alpha * (cellvol * ((S0 + S1) + S2))
 void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s);
 void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,

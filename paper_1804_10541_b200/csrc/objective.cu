@@ -136,7 +136,7 @@ std::vector<int> plan_base_axis(idx_t mt, idx_t ms) {
     return hb;
 }
 
-std::vector<SlabInfo> slab_partition(const Grid& img, const Grid& dg, int nr) {
+std::vector<SlabInfo> slab_partition(const Grid& img, const Grid& dg, int nr, bool parity) {
     validate_grid(dg, true);
     validate_grid(img, false);
     if (nr < 1) throw std::invalid_argument("slab_partition: nranks must be >= 1");
@@ -161,7 +161,14 @@ std::vector<SlabInfo> slab_partition(const Grid& img, const Grid& dg, int nr) {
         s.bnd = r == nr - 1 ? 0 : std::max(0, b[s.zhi - 1] + 2 - s.own_hi);
         // operand planes read: the warp over [zlo-3, zhi+3) and the curvature stencil
         // (Lap Lap: +-2 nodal planes) of the owned planes
-        const int wlo = std::max(0, s.zlo - 3), whi = std::min(mz, s.zhi + 3);
+        int wlo = std::max(0, s.zlo - 3), whi = std::min(mz, s.zhi + 3);
+        if (parity) {  // the warp over [first plane of nodal slab own_lo - 1, zhi) +- 2 planes
+            int z = s.zlo;
+            if (s.own_lo > 0)
+                while (z > 0 && b[z - 1] >= s.own_lo - 1) --z;
+            wlo = std::max(0, z - 2);
+            whi = std::min(mz, s.zhi + 2);
+        }
         s.need_lo = std::max(0, std::min(b[wlo], s.own_lo - 2));
         s.need_hi = std::min(ms, std::max(b[whi - 1] + 2, s.own_hi + 2));
     }
@@ -295,11 +302,13 @@ void DeviceNgf::populate_points(const double* T_dev, const double* pts_dev) {
     check_launch("populate_ngf_workspace");
 }
 
-void DeviceNgf::populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev) {
+void DeviceNgf::populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev, int wlo, int whi, int slo,
+                              int shi) {
     ensure_ws();
     if (!(tau_ > 0.0) || !(rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
-    launch_warp(P, y_dev, T_dev, Tw.get(), dT.get(), s_);
-    launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_);
+    const int mz = static_cast<int>(g_.m[2]);
+    launch_warp(P, y_dev, T_dev, Tw.get(), dT.get(), s_, std::max(0, wlo), whi < 0 ? -1 : std::min(whi, mz));
+    launch_ngf_ws(g_, R_, Tw.get(), tau_, rho_, r.get(), inv1.get(), inv2.get(), rh.get(), s_, slo, shi);
     check_launch("warp + workspace");
 }
 
@@ -307,13 +316,13 @@ void DeviceNgf::value_async(double* out_dev) {
     red_.sum(SUM_ONE_MINUS_SQ, g_.count(), r.get(), nullptr, out_dev, g_.cell_volume(), s_);
 }
 
-void DeviceNgf::gradient(double* out3n) {
-    launch_ngf_gradient(g_, r.get(), rh.get(), dT.get(), out3n, s_);
+void DeviceNgf::gradient(double* out3n, int zlo, int zhi) {
+    launch_ngf_gradient(g_, r.get(), rh.get(), dT.get(), out3n, s_, zlo, zhi);
     check_launch("ngf_gradient");
 }
 
-void DeviceNgf::hessian_vec_image(const double* svp, double* out3n) {
-    if (mode_ == Mode::Parity) launch_hv_closed(g_, tab_, rh.get(), svp, dT.get(), out3n, s_);
+void DeviceNgf::hessian_vec_image(const double* svp, double* out3n, int zlo, int zhi) {
+    if (mode_ == Mode::Parity) launch_hv_closed(g_, tab_, rh.get(), svp, dT.get(), out3n, s_, zlo, zhi);
     else launch_hv_factored(g_, rh.get(), svp, dT.get(), wbuf.get(), out3n, s_);
     check_launch("ngf_hessian_vec");
 }
@@ -353,13 +362,34 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
     check_launch("identity");
     sliced_ = !slab.full(static_cast<int>(img_.m[2]), static_cast<int>(dg_.m[2]));
     if (sliced_) {
-        if (mode == Mode::Parity) throw std::invalid_argument("z slabs require fast mode");
+        if (mode == Mode::Fast32) throw std::invalid_argument("z slabs run in fast or parity mode");
         const auto parts = slab_partition(img_, dg_, 1);  // validates the grids
         (void)parts;
         const int mz = static_cast<int>(img_.m[2]), msz = static_cast<int>(dg_.m[2]);
         if (!(0 <= slab.zlo && slab.zlo < slab.zhi && slab.zhi <= mz && 0 <= slab.own_lo &&
               slab.own_lo < slab.own_hi && slab.own_hi <= msz))
             throw std::invalid_argument("slab: invalid z window");
+        if (mode == Mode::Parity) {
+            // the owned nodes' P^T reads the image planes of nodal slabs own_lo-1 .. own_hi-1, i.e.
+            // [wlo, zhi); their per-voxel terms read the workspace one plane further, which reads
+            // T_w one more; s = dT.(P p) is read two planes out by the 25-point Hv stencil
+            const auto& bz = plan_.host_base[2];
+            int wlo = 0;
+            if (slab.own_lo > 0) {
+                wlo = slab.zlo;
+                while (wlo > 0 && bz[wlo - 1] >= slab.own_lo - 1) --wlo;
+            }
+            pw_.out_lo = wlo;
+            pw_.out_hi = slab.zhi;
+            pw_.ws_lo = std::max(0, wlo - 1);
+            pw_.ws_hi = std::min(mz, slab.zhi + 1);
+            pw_.warp_lo = pw_.s_lo = std::max(0, wlo - 2);
+            pw_.warp_hi = pw_.s_hi = std::min(mz, slab.zhi + 2);
+            pw_.n_lo = slab.own_lo;
+            pw_.n_hi = slab.own_hi;
+            pw_.l_lo = std::max(0, slab.own_lo - 1);
+            pw_.l_hi = std::min(msz, slab.own_hi + 1);
+        }
     }
     if (mode != Mode::Parity) {
         fused_ = std::make_unique<FusedPlan>(plan_, ngf_.state_R(), ngf_.state_Tw(), ngf_.state_dT(), ngf_.state_frh(),
@@ -532,6 +562,7 @@ void DeviceObjective::eval_begin(const double* y, double* grad) {
         stale_ = lazy;
         return;  // the finalize wrote D and alpha S to the mapped host scalars
     }
+    if (sliced_) throw std::logic_error("parity z slab: eval through SlabProblem");
     ngf_.populate_warp(plan_.view(), y, T_);
     ngf_.value_async(sc_.dev(0));
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
@@ -545,6 +576,21 @@ void DeviceObjective::eval_begin(const double* y, double* grad) {
     }
     check_launch("Objective::eval");
     sc_.fetch_async(2, s_);
+}
+
+void DeviceObjective::parity_eval_local(const double* y, double* grad) {
+    if (fused_) throw std::logic_error("parity_eval_local: parity-mode objectives only");
+    const idx_t ny = dg_.count();
+    ngf_.populate_warp(plan_.view(), y, T_, pw_.warp_lo, pw_.warp_hi, pw_.ws_lo, pw_.ws_hi);
+    launch_sub(3 * ny, y, xid_.get(), u_.get(), s_);
+    launch_lap3(dg_, u_.get(), lapu_.get(), s_, pw_.l_lo, pw_.l_hi);
+    if (grad) {
+        ngf_.gradient(img3_.get(), pw_.out_lo, pw_.out_hi);
+        launch_transfer_T(plan_.view(), img3_.get(), grad, s_, pw_.n_lo, pw_.n_hi);
+        if (alpha_ != 0.0)
+            launch_bilap(dg_, lapu_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, grad, s_, pw_.n_lo, pw_.n_hi);
+    }
+    check_launch("Objective::eval (parity slab)");
 }
 
 double DeviceObjective::eval_end() {
@@ -562,20 +608,20 @@ void DeviceObjective::gn_hessian_vec(const double* p, double* q) {
                     [&](cudaStream_t cs) { enqueue_hv_fast(p, q, nullptr, nullptr, nullptr, cs); });
         return;
     }
-    launch_Pp_s(plan_.view(), p, ngf_.dT.get(), ngf_.sv.get(), s_);
-    ngf_.hessian_vec_image(ngf_.sv.get(), img3_.get());
-    launch_transfer_T(plan_.view(), img3_.get(), q, s_);
+    launch_Pp_s(plan_.view(), p, ngf_.dT.get(), ngf_.sv.get(), s_, pw_.s_lo, pw_.s_hi);
+    ngf_.hessian_vec_image(ngf_.sv.get(), img3_.get(), pw_.out_lo, pw_.out_hi);
+    launch_transfer_T(plan_.view(), img3_.get(), q, s_, pw_.n_lo, pw_.n_hi);
     if (alpha_ != 0.0) {
-        launch_lap3(dg_, p, lapp_.get(), s_);
-        launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, q, s_);
+        launch_lap3(dg_, p, lapp_.get(), s_, pw_.l_lo, pw_.l_hi);
+        launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 1, alpha_, 0.0, nullptr, q, s_, pw_.n_lo, pw_.n_hi);
     }
     check_launch("Objective::gn_hessian_vec");
 }
 
 // optimizer.cpp:106-111
 void DeviceObjective::seed_hessian_vec(const double* p, double gamma, double* q) {
-    launch_lap3(dg_, p, lapp_.get(), s_);
-    launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 2, 0.0, gamma, p, q, s_);
+    launch_lap3(dg_, p, lapp_.get(), s_, pw_.l_lo, pw_.l_hi);
+    launch_bilap(dg_, lapp_.get(), 2.0 * dg_.cell_volume(), 2, 0.0, gamma, p, q, s_, pw_.n_lo, pw_.n_hi);
     check_launch("Objective::seed_hessian_vec");
 }
 

@@ -128,7 +128,9 @@ struct SlabSpec {
 struct SlabInfo {
     int zlo, zhi, own_lo, own_hi, need_lo, need_hi, bnd;
 };
-std::vector<SlabInfo> slab_partition(const Grid& image, const Grid& deform, int nranks);
+// parity: the operand halo of the parity-mode slabs (their owned nodes' P^T reads the image
+// planes of the nodal slab below the first owned plane, recomputed from the operand)
+std::vector<SlabInfo> slab_partition(const Grid& image, const Grid& deform, int nranks, bool parity = false);
 
 // CUDA graphs for fixed launch sequences, keyed by the pointers they bake in
 // (replayed on the caller's stream; LRU-bounded). MFREG_NO_GRAPHS=1 disables.
@@ -282,10 +284,13 @@ public:
     void ensure_ws();
     void populate_points(const double* T_dev, const double* pts_dev);
     // populate from the nodal deformation (transfer_apply + populate fused)
-    void populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev);
+    // (windows: image planes [lo, hi) of the warp / workspace / outputs, default the whole grid;
+    // parity-mode z slabs compute only what their owned nodes read)
+    void populate_warp(const DevPlan& P, const double* y_dev, const double* T_dev, int wlo = 0, int whi = -1,
+                       int slo = 0, int shi = -1);
     void value_async(double* out_dev);                 // D (ngf.cpp:225-231)
-    void gradient(double* out3n);                      // dD/dP (ngf.cpp:66-103)
-    void hessian_vec_image(const double* sv, double* out3n);  // from s = dT.(P p)
+    void gradient(double* out3n, int zlo = 0, int zhi = -1);  // dD/dP (ngf.cpp:66-103)
+    void hessian_vec_image(const double* sv, double* out3n, int zlo = 0, int zhi = -1);  // from s = dT.(P p)
     void hessian_vec(const double* p3n, double* out3n);        // image-grid p (ngf.cpp:253-258)
     const Grid& grid() const { return g_; }
     Mode mode() const { return mode_; }
@@ -339,6 +344,11 @@ public:
     void prepare_operator() override { refresh_state(); }
     void apply_dot(int op, double gamma, const double* p, double* q, double* pq_dev, const int* skip) override;
     const double* identity_dev() const { return xid_.get(); }
+    // parity-mode z slabs (slab.cu): the windowed eval without its value reductions; the slab
+    // problem assembles D and S across ranks (DistSum) from r and Lap u
+    void parity_eval_local(const double* y, double* grad);
+    const double* parity_r() const { return ngf_.r.get(); }
+    const double* lap_u() const { return lapu_.get(); }
     const Grid& image_grid() const { return img_; }
     const Grid& deform_grid() const { return dg_; }
     DeviceNgf& ngf() { return ngf_; }
@@ -362,6 +372,12 @@ private:
     Grid img_, dg_;
     SlabSpec slab_;
     bool sliced_ = false;
+    // parity-mode slab windows: warp, workspace, image outputs, s (image planes); P^T / curvature
+    // outputs and Lap (nodal planes). Whole grid by default.
+    struct PWin {
+        int warp_lo = 0, warp_hi = -1, ws_lo = 0, ws_hi = -1, out_lo = 0, out_hi = -1, s_lo = 0, s_hi = -1;
+        int n_lo = 0, n_hi = -1, l_lo = 0, l_hi = -1;
+    } pw_;
     bool stale_ = false;  // Hv state belongs to ylazy_, not yet rebuilt (lazy value-only eval)
     DVec ylazy_;
     double alpha_;

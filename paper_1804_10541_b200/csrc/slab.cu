@@ -219,14 +219,130 @@ std::vector<std::unique_ptr<SlabComm>> make_local_comms(int nranks) {
     return out;
 }
 
+// ---------------------------------------------------------------- DistSum
+DistSum::DistSum(idx_t N, const std::vector<std::vector<Seg>>& segs, int rank) {
+    const idx_t C = kChunk;
+    nch_ = (N + C - 1) / C;
+    const int nr = static_cast<int>(segs.size());
+    // per rank: interior chunk partials first (in segment / chunk order), then one C-slot per piece
+    struct Piece {
+        int r;
+        idx_t lo, hi;
+        std::size_t slot;
+    };
+    std::vector<std::vector<std::pair<idx_t, std::size_t>>> interior(nr);  // (chunk, slot)
+    std::vector<std::vector<Piece>> pieces(nr);
+    std::size_t ni_max = 0, np_max = 0;
+    for (int r = 0; r < nr; ++r) {
+        for (const Seg& sg : segs[r]) {
+            if (sg.b <= sg.a) continue;
+            for (idx_t c = sg.a / C; c * C < sg.b; ++c) {
+                const idx_t c_lo = c * C, c_hi = std::min(N, c_lo + C);
+                const idx_t lo = std::max(sg.a, c_lo), hi = std::min(sg.b, c_hi);
+                if (lo == c_lo && hi == c_hi) interior[r].push_back({c, interior[r].size()});
+                else pieces[r].push_back({r, lo, hi, 0});
+            }
+        }
+        ni_max = std::max(ni_max, interior[r].size());
+        np_max = std::max(np_max, pieces[r].size());
+    }
+    B_ = std::max<std::size_t>(1, ni_max + np_max * C);
+    for (int r = 0; r < nr; ++r)
+        for (std::size_t k = 0; k < pieces[r].size(); ++k) pieces[r][k].slot = ni_max + k * C;
+    // assembly table: chunk -> interior block entry, or its pieces in index order
+    std::vector<long long> off(nch_, -1);
+    std::vector<int> cnt(nch_, 0);
+    std::vector<std::vector<Piece>> per_chunk(nch_);
+    for (int r = 0; r < nr; ++r) {
+        for (const auto& [c, slot] : interior[r]) {
+            if (off[c] >= 0 || !per_chunk[c].empty()) throw std::invalid_argument("DistSum: overlapping segments");
+            off[c] = static_cast<long long>(r) * B_ + slot;
+        }
+        for (const Piece& pc : pieces[r]) per_chunk[pc.lo / C].push_back(pc);
+    }
+    std::vector<ChunkPiece> plist;
+    for (idx_t c = 0; c < nch_; ++c) {
+        auto& v = per_chunk[c];
+        if (v.empty()) {
+            if (off[c] < 0) throw std::invalid_argument("DistSum: segments do not cover the index space");
+            continue;
+        }
+        if (off[c] >= 0) throw std::invalid_argument("DistSum: overlapping segments");
+        std::sort(v.begin(), v.end(), [](const Piece& x, const Piece& y) { return x.lo < y.lo; });
+        idx_t at = c * C;
+        for (const Piece& pc : v) {
+            if (pc.lo != at) throw std::invalid_argument("DistSum: segments do not cover the index space");
+            at = pc.hi;
+        }
+        if (at != std::min(N, (c + 1) * C)) throw std::invalid_argument("DistSum: segments do not cover the index space");
+        off[c] = static_cast<long long>(plist.size());
+        cnt[c] = static_cast<int>(v.size());
+        for (const Piece& pc : v)
+            plist.push_back({static_cast<long long>(pc.r) * static_cast<long long>(B_) + static_cast<long long>(pc.slot),
+                             static_cast<int>(pc.hi - pc.lo)});
+    }
+    // my local launches: one partials run per maximal stretch of consecutive interior chunks
+    const auto& mine = interior[rank];
+    for (std::size_t k = 0; k < mine.size();) {
+        std::size_t e = k + 1;
+        while (e < mine.size() && mine[e].first == mine[e - 1].first + 1) ++e;
+        const idx_t lo = mine[k].first * C, hi = std::min(N, (mine[e - 1].first + 1) * C);
+        runs_.push_back({false, lo, hi - lo, mine[k].second});
+        k = e;
+    }
+    for (const Piece& pc : pieces[rank]) runs_.push_back({true, pc.lo, pc.hi - pc.lo, pc.slot});
+    off_.resize(std::max<idx_t>(1, nch_));
+    cnt_.resize(std::max<idx_t>(1, nch_));
+    pieces_.resize(std::max<std::size_t>(1, plist.size()));
+    vals_.resize(std::max<idx_t>(1, nch_));
+    if (nch_) {
+        MFREG_CUDA(cudaMemcpy(off_.get(), off.data(), nch_ * sizeof(long long), cudaMemcpyHostToDevice));
+        MFREG_CUDA(cudaMemcpy(cnt_.get(), cnt.data(), nch_ * sizeof(int), cudaMemcpyHostToDevice));
+    }
+    if (!plist.empty())
+        MFREG_CUDA(cudaMemcpy(pieces_.get(), plist.data(), plist.size() * sizeof(ChunkPiece), cudaMemcpyHostToDevice));
+}
+
+void DistSum::local(int kind, const double* a, const double* b, double* blk, cudaStream_t s) const {
+    for (const Run& r : runs_) {
+        const double* ap = a + r.lo;
+        const double* bp = b ? b + r.lo : nullptr;
+        if (r.terms) launch_sum_terms(kind, r.n, ap, bp, blk + r.slot, s);
+        else launch_chunk_partials(kind, r.n, ap, bp, blk + r.slot, s);
+    }
+}
+
+void DistSum::assemble(const double* gathered, double scale, double* out, cudaStream_t s) {
+    launch_chunk_assemble(nch_, off_.get(), cnt_.get(), pieces_.get(), gathered, vals_.get(), scale, out, s);
+}
+
 // ---------------------------------------------------------------- SlabProblem
 SlabProblem::SlabProblem(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform, double tau,
-                         double rho, double alpha, SlabComm& comm, cudaStream_t s)
-    : img_(image), dg_(deform), comm_(comm), s_(s), parts_(slab_partition(image, deform, comm.size())),
-      red_(Mode::Fast, 3 * deform.count()), sc_(16) {
+                         double rho, double alpha, SlabComm& comm, cudaStream_t s, Mode mode)
+    : img_(image), dg_(deform), comm_(comm), s_(s),
+      parts_(slab_partition(image, deform, comm.size(), mode == Mode::Parity)), red_(Mode::Fast, 3 * deform.count()),
+      sc_(16) {
+    if (mode == Mode::Fast32) throw std::invalid_argument("z slabs run in fast or parity mode");
+    parity_ = mode == Mode::Parity;
     me_ = parts_[static_cast<std::size_t>(comm.rank())];
     const SlabSpec spec{me_.zlo, me_.zhi, me_.own_lo, me_.own_hi};
-    obj_ = std::make_unique<DeviceObjective>(R_dev, T_dev, image, deform, tau, rho, alpha, Mode::Fast, s, spec);
+    obj_ = std::make_unique<DeviceObjective>(R_dev, T_dev, image, deform, tau, rho, alpha, mode, s, spec);
+    if (parity_) {
+        const idx_t pl = image.m[0] * image.m[1], pn = deform.m[0] * deform.m[1], ny = deform.count();
+        std::vector<std::vector<DistSum::Seg>> sd, ss, sdot;
+        for (const SlabInfo& p : parts_) {
+            sd.push_back({{p.zlo * pl, p.zhi * pl}});
+            ss.push_back({{p.own_lo * pn, p.own_hi * pn}});
+            sdot.push_back({});
+            for (int d = 0; d < 3; ++d) sdot.back().push_back({d * ny + p.own_lo * pn, d * ny + p.own_hi * pn});
+        }
+        dsD_ = DistSum(image.count(), sd, comm.rank());
+        dsS_ = DistSum(ny, ss, comm.rank());
+        dsDot_ = DistSum(3 * ny, sdot, comm.rank());
+        const std::size_t B = std::max({dsD_.block(), dsS_.block(), dsDot_.block()});
+        blk_.resize(B);
+        gat_.resize(B * static_cast<std::size_t>(comm.size()));
+    }
     sc_dev_.resize(16);
     gath_.resize(static_cast<std::size_t>(4 * comm.size()));
     const int bnd_in = comm.rank() > 0 ? parts_[static_cast<std::size_t>(comm.rank() - 1)].bnd : 0;
@@ -283,10 +399,31 @@ void SlabProblem::rank_sum(const double* gathered, int count, double* out) {
     k_rank_sum<<<1, 32, 0, s_>>>(gathered, comm_.size(), count, out);
 }
 
+void SlabProblem::dist_sum(DistSum& ds, int kind, const double* a, const double* b, double scale, double* out_dev) {
+    ds.local(kind, a, b, blk_.get(), s_);
+    comm_.allgather(blk_.get(), gat_.get(), static_cast<int>(ds.block()), s_);
+    ds.assemble(gat_.get(), scale, out_dev, s_);
+    check_launch("slab chunked sum");
+}
+
 double SlabProblem::eval(const double* y, double* grad) {
+    if (parity_) {  // optimizer.cpp:64-92 with the reference's reductions across ranks
+        halo(y);
+        obj_->parity_eval_local(y, grad);
+        const idx_t ny = dg_.count();
+        dist_sum(dsD_, SUM_ONE_MINUS_SQ, obj_->parity_r(), nullptr, img_.cell_volume(), sc_.dev(0));  // ngf.cpp:225-231
+        for (int d = 0; d < 3; ++d)  // curvature.cpp:31-45, per component
+            dist_sum(dsS_, SUM_SQ, obj_->lap_u() + d * ny, nullptr, 1.0, sc_dev_.get() + 12 + d);
+        launch_curv_finalize(sc_dev_.get() + 12, dg_.cell_volume(), obj_->alpha(), sc_.dev(1), s_);
+        check_launch("slab eval (parity)");
+        const double* v = sc_.fetch(2, s_);
+        last_d_ = v[0];
+        last_s_ = v[1];
+        return last_d_ + last_s_;
+    }
     halo(y);
     obj_->eval(y, grad);
-    if (grad) boundary(grad);
+    if (grad) boundary(grad);  // (fast mode)
     const double loc[2] = {obj_->last_distance(), obj_->last_regularizer()};
     MFREG_CUDA(cudaMemcpyAsync(sc_dev_.get() + 8, loc, sizeof(loc), cudaMemcpyHostToDevice, s_));
     comm_.allgather(sc_dev_.get() + 8, gath_.get(), 2, s_);
@@ -300,7 +437,7 @@ double SlabProblem::eval(const double* y, double* grad) {
 void SlabProblem::gn_hessian_vec(const double* p, double* q) {
     halo(p);
     obj_->gn_hessian_vec(p, q);
-    boundary(q);
+    if (!parity_) boundary(q);  // (parity: each owned node's gather ran complete here)
 }
 
 void SlabProblem::seed_hessian_vec(const double* p, double gamma, double* q) {
@@ -317,6 +454,10 @@ void SlabProblem::local_dot(const double* a, const double* b, double* dev) {
 }
 
 void SlabProblem::dot_async(const double* a, const double* b, double* out_dev) {
+    if (parity_) {  // optimizer.cpp:12-19: one chunked sum over the 3 m^y elements
+        dist_sum(dsDot_, SUM_DOT, a, b, 1.0, out_dev);
+        return;
+    }
     local_dot(a, b, sc_dev_.get());
     comm_.allgather(sc_dev_.get() + 3, gath_.get(), 1, s_);
     rank_sum(gath_.get(), 1, out_dev);
@@ -358,7 +499,7 @@ void SlabProblem::gather_full(double* v) {
 // ---------------------------------------------------------------- sharded multilevel driver
 MultilevelResult register_multilevel_slabs(const double* R_dev, const double* T_dev, const Grid& image,
                                            const MultilevelConfig& cfg, SlabComm& comm, cudaStream_t s) {
-    if (cfg.mode != Mode::Fast) throw std::invalid_argument("z slabs run in fast mode");
+    if (cfg.mode == Mode::Fast32) throw std::invalid_argument("z slabs run in fast or parity mode");
     if (cfg.levels < 1) throw std::invalid_argument("build_pyramid: levels must be >= 1");
     validate_grid(image, false);
     for (int a = 0; a < 3; ++a) {  // multilevel.cpp:13-29
@@ -396,14 +537,14 @@ MultilevelResult register_multilevel_slabs(const double* R_dev, const double* T_
         bool sharded = comm.size() > 1;
         if (sharded) {
             try {
-                (void)slab_partition(G[l], dg, comm.size());
+                (void)slab_partition(G[l], dg, comm.size(), cfg.mode == Mode::Parity);
             } catch (const std::invalid_argument&) {
                 sharded = false;  // too thin for the slab halo: this level runs replicated
             }
         }
         MinimizeResult res;
         if (sharded) {
-            SlabProblem P(rp, tp, G[l], dg, cfg.tau, cfg.rho, cfg.alpha, comm, s);
+            SlabProblem P(rp, tp, G[l], dg, cfg.tau, cfg.rho, cfg.alpha, comm, s, cfg.mode);
             if (have_prev) launch_prolong(prev, dg, y.get(), y0.get(), s);
             else MFREG_CUDA(cudaMemcpyAsync(y0.get(), P.identity_dev(), n * sizeof(double), cudaMemcpyDeviceToDevice, s));
             res = cfg.method == Method::Lbfgs ? lbfgs_minimize(P, y0.get(), yl.get(), cfg.opt)
@@ -482,7 +623,7 @@ int mfreg_cu_comm_rank(mfreg_cu_comm* c, int* rank, int* size) {
 }
 
 int mfreg_cu_slab_create(mfreg_cu_comm* comm, const double* ref, const double* tpl, const mfreg_cu_grid* image,
-                         const mfreg_cu_grid* deform, double tau, double rho, double alpha, int where,
+                         const mfreg_cu_grid* deform, double tau, double rho, double alpha, int mode, int where,
                          mfreg_cu_slab** out) {
     return guard([&] {
         if (!comm) throw std::invalid_argument("null communicator");
@@ -497,7 +638,8 @@ int mfreg_cu_slab_create(mfreg_cu_comm* comm, const double* ref, const double* t
         const auto kind = where == MFREG_CU_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
         MFREG_CUDA(cudaMemcpyAsync(h->R.get(), ref, n * sizeof(double), kind, kStream));
         MFREG_CUDA(cudaMemcpyAsync(h->T.get(), tpl, n * sizeof(double), kind, kStream));
-        h->p = std::make_unique<SlabProblem>(h->R.get(), h->T.get(), h->img, h->dg, tau, rho, alpha, *comm->c, kStream);
+        h->p = std::make_unique<SlabProblem>(h->R.get(), h->T.get(), h->img, h->dg, tau, rho, alpha, *comm->c, kStream,
+                                             to_mode(mode));
         MFREG_CUDA(cudaStreamSynchronize(kStream));
         *out = h.release();
     });

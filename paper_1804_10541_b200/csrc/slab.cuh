@@ -17,6 +17,7 @@
 #include <mutex>
 #include <vector>
 
+#include "kernels.cuh"
 #include "objective.cuh"
 
 namespace mfreg_b200 {
@@ -50,12 +51,55 @@ void nccl_unique_id(void* out128);
 class LocalHub;
 std::vector<std::unique_ptr<SlabComm>> make_local_comms(int nranks);
 
-// One rank's share of the objective (fast mode) as a DeviceProblem: the device-resident
+// chunked_sum (parallel.cpp:51-73) over a global index space [0, N) whose indices are split
+// between ranks (each rank: ascending disjoint segments; together they cover [0, N) once), with
+// the reference's exact result: every chunk is the sequential sum of its 4096 terms from 0.0 and
+// the chunks are added in order. A rank contributes the partials of the chunks inside one of its
+// segments and the raw terms of the chunks it owns only part of; after an all-gather of the
+// fixed-size blocks every rank assembles the same bits.
+class DistSum {
+public:
+    struct Seg {
+        idx_t a, b;
+    };
+    DistSum() = default;
+    DistSum(idx_t N, const std::vector<std::vector<Seg>>& segs, int rank);
+    std::size_t block() const { return B_; }  // doubles per rank block
+    // my block: interior chunk partials and piece terms of sum_term(kind, a, b, i), a / b
+    // indexed globally
+    void local(int kind, const double* a, const double* b, double* blk, cudaStream_t s) const;
+    // out = scale * sum over chunks in order, from the rank-major gathered blocks
+    void assemble(const double* gathered, double scale, double* out, cudaStream_t s);
+
+private:
+    struct Run {  // a launch of my local part
+        bool terms;
+        idx_t lo, n;       // global index range
+        std::size_t slot;  // offset in my block
+    };
+    idx_t nch_ = 0;
+    std::size_t B_ = 0;
+    std::vector<Run> runs_;
+    DevArray<long long> off_;
+    DevArray<int> cnt_;
+    DevArray<ChunkPiece> pieces_;
+    DVec vals_;
+};
+
+// One rank's share of the objective as a DeviceProblem: the device-resident
 // gauss_newton_minimize / lbfgs_minimize / cg_solve run sharded on it unchanged.
+//   fast mode: the fused kernels on the rank's window; shared P^T planes summed on the owner;
+//     scalars (D, alpha S, dots) summed in rank order (bit-identical on every rank, within the
+//     fast-mode tolerance of the single-GPU objective);
+//   parity mode: every quantity bitwise the single-GPU parity objective's (= the reference's):
+//     the rank recomputes the per-voxel terms of the nodal slab below its first owned plane
+//     from the operand halo, so each owned node's P^T gather runs complete in the reference's
+//     red-black order on one rank, and D, S and every vec_dot are the reference's 4096-chunk
+//     sums across ranks (DistSum).
 class SlabProblem : public DeviceProblem {
 public:
     SlabProblem(const double* R_dev, const double* T_dev, const Grid& image, const Grid& deform, double tau,
-                double rho, double alpha, SlabComm& comm, cudaStream_t s);
+                double rho, double alpha, SlabComm& comm, cudaStream_t s, Mode mode = Mode::Fast);
     ~SlabProblem() override;
     idx_t dof() const override { return 3 * dg_.count(); }
     // y / p are full-length nodal vectors valid on the owned planes; their halo planes are
@@ -94,6 +138,11 @@ private:
     std::vector<SlabInfo> parts_;
     SlabInfo me_{};
     std::unique_ptr<DeviceObjective> obj_;
+    bool parity_ = false;
+    DistSum dsD_, dsS_, dsDot_;  // parity: D over the image, S per component, vec_dot over 3 m^y
+    DVec blk_, gat_;
+    // parity: my block of ds, all-gathered, assembled into out_dev (scale * chunked_sum)
+    void dist_sum(DistSum& ds, int kind, const double* a, const double* b, double scale, double* out_dev);
     Reducer red_;
     DVec stage_, sc_dev_, gath_;
     Scalars sc_;

@@ -42,11 +42,13 @@ class SlabInfo:
     bnd: int       # P^T planes [own_hi, own_hi + bnd) shared with rank r+1
 
 
-def slab_partition(image: GridDesc, deform: GridDesc, nranks: int) -> list[SlabInfo]:
+def slab_partition(image: GridDesc, deform: GridDesc, nranks: int, mode: int = 1) -> list[SlabInfo]:
     """Split the image z axis over `nranks` ranks (ValueError when the slabs would be
-    thinner than the operator halo)."""
+    thinner than the operator halo); `mode` Mode.PARITY widens the operand halo to what the
+    parity-mode slabs recompute."""
     tab = (C.c_int32 * (7 * nranks))()
-    _check(lib().mfreg_cu_slab_partition(C.byref(image.c()), C.byref(_nodal(deform).c()), int(nranks), tab))
+    _check(lib().mfreg_cu_slab_partition_mode(C.byref(image.c()), C.byref(_nodal(deform).c()), int(nranks), int(mode),
+                                              tab))
     return [SlabInfo(*tab[7 * r:7 * r + 7]) for r in range(nranks)]
 
 
@@ -448,14 +450,15 @@ class NativeSlab:
     length 3 m^y; eval / gn_hessian_vec / dot return global values identical on every rank."""
 
     def __init__(self, comm: NativeComm, reference, tpl, image: GridDesc, deform: GridDesc,
-                 params: NgfParams = NgfParams(), alpha: float = 1.0):
+                 params: NgfParams = NgfParams(), alpha: float = 1.0, mode: int = 1):
+        """mode: Mode.FAST (default) or Mode.PARITY (bitwise the one-GPU parity objective)."""
         self.comm, self.image, self.deform = comm, image, _nodal(deform)
         w = _where_of(reference, tpl)
         reference, tpl = _as_input(reference, w), _as_input(tpl, w)
         h = _vp()
         _check(lib().mfreg_cu_slab_create(comm._h, _ptr(reference)[0], _ptr(tpl)[0], C.byref(image.c()),
                                           C.byref(self.deform.c()), float(params.tau), float(params.rho), float(alpha),
-                                          w, C.byref(h)))
+                                          int(mode), w, C.byref(h)))
         self._h = h
         tab = (C.c_int32 * 7)()
         _check(lib().mfreg_cu_slab_info(self._h, tab))
@@ -520,7 +523,8 @@ class NativeSlab:
 
 
 def register_multilevel_native(comm: NativeComm, reference, tpl, image: GridDesc, cfg=None):
-    """register_multilevel (multilevel.cpp:117-145) over the communicator's z slabs, fast mode.
+    """register_multilevel (multilevel.cpp:117-145) over the communicator's z slabs (cfg.mode FAST
+    or PARITY).
     Returns (y, deform_grid, per-level (trace, line_search_failed)), identical on every rank."""
     from . import FAST, MultilevelConfig, _empty_like_kind, _Grid, _IterRecord, _MlConfig, _records, deformation_grid_for
     cfg = cfg or MultilevelConfig(mode=FAST)

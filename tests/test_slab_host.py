@@ -71,6 +71,36 @@ def test_partition_invariants(pkg, m, h, ratio, n):
     assert max(sizes) - min(sizes) <= 2 * (mz / (ms - 1)) + 1
 
 
+@pytest.mark.parametrize("m,h,ratio,n", [
+    ((20, 18, 40), (1.0, 1.0, 1.5), 4, 2), ((16, 16, 128), (1.0, 1.0, 1.0), 4, 4),
+    ((16, 16, 1024), (1.0, 1.0, 1.0), 4, 8), ((12, 12, 97), (0.97, 0.97, 2.5), 3, 5),
+])
+def test_partition_parity_halo(pkg, m, h, ratio, n):
+    """Parity-mode slabs recompute the per-voxel terms of the nodal slab below own_lo so each
+    owned node's P^T gather runs complete on its rank: the operand halo covers the warp of
+    [first plane of nodal slab own_lo - 1, zhi) +- 2 image planes, and still comes from the
+    neighbours' owned planes only."""
+    img = pkg.make_image_grid(m, h)
+    dg = pkg.deformation_grid_for(img, ratio)
+    fast = pkg.slab.slab_partition(img, dg, n)
+    parts = pkg.slab.slab_partition(img, dg, n, pkg.Mode.PARITY)
+    mz, ms = m[2], dg.m[2]
+    b = _base(mz, ms)
+    for r, (s, f) in enumerate(zip(parts, fast)):
+        assert (s.zlo, s.zhi, s.own_lo, s.own_hi) == (f.zlo, f.zhi, f.own_lo, f.own_hi)  # same split
+        z = s.zlo
+        while s.own_lo > 0 and z > 0 and b[z - 1] >= s.own_lo - 1:
+            z -= 1
+        if s.own_lo > 0:
+            assert b[z] == s.own_lo - 1  # first image plane of the nodal slab below own_lo
+        wlo, whi = max(0, z - 2), min(mz, s.zhi + 2)
+        assert s.need_lo <= b[wlo] and s.need_hi >= b[whi - 1] + 2
+        if r:
+            assert s.need_lo >= parts[r - 1].own_lo
+        if r + 1 < n:
+            assert s.need_hi <= parts[r + 1].own_hi
+
+
 def test_partition_rejects_thin_slabs(pkg):
     img = pkg.make_image_grid((16, 16, 16))
     dg = pkg.deformation_grid_for(img, 4)
