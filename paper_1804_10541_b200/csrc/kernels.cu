@@ -166,7 +166,9 @@ __global__ void k_warp(DevPlan P, const double* __restrict__ y, const double* __
 #endif
 // trilinear T at the sample point pt (the reference's cell choice) and its analytic
 // gradient, stored at image index (x, yy, z); shared by the two fast warp kernels
-template <typename OutT>
+// EXACT_S = false: the sample coordinate p/h - 0.5 as one FMA with the reciprocal (callers
+// guarantee the point is not within 1e-9 of a cell face, so the cell is the reference's)
+template <typename OutT, bool EXACT_S = true>
 __device__ __forceinline__ void warp_sample_store(const DevPlan& P, const double* __restrict__ T, const double pt[3],
                                                   int x, int yy, int z, int mx, int my, int mz,
                                                   OutT* __restrict__ Tw, OutT* __restrict__ dT) {
@@ -176,7 +178,7 @@ __device__ __forceinline__ void warp_sample_store(const DevPlan& P, const double
     bool ok0[3], ok1[3];
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        const double sa = div_rn(pt[a], P.tgt.h[a], P.tgt.ih[a]) - 0.5;
+        const double sa = EXACT_S ? div_rn(pt[a], P.tgt.h[a], P.tgt.ih[a]) - 0.5 : fma(pt[a], P.tgt.ih[a], -0.5);
         const double c = fmin(fmax(ceil(sa), -4.0), static_cast<double>(m3[a]) + 4.0);  // far outside: all zero
         const int b0 = static_cast<int>(c) - 1;
         f[a] = sa - static_cast<double>(static_cast<long long>(ceil(sa)) - 1);
@@ -1062,10 +1064,15 @@ constexpr int WZ_NXF = 34, WZ_NYF = 10;
 #ifndef MFREG_WARPZ_MINB
 #define MFREG_WARPZ_MINB 5  // measured at C4: 5 blocks (48 regs) 3.01 ms, 6 (40, spills) 2.96, 4 (64) 3.16; nodal values in registers, 2 blocks: 3.90; per-voxel kernel 3.52
 #endif  // nodal footprint bound of a 32x8 column block (ratio >= 1)
+// fastpy: P y from the column's x-y bilinear interpolants of the cell's two nodal planes and a
+// z lerp (FMA; a few ulp from the reference's exact sum, i.e. the sample moves by < 1e-12 voxel),
+// and the reference's exact P y and IEEE p/h only for points within 1e-9 of a cell face, where
+// that difference could change the cell (and dT by O(1)): cell choice bitwise the reference's,
+// T_w / dT within ~1e-15 relative (fast-mode tolerance 1e-9). MFREG_EXACT_PY=1: exact for all.
 template <typename OutT>
 __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, const double* __restrict__ y,
                                                    const double* __restrict__ T, OutT* __restrict__ Tw,
-                                                   OutT* __restrict__ dT, int zlo, int zhi, int zc) {
+                                                   OutT* __restrict__ dT, int zlo, int zhi, int zc, int fastpy) {
     __shared__ double sy[3][2][WZ_NYF][WZ_NXF];
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // the eval pass (PDL) may queue behind
     const int mx = static_cast<int>(P.tgt.m[0]), my = static_cast<int>(P.tgt.m[1]), mz = static_cast<int>(P.tgt.m[2]);
@@ -1110,6 +1117,7 @@ __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, con
         }
     };
     int cur = -1;
+    double Pa[3] = {0.0, 0.0, 0.0}, Pd[3] = {0.0, 0.0, 0.0};  // fastpy: bilinear at plane bz, (bz+1) - bz
 #pragma unroll 1
     for (int z = zb; z < ze;) {
         const int bz = __ldg(&P.base[2][z]);
@@ -1122,11 +1130,40 @@ __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, con
                     __ldg(y + (gd >> 1) * ns + (bz + (gd & 1)) * sm01 + (fy0 + iy) * sm0 + fx0 + ix);
             }
             __syncthreads();
+            if (fastpy) {
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    double pg[2];
+#pragma unroll
+                    for (int g = 0; g < 2; ++g) {
+                        const double c0 = fma(rx, sy[d][g][ly][lx + 1] - sy[d][g][ly][lx], sy[d][g][ly][lx]);
+                        const double c1 = fma(rx, sy[d][g][ly + 1][lx + 1] - sy[d][g][ly + 1][lx], sy[d][g][ly + 1][lx]);
+                        pg[g] = fma(ry, c1 - c0, c0);
+                    }
+                    Pa[d] = pg[0];
+                    Pd[d] = pg[1] - pg[0];
+                }
+            }
         }
         if (in) {
+            const double rz = __ldg(&P.rem[2][z]);
             double pt[3];
-            ptof(__ldg(&P.rem[2][z]), pt);
-            warp_sample_store(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+            bool near = true;
+            if (fastpy) {
+                near = false;
+#pragma unroll
+                for (int d = 0; d < 3; ++d) {
+                    pt[d] = fma(rz, Pd[d], Pa[d]);
+                    const double sa = fma(pt[d], P.tgt.ih[d], -0.5);
+                    near = near || fabs(sa - rint(sa)) < 1e-9;
+                }
+            }
+            if (near) {
+                ptof(rz, pt);
+                warp_sample_store(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+            } else {
+                warp_sample_store<OutT, false>(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+            }
         }
         ++z;
     }
@@ -1182,7 +1219,11 @@ void warp_fast_impl(const DevPlan& P0, const double* y, const double* T, OutT* T
         const int nch = std::max<int>((nz + 63) / 64, static_cast<int>(std::min<long long>(nz, (148LL * 8 + cols - 1) / cols)));
         const int zc = (nz + nch - 1) / nch;
         const dim3 gr(gx, gy, static_cast<unsigned>((nz + zc - 1) / zc));
-        note_launch(), k_warp_z<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo, zhi, zc);
+        static const int fastpy = [] {
+            const char* e = std::getenv("MFREG_EXACT_PY");
+            return (e && e[0] == '1') ? 0 : 1;
+        }();
+        note_launch(), k_warp_z<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo, zhi, zc, fastpy);
         return;
     }
     const dim3 gr(gx, gy, static_cast<unsigned>(zhi - zlo));

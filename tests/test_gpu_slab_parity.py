@@ -35,6 +35,14 @@ g_full = torch.empty_like(y); q_full = torch.empty_like(y)
 J = full.eval(y, g_full); D, Sreg = full.last_distance(), full.last_regularizer()
 full.gn_hessian_vec(p, q_full)
 pq_full = full.dot(p, q_full)
+# the single-GPU parity objective is the reference library's objective bit for bit
+sys.path.insert(0, {root!r} + "/oracle/..")
+from oracle.oracle import Oracle, available
+if available("ref"):
+    o = Oracle("ref").objective(R.cpu().numpy(), T.cpu().numpy(), {m}, {h}, tuple(dg.m), 10.0, 10.0, 1.0)
+    Jr, Dr, Sr, gr = o.eval(y.cpu().numpy())
+    assert (J, D, Sreg) == (Jr, Dr, Sr) and np.array_equal(g_full.cpu().numpy(), gr)
+    assert np.array_equal(q_full.cpu().numpy(), o.gn_hessian_vec(p.cpu().numpy()))
 cfg = P.OptimizerConfig(max_iters=3, cg_max_iters=60)
 yg_full, tr_full, _ = P.gauss_newton_minimize(full, y.clone(), cfg)
 yl_full, trl_full, _ = P.lbfgs_minimize(full, y.clone(), P.OptimizerConfig(max_iters=4))
