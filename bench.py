@@ -485,13 +485,12 @@ def run_slabs(args, rank, world, local):
     import paper_1804_10541_b200 as P
     from paper_1804_10541_b200 import slab as S
     torch.cuda.set_device(local)
-    if args.mode != "fast":
-        raise SystemExit("z slabs run in fast mode")
+    md = P.PARITY if args.mode == "parity" else P.FAST  # parity: bitwise the one-GPU parity objective
     wl = WORKLOADS[args.workload]
     img, dg, R, T, y, p = make_inputs_gpu(P, torch, args.workload)
     nd = 3 * dg.count()
     comm = S.NativeComm.nccl()
-    sl = S.NativeSlab(comm, R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0)
+    sl = S.NativeSlab(comm, R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, md)
     s = sl.info
     n_loc = (s.zhi - s.zlo) * wl["m"][0] * wl["m"][1]
     n_glob = img.count()
@@ -553,7 +552,7 @@ def run_slabs(args, rank, world, local):
                 "algorithmic_bytes_per_voxel": B_CANON_HV, "units_per_launch": n_loc, "peak_source": peak_kind}
     gn = None
     if not args.no_gn:
-        cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=P.FAST)
+        cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
         walls = []
         for _ in range(2):  # cold, then warm
             barrier(world)
