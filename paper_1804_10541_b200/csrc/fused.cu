@@ -22,7 +22,7 @@ int hv2_threads();
 void hv2_set_smem_cap(int bytes);
 void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
 // hv3.cu
-std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32);
+std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32, bool stored);
 int hv3_tile_x();
 int hv3_tile_y();
 int hv3_threads();
@@ -31,7 +31,8 @@ int hv3_box_rows();
 int hv3_box_origin(bool fp32);
 void hv3_set_smem_cap(int bytes);
 bool hv3_fp32_ok();
-void hv3_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
+void hv3_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32,
+                bool stored);
 // ev_fast.cu
 std::size_t ev2_smem_bytes(int nlx, bool fp32);
 void ev2_set_smem_cap(int bytes);
@@ -1081,7 +1082,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     const char* noe = std::getenv("MFREG_NO_EV2");
     ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
     if (ev2_) ev2_set_smem_cap(kSmem2Cta);
-    setup_hv3(plan, R, Tw, dT, zok, max_optin);
+    setup_hv3(plan, R, Tw, dT, frh, zok, max_optin);
     // FAST32 runs only on the two-CTA kernels (the legacy fused kernels are fp64)
     if (fp32_ && !(hv2_ && ev2_))
         throw std::invalid_argument(
@@ -1095,11 +1096,13 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
 // -- the recomputation adds ~90 fp64 operations per voxel on B200's 60-per-clock fp64 pipe, and the
 // one-CTA-per-SM uniform-warp schedule issues at ~50%. Off when TMA cannot address the grid, nodal z
 // cells span < 2 image planes or a tile's nodal footprint exceeds one node per thread.
-void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, bool zok,
-                          int max_optin) {
-    const char* on = std::getenv("MFREG_HV3");
+void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
+                          bool zok, int max_optin) {
+    const char* on = std::getenv("MFREG_HV3");   // recompute variant
+    const char* on4 = std::getenv("MFREG_HV4");  // stored-coefficient variant
     const char* off = std::getenv("MFREG_NO_HV3");
-    if (!(on && on[0] == '1') || (off && off[0] == '1') || !tma_ || !zok || (fp32_ && !hv3_fp32_ok())) return;
+    const bool recompute = on && on[0] == '1', stored = !recompute && on4 && on4[0] == '1';
+    if (!(recompute || stored) || (off && off[0] == '1') || !tma_ || !zok || (fp32_ && !hv3_fp32_ok())) return;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -1178,7 +1181,7 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
         }
         fp[a2] = mxf;
     }
-    const std::size_t smem = hv3_smem_bytes(t.nlx, fp[0] * fp[1] * 3, t.zc, fp32_);
+    const std::size_t smem = hv3_smem_bytes(t.nlx, fp[0] * fp[1] * 3, t.zc, fp32_, stored);
     if (fp[0] * fp[1] * 3 > hv3_threads() || 3 * t.nlx * t.nly > hv3_threads() ||
         smem > static_cast<std::size_t>(max_optin))
         return;
@@ -1186,11 +1189,12 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
     const int es = fp32_ ? 4 : 8;
     if ((g.m[0] * es) % 16 != 0) return;
     const cuuint64_t mx = g.m[0], my = g.m[1], mzz = g.m[2], n = g.count();
-    auto enc = [&](CUtensorMap* m, const void* base, int rank, cuuint64_t comps, cuuint32_t bc) {
+    auto enc = [&](CUtensorMap* m, const void* base, int rank, cuuint64_t comps, cuuint32_t bc, int rows_less = 0) {
         const cuuint64_t e = static_cast<cuuint64_t>(es);
         const cuuint64_t dims[4] = {mx, my, mzz, comps};
         const cuuint64_t strides[3] = {mx * e, mx * my * e, n * e};
-        const cuuint32_t box[4] = {static_cast<cuuint32_t>(hv3_box_width(fp32_)), static_cast<cuuint32_t>(hv3_box_rows()), 1, bc};
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(hv3_box_width(fp32_)),
+                                   static_cast<cuuint32_t>(hv3_box_rows() - rows_less), 1, bc};
         const cuuint32_t est[4] = {1, 1, 1, 1};
         return encode(m, fp32_ ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
                       const_cast<void*>(base), dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1198,7 +1202,9 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
     TmaMaps maps{};
-    if (!(enc(&maps.a, R, 3, 1, 1) && enc(&maps.b, Tw, 3, 1, 1) && enc(&maps.c, dT, 4, 3, 3))) return;
+    const bool ok = stored ? (enc(&maps.b, frh, 4, 6, 6, 2) && enc(&maps.c, dT, 4, 3, 3))
+                           : (enc(&maps.a, R, 3, 1, 1) && enc(&maps.b, Tw, 3, 1, 1) && enc(&maps.c, dT, 4, 3, 3));
+    if (!ok) return;
     std::memcpy(maps_hv3_, &maps, sizeof(TmaMaps));
     for (int a = 0; a < 3; ++a) {
         goff3_[a].resize(off3[a].size());
@@ -1218,6 +1224,7 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
     hv3_smem_ = smem;
     hv3_set_smem_cap(max_optin);
     hv3_ = true;
+    hv3_stored_ = stored;
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh) {
@@ -1292,7 +1299,7 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
         note_launch();
         const TileMeta& t3 = fp.meta3();
         hv3_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv3()), dim3(t3.ntx, t3.nty, t3.ntz), fp.hv3_smem(), s,
-                   fp.fp32());
+                   fp.fp32(), fp.hv3_stored());
         return;
     }
     const TileMeta& t = fp.meta();

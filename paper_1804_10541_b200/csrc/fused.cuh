@@ -66,9 +66,12 @@ public:
     const void* maps_hv2() const { return maps_hv2_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
-    // Hv pass with recomputed coefficients (hv3.cu): own tiling (28 x 12 output tiles), own
-    // partials; when on, the Hv state is R, T_w, dT and the eval pass stores no rho-hat
+    // uniform-warp Hv pass (hv3.cu): own tiling (28 x 12 output tiles), own partials; it streams
+    // the stored rho-hat (hv3_stored) or recomputes it from R and T_w (then the Hv state is R,
+    // T_w, dT and the eval pass stores no rho-hat)
     bool hv3() const { return hv3_; }
+    bool hv3_stored() const { return hv3_stored_; }
+    bool hv3_recompute() const { return hv3_ && !hv3_stored_; }
     const TileMeta& meta3() const { return meta3_; }
     double* partials3() { return part3_.get(); }
     int ntiles3() const { return meta3_.ntx * meta3_.nty * meta3_.ntz; }
@@ -113,6 +116,7 @@ private:
     alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
     alignas(64) unsigned char maps_ev_[3 * 128];
     bool hv3_ = false;
+    bool hv3_stored_ = false;
     TileMeta meta3_{};
     DevArray<int> goff3_[3];
     DevArray<int2> gent3_[3];
@@ -121,7 +125,8 @@ private:
     int gmax3_ = 0;
     std::size_t hv3_smem_ = 0;
     alignas(64) unsigned char maps_hv3_[3 * 128];
-    void setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, bool zok, int max_optin);
+    void setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh, bool zok,
+                   int max_optin);
     bool fp32_ = false;
     const void* state_R_ = nullptr;
     const void* state_Tw_ = nullptr;

@@ -38,19 +38,28 @@ constexpr int OX = LX - 4;     // output columns per tile (lanes 2..29)
 constexpr int OY = MFREG_HV3_OY;  // output rows per tile
 constexpr int NR = OY + 4;     // warps = staged rows
 constexpr int NT = LX * NR;    // 512 threads
-constexpr int RING = 5;        // staging slots
-constexpr int AHEAD = RING - 1;  // planes in flight after a step
 constexpr int NSL = 4;         // nodal plane ring (power of 2)
 
-template <typename Real>
+// STORED = false (recompute): slot of plane m = R, T_w, dT of plane m; the coefficients of
+//   plane j read R / T_w of planes j-1 .. j+1 -> ring of 5, 4 planes in flight.
+// STORED = true: slot of plane m = dT of plane m and the stored rho-hat of plane m-1 (rows
+//   1..14 only), i.e. exactly what step m reads -> ring of 3, each slot refilled as soon as its
+//   step ends (hv2's staging rule).
+template <typename Real, bool STORED>
 struct Geo3 {
     static constexpr int XO = sizeof(Real) == 8 ? 0 : 2;  // lane l <-> box column l + XO
     static constexpr int BX = LX + 2 * XO;                // box width (fp32 boxes start x0 - 4: 16-B aligned)
-    static constexpr int BOX = static_cast<int>((BX * NR * sizeof(Real) + 127) / 128 * 128 / sizeof(Real));  // padded
-    static constexpr int SR = 0, ST = BOX, SD = 2 * BOX;  // R, T_w, dT[3] (components BOX apart: one 4-D box
-    static constexpr int SLOT = 5 * BOX;                  //  lands them BX * NR apart, so BOX must equal that)
+    static constexpr int BOX = BX * NR;                   // one field, one plane (the 4-D dT box lands its
+                                                          // components BOX apart)
+    static constexpr int BOXR = BX * (NR - 2);            // one rho-hat component (rows 1..NR-2)
+    static constexpr int SR = 0, ST = BOX;                // recompute: R, T_w
+    static constexpr int SD = STORED ? 0 : 2 * BOX;       // dT[3]
+    static constexpr int SRH = 3 * BOX;                   // stored: rho-hat[6]
+    static constexpr int TX_ELEMS = STORED ? 3 * BOX + 6 * BOXR : 5 * BOX;  // bytes / sizeof(Real) per plane
+    static constexpr int SLOT = static_cast<int>((TX_ELEMS * sizeof(Real) + 127) / 128 * 128 / sizeof(Real));
+    static constexpr int RING = STORED ? 3 : 5;
+    static constexpr int LAG = STORED ? 0 : 1;            // the slot freed after step k holds plane k - LAG
     static_assert((BOX * sizeof(Real)) % 128 == 0, "TMA destinations 128-byte aligned");
-    static_assert(BOX == BX * NR, "the dT box's component planes are BX * NR apart");
 };
 
 template <int P_>
@@ -61,10 +70,11 @@ struct Par {
 __device__ __forceinline__ double rsq3(double v) { return rsqrt(v); }
 __device__ __forceinline__ float rsq3(float v) { return rsqrtf(v); }
 
-template <typename Real>
+template <typename Real, bool STORED>
 __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
-    using G = Geo3<Real>;
+    using G = Geo3<Real, STORED>;
     constexpr int XO = G::XO, BX = G::BX, SR = G::SR, ST = G::ST, SD = G::SD, SLOT = G::SLOT, BOX = G::BOX;
+    constexpr int SRH = G::SRH, BOXR = G::BOXR, RING = G::RING, LAG = G::LAG;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     if (a.skip && *a.skip) return;  // uniform
     const TileMeta& tm = a.tm;
@@ -175,9 +185,13 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
             const int rr_ = ((m_) - kfirst) % RING;                                        \
             Real* st_ = stg + rr_ * SLOT;                                                  \
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                  \
-            mbar_expect_tx(&bars[rr_], SLOT * sizeof(Real));                               \
-            tma_load_3d(st_ + SR, &maps.a, xb - 2 - XO, yb - 2, (m_), &bars[rr_]);          \
-            tma_load_3d(st_ + ST, &maps.b, xb - 2 - XO, yb - 2, (m_), &bars[rr_]);          \
+            mbar_expect_tx(&bars[rr_], G::TX_ELEMS * sizeof(Real));                        \
+            if constexpr (STORED) {                                                        \
+                tma_load_4d(st_ + SRH, &maps.b, xb - 2 - XO, yb - 1, (m_) - 1, 0, &bars[rr_]); \
+            } else {                                                                       \
+                tma_load_3d(st_ + SR, &maps.a, xb - 2 - XO, yb - 2, (m_), &bars[rr_]);      \
+                tma_load_3d(st_ + ST, &maps.b, xb - 2 - XO, yb - 2, (m_), &bars[rr_]);      \
+            }                                                                              \
             tma_load_4d(st_ + SD, &maps.c, xb - 2 - XO, yb - 2, (m_), 0, &bars[rr_]);       \
         }                                                                                  \
     } while (0)
@@ -244,7 +258,7 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
             slab_store(nz);
         }
     }
-    for (int m = 0; m < AHEAD; ++m)
+    for (int m = 0; m < RING - LAG; ++m)
         if (kfirst + m <= klast) HV3_ISSUE(kfirst + m);
     int slot = 0;        // ring slot of plane k
     unsigned phase = 0;  // its mbarrier parity
@@ -298,11 +312,36 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
         const Real D0 = st[SD + cb], D1 = st[SD + BOX + cb], D2 = st[SD + 2 * BOX + cb];
         const Real s_k = fma(D0, lerp(rzk, Pa0, Pb0), fma(D1, lerp(rzk, Pa1, Pb1), D2 * lerp(rzk, Pa2, Pb2)));
         sS[P * NR * LX + tid] = s_k;
-        const Real R_k = st[SR + cb], T_k = st[ST + cb];
+        Real R_k = Real(0), T_k = Real(0);
+        if constexpr (!STORED) {
+            R_k = st[SR + cb];
+            T_k = st[ST + cb];
+        }
         // ---- coefficients and w at plane j = k-1 (rows 1..14)
         const int j = k - 1;
         Real fzm = 0, fzp_new = 0, sw_new = 0, gx_new = 0;
-        if (cw && k >= kfirst + 2) {  // uniform
+        if (STORED && cw && k >= kfirst + 2) {  // uniform; the coefficients as the eval pass stored them
+            const Real* rh = st + SRH + (row - 1) * BX + lane + XO;  // (zero across the boundary / outside)
+            const Real c0 = rh[0], c1 = rh[BOXR], c2 = rh[2 * BOXR], c3 = rh[3 * BOXR], c4 = rh[4 * BOXR],
+                       c5 = rh[5 * BOXR];
+            const Real sj = sh[1 - P];
+            const Real* sn = sS + (1 - P) * NR * LX + tid;  // plane j (written last step)
+            const Real sxm = __shfl_up_sync(0xffffffffu, sj, 1), sxp = __shfl_down_sync(0xffffffffu, sj, 1);
+            const Real wa = fma(c1, sxp - sj, c0 * (sxm - sj));
+            const Real wb = fma(c3, sn[LX] - sj, c2 * (sn[-LX] - sj));
+            const Real wc = fma(c5, s_k - sj, c4 * (sh[P] - sj));
+            const Real w = (wa + wb) + wc;
+            const Real fpx = __shfl_up_sync(0xffffffffu, c1 * w, 1);    // from lane - 1 (its +x)
+            const Real fmx = __shfl_down_sync(0xffffffffu, c0 * w, 1);  // from lane + 1 (its -x)
+            gx_new = fpx + fmx;
+            Real* const Fj = sF + P * 2 * NR * LX + tid;
+            Fj[0] = c3 * w;        // +y flux (row + 1 reads it)
+            Fj[NR * LX] = c2 * w;  // -y flux (row - 1 reads it)
+            fzm = c4 * w;
+            fzp_new = c5 * w;
+            sw_new = (((c0 + c1) + (c2 + c3)) + (c4 + c5)) * w;
+        }
+        if (!STORED && cw && k >= kfirst + 2) {  // uniform
             const Real Rj = Rh[1 - P], Tj = Th[1 - P];
             const bool ok = inx && iny && j >= 0 && j < mz;
             const bool mzm = j > 0, mzp = j + 1 < mz;
@@ -380,8 +419,10 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
             cur = bz;
         }
         // ---- histories (parity P slots now hold plane k)
-        Rh[P] = R_k;
-        Th[P] = T_k;
+        if constexpr (!STORED) {
+            Rh[P] = R_k;
+            Th[P] = T_k;
+        }
         sh[P] = s_k;
         dq[P][0] = D0;
         dq[P][1] = D1;
@@ -391,8 +432,8 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
         gxv[P] = gx_new;
         if (slab_pending) slab_store(slab_nz);
         __syncthreads();
-        // the slot of plane k-1 is free: refill it with plane k+4
-        if (k + AHEAD <= klast) HV3_ISSUE(k + AHEAD);
+        // the slot of plane k - LAG is free: refill it with plane k - LAG + RING
+        if (k - LAG + RING <= klast) HV3_ISSUE(k - LAG + RING);
         if (++slot == RING) {
             slot = 0;
             phase ^= 1u;
@@ -418,9 +459,10 @@ __global__ void __launch_bounds__(NT, 1) k_hv3(const __grid_constant__ FArgs a, 
 }
 
 template <typename Real>
-std::size_t smem3(int nlx, int nsl, int zc) {
+std::size_t smem3(int nlx, int nsl, int zc, bool stored) {
     const std::size_t bx = sizeof(Real) == 8 ? LX : LX + 4;
-    return static_cast<std::size_t>(RING) * 5 * bx * NR * sizeof(Real) + 64 +
+    const std::size_t slot = ((stored ? 3 * bx * NR + 6 * bx * (NR - 2) : 5 * bx * NR) * sizeof(Real) + 127) / 128 * 128;
+    return static_cast<std::size_t>(stored ? 3 : 5) * slot + 64 +
            (static_cast<std::size_t>(zc) + 8 + OY) * sizeof(double) +
            (static_cast<std::size_t>(NSL) * nsl + 2 * NR * LX + 4 * NR * LX + 3 * OY * static_cast<std::size_t>(nlx)) *
                sizeof(Real) +
@@ -429,8 +471,8 @@ std::size_t smem3(int nlx, int nsl, int zc) {
 
 }  // namespace
 
-std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32) {
-    return fp32 ? smem3<float>(nlx, nsl, zc) : smem3<double>(nlx, nsl, zc);  // (sizes only: no instantiation)
+std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32, bool stored) {
+    return fp32 ? smem3<float>(nlx, nsl, zc, stored) : smem3<double>(nlx, nsl, zc, stored);
 }
 int hv3_tile_x() { return OX; }
 int hv3_tile_y() { return OY; }
@@ -447,20 +489,25 @@ int hv3_box_origin(bool fp32) { return fp32 ? 4 : 2; }  // box x0 = tile x0 - th
 bool hv3_fp32_ok() { return MFREG_HV3_F32 != 0; }
 
 void hv3_set_smem_cap(int bytes) {
-    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 #if MFREG_HV3_F32
-    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv3<float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 #endif
 }
 
-void hv3_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
+void hv3_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32,
+                bool stored) {
 #if MFREG_HV3_F32
     if (fp32) {
-        launch_pdl(k_hv3<float>, grid, dim3(NT), smem, s, a, maps);
+        if (stored) launch_pdl(k_hv3<float, true>, grid, dim3(NT), smem, s, a, maps);
+        else launch_pdl(k_hv3<float, false>, grid, dim3(NT), smem, s, a, maps);
         return;
     }
 #endif
-    launch_pdl(k_hv3<double>, grid, dim3(NT), smem, s, a, maps);
+    if (stored) launch_pdl(k_hv3<double, true>, grid, dim3(NT), smem, s, a, maps);
+    else launch_pdl(k_hv3<double, false>, grid, dim3(NT), smem, s, a, maps);
 }
 
 }  // namespace mfreg_b200

@@ -419,14 +419,16 @@ void DeviceObjective::warp_state(const double* y, cudaStream_t s, int zlo, int z
         launch_warp_fast(plan_.view(), y, T_, ngf_.Tw.get(), state ? ngf_.dT.get() : nullptr, s, zlo, zhi);
 }
 
-double* DeviceObjective::frh_out() { return fused_->hv3() ? nullptr : static_cast<double*>(ngf_.state_frh()); }
+double* DeviceObjective::frh_out() {
+    return fused_->hv3_recompute() ? nullptr : static_cast<double*>(ngf_.state_frh());
+}
 
 // a14: Hv uses the state of the last eval, value-only included. A lazy value-only
 // eval skipped writing that state (dT, rho-hat); rebuild it at the recorded point.
 void DeviceObjective::refresh_state() {
     if (!stale_) return;
     warp_state(ylazy_.get(), s_, 0, -1, true);
-    if (!fused_->hv3())  // (hv3 recomputes the coefficients: T_w and dT are the whole state)
+    if (!fused_->hv3_recompute())  // (the recomputing Hv pass: T_w and dT are the whole state)
         launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
                           static_cast<double*>(ngf_.state_frh()), false, s_);
     check_launch("Objective: Hv state refresh");

@@ -19,9 +19,10 @@ def max_rel(a, b):
 @pytest.mark.parametrize("case", [((64, 48, 40), (1.0, 1.0, 1.0), 4), ((128, 36, 23), (0.97, 0.97, 2.5), 4),
                                   ((32, 20, 9), (1.0, 1.2, 0.8), 3), ((40, 24, 30), (0.7, 0.7, 0.7), 2)],
                          ids=lambda c: "x".join(map(str, c[0])))
-@pytest.mark.parametrize("hv3", [False, True], ids=["hv2", "hv3"])
-def test_fast32_operators_vs_reference(P, oracle, case, hv3, monkeypatch):
-    monkeypatch.setenv("MFREG_HV3", "1" if hv3 else "0")  # Hv pass with recomputed coefficients (opt-in)
+@pytest.mark.parametrize("hv", ["hv2", "hv3", "hv4"])
+def test_fast32_operators_vs_reference(P, oracle, case, hv, monkeypatch):
+    monkeypatch.setenv("MFREG_HV3", "1" if hv == "hv3" else "0")  # uniform-warp Hv pass, recomputed coefficients
+    monkeypatch.setenv("MFREG_HV4", "1" if hv == "hv4" else "0")  # the same on the stored coefficients
     m, h, ratio = case
     R = oracle.make_phantom(m, h) * 1000.0
     T = oracle.warp_sinusoid(R, m, h, 3.0, 42)

@@ -21,9 +21,10 @@ def max_rel(a, b):
     return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300))
 
 
-VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0"},
-            "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0"},
-            "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1"}}
+VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0", "MFREG_HV4": "0"},
+            "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "0"},
+            "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1", "MFREG_HV4": "0"},
+            "hv4": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "1"}}
 
 
 def _objective(P, R, T, m, h, ratio, variant):
