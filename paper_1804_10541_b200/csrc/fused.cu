@@ -15,12 +15,14 @@
 namespace mfreg_b200 {
 
 // hv_fast.cu
-std::size_t hv2_smem_bytes(int nlx, int nsl, int zc, bool fp32);
+std::size_t hv2_smem_bytes(int nlx, int nly, int segw, int zc, int nsl, bool fp32, int ty);
+int hv2_nsl_max(int ty);
 int hv2_box_origin(bool fp32);
-int hv2_nsl_max();
-int hv2_threads();
-void hv2_set_smem_cap(int bytes);
-void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
+int hv2_nlx_max();
+int hv2_threads(int ty);
+void hv2_set_smem_cap(int bytes, int ty);
+void hv2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32,
+                int ty);
 // hv3.cu
 std::size_t hv3_smem_bytes(int nlx, int nsl, int zc, bool fp32, bool stored);
 int hv3_tile_x();
@@ -1070,17 +1072,17 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
             segw_ = std::max(segw_, run);
         }
     }
-    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, slab_[0] * slab_[1] * 3, t.zc, fp32_);
+    const std::size_t hv2_smem = hv2_smem_bytes(t.nlx, t.nly, segw_, t.zc, slab_[0] * slab_[1] * 3, fp32_, 8);
     const char* no2 = std::getenv("MFREG_NO_HV2");
-    hv2_ = tma_ && zok && (fp32_ || !(no2 && no2[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() &&
-           slab_[0] * slab_[1] * 3 <= hv2_nsl_max() && hv2_smem <= static_cast<std::size_t>(kSmem2Cta);
+    hv2_ = tma_ && zok && (fp32_ || !(no2 && no2[0] == '1')) && t.nlx <= hv2_nlx_max() &&
+           slab_[0] * slab_[1] * 3 <= hv2_nsl_max(8) && hv2_smem <= static_cast<std::size_t>(kSmem2Cta);
     hv2_smem_ = hv2_smem;
     // (process-wide per-kernel cap: always the 2-CTA bound, so plans never lower each other's)
-    if (hv2_) hv2_set_smem_cap(kSmem2Cta);
+    if (hv2_) hv2_set_smem_cap(kSmem2Cta, 8);
     // two-CTA/SM eval kernel (ev_fast.cu): same conditions
     ev2_smem_ = ev2_smem_bytes(t.nlx, fp32_);
     const char* noe = std::getenv("MFREG_NO_EV2");
-    ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
+    ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads(8) && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
     if (ev2_) ev2_set_smem_cap(kSmem2Cta);
     setup_hv3(plan, R, Tw, dT, frh, zok, max_optin);
     // FAST32 runs only on the two-CTA kernels (the legacy fused kernels are fp64)
@@ -1101,8 +1103,11 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
     const char* on = std::getenv("MFREG_HV3");   // recompute variant
     const char* on4 = std::getenv("MFREG_HV4");  // stored-coefficient variant
     const char* off = std::getenv("MFREG_NO_HV3");
+    const char* on16 = std::getenv("MFREG_HV16");  // k_hv2 on 32 x 16 tiles, one CTA per SM
     const bool recompute = on && on[0] == '1', stored = !recompute && on4 && on4[0] == '1';
-    if (!(recompute || stored) || (off && off[0] == '1') || !tma_ || !zok || (fp32_ && !hv3_fp32_ok())) return;
+    const bool h16 = !recompute && !stored && on16 && on16[0] == '1';
+    if (!(recompute || stored || h16) || (off && off[0] == '1') || !tma_ || !zok) return;
+    if (!h16 && fp32_ && !hv3_fp32_ok()) return;
     static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
         void* fn = nullptr;
         cudaDriverEntryPointQueryResult q{};
@@ -1114,7 +1119,7 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
     if (!encode) return;
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
-    const int tsx = hv3_tile_x(), tsy = hv3_tile_y();
+    const int tsx = h16 ? FT_X : hv3_tile_x(), tsy = h16 ? 16 : hv3_tile_y();
     TileMeta t{};
     t.ntx = static_cast<int>((g.m[0] + tsx - 1) / tsx);
     t.nty = static_cast<int>((g.m[1] + tsy - 1) / tsy);
@@ -1181,10 +1186,12 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
         }
         fp[a2] = mxf;
     }
-    const std::size_t smem = hv3_smem_bytes(t.nlx, fp[0] * fp[1] * 3, t.zc, fp32_, stored);
-    if (fp[0] * fp[1] * 3 > hv3_threads() || 3 * t.nlx * t.nly > hv3_threads() ||
-        smem > static_cast<std::size_t>(max_optin))
+    const std::size_t smem = h16 ? hv2_smem_bytes(t.nlx, t.nly, segw_, t.zc, fp[0] * fp[1] * 3, fp32_, 16)
+                                 : hv3_smem_bytes(t.nlx, fp[0] * fp[1] * 3, t.zc, fp32_, stored);
+    if (h16 ? (t.nlx > hv2_nlx_max() || fp[0] * fp[1] * 3 > hv2_nsl_max(16))
+            : (fp[0] * fp[1] * 3 > hv3_threads() || 3 * t.nlx * t.nly > hv3_threads()))
         return;
+    if (smem > static_cast<std::size_t>(max_optin)) return;
     // tensor maps: R, T_w (3-D boxes BX x 16), dT (4-D, 3 components); fp32 needs 16-byte rows
     const int es = fp32_ ? 4 : 8;
     if ((g.m[0] * es) % 16 != 0) return;
@@ -1193,8 +1200,10 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
         const cuuint64_t e = static_cast<cuuint64_t>(es);
         const cuuint64_t dims[4] = {mx, my, mzz, comps};
         const cuuint64_t strides[3] = {mx * e, mx * my * e, n * e};
-        const cuuint32_t box[4] = {static_cast<cuuint32_t>(hv3_box_width(fp32_)),
-                                   static_cast<cuuint32_t>(hv3_box_rows() - rows_less), 1, bc};
+        // (32 x 16 k_hv2: boxes start x0 - XO, 32 + 2 XO wide; dT 20 rows, rho-hat 18)
+        const int bw = h16 ? FT_X + 2 * hv2_box_origin(fp32_) : hv3_box_width(fp32_);
+        const int br = h16 ? 20 - rows_less : hv3_box_rows() - rows_less;
+        const cuuint32_t box[4] = {static_cast<cuuint32_t>(bw), static_cast<cuuint32_t>(br), 1, bc};
         const cuuint32_t est[4] = {1, 1, 1, 1};
         return encode(m, fp32_ ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank,
                       const_cast<void*>(base), dims, strides, box, est, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -1202,7 +1211,8 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
     TmaMaps maps{};
-    const bool ok = stored ? (enc(&maps.b, frh, 4, 6, 6, 2) && enc(&maps.c, dT, 4, 3, 3))
+    const bool ok = h16 ? (enc(&maps.a, dT, 4, 3, 3) && enc(&maps.b, frh, 4, 6, 6, 2))
+                  : stored ? (enc(&maps.b, frh, 4, 6, 6, 2) && enc(&maps.c, dT, 4, 3, 3))
                            : (enc(&maps.a, R, 3, 1, 1) && enc(&maps.b, Tw, 3, 1, 1) && enc(&maps.c, dT, 4, 3, 3));
     if (!ok) return;
     std::memcpy(maps_hv3_, &maps, sizeof(TmaMaps));
@@ -1222,9 +1232,11 @@ void FusedPlan::setup_hv3(const DevicePlanOwner& plan, const void* R, const void
     slab3_[1] = fp[1];
     gmax3_ = gmax;
     hv3_smem_ = smem;
-    hv3_set_smem_cap(max_optin);
+    if (h16) hv2_set_smem_cap(max_optin, 16);
+    else hv3_set_smem_cap(max_optin);
     hv3_ = true;
-    hv3_stored_ = stored;
+    hv3_stored_ = stored || h16;
+    hv16_ = h16;
 }
 
 bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, const void* dT, const void* frh) {
@@ -1298,8 +1310,12 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
         a.Tw = static_cast<const double*>(fp.state_Tw());
         note_launch();
         const TileMeta& t3 = fp.meta3();
-        hv3_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv3()), dim3(t3.ntx, t3.nty, t3.ntz), fp.hv3_smem(), s,
-                   fp.fp32(), fp.hv3_stored());
+        if (fp.hv16())
+            hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv3()), dim3(t3.ntx, t3.nty, t3.ntz), fp.hv3_smem(),
+                       s, fp.fp32(), 16);
+        else
+            hv3_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv3()), dim3(t3.ntx, t3.nty, t3.ntz), fp.hv3_smem(),
+                       s, fp.fp32(), fp.hv3_stored());
         return;
     }
     const TileMeta& t = fp.meta();
@@ -1307,7 +1323,7 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
     if (fp.hv2()) {
         hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, t.ntz), fp.hv2_smem(), s,
-                   fp.fp32());
+                   fp.fp32(), 8);
         return;
     }
     const TmaMaps& maps = *reinterpret_cast<const TmaMaps*>(fp.maps_hv());

@@ -71,6 +71,7 @@ public:
     // T_w, dT and the eval pass stores no rho-hat)
     bool hv3() const { return hv3_; }
     bool hv3_stored() const { return hv3_stored_; }
+    bool hv16() const { return hv16_; }  // the own-tiling Hv pass is k_hv2 on 32 x 16 tiles (default)
     bool hv3_recompute() const { return hv3_ && !hv3_stored_; }
     const TileMeta& meta3() const { return meta3_; }
     double* partials3() { return part3_.get(); }
@@ -117,6 +118,7 @@ private:
     alignas(64) unsigned char maps_ev_[3 * 128];
     bool hv3_ = false;
     bool hv3_stored_ = false;
+    bool hv16_ = false;
     TileMeta meta3_{};
     DevArray<int> goff3_[3];
     DevArray<int2> gent3_[3];

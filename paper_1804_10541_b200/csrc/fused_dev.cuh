@@ -48,6 +48,13 @@ __device__ __forceinline__ double lerp(double t, double a, double b) { return fm
 __device__ __forceinline__ float lerp(float t, float a, float b) { return fmaf(t, b - a, a); }
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+// shared-memory load the compiler may neither hoist nor merge (per-use reload of packed tables,
+// cheaper than keeping the values live across a long loop)
+__device__ __forceinline__ int lds_v(const int* p) {
+    int v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)));
+    return v;
+}
 
 // Programmatic dependent launch: kernels launched with launch_pdl() may start while the
 // previous kernel in the stream drains; everything that reads that kernel's output must

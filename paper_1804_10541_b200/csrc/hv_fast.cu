@@ -34,6 +34,9 @@
 #ifndef MFREG_REVMAP
 #define MFREG_REVMAP 1
 #endif
+#ifndef MFREG_HV2_EXP
+#define MFREG_HV2_EXP 0  // timing experiments only (wrong results): 1 no P^T collapse, 2 no halo items
+#endif
 
 namespace mfreg_b200 {
 
@@ -41,46 +44,63 @@ namespace {
 
 using namespace fdev;
 
-constexpr int TX = FT_X, TY = FT_Y;                    // 32 x 8 output tile
-constexpr int SY = TY + 4, WY = TY + 2;                // s region rows / rho-hat rows
-constexpr int NT = TX * TY;                            // 256 threads
-constexpr int RING = 3;                                // staging slots (2 planes ahead)
-constexpr int NX_W = 80;                               // extra items [0, 80): ring-1 edges (P + W)
-constexpr int NX_P = 164;                              // extra items [80, 164): P only
+constexpr int TX = FT_X;                               // 32-column output tiles
+constexpr int DRING = 3;                               // dT staging slots (2 planes ahead)
+#ifndef MFREG_HV2_RRING
+#define MFREG_HV2_RRING 3  // measured: 2 (one plane ahead) is 3% slower at C4 even with the smem freed
+#endif
+#ifndef MFREG_HV2_SLAB
+#define MFREG_HV2_SLAB 0   // nodal footprint in shared memory (1) or the interpolants read from L1/L2 (0)
+#endif
+constexpr int RRING = MFREG_HV2_RRING;                 // rho-hat staging slots (RRING - 1 planes ahead)
 constexpr int NSL = 4;                                 // nodal plane ring (power of 2)
+
+// Tile height variants: 32 x 8 (256 threads, two CTAs per SM; shares the eval pass's tiling) and
+// 32 x 16 (512 threads, one CTA per SM, own tiling): the halo columns per output column drop
+// from 0.64 (P) / 0.31 (W) to 0.38 / 0.19
+template <int TY_>
+struct Tl {
+    static constexpr int TY = TY_;
+    static constexpr int SY = TY + 4, WY = TY + 2;          // s region rows / rho-hat rows
+    static constexpr int NT = TX * TY;                      // threads
+    static constexpr int NX_W = 2 * TX + 2 * TY;            // extra items [0, NX_W): ring-1 edges (P + W)
+    static constexpr int NX_P = NX_W + 4 + 2 * TX + 2 * TY;  // then ring-1 corners, ring-2 edges (P only)
+    static constexpr int MINB = TY == 8 ? 2 : 1;            // CTAs per SM
+};
 
 // Box geometry per state precision: a TMA box must start 16-byte aligned in x, so the
 // boxes start XO columns left of the tile (x0 - 2 for fp64, x0 - 4 for fp32) and are
 // SX = 32 + 2 XO wide; the s frame is SX x 12, the rho-hat box SX x 10 (one row lower).
-template <typename Real>
+template <typename Real, int TY_>
 struct Geo {
+    static constexpr int SY = Tl<TY_>::SY, WY = Tl<TY_>::WY;
     static constexpr int XO = sizeof(Real) == 8 ? 2 : 4;
     static constexpr int SX = TX + 2 * XO, NS = SX * SY, NW = SX * WY;
     static constexpr int SLOT_DT = 3 * NS;              // dT box [3][12][SX]
     static constexpr int SLOT_RH = 6 * NW;              // rho-hat box [6][10][SX]
-    static constexpr int SLOT = static_cast<int>(((SLOT_DT + SLOT_RH) * sizeof(Real) + 127) / 128 * 128 / sizeof(Real));
-    static_assert((SLOT_DT * sizeof(Real)) % 128 == 0, "rho-hat box must land 128-byte aligned");
+    static_assert((SLOT_DT * sizeof(Real)) % 128 == 0 && (SLOT_RH * sizeof(Real)) % 128 == 0, "TMA boxes 128-byte aligned");
 };
 
 // extra work item e -> column (lx, ly) in the s frame (tile columns at lx = XO .. XO+31);
 // `dir` = consumer flux array of a ring-1 edge item (0: +x, 1: -x, 2: +y, 3: -y)
-template <int XO>
+template <int XO, int TY_>
 __device__ __forceinline__ void extra_item(int e, int& lx, int& ly, int& dir) {
+    constexpr int TY = TY_, SY = Tl<TY_>::SY, NX_W = Tl<TY_>::NX_W;
     dir = -1;
-    if (e < 32) { lx = XO + e; ly = 1; dir = 2; }                       // ring-1, y = -1 row: feeds +y
-    else if (e < 64) { lx = XO + e - 32; ly = SY - 2; dir = 3; }        // ring-1, y = TY row: feeds -y
-    else if (e < 72) { lx = XO - 1; ly = 2 + e - 64; dir = 0; }         // ring-1, x = -1: feeds +x
-    else if (e < 80) { lx = XO + TX; ly = 2 + e - 72; dir = 1; }        // ring-1, x = TX: feeds -x
-    else if (e < 84) {                                                  // ring-1 corners
-        const int q = e - 80;
+    if (e < TX) { lx = XO + e; ly = 1; dir = 2; }                               // ring-1, y = -1 row: feeds +y
+    else if (e < 2 * TX) { lx = XO + e - TX; ly = SY - 2; dir = 3; }            // ring-1, y = TY row: feeds -y
+    else if (e < 2 * TX + TY) { lx = XO - 1; ly = 2 + e - 2 * TX; dir = 0; }   // ring-1, x = -1: feeds +x
+    else if (e < NX_W) { lx = XO + TX; ly = 2 + e - 2 * TX - TY; dir = 1; }     // ring-1, x = TX: feeds -x
+    else if (e < NX_W + 4) {                                                    // ring-1 corners
+        const int q = e - NX_W;
         lx = (q & 1) ? XO + TX : XO - 1;
         ly = (q & 2) ? SY - 2 : 1;
-    } else {                                                            // ring-2 edges
-        const int r = e - 84;
-        if (r < 32) { lx = XO + r; ly = 0; }
-        else if (r < 64) { lx = XO + r - 32; ly = SY - 1; }
-        else if (r < 72) { lx = XO - 2; ly = 2 + r - 64; }
-        else { lx = XO + TX + 1; ly = 2 + r - 72; }
+    } else {                                                                    // ring-2 edges
+        const int r = e - NX_W - 4;
+        if (r < TX) { lx = XO + r; ly = 0; }
+        else if (r < 2 * TX) { lx = XO + r - TX; ly = SY - 1; }
+        else if (r < 2 * TX + TY) { lx = XO - 2; ly = 2 + r - 2 * TX; }
+        else { lx = XO + TX + 1; ly = 2 + r - 2 * TX - TY; }
     }
 }
 
@@ -89,11 +109,17 @@ struct Par {
     static constexpr int P = P_;
 };
 
-template <typename Real>
-__global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
-    using G = Geo<Real>;
-    constexpr int XO = G::XO, SX = G::SX, NS = G::NS, NW = G::NW, SLOT_DT = G::SLOT_DT, SLOT_RH = G::SLOT_RH,
-                  SLOT = G::SLOT;
+// P^T collapse buffers: a row holds three components of 32 columns, then the x-collapsed nodes
+// in place (3 nlx); a node's x window spans two nodal cells
+__host__ __device__ constexpr int xrow_len(int nlx) { return 3 * nlx > 3 * TX ? 3 * nlx : 3 * TX; }
+__host__ __device__ constexpr int xwin(int segw) { return 2 * segw < TX ? 2 * segw : TX; }
+
+template <typename Real, int TY_>
+__global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
+    using G = Geo<Real, TY_>;
+    constexpr int TY = TY_, SY = Tl<TY_>::SY, NT = Tl<TY_>::NT, NX_W = Tl<TY_>::NX_W, NX_P = Tl<TY_>::NX_P;
+    (void)SY;
+    constexpr int XO = G::XO, SX = G::SX, NS = G::NS, NW = G::NW, SLOT_DT = G::SLOT_DT, SLOT_RH = G::SLOT_RH;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     if (a.skip && *a.skip) return;  // uniform
     const TileMeta& tm = a.tm;
@@ -112,108 +138,151 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
     const int msx = static_cast<int>(a.P.src.m[0]), msy = static_cast<int>(a.P.src.m[1]);
     const int msz = static_cast<int>(a.P.src.m[2]);
-    const int nxf = a.nxf, nyf = a.nyf, nsl = nxf * nyf * 3, segw = a.segw;
+    const int segw = a.segw;
 
-    // ---- shared memory: ring | barriers | nodal ring, row/z tables (fp64) | s planes, fluxes,
-    // item-1 interpolants, x-collapsed rows (Real) | int tables
-    Real* const stg = reinterpret_cast<Real*>(smem_raw);
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (32 B)
-    Real* const slab = reinterpret_cast<Real*>(bars + 4);  // [NSL][nsl] nodal p (NSL * nsl is a multiple of 4)
-    double* const sry = reinterpret_cast<double*>(slab + NSL * nsl);  // [TY]
-    double* const sZr = sry + TY;               // [zc + 8] rem_z of the planes kfirst ..
-    Real* const sS = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [2][NS] by plane parity
+    // ---- shared memory: dT ring | rho-hat ring | barriers | z table (fp64) | nodal ring, s planes,
+    // fluxes, item-1 interpolants, P^T rows (Real) | int tables
+    Real* const stgD = reinterpret_cast<Real*>(smem_raw);       // [DRING][SLOT_DT]
+    Real* const stgR = stgD + DRING * SLOT_DT;                   // [RRING][SLOT_RH]
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stgR + RRING * SLOT_RH);  // [DRING + RRING]
+    double* const sZr = reinterpret_cast<double*>(bars + 8);  // [zc + 8] rem_z of the planes kfirst ..
+    const int nxf = a.nxf, nyf = a.nyf, pl = nxf * nyf, nsl = 3 * pl;
+    Real* const slab = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [NSL][3][nyf][nxf] nodal p footprint
+    Real* const sS = slab + (MFREG_HV2_SLAB ? NSL * nsl : 0);  // [2][NS] by plane parity
     Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
     Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
                                                 // then 2 zero entries (the edge-flux slot of inner lanes)
     Real* const sQ1 = sE + 2 * 2 * TY + 2;      // [6][NX_P] item-1 P p at nodal planes bz, bz+1
-    Real* const sQx = sQ1 + 6 * NX_P;           // [3][TY][nlx] (completions >= 2 steps apart)
-    int* const sby = reinterpret_cast<int*>(sQx + 3 * TY * nlx);  // [TY]
-    int* const sZb = sby + TY;                  // [zc + 8] base_z of the planes kfirst ..
-    const unsigned bar0 = smem_u32(bars);
+    // P^T of a completed nodal plane: each warp stores its row's z-weighted sums [3][32] in sA and
+    // collapses x in place (node j of component d at d * nlx_t + j); one step later the y collapse
+    // reads every row (completions are >= 2 steps apart)
+    const int XR = xrow_len(nlx), WXP = xwin(segw);
+    Real* const sA = sQ1 + 6 * NX_P;            // [TY][XR]
+    Real* const sWx = sA + TY * XR;             // [nlx][WXP] x weights of node j over columns sXs[j] ..
+    Real* const sWy = sWx + nlx * WXP;          // [nly][TY] y weights of node row lyn over the tile rows
+    int* const sZb = reinterpret_cast<int*>(sWy + tm.nly * TY);  // [zc + 8] base_z of the planes kfirst ..
+    int* const sXs = sZb + tm.zc + 8;           // [nlx] first column of node j's x window
+    int* const sXi = sXs + nlx;                 // [3 nlx] x item L: window offset | weight offset << 8 | (d, j)
+    int* const sI1 = sXi + 3 * nlx;             // [NX_P] packed item-1 geometry
+    const unsigned barD = smem_u32(bars), barR = barD + 8 * DRING;
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
     const int tx = lane, ty = row;
     const int c0 = (tx + XO) + (ty + 2) * SX, w0 = c0 - SX;  // s frame / rho-hat frame (one row lower)
     const int gx0 = x0 + tx, gy0 = y0 + ty;
-    const bool has1 = tid < NX_P, w1 = tid < NX_W;  // warp-aligned except warp 2 (split P+W / P) and warp 5
-    int lx1 = 0, ly1 = 0, dir1 = -1;
-    if (has1) extra_item<XO>(tid, lx1, ly1, dir1);
-    const int c1 = lx1 + ly1 * SX, w1i = c1 - SX;
-    // where the ring-1 edge flux goes: y edges -> consumer-indexed sF (+y: 0, -y: 1), x edges -> sE
-    const bool xedge = dir1 == 0 || dir1 == 1;
-    const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
-                         : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+    const bool has1 = (MFREG_HV2_EXP & 2) ? false : tid < NX_P, w1 = (MFREG_HV2_EXP & 2) ? false : tid < NX_W;  // warp-aligned except warp 2 (split P+W / P) and warp 5
+    // item-1 geometry, packed once into shared memory and re-read where it is used (keeping it
+    // live in registers across the plane loop costs more than the loads): bits 0-9 the s-frame
+    // index c1, 10-19 the flux slot f1, 20-21 the coefficient toward the tile, 22 x edge
+    if (has1) {
+        int lx1 = 0, ly1 = 0, dir1 = -1;
+        extra_item<XO, TY>(tid, lx1, ly1, dir1);
+        // where the ring-1 edge flux goes: y edges -> consumer-indexed sF (+y: 0, -y: 1), x edges -> sE
+        const bool xedge = dir1 == 0 || dir1 == 1;
+        const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
+                             : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+        const int ci = dir1 == 0 ? 1 : (dir1 == 1 ? 0 : (dir1 == 2 ? 3 : 2));
+        static_assert(G::NS <= 1024 && 2 * NT <= 1024, "item-1 packing");
+        sI1[tid] = (lx1 + ly1 * SX) | (max(f1, 0) << 10) | (ci << 20) | (xedge ? 1 << 22 : 0);
+    }
 
-    // nodal slab geometry (P p): x-y footprint of the s region, bilinear weights per column
-    const int fx0 = __ldg(&a.P.base[0][max(x0 - 2, 0)]);
-    const int fy0 = __ldg(&a.P.base[1][max(y0 - 2, 0)]);
+    // P p: the tile's nodal footprint (nxf x nyf nodes from (fx0, fy0), clamped at the last node)
+    // of four nodal planes in shared memory, each plane loaded one step before its first use (<= 2
+    // elements per thread, held in registers across the step); a column's bilinear interpolant
+    // reads its cell's four nodes from there
+    const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = sm0 * a.P.src.m[1];
+    const int fx0 = __ldg(&a.P.base[0][max(x0 - 2, 0)]), fy0 = __ldg(&a.P.base[1][max(y0 - 2, 0)]);
     auto col_geom = [&](int gx, int gy, int& off, double& rx, double& ry) {
         const int gxc = min(max(gx, 0), mx - 1), gyc = min(max(gy, 0), my - 1);
-        off = (__ldg(&a.P.base[0][gxc]) - fx0) + (__ldg(&a.P.base[1][gyc]) - fy0) * nxf;
+        const int bx = __ldg(&a.P.base[0][gxc]), by = __ldg(&a.P.base[1][gyc]);
+        off = MFREG_HV2_SLAB ? (bx - fx0) + (by - fy0) * nxf : bx + by * static_cast<int>(sm0);
         rx = __ldg(&a.P.rem[0][gxc]);
         ry = __ldg(&a.P.rem[1][gyc]);
     };
-    const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
-    // edge-flux slot of the tile column (lanes 0 / 31 read a ring-1 x edge, the others a zero
-    // slot past both parity halves) and the ring-1 item's coefficient offset toward the tile
-    const int eoff = tx == 0 ? ty : (tx == TX - 1 ? TY + ty : -1);
-    const int cfo = dir1 == 0 ? 1 * NW : (dir1 == 1 ? 0 : (dir1 == 2 ? 3 * NW : 2 * NW));
-    const Real mpx = tx > 0 ? Real(1) : Real(0), mmx = tx + 1 < TX ? Real(1) : Real(0);
-
-    // nodal p elements this thread loads (<= 2 per thread; host guarantees nsl <= 2 * NT)
-    const long long ns = a.P.src.count(), sm0 = a.P.src.m[0], sm01 = sm0 * a.P.src.m[1];
-    // (offsets within one component plane; component d adds d * ns)
-    int slab_off[2], slab_d[2];
-    Real slab_v[2] = {Real(0), Real(0)};
+    auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
+        if constexpr (MFREG_HV2_SLAB) {
+            const Real* q = slab + (nz & (NSL - 1)) * nsl + off;
+            o0 = lerp(ry, lerp(rx, q[0], q[1]), lerp(rx, q[nxf], q[nxf + 1]));
+            o1 = lerp(ry, lerp(rx, q[pl], q[pl + 1]), lerp(rx, q[pl + nxf], q[pl + nxf + 1]));
+            o2 = lerp(ry, lerp(rx, q[2 * pl], q[2 * pl + 1]), lerp(rx, q[2 * pl + nxf], q[2 * pl + nxf + 1]));
+        } else {
+            // one row pointer per component and y, +1 for x (the transfer plan clamps base to
+            // [0, m-2], transfer.cpp:30-33, so the +x / +y neighbours exist)
+            const double* q0 = a.p + (static_cast<long long>(nz) * sm01 + off);
+            const double* q1 = q0 + ns;
+            const double* q2 = q1 + ns;
+            auto v = [](const double* q) { return static_cast<Real>(__ldg(q)); };
+            o0 = lerp(ry, lerp(rx, v(q0), v(q0 + 1)), lerp(rx, v(q0 + sm0), v(q0 + sm0 + 1)));
+            o1 = lerp(ry, lerp(rx, v(q1), v(q1 + 1)), lerp(rx, v(q1 + sm0), v(q1 + sm0 + 1)));
+            o2 = lerp(ry, lerp(rx, v(q2), v(q2 + 1)), lerp(rx, v(q2 + sm0), v(q2 + sm0 + 1)));
+        }
+    };
+    // footprint elements of this thread (highest threads first: the halo items sit on the lowest)
+    const int rt = NT - 1 - tid;
+    int sl_off[2];  // element index within nodal plane 0 (component included), -1: none
+    Real sl_v[2] = {Real(0), Real(0)};
 #pragma unroll
     for (int u = 0; u < 2; ++u) {
-        const int t = (MFREG_REVMAP ? NT - 1 - tid : tid) + u * NT;
-        slab_off[u] = -1;
-        slab_d[u] = 0;
+        const int t = rt + u * NT;
+        sl_off[u] = -1;
         if (t < nsl) {
-            const int ix = t % nxf, iy = (t / nxf) % nyf;
-            slab_d[u] = t / (nxf * nyf);
-            slab_off[u] = min(fx0 + ix, msx - 1) + min(fy0 + iy, msy - 1) * static_cast<int>(sm0);
+            const int d = t / pl, r = t - d * pl, iy = r / nxf, ix = r - iy * nxf;
+            sl_off[u] = static_cast<int>(d * ns + min(fy0 + iy, msy - 1) * sm0 + min(fx0 + ix, msx - 1));
         }
     }
     auto slab_load = [&](int nz) {
+        if constexpr (!MFREG_HV2_SLAB) return;
+        const double* q = a.p + static_cast<long long>(nz) * sm01;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-            if (slab_off[u] >= 0)
-                slab_v[u] = static_cast<Real>(__ldg(a.p + slab_d[u] * ns + static_cast<long long>(nz) * sm01 + slab_off[u]));
+            if (sl_off[u] >= 0) sl_v[u] = static_cast<Real>(__ldg(q + sl_off[u]));
     };
     auto slab_store = [&](int nz) {
+        if constexpr (!MFREG_HV2_SLAB) return;
         Real* dst = slab + (nz & (NSL - 1)) * nsl;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
-            if (slab_off[u] >= 0) dst[(MFREG_REVMAP ? NT - 1 - tid : tid) + u * NT] = slab_v[u];
-    };
-    auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
-        const Real* q = slab + (nz & (NSL - 1)) * nsl + off;
-        const int pl = nxf * nyf;
-        auto v = [&](int i) { return static_cast<Real>(q[i]); };
-        o0 = lerp(ry, lerp(rx, v(0), v(1)), lerp(rx, v(nxf), v(nxf + 1)));
-        o1 = lerp(ry, lerp(rx, v(pl), v(pl + 1)), lerp(rx, v(pl + nxf), v(pl + nxf + 1)));
-        o2 = lerp(ry, lerp(rx, v(2 * pl), v(2 * pl + 1)), lerp(rx, v(2 * pl + nxf), v(2 * pl + nxf + 1)));
+            if (sl_off[u] >= 0) dst[rt + u * NT] = sl_v[u];
     };
 
-    // x collapse geometry of the tile column: nodal cell, weight, segment of equal cells in the warp
-    // (columns past the volume form one-lane segments of their own and write nothing)
-    const int gxc0 = min(gx0, mx - 1);
-    const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
-    const int bxc = __ldg(&a.P.base[0][gxc0]) - nxA;
-    const int bx = xin ? bxc : 1024 + lane;
-    const Real rxq = __ldg(&a.P.rem[0][gxc0]);
-    const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
-    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
-    const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));  // first lane of my segment
-    const bool send = lane == 31 || ((starts >> (lane + 1)) & 1u);
+    // edge-flux slot of the tile column (lanes 0 / 31 read a ring-1 x edge, the others a zero
+    // slot past both parity halves); in-row x flux masks
+    const int eoff = tx == 0 ? ty : (tx == TX - 1 ? TY + ty : -1);
+    const Real mpx = tx > 0 ? Real(1) : Real(0), mmx = tx + 1 < TX ? Real(1) : Real(0);
 
+    // P^T collapse tables: node j (x) takes columns of cell j-1 with weight rem_x and of cell j
+    // with 1 - rem_x, a window of <= WXP columns starting at sXs[j]; node row lyn (y) takes the tile
+    // rows of cell lyn-1 with rem_y and of cell lyn with 1 - rem_y. Columns / rows past the volume
+    // weigh 0 (their sums are 0 as well: dT vanishes there).
     if (tid < 2) sE[4 * TY + tid] = Real(0);
-    if (tid < TY) {
-        const int gyc = min(y0 + tid, my - 1);
-        sby[tid] = __ldg(&a.P.base[1][gyc]) - nyA;
-        sry[tid] = __ldg(&a.P.rem[1][gyc]);
+    const int nxi = 3 * nlx_t;  // x items (d, j) per row
+    if (tid < nlx_t) {
+        const int j = tid;
+        int lo = TX;
+        for (int c = TX - 1; c >= 0; --c)
+            if (x0 + c < mx && __ldg(&a.P.base[0][x0 + c]) - nxA >= j - 1) lo = c;
+        const int st = max(0, min(lo, TX - WXP));
+        sXs[j] = st;
+        for (int t = 0; t < WXP; ++t) {
+            const int c = st + t, gx = x0 + c;
+            Real w = Real(0);
+            if (gx < mx) {
+                const int b = __ldg(&a.P.base[0][gx]) - nxA;
+                const Real r = static_cast<Real>(__ldg(&a.P.rem[0][gx]));
+                w = b == j ? Real(1) - r : (b == j - 1 ? r : Real(0));
+            }
+            sWx[j * WXP + t] = w;
+        }
+    }
+    for (int t = tid; t < tm.nly * TY; t += NT) {
+        const int lyn = t / TY, r = t % TY, gy = y0 + r;
+        Real w = Real(0);
+        if (gy < my && lyn < nly_t) {
+            const int b = __ldg(&a.P.base[1][gy]) - nyA;
+            const Real ry = static_cast<Real>(__ldg(&a.P.rem[1][gy]));
+            w = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
+        }
+        sWy[t] = w;
     }
     for (int t = tid; t < tm.zc + 8; t += NT) {
         const int kk = min(max(z0 - 2 + t, 0), mz - 1);
@@ -221,72 +290,82 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         sZr[t] = __ldg(&a.P.rem[2][kk]);
     }
     if (tid == 0) {
-        for (int b = 0; b < RING; ++b) mbar_init(&bars[b], 1);
+        for (int b = 0; b < DRING + RRING; ++b) mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
     const int kfirst = z0 - 2, klast = z1 + 1;
-    // step m: dT of plane m, rho-hat of plane m-1 (one thread; inlined so the tensor
-    // maps stay in the kernel's parameter space)
-#define HV2_ISSUE(m_, r_)                                                               \
-    do {                                                                                \
-        if (tid == 0) {                                                                 \
-            const int rr_ = (r_);                                                       \
-            Real* st_ = stg + rr_ * SLOT;                                              \
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");               \
-            mbar_expect_tx(&bars[rr_], (SLOT_DT + SLOT_RH) * sizeof(Real));              \
-            tma_load_4d(st_, &maps.a, x0 - XO, y0 - 2, (m_), 0, &bars[rr_]);             \
-            tma_load_4d(st_ + SLOT_DT, &maps.b, x0 - XO, y0 - 1, (m_) - 1, 0, &bars[rr_]); \
-        }                                                                               \
+    // dT of plane m into dT slot r (read by P of step m); rho-hat of plane m into rho-hat slot r
+    // (read by W of step m + 1). One thread; inlined so the tensor maps stay in the kernel's
+    // parameter space.
+#define HV2_ISSUE_D(m_, r_)                                                               \
+    do {                                                                                  \
+        if (tid == 0) {                                                                   \
+            const int rr_ = (r_);                                                         \
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                 \
+            mbar_expect_tx(&bars[rr_], SLOT_DT * sizeof(Real));                            \
+            tma_load_4d(stgD + rr_ * SLOT_DT, &maps.a, x0 - XO, y0 - 2, (m_), 0, &bars[rr_]); \
+        }                                                                                 \
+    } while (0)
+#define HV2_ISSUE_R(m_, r_)                                                               \
+    do {                                                                                  \
+        if (tid == 0) {                                                                   \
+            const int rr_ = (r_);                                                         \
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");                 \
+            mbar_expect_tx(&bars[DRING + rr_], SLOT_RH * sizeof(Real));                    \
+            tma_load_4d(stgR + rr_ * SLOT_RH, &maps.b, x0 - XO, y0 - 1, (m_), 0, &bars[DRING + rr_]); \
+        }                                                                                 \
     } while (0)
     auto zbase = [&](int k) { return sZb[k - kfirst]; };  // k in [kfirst, klast + 3]
     auto zrem = [&](int k) { return sZr[k - kfirst]; };
 
-    // x collapse of one completed nodal plane (tile row = warp) into sQx[par]
-    auto xcollapse = [&](Real v0, Real v1, Real v2) {
-        Real* dst = sQx + row * nlx;
-        Real A[3] = {(Real(1) - rxq) * v0, (Real(1) - rxq) * v1, (Real(1) - rxq) * v2};
-        Real B[3] = {rxq * v0, rxq * v1, rxq * v2};
-        // segmented inclusive scan over the lanes of equal nodal cell (segments <= segw lanes)
+    // x collapse of one completed nodal plane, in place in the warp's row of sA
+    const int npx = (nxi + 31) >> 5;  // passes over the x items (host: nlx <= 42)
+    auto xstage = [&](Real v0, Real v1, Real v2) {
+        Real* ar = sA + row * XR;
+        ar[lane] = v0;
+        ar[32 + lane] = v1;
+        ar[64 + lane] = v2;
+        __syncwarp();
+        Real o[4];
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            if (o >= segw) break;  // uniform
-            const bool in = lane - o >= sst;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const Real ua = __shfl_up_sync(0xffffffffu, A[d], o);
-                const Real ub = __shfl_up_sync(0xffffffffu, B[d], o);
-                A[d] = in ? A[d] + ua : A[d];
-                B[d] = in ? B[d] + ub : B[d];
+        for (int u = 0; u < 4; ++u) {
+            const int L = lane + 32 * u;
+            o[u] = Real(0);
+            if (u < npx && L < nxi) {
+                const int e = sXi[L];
+                const Real* v = ar + (e & 0xff);
+                const Real* w = sWx + ((e >> 8) & 0xfff);
+                Real acc0 = Real(0), acc1 = Real(0);  // WXP is even: two chains
+#pragma unroll 2
+                for (int t = 0; t < WXP; t += 2) {
+                    acc0 = fma(w[t], v[t], acc0);
+                    acc1 = fma(w[t + 1], v[t + 1], acc1);
+                }
+                o[u] = acc0 + acc1;
             }
         }
+        __syncwarp();
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const Real bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
-            if (send && xin) {
-                dst[d * TY * nlx + bx] = sst > 0 ? A[d] + bp : A[d];
-                if (xlast) dst[d * TY * nlx + bx + 1] = B[d];
-            }
+        for (int u = 0; u < 4; ++u) {
+            const int L = lane + 32 * u;
+            if (u < npx && L < nxi) ar[L] = o[u];
         }
     };
-    // y collapse of sQx into the tile partial of nodal plane nzp
-    const int nyi = 3 * nly_t * nlx_t;
-    // the y collapse (and the nodal-plane loads) run on the highest threads: the halo items sit on
-    // the lowest ones, so this evens out the warps' work between barriers
-    const int rtid = MFREG_REVMAP ? NT - 1 - tid : tid;
-    auto ycollapse = [&](int nzp) {
-        if (rtid < nyi) {
-            const int lxn = rtid % nlx_t, lyn = (rtid / nlx_t) % nly_t, d = rtid / (nlx_t * nly_t);
-            const Real* q = sQx + d * TY * nlx + lxn;
-            Real v = 0.0;
+    // y collapse of the x-collapsed rows into the tile partial of nodal plane nzp (node rows on the
+    // highest warps: the halo items sit on the lowest ones)
+    auto ystage = [&](int nzp) {
+        Real* const pz = part + static_cast<std::size_t>(nzp - nzA) * pstride;
+        for (int lyn = MFREG_REVMAP ? TY - 1 - row : row; lyn < nly_t; lyn += TY) {
+            const Real* w = sWy + lyn * TY;
+            for (int L = lane; L < nxi; L += 32) {
+                const int e = sXi[L];
+                const int j = (e >> 20) & 0x3f, d = e >> 26;
+                Real v = Real(0);
 #pragma unroll
-            for (int r = 0; r < TY; ++r) {
-                const int b = sby[r];
-                const Real ry = sry[r];
-                const Real wgt = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
-                v = fma(wgt, q[r * nlx], v);
+                for (int r = 0; r < TY; ++r) v = fma(w[r], sA[r * XR + L], v);
+                pz[(lyn * nlx + j) * 3 + d] = v;
             }
-            part[static_cast<std::size_t>(nzp - nzA) * pstride + (lyn * nlx + lxn) * 3 + d] = v;
         }
     };
 
@@ -295,6 +374,10 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
     // first two nodal planes, synchronously; first two staged planes
     // (the planes steps kfirst .. kfirst+2 read; later steps prefetch one plane each,
     // the host guarantees base_z advances by <= 1 per plane and <= 2 per 3 planes)
+    for (int L = tid; L < nxi; L += NT) {
+        const int d = L / nlx_t, j = L - d * nlx_t;
+        sXi[L] = (d * 32 + sXs[j]) | ((j * WXP) << 8) | (j << 20) | (d << 26);
+    }
     int slab_hi;
     {
         const int nz0 = zbase(kfirst);
@@ -304,10 +387,12 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             slab_store(nz);
         }
     }
-    HV2_ISSUE(kfirst, 0);
-    if (kfirst + 1 <= klast) HV2_ISSUE(kfirst + 1, 1);
-    int slot = 0;         // ring slot of the current step
-    unsigned phase = 0;   // its mbarrier phase parity
+    HV2_ISSUE_D(kfirst, 0);
+    if (kfirst + 1 <= klast) HV2_ISSUE_D(kfirst + 1, 1);
+    for (int m = 0; m < RRING - 1; ++m)
+        if (kfirst + m <= klast) HV2_ISSUE_R(kfirst - 1 + m, m);
+    int dslot = 0, rslot = 0;        // ring slots of the current step
+    unsigned dphase = 0, rphase = 0;  // their mbarrier phase parities
     __syncthreads();
 
     // ---- loop state (parity-named histories, P = (k - kfirst) & 1)
@@ -324,32 +409,36 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
 
     auto step = [&](auto parc, int k) {
         constexpr int P = decltype(parc)::P;
-        if (k + 2 <= klast) HV2_ISSUE(k + 2, slot == 0 ? 2 : slot - 1);
-        if (ypend >= 0) {  // y collapse of the plane completed last step (sQx published by the barrier)
-            ycollapse(ypend);
-            ypend = -1;
-        }
+        // refill the slots step k-1 read (free since the barrier)
+        if (k + 2 <= klast) HV2_ISSUE_D(k + 2, dslot == 0 ? DRING - 1 : dslot - 1);
+        if (k + RRING - 1 <= klast) HV2_ISSUE_R(k + RRING - 2, rslot == 0 ? RRING - 1 : rslot - 1);
         bool slab_pending = false;
         int slab_nz = 0;
         {
             const int nzq = min(zbase(k + 3) + 1, msz - 1);
-            if (nzq > slab_hi) {
+            if (MFREG_HV2_SLAB && nzq > slab_hi) {  // uniform
                 slab_load(nzq);
                 slab_pending = true;
                 slab_nz = nzq;
                 slab_hi = nzq;
             }
         }
+        if (ypend >= 0) {  // y collapse of the plane completed last step (sA published by the barrier)
+            ystage(ypend);
+            ypend = -1;
+        }
         const int bzk = zbase(k);
         const Real rzk = zrem(k);
         if (bzk != pz) {  // uniform: new nodal plane pair
             Real* q1 = sQ1 + tid;  // item 1: [0..2] plane bz, [3..5] plane bz+1 (own entries only)
-            // item 0 geometry from the x-collapse registers and the row tables; item 1 from global
-            const int off0 = (bxc + nxA - fx0) + (sby[row] + nyA - fy0) * nxf;
-            const Real ry0 = sry[row];
-            int off1 = 0;
-            double rx1 = 0.0, ry1 = 0.0;
-            if (has1) col_geom(gx1, gy1, off1, rx1, ry1);
+            int off0, off1 = 0;
+            double rx0d, ry0d, rx1 = 0.0, ry1 = 0.0;
+            col_geom(gx0, gy0, off0, rx0d, ry0d);
+            if (has1) {
+                const int c1 = lds_v(sI1 + tid) & 0x3ff;
+                col_geom(x0 - XO + c1 % SX, y0 - 2 + c1 / SX, off1, rx1, ry1);
+            }
+            const Real rxq = static_cast<Real>(rx0d), ry0 = static_cast<Real>(ry0d);
             const Real rx1r = static_cast<Real>(rx1), ry1r = static_cast<Real>(ry1);
             if (bzk == pz + 1) {
                 Pa0 = Pb0; Pa1 = Pb1; Pa2 = Pb2;
@@ -367,8 +456,10 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             if (has1) bilerp(bz1, off1, rx1r, ry1r, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
             pz = bzk;
         }
-        mbar_wait_at(bar0 + 8 * slot, phase);
-        const Real* st = stg + slot * SLOT;
+        mbar_wait_at(barD + 8 * dslot, dphase);
+        mbar_wait_at(barR + 8 * rslot, rphase);
+        const Real* st = stgD + dslot * SLOT_DT;
+        const Real* sr = stgR + rslot * SLOT_RH;
         // ---- P: plane k
         const Real pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
         const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
@@ -376,6 +467,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         sS[P * NS + c0] = s0;
         Real s1 = 0.0;
         if (has1) {
+            const int c1 = lds_v(sI1 + tid) & 0x3ff;
             const Real* q1 = sQ1 + tid;
             s1 = fma(st[c1], lerp(rzk, q1[0], q1[3 * NX_P]),
                      fma(st[NS + c1], lerp(rzk, q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * lerp(rzk, q1[2 * NX_P], q1[5 * NX_P])));
@@ -383,7 +475,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         }
         // ---- W: plane j = k-1 (in-plane neighbours' s from the other parity buffer)
         const Real* sn = sS + (1 - P) * NS;
-        const Real* rh = st + SLOT_DT + w0;  // rho-hat of plane j, [6][NW]
+        const Real* rh = sr + w0;  // rho-hat of plane j, [6][NW]
         Real* const Fj = sF + (1 - P) * 2 * NT;
         Real fzm, fzp_new, sw_new, gx_new;
         {
@@ -404,14 +496,15 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             sw_new = sg * w;
         }
         if (w1) {  // ring-1 edge column: only the flux toward the tile
-            const Real* rg = st + SLOT_DT + w1i;
+            const int e1 = lds_v(sI1 + tid), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff;
+            const Real* rg = sr + c1 - SX;
             const Real sj = sh1[1 - P];
             const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
             const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
             const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
             const Real w = (wa + wb) + wc;
-            const Real cf = rg[cfo];
-            if (xedge) sE[(1 - P) * 2 * TY + f1] = cf * w;
+            const Real cf = rg[((e1 >> 20) & 3) * NW];
+            if (e1 & (1 << 22)) sE[(1 - P) * 2 * TY + f1] = cf * w;
             else Fj[f1] = cf * w;
         }
         // ---- Z: plane i = k-2 (tile columns)
@@ -425,7 +518,7 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
             const int bz = zbase(i);
             const Real rz = zrem(i);
             if (bz > cur) {  // nodal plane `cur` complete: x collapse now, y collapse after the barrier
-                xcollapse(acc00, acc01, acc02);
+                xstage(acc00, acc01, acc02);
                 ypend = cur;
                 acc00 = acc10;
                 acc01 = acc11;
@@ -449,64 +542,89 @@ __global__ void __launch_bounds__(NT, 2) k_hv2(const __grid_constant__ FArgs a, 
         fzp[P] = fzp_new;
         sw = sw_new;
         gx = gx_new;
-        if (++slot == RING) {
-            slot = 0;
-            phase ^= 1u;
+        if (++dslot == DRING) {
+            dslot = 0;
+            dphase ^= 1u;
+        }
+        if (++rslot == RRING) {
+            rslot = 0;
+            rphase ^= 1u;
         }
         if (slab_pending) slab_store(slab_nz);
         __syncthreads();
     };
+    // pairs of steps without a conditional second step (no register moves on the back edge),
+    // then the odd last step
+    int k = kfirst;
 #pragma unroll 1
-    for (int k = kfirst; k <= klast; k += 2) {
+    for (; k + 1 <= klast; k += 2) {
         step(Par<0>{}, k);
-        if (k + 1 <= klast) step(Par<1>{}, k + 1);
+        step(Par<1>{}, k + 1);
     }
+    if (k <= klast) step(Par<0>{}, k);
     pdl_trigger();  // the finalize may be scheduled while the tiles flush
     // ---- flush: pending y collapse, then the last two nodal planes
-    if (ypend >= 0) ycollapse(ypend);
+    if (ypend >= 0) ystage(ypend);
     __syncthreads();
-    xcollapse(acc00, acc01, acc02);
+    xstage(acc00, acc01, acc02);
     __syncthreads();
-    ycollapse(cur);
+    ystage(cur);
     __syncthreads();
-    xcollapse(acc10, acc11, acc12);
+    xstage(acc10, acc11, acc12);
     __syncthreads();
-    ycollapse(cur + 1);
-#undef HV2_ISSUE
+    ystage(cur + 1);
+#undef HV2_ISSUE_D
+#undef HV2_ISSUE_R
 }
 
 }  // namespace
 
 namespace {
-template <typename Real>
-std::size_t smem_bytes(int nlx, int nsl, int zc) {
-    using G = Geo<Real>;
-    const std::size_t ring = static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 32;
-    const std::size_t dbl = static_cast<std::size_t>(NSL) * nsl * sizeof(Real) + (TY + zc + 8) * sizeof(double);
-    const std::size_t real = (2 * static_cast<std::size_t>(G::NS) + 2 * 2 * NT + 2 * 2 * TY + 2 + 6 * NX_P +
-                              3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real);
-    return ring + dbl + real + (TY + zc + 8) * sizeof(int);
+template <typename Real, int TY_>
+std::size_t smem_bytes(int nlx, int nly, int segw, int zc, int nsl) {
+    using G = Geo<Real, TY_>;
+    using T = Tl<TY_>;
+    const std::size_t ring = (static_cast<std::size_t>(DRING) * G::SLOT_DT + RRING * G::SLOT_RH) * sizeof(Real) + 64;
+    const std::size_t dbl = (zc + 8) * sizeof(double);
+    const std::size_t real = (static_cast<std::size_t>(MFREG_HV2_SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * 2 * T::NT + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
+                              static_cast<std::size_t>(T::TY) * xrow_len(nlx) +
+                              static_cast<std::size_t>(nlx) * xwin(segw) + static_cast<std::size_t>(nly) * T::TY) *
+                             sizeof(Real);
+    return ring + dbl + real + (zc + 8 + 4 * nlx + T::NX_P) * sizeof(int);
 }
 }  // namespace
 
-// fp32 = true: the Hv state (dT, rho-hat) and the arithmetic in single precision (FAST32 mode)
-std::size_t hv2_smem_bytes(int nlx, int nsl, int zc, bool fp32) {
-    return fp32 ? smem_bytes<float>(nlx, nsl, zc) : smem_bytes<double>(nlx, nsl, zc);
+// fp32 = true: the Hv state (dT, rho-hat) and the arithmetic in single precision (FAST32 mode);
+// ty = tile height (8: two CTAs per SM, 16: one)
+std::size_t hv2_smem_bytes(int nlx, int nly, int segw, int zc, int nsl, bool fp32, int ty) {
+    if (ty == 16)
+        return fp32 ? smem_bytes<float, 16>(nlx, nly, segw, zc, nsl) : smem_bytes<double, 16>(nlx, nly, segw, zc, nsl);
+    return fp32 ? smem_bytes<float, 8>(nlx, nly, segw, zc, nsl) : smem_bytes<double, 8>(nlx, nly, segw, zc, nsl);
+}
+int hv2_nsl_max(int ty) { return 2 * TX * ty; }  // footprint elements: <= 2 per thread
+
+int hv2_nlx_max() { return 42; }  // x items of a row in <= 4 warp passes
+int hv2_threads(int ty) { return TX * ty; }
+int hv2_box_origin(bool fp32) { return fp32 ? Geo<float, 8>::XO : Geo<double, 8>::XO; }
+
+void hv2_set_smem_cap(int bytes, int ty) {
+    if (ty == 16) {
+        MFREG_CUDA(cudaFuncSetAttribute(k_hv2<double, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        MFREG_CUDA(cudaFuncSetAttribute(k_hv2<float, 16>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+        return;
+    }
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<double, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<float, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-int hv2_nsl_max() { return 2 * NT; }
-int hv2_ring_planes() { return NSL; }
-int hv2_threads() { return NT; }
-int hv2_box_origin(bool fp32) { return fp32 ? Geo<float>::XO : Geo<double>::XO; }
-
-void hv2_set_smem_cap(int bytes) {
-    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    MFREG_CUDA(cudaFuncSetAttribute(k_hv2<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-}
-
-void hv2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32) {
-    if (fp32) launch_pdl(k_hv2<float>, grid, dim3(NT), smem, s, a, maps);
-    else launch_pdl(k_hv2<double>, grid, dim3(NT), smem, s, a, maps);
+void hv2_launch(const FArgs& a, const TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32, int ty) {
+    if (ty == 16) {
+        if (fp32) launch_pdl(k_hv2<float, 16>, grid, dim3(TX * 16), smem, s, a, maps);
+        else launch_pdl(k_hv2<double, 16>, grid, dim3(TX * 16), smem, s, a, maps);
+        return;
+    }
+    if (fp32) launch_pdl(k_hv2<float, 8>, grid, dim3(TX * 8), smem, s, a, maps);
+    else launch_pdl(k_hv2<double, 8>, grid, dim3(TX * 8), smem, s, a, maps);
 }
 
 }  // namespace mfreg_b200

@@ -21,10 +21,11 @@ def max_rel(a, b):
     return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300))
 
 
-VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0", "MFREG_HV4": "0"},
-            "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "0"},
-            "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1", "MFREG_HV4": "0"},
-            "hv4": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "1"}}
+VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "0"},
+            "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "0"},
+            "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1", "MFREG_HV4": "0", "MFREG_HV16": "0"},
+            "hv4": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "1", "MFREG_HV16": "0"},
+            "hv16": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "1"}}
 
 
 def _objective(P, R, T, m, h, ratio, variant):
@@ -62,7 +63,7 @@ def test_hv_kernel_variants(P, oracle, case):
         j = obj.eval(y, g)
         q = obj.gn_hessian_vec(p)
         q2 = obj.gn_hessian_vec(p)
-        assert np.array_equal(q, q2)  # deterministic
+        assert np.array_equal(q, q2), (legacy, max_rel(q, q2))  # deterministic
         assert max_rel(j, J) <= FAST_TOL and max_rel(g, grad) <= FAST_TOL
         assert max_rel(q, hv) <= FAST_TOL, (legacy, max_rel(q, hv))
         j2 = obj.eval(y, None)  # value-only eval refreshes the same state
