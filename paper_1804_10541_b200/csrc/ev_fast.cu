@@ -22,7 +22,7 @@
 // the volume boundary are masked to zero, coefficients outside are zero.
 #include <cstdint>
 
-#include "fused_dev.cuh"
+#include "ptc.cuh"
 
 #ifndef MFREG_REVMAP
 #define MFREG_REVMAP 1
@@ -128,15 +128,15 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     const int segw = a.segw;
     const bool grad = a.grad != 0;
 
-    // ---- shared memory: ring | barriers | row tables, reduction (fp64) | fluxes, x-collapsed rows (Real) | ints
+    // ---- shared memory: ring | barriers | reduction (fp64) | fluxes, P^T buffers (Real) | ints
     Real* const stg = reinterpret_cast<Real*>(smem_raw);
     unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (48 B)
-    double* const sry = reinterpret_cast<double*>(bars + 6);  // [TY]
-    double* const sred = sry + TY;              // [NT / 32]
+    double* const sred = reinterpret_cast<double*>(bars + 6);  // [NT / 32]
     Real* const sF = reinterpret_cast<Real*>(sred + NT / 32);  // [2][2][NT] consumer-indexed y fluxes
     Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
-    Real* const sQx = sE + 2 * 2 * TY;          // [3][TY][nlx]
-    int* const sby = reinterpret_cast<int*>(sQx + 3 * TY * nlx);  // [TY]
+    Real* const sPt = sE + 2 * 2 * TY;          // P^T collapse buffers and tables (ptc.cuh)
+    int* const sI1 = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw));  // [NX_A] packed item 1
+    Ptc<Real, TY> ptc(sPt, sI1 + NX_A, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned bar0 = smem_u32(bars);
 
     // ---- columns: item 0 = tile column (lane, row); item 1 (threads < 80) = ring-1 edge column
@@ -144,38 +144,30 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     const int c0 = (tx + XO) + (ty + 2) * SX;
     const int gx0 = x0 + tx, gy0 = y0 + ty;
     const bool w1 = tid < NX_A;
-    int lx1 = XO, ly1 = 2, dir1 = 0;
-    if (w1) edge_item<XO>(tid, lx1, ly1, dir1);
-    const int c1 = lx1 + ly1 * SX;
-    const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
-    const bool xedge = dir1 == 0 || dir1 == 1;
-    const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
-                         : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+    // item-1 geometry packed once into shared memory and re-read per step (cheaper than keeping it
+    // live across the plane loop): bits 0-9 the box index c1, 10-19 the flux slot f1, 20-21 the
+    // direction toward the tile, 22 x edge, 23-26 the in-volume neighbour masks (-x, +x, -y, +y),
+    // 27 the column inside the volume
+    if (w1) {
+        int lx1 = XO, ly1 = 2, dir1 = 0;
+        edge_item<XO>(tid, lx1, ly1, dir1);
+        const int gx1 = x0 - XO + lx1, gy1 = y0 - 2 + ly1;
+        const bool xedge = dir1 == 0 || dir1 == 1;
+        const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
+                             : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+        static_assert(NS <= 1024 && 2 * NT <= 1024, "item-1 packing");
+        sI1[tid] = (lx1 + ly1 * SX) | (f1 << 10) | (dir1 << 20) | (xedge ? 1 << 22 : 0) | (gx1 > 0 ? 1 << 23 : 0) |
+                   (gx1 + 1 < mx ? 1 << 24 : 0) | (gy1 > 0 ? 1 << 25 : 0) | (gy1 + 1 < my ? 1 << 26 : 0) |
+                   (gx1 >= 0 && gx1 < mx && gy1 >= 0 && gy1 < my ? 1 << 27 : 0);
+    }
     // boundary masks of the in-plane differences (reference clamped neighbours) and
-    // "inside the volume" flags of the two columns
+    // "inside the volume" flag of the tile column
     const Real m0xm = gx0 > 0 ? Real(1) : Real(0), m0xp = gx0 + 1 < mx ? Real(1) : Real(0);
     const Real m0ym = gy0 > 0 ? Real(1) : Real(0), m0yp = gy0 + 1 < my ? Real(1) : Real(0);
-    const Real m1xm = gx1 > 0 ? Real(1) : Real(0), m1xp = gx1 + 1 < mx ? Real(1) : Real(0);
-    const Real m1ym = gy1 > 0 ? Real(1) : Real(0), m1yp = gy1 + 1 < my ? Real(1) : Real(0);
     const bool in0 = gx0 < mx && gy0 < my;
-    const bool in1c = gx1 >= 0 && gx1 < mx && gy1 >= 0 && gy1 < my;
     const long long col0 = in0 ? static_cast<long long>(gx0) + static_cast<long long>(gy0) * mx : 0;
 
-    // x collapse geometry (as k_hv2)
-    const int gxc0 = min(gx0, mx - 1);
-    const bool xin = gx0 < mx, xlast = gx0 == xe - 1;
-    const int bx = xin ? __ldg(&a.P.base[0][gxc0]) - nxA : 1024 + lane;
-    const Real rxq = __ldg(&a.P.rem[0][gxc0]);
-    const int bx_prev = __shfl_up_sync(0xffffffffu, bx, 1);
-    const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != bx);
-    const int sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
-    const bool send = lane == 31 || ((starts >> (lane + 1)) & 1u);
-
-    if (tid < TY) {
-        const int gyc = min(y0 + tid, my - 1);
-        sby[tid] = __ldg(&a.P.base[1][gyc]) - nyA;
-        sry[tid] = __ldg(&a.P.rem[1][gyc]);
-    }
+    ptc.build_tables(a, tid, NT, x0, y0, nxA, nyA, tm.nly);
     if (tid == 0) {
         for (int b = 0; b < RING; ++b) mbar_init(&bars[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -196,55 +188,14 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         }                                                                          \
     } while (0)
 
-    auto xcollapse = [&](Real v0, Real v1, Real v2) {
-        Real* dst = sQx + row * nlx;
-        Real A[3] = {(Real(1) - rxq) * v0, (Real(1) - rxq) * v1, (Real(1) - rxq) * v2};
-        Real B[3] = {rxq * v0, rxq * v1, rxq * v2};
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            if (o >= segw) break;  // uniform
-            const bool in = lane - o >= sst;
-#pragma unroll
-            for (int d = 0; d < 3; ++d) {
-                const Real ua = __shfl_up_sync(0xffffffffu, A[d], o);
-                const Real ub = __shfl_up_sync(0xffffffffu, B[d], o);
-                A[d] = in ? A[d] + ua : A[d];
-                B[d] = in ? B[d] + ub : B[d];
-            }
-        }
-#pragma unroll
-        for (int d = 0; d < 3; ++d) {
-            const Real bp = __shfl_sync(0xffffffffu, B[d], max(sst - 1, 0));
-            if (send && xin) {
-                dst[d * TY * nlx + bx] = sst > 0 ? A[d] + bp : A[d];
-                if (xlast) dst[d * TY * nlx + bx + 1] = B[d];
-            }
-        }
-    };
-    const int nyi = 3 * nly_t * nlx_t;
-    // the y collapse (and the nodal-plane loads) run on the highest threads: the halo items sit on
-    // the lowest ones, so this evens out the warps' work between barriers
-    const int rtid = MFREG_REVMAP ? NT - 1 - tid : tid;
-    auto ycollapse = [&](int nzp) {
-        if (rtid < nyi) {
-            const int lxn = rtid % nlx_t, lyn = (rtid / nlx_t) % nly_t, d = rtid / (nlx_t * nly_t);
-            const Real* q = sQx + d * TY * nlx + lxn;
-            Real v = 0.0;
-#pragma unroll
-            for (int r = 0; r < TY; ++r) {
-                const int b = sby[r];
-                const Real ry = sry[r];
-                const Real wgt = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
-                v = fma(wgt, q[r * nlx], v);
-            }
-            part[static_cast<std::size_t>(nzp - nzA) * pstride + (lyn * nlx + lxn) * 3 + d] = v;
-        }
-    };
+    auto xcollapse = [&](Real v0, Real v1, Real v2) { ptc.xstage(row, lane, v0, v1, v2); };
+    auto ycollapse = [&](int nzp) { ptc.ystage(row, lane, part + static_cast<std::size_t>(nzp - nzA) * pstride); };
     auto zbase = [&](int k) { return __ldg(&a.P.base[2][min(max(k, 0), mz - 1)]); };
     auto zrem = [&](int k) { return __ldg(&a.P.rem[2][min(max(k, 0), mz - 1)]); };
 
     pdl_wait();       // T_w, dT (the warp kernel before this launch) from here on
     __syncthreads();  // tables, barriers
+    ptc.build_items(tid, NT);
     for (int m = 0; m < RING - 2; ++m)
         if (kfirst + m <= klast) EV2_ISSUE(kfirst + m, m);
     int slot = 0, slot_prev = RING - 1;  // ring slots of this step and the previous one
@@ -305,6 +256,10 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
             sw_new = (((cf.e[0] + cf.e[1]) + (cf.e[2] + cf.e[3])) + (cf.e[4] + cf.e[5])) * r;
         }
         if (w1) {  // ring-1 edge column: the flux toward the tile
+            const int e1 = lds_v(sI1 + tid), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff, dir1 = (e1 >> 20) & 3;
+            const Real m1xm = (e1 >> 23) & 1 ? Real(1) : Real(0), m1xp = (e1 >> 24) & 1 ? Real(1) : Real(0);
+            const Real m1ym = (e1 >> 25) & 1 ? Real(1) : Real(0), m1yp = (e1 >> 26) & 1 ? Real(1) : Real(0);
+            const bool in1c = (e1 >> 27) & 1;
             const Real Rj = sp[SLOT_R + c1], Tj = sp[SLOT_T + c1];
             const Real Rp = st[SLOT_R + c1], Tp = st[SLOT_T + c1];
             const Coef cf = ngf_coef(a, m1xm * (sp[SLOT_R + c1 - 1] - Rj), m1xp * (sp[SLOT_R + c1 + 1] - Rj),
@@ -316,7 +271,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
             Rm1 = Rj;
             Tm1 = Tj;
             const Real e = dir1 == 0 ? cf.e[1] : (dir1 == 1 ? cf.e[0] : (dir1 == 2 ? cf.e[3] : cf.e[2]));
-            if (xedge) sE[(1 - P) * 2 * TY + f1] = e * cf.r;
+            if ((e1 >> 22) & 1) sE[(1 - P) * 2 * TY + f1] = e * cf.r;
             else sF[(1 - P) * 2 * NT + f1] = e * cf.r;
         }
         // ---- Z: plane i = k-2 (tile columns): gradient -2h dT (dr^T r) -> P^T
@@ -357,11 +312,14 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         }
         __syncthreads();
     };
+    // pairs of steps without a conditional second step, then the odd last step
+    int k = kfirst;
 #pragma unroll 1
-    for (int k = kfirst; k <= klast; k += 2) {
+    for (; k + 1 <= klast; k += 2) {
         step(Par<0>{}, k);
-        if (k + 1 <= klast) step(Par<1>{}, k + 1);
+        step(Par<1>{}, k + 1);
     }
+    if (k <= klast) step(Par<0>{}, k);
 #undef EV2_ISSUE
     pdl_trigger();  // the finalize may be scheduled while the tiles flush
     if (grad) {  // flush: pending y collapse, then the last two nodal planes
@@ -519,14 +477,17 @@ __global__ void __launch_bounds__(NT) k_ev_value(const __grid_constant__ FArgs a
 
 namespace {
 template <typename Real>
-std::size_t smem_bytes(int nlx) {
+std::size_t smem_bytes(int nlx, int nly, int segw) {
     using G = Geo<Real>;
-    return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 48 + (TY + NT / 32) * sizeof(double) +
-           (2 * 2 * NT + 2 * 2 * TY + 3 * static_cast<std::size_t>(TY) * nlx) * sizeof(Real) + TY * sizeof(int);
+    return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 48 + (NT / 32) * sizeof(double) +
+           (2 * 2 * NT + 2 * 2 * TY + static_cast<std::size_t>(ptc_reals(TY, nlx, nly, segw))) * sizeof(Real) +
+           (NX_A + ptc_ints(nlx)) * sizeof(int);
 }
 }  // namespace
 
-std::size_t ev2_smem_bytes(int nlx, bool fp32) { return fp32 ? smem_bytes<float>(nlx) : smem_bytes<double>(nlx); }
+std::size_t ev2_smem_bytes(int nlx, int nly, int segw, bool fp32) {
+    return fp32 ? smem_bytes<float>(nlx, nly, segw) : smem_bytes<double>(nlx, nly, segw);
+}
 
 void ev2_set_smem_cap(int bytes) {
     MFREG_CUDA(cudaFuncSetAttribute(k_ev2<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));

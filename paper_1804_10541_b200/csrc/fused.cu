@@ -36,7 +36,7 @@ bool hv3_fp32_ok();
 void hv3_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32,
                 bool stored);
 // ev_fast.cu
-std::size_t ev2_smem_bytes(int nlx, bool fp32);
+std::size_t ev2_smem_bytes(int nlx, int nly, int segw, bool fp32);
 void ev2_set_smem_cap(int bytes);
 void ev_value_launch(const fdev::FArgs& a, const void* R, const void* Tw, dim3 grid, cudaStream_t s, bool fp32);
 void ev2_launch(const fdev::FArgs& a, const fdev::TmaMaps& maps, dim3 grid, std::size_t smem, cudaStream_t s, bool fp32);
@@ -1080,9 +1080,9 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     // (process-wide per-kernel cap: always the 2-CTA bound, so plans never lower each other's)
     if (hv2_) hv2_set_smem_cap(kSmem2Cta, 8);
     // two-CTA/SM eval kernel (ev_fast.cu): same conditions
-    ev2_smem_ = ev2_smem_bytes(t.nlx, fp32_);
+    ev2_smem_ = ev2_smem_bytes(t.nlx, t.nly, segw_, fp32_);
     const char* noe = std::getenv("MFREG_NO_EV2");
-    ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && 3 * t.nlx * t.nly <= hv2_threads(8) && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
+    ev2_ = tma_ && zok && (fp32_ || !(noe && noe[0] == '1')) && t.nlx <= hv2_nlx_max() && ev2_smem_ <= static_cast<std::size_t>(kSmem2Cta);
     if (ev2_) ev2_set_smem_cap(kSmem2Cta);
     setup_hv3(plan, R, Tw, dT, frh, zok, max_optin);
     // FAST32 runs only on the two-CTA kernels (the legacy fused kernels are fp64)

@@ -29,7 +29,7 @@
 // outside the volume, and the eval pass stores zero coefficients across it.
 #include <cstdint>
 
-#include "fused_dev.cuh"
+#include "ptc.cuh"
 
 #ifndef MFREG_REVMAP
 #define MFREG_REVMAP 1
@@ -109,14 +109,12 @@ struct Par {
     static constexpr int P = P_;
 };
 
-// P^T collapse buffers: a row holds three components of 32 columns, then the x-collapsed nodes
-// in place (3 nlx); a node's x window spans two nodal cells
-__host__ __device__ constexpr int xrow_len(int nlx) { return 3 * nlx > 3 * TX ? 3 * nlx : 3 * TX; }
-__host__ __device__ constexpr int xwin(int segw) { return 2 * segw < TX ? 2 * segw : TX; }
-
 template <typename Real, int TY_>
 __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
     using G = Geo<Real, TY_>;
+    // FAST32 keeps the nodal footprint in shared memory (its smem has room; the L1/L2 reads of the
+    // interpolants at a plane change stall it); fp64 reads them from L1/L2 (no room for the ring)
+    constexpr bool SLAB = MFREG_HV2_SLAB || sizeof(Real) == 4;
     constexpr int TY = TY_, SY = Tl<TY_>::SY, NT = Tl<TY_>::NT, NX_W = Tl<TY_>::NX_W, NX_P = Tl<TY_>::NX_P;
     (void)SY;
     constexpr int XO = G::XO, SX = G::SX, NS = G::NS, NW = G::NW, SLOT_DT = G::SLOT_DT, SLOT_RH = G::SLOT_RH;
@@ -148,22 +146,16 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     double* const sZr = reinterpret_cast<double*>(bars + 8);  // [zc + 8] rem_z of the planes kfirst ..
     const int nxf = a.nxf, nyf = a.nyf, pl = nxf * nyf, nsl = 3 * pl;
     Real* const slab = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [NSL][3][nyf][nxf] nodal p footprint
-    Real* const sS = slab + (MFREG_HV2_SLAB ? NSL * nsl : 0);  // [2][NS] by plane parity
+    Real* const sS = slab + (SLAB ? NSL * nsl : 0);  // [2][NS] by plane parity
     Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
     Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
                                                 // then 2 zero entries (the edge-flux slot of inner lanes)
     Real* const sQ1 = sE + 2 * 2 * TY + 2;      // [6][NX_P] item-1 P p at nodal planes bz, bz+1
-    // P^T of a completed nodal plane: each warp stores its row's z-weighted sums [3][32] in sA and
-    // collapses x in place (node j of component d at d * nlx_t + j); one step later the y collapse
-    // reads every row (completions are >= 2 steps apart)
-    const int XR = xrow_len(nlx), WXP = xwin(segw);
-    Real* const sA = sQ1 + 6 * NX_P;            // [TY][XR]
-    Real* const sWx = sA + TY * XR;             // [nlx][WXP] x weights of node j over columns sXs[j] ..
-    Real* const sWy = sWx + nlx * WXP;          // [nly][TY] y weights of node row lyn over the tile rows
-    int* const sZb = reinterpret_cast<int*>(sWy + tm.nly * TY);  // [zc + 8] base_z of the planes kfirst ..
-    int* const sXs = sZb + tm.zc + 8;           // [nlx] first column of node j's x window
-    int* const sXi = sXs + nlx;                 // [3 nlx] x item L: window offset | weight offset << 8 | (d, j)
-    int* const sI1 = sXi + 3 * nlx;             // [NX_P] packed item-1 geometry
+    // P^T collapse buffers and tables (ptc.cuh)
+    Real* const sPt = sQ1 + 6 * NX_P;
+    int* const sZb = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw));  // [zc + 8] base_z of planes kfirst ..
+    int* const sI1 = sZb + tm.zc + 8;           // [NX_P] packed item-1 geometry
+    Ptc<Real, TY> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned barD = smem_u32(bars), barR = barD + 8 * DRING;
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
@@ -195,12 +187,12 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     auto col_geom = [&](int gx, int gy, int& off, double& rx, double& ry) {
         const int gxc = min(max(gx, 0), mx - 1), gyc = min(max(gy, 0), my - 1);
         const int bx = __ldg(&a.P.base[0][gxc]), by = __ldg(&a.P.base[1][gyc]);
-        off = MFREG_HV2_SLAB ? (bx - fx0) + (by - fy0) * nxf : bx + by * static_cast<int>(sm0);
+        off = SLAB ? (bx - fx0) + (by - fy0) * nxf : bx + by * static_cast<int>(sm0);
         rx = __ldg(&a.P.rem[0][gxc]);
         ry = __ldg(&a.P.rem[1][gyc]);
     };
     auto bilerp = [&](int nz, int off, Real rx, Real ry, Real& o0, Real& o1, Real& o2) {
-        if constexpr (MFREG_HV2_SLAB) {
+        if constexpr (SLAB) {
             const Real* q = slab + (nz & (NSL - 1)) * nsl + off;
             o0 = lerp(ry, lerp(rx, q[0], q[1]), lerp(rx, q[nxf], q[nxf + 1]));
             o1 = lerp(ry, lerp(rx, q[pl], q[pl + 1]), lerp(rx, q[pl + nxf], q[pl + nxf + 1]));
@@ -231,14 +223,14 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         }
     }
     auto slab_load = [&](int nz) {
-        if constexpr (!MFREG_HV2_SLAB) return;
+        if constexpr (!SLAB) return;
         const double* q = a.p + static_cast<long long>(nz) * sm01;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
             if (sl_off[u] >= 0) sl_v[u] = static_cast<Real>(__ldg(q + sl_off[u]));
     };
     auto slab_store = [&](int nz) {
-        if constexpr (!MFREG_HV2_SLAB) return;
+        if constexpr (!SLAB) return;
         Real* dst = slab + (nz & (NSL - 1)) * nsl;
 #pragma unroll
         for (int u = 0; u < 2; ++u)
@@ -250,40 +242,8 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     const int eoff = tx == 0 ? ty : (tx == TX - 1 ? TY + ty : -1);
     const Real mpx = tx > 0 ? Real(1) : Real(0), mmx = tx + 1 < TX ? Real(1) : Real(0);
 
-    // P^T collapse tables: node j (x) takes columns of cell j-1 with weight rem_x and of cell j
-    // with 1 - rem_x, a window of <= WXP columns starting at sXs[j]; node row lyn (y) takes the tile
-    // rows of cell lyn-1 with rem_y and of cell lyn with 1 - rem_y. Columns / rows past the volume
-    // weigh 0 (their sums are 0 as well: dT vanishes there).
     if (tid < 2) sE[4 * TY + tid] = Real(0);
-    const int nxi = 3 * nlx_t;  // x items (d, j) per row
-    if (tid < nlx_t) {
-        const int j = tid;
-        int lo = TX;
-        for (int c = TX - 1; c >= 0; --c)
-            if (x0 + c < mx && __ldg(&a.P.base[0][x0 + c]) - nxA >= j - 1) lo = c;
-        const int st = max(0, min(lo, TX - WXP));
-        sXs[j] = st;
-        for (int t = 0; t < WXP; ++t) {
-            const int c = st + t, gx = x0 + c;
-            Real w = Real(0);
-            if (gx < mx) {
-                const int b = __ldg(&a.P.base[0][gx]) - nxA;
-                const Real r = static_cast<Real>(__ldg(&a.P.rem[0][gx]));
-                w = b == j ? Real(1) - r : (b == j - 1 ? r : Real(0));
-            }
-            sWx[j * WXP + t] = w;
-        }
-    }
-    for (int t = tid; t < tm.nly * TY; t += NT) {
-        const int lyn = t / TY, r = t % TY, gy = y0 + r;
-        Real w = Real(0);
-        if (gy < my && lyn < nly_t) {
-            const int b = __ldg(&a.P.base[1][gy]) - nyA;
-            const Real ry = static_cast<Real>(__ldg(&a.P.rem[1][gy]));
-            w = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
-        }
-        sWy[t] = w;
-    }
+    ptc.build_tables(a, tid, NT, x0, y0, nxA, nyA, tm.nly);
     for (int t = tid; t < tm.zc + 8; t += NT) {
         const int kk = min(max(z0 - 2 + t, 0), mz - 1);
         sZb[t] = __ldg(&a.P.base[2][kk]);
@@ -319,65 +279,15 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     auto zbase = [&](int k) { return sZb[k - kfirst]; };  // k in [kfirst, klast + 3]
     auto zrem = [&](int k) { return sZr[k - kfirst]; };
 
-    // x collapse of one completed nodal plane, in place in the warp's row of sA
-    const int npx = (nxi + 31) >> 5;  // passes over the x items (host: nlx <= 42)
-    auto xstage = [&](Real v0, Real v1, Real v2) {
-        Real* ar = sA + row * XR;
-        ar[lane] = v0;
-        ar[32 + lane] = v1;
-        ar[64 + lane] = v2;
-        __syncwarp();
-        Real o[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int L = lane + 32 * u;
-            o[u] = Real(0);
-            if (u < npx && L < nxi) {
-                const int e = sXi[L];
-                const Real* v = ar + (e & 0xff);
-                const Real* w = sWx + ((e >> 8) & 0xfff);
-                Real acc0 = Real(0), acc1 = Real(0);  // WXP is even: two chains
-#pragma unroll 2
-                for (int t = 0; t < WXP; t += 2) {
-                    acc0 = fma(w[t], v[t], acc0);
-                    acc1 = fma(w[t + 1], v[t + 1], acc1);
-                }
-                o[u] = acc0 + acc1;
-            }
-        }
-        __syncwarp();
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int L = lane + 32 * u;
-            if (u < npx && L < nxi) ar[L] = o[u];
-        }
-    };
-    // y collapse of the x-collapsed rows into the tile partial of nodal plane nzp (node rows on the
-    // highest warps: the halo items sit on the lowest ones)
-    auto ystage = [&](int nzp) {
-        Real* const pz = part + static_cast<std::size_t>(nzp - nzA) * pstride;
-        for (int lyn = MFREG_REVMAP ? TY - 1 - row : row; lyn < nly_t; lyn += TY) {
-            const Real* w = sWy + lyn * TY;
-            for (int L = lane; L < nxi; L += 32) {
-                const int e = sXi[L];
-                const int j = (e >> 20) & 0x3f, d = e >> 26;
-                Real v = Real(0);
-#pragma unroll
-                for (int r = 0; r < TY; ++r) v = fma(w[r], sA[r * XR + L], v);
-                pz[(lyn * nlx + j) * 3 + d] = v;
-            }
-        }
-    };
+    auto xstage = [&](Real v0, Real v1, Real v2) { ptc.xstage(row, lane, v0, v1, v2); };
+    auto ystage = [&](int nzp) { ptc.ystage(row, lane, part + static_cast<std::size_t>(nzp - nzA) * pstride); };
 
     pdl_wait();       // p (the CG update before this launch) from here on
     __syncthreads();  // tables, barriers
     // first two nodal planes, synchronously; first two staged planes
     // (the planes steps kfirst .. kfirst+2 read; later steps prefetch one plane each,
     // the host guarantees base_z advances by <= 1 per plane and <= 2 per 3 planes)
-    for (int L = tid; L < nxi; L += NT) {
-        const int d = L / nlx_t, j = L - d * nlx_t;
-        sXi[L] = (d * 32 + sXs[j]) | ((j * WXP) << 8) | (j << 20) | (d << 26);
-    }
+    ptc.build_items(tid, NT);
     int slab_hi;
     {
         const int nz0 = zbase(kfirst);
@@ -416,7 +326,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         int slab_nz = 0;
         {
             const int nzq = min(zbase(k + 3) + 1, msz - 1);
-            if (MFREG_HV2_SLAB && nzq > slab_hi) {  // uniform
+            if (SLAB && nzq > slab_hi) {  // uniform
                 slab_load(nzq);
                 slab_pending = true;
                 slab_nz = nzq;
@@ -586,11 +496,11 @@ std::size_t smem_bytes(int nlx, int nly, int segw, int zc, int nsl) {
     using T = Tl<TY_>;
     const std::size_t ring = (static_cast<std::size_t>(DRING) * G::SLOT_DT + RRING * G::SLOT_RH) * sizeof(Real) + 64;
     const std::size_t dbl = (zc + 8) * sizeof(double);
-    const std::size_t real = (static_cast<std::size_t>(MFREG_HV2_SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * 2 * T::NT + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
-                              static_cast<std::size_t>(T::TY) * xrow_len(nlx) +
-                              static_cast<std::size_t>(nlx) * xwin(segw) + static_cast<std::size_t>(nly) * T::TY) *
+    constexpr bool SLAB = MFREG_HV2_SLAB || sizeof(Real) == 4;
+    const std::size_t real = (static_cast<std::size_t>(SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * 2 * T::NT + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
+                              ptc_reals(T::TY, nlx, nly, segw)) *
                              sizeof(Real);
-    return ring + dbl + real + (zc + 8 + 4 * nlx + T::NX_P) * sizeof(int);
+    return ring + dbl + real + (zc + 8 + ptc_ints(nlx) + T::NX_P) * sizeof(int);
 }
 }  // namespace
 

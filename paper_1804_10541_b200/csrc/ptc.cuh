@@ -1,0 +1,140 @@
+// P^T collapse of a fused pass's tile (k_hv2, k_ev2): every output column keeps the
+// z-weighted sums of its q^ for the two nodal z planes of its cell in registers; when a nodal plane
+// completes, its sums are spread over the tile's nodes in x and y:
+//  * x stage (per warp = tile row, right at the completion): the row's three components go to a
+//    shared row buffer, and lane L = (d, j) sums node j's window of <= WX columns (the columns of
+//    cell j-1 weighted rem_x, of cell j weighted 1 - rem_x) from a per-tile weight table, written
+//    back in place at position L (two FMA chains per item);
+//  * y stage (one step later, after the CTA barrier): node row lyn (a warp) sums the tile rows
+//    with a per-tile weight table and writes the tile partial of that nodal plane.
+// Replaces the segmented shuffle scan (fp64 shuffles are two SHFL + moves + selects per level and
+// value). Tables are built once per CTA; completions are >= 2 steps apart (host guarantee).
+#pragma once
+
+#include "fused_dev.cuh"
+
+namespace mfreg_b200 {
+namespace fdev {
+
+constexpr int kPtcTX = FT_X;
+
+__host__ __device__ constexpr int ptc_row_len(int nlx) { return 3 * nlx > 3 * kPtcTX ? 3 * nlx : 3 * kPtcTX; }
+__host__ __device__ constexpr int ptc_win(int segw) { return 2 * segw < kPtcTX ? 2 * segw : kPtcTX; }
+// shared-memory footprint: Reals (row buffers, weights) and ints (window starts, items)
+__host__ __device__ constexpr int ptc_reals(int ty, int nlx, int nly, int segw) {
+    return ty * ptc_row_len(nlx) + nlx * ptc_win(segw) + nly * ty;
+}
+__host__ __device__ constexpr int ptc_ints(int nlx) { return 4 * nlx; }
+
+template <typename Real, int TY>
+struct Ptc {
+    Real* sA;   // [TY][XR] row buffers
+    Real* sWx;  // [nlx][WX] x weights of node j over columns xs[j] ..
+    Real* sWy;  // [nly][TY] y weights of node row lyn over the tile rows
+    int* sXs;   // [nlx] first column of node j's window
+    int* sXi;   // [3 nlx] item L = d * nlx_t + j: window offset | weight offset << 8 | j << 20 | d << 26
+    int XR, WX, nxi, nlx, nly_t;
+
+    __device__ Ptc(Real* reals, int* ints, int nlx_, int nly_, int segw, int nlx_t, int nly_t_)
+        : XR(ptc_row_len(nlx_)), WX(ptc_win(segw)), nxi(3 * nlx_t), nlx(nlx_), nly_t(nly_t_) {
+        sA = reals;
+        sWx = sA + TY * XR;
+        sWy = sWx + nlx_ * WX;
+        sXs = ints;
+        sXi = sXs + nlx_;
+        (void)nly_;
+    }
+
+    // weight tables (before the CTA's first barrier)
+    __device__ void build_tables(const FArgs& a, int tid, int nthreads, int x0, int y0, int nxA, int nyA, int nly) {
+        const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]);
+        const int nlx_t = nxi / 3;
+        if (tid < nlx_t) {
+            const int j = tid;
+            int lo = kPtcTX;
+            for (int c = kPtcTX - 1; c >= 0; --c)
+                if (x0 + c < mx && __ldg(&a.P.base[0][x0 + c]) - nxA >= j - 1) lo = c;
+            const int st = max(0, min(lo, kPtcTX - WX));
+            sXs[j] = st;
+            for (int t = 0; t < WX; ++t) {
+                const int gx = x0 + st + t;
+                Real w = Real(0);
+                if (gx < mx) {
+                    const int b = __ldg(&a.P.base[0][gx]) - nxA;
+                    const Real r = static_cast<Real>(__ldg(&a.P.rem[0][gx]));
+                    w = b == j ? Real(1) - r : (b == j - 1 ? r : Real(0));
+                }
+                sWx[j * WX + t] = w;
+            }
+        }
+        for (int t = tid; t < nly * TY; t += nthreads) {
+            const int lyn = t / TY, r = t % TY, gy = y0 + r;
+            Real w = Real(0);
+            if (gy < my && lyn < nly_t) {
+                const int b = __ldg(&a.P.base[1][gy]) - nyA;
+                const Real ry = static_cast<Real>(__ldg(&a.P.rem[1][gy]));
+                w = b == lyn ? Real(1) - ry : (b == lyn - 1 ? ry : Real(0));
+            }
+            sWy[t] = w;
+        }
+    }
+    // item table (after the first barrier: reads sXs)
+    __device__ void build_items(int tid, int nthreads) {
+        const int nlx_t = nxi / 3;
+        for (int L = tid; L < nxi; L += nthreads) {
+            const int d = L / nlx_t, j = L - d * nlx_t;
+            sXi[L] = (d * kPtcTX + sXs[j]) | ((j * WX) << 8) | (j << 20) | (d << 26);
+        }
+    }
+    // x stage of tile row `row` (whole warp)
+    __device__ void xstage(int row, int lane, Real v0, Real v1, Real v2) const {
+        Real* ar = sA + row * XR;
+        ar[lane] = v0;
+        ar[kPtcTX + lane] = v1;
+        ar[2 * kPtcTX + lane] = v2;
+        __syncwarp();
+        const int npx = (nxi + 31) >> 5;  // host: nlx <= 42
+        Real o[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int L = lane + 32 * u;
+            o[u] = Real(0);
+            if (u < npx && L < nxi) {
+                const int e = sXi[L];
+                const Real* v = ar + (e & 0xff);
+                const Real* w = sWx + ((e >> 8) & 0xfff);
+                Real acc0 = Real(0), acc1 = Real(0);  // WX is even: two chains
+#pragma unroll 2
+                for (int t = 0; t < WX; t += 2) {
+                    acc0 = fma(w[t], v[t], acc0);
+                    acc1 = fma(w[t + 1], v[t + 1], acc1);
+                }
+                o[u] = acc0 + acc1;
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int L = lane + 32 * u;
+            if (u < npx && L < nxi) ar[L] = o[u];
+        }
+    }
+    // y stage into the tile partial of one nodal plane (node row lyn on warp TY-1-lyn: the halo
+    // items sit on the lowest warps)
+    __device__ void ystage(int row, int lane, Real* pz) const {
+        for (int lyn = TY - 1 - row; lyn < nly_t; lyn += TY) {
+            const Real* w = sWy + lyn * TY;
+            for (int L = lane; L < nxi; L += 32) {
+                const int e = sXi[L];
+                const int j = (e >> 20) & 0x3f, d = e >> 26;
+                Real v = Real(0);
+#pragma unroll
+                for (int r = 0; r < TY; ++r) v = fma(w[r], sA[r * XR + L], v);
+                pz[(lyn * nlx + j) * 3 + d] = v;
+            }
+        }
+    }
+};
+
+}  // namespace fdev
+}  // namespace mfreg_b200
