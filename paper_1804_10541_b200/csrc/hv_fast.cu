@@ -177,6 +177,9 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         static_assert(G::NS <= 1024 && 2 * NT <= 1024, "item-1 packing");
         sI1[tid] = (lx1 + ly1 * SX) | (max(f1, 0) << 10) | (ci << 20) | (xedge ? 1 << 22 : 0);
     }
+    // (FAST32 has registers to spare: it keeps the packed word in one instead of reloading it)
+    const int e1r = has1 ? sI1[tid] : 0;
+    auto item1 = [&]() { return sizeof(Real) == 8 ? lds_v(sI1 + tid) : e1r; };
 
     // P p: the tile's nodal footprint (nxf x nyf nodes from (fx0, fy0), clamped at the last node)
     // of four nodal planes in shared memory, each plane loaded one step before its first use (<= 2
@@ -345,7 +348,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             double rx0d, ry0d, rx1 = 0.0, ry1 = 0.0;
             col_geom(gx0, gy0, off0, rx0d, ry0d);
             if (has1) {
-                const int c1 = lds_v(sI1 + tid) & 0x3ff;
+                const int c1 = item1() & 0x3ff;
                 col_geom(x0 - XO + c1 % SX, y0 - 2 + c1 / SX, off1, rx1, ry1);
             }
             const Real rxq = static_cast<Real>(rx0d), ry0 = static_cast<Real>(ry0d);
@@ -377,7 +380,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         sS[P * NS + c0] = s0;
         Real s1 = 0.0;
         if (has1) {
-            const int c1 = lds_v(sI1 + tid) & 0x3ff;
+            const int c1 = item1() & 0x3ff;
             const Real* q1 = sQ1 + tid;
             s1 = fma(st[c1], lerp(rzk, q1[0], q1[3 * NX_P]),
                      fma(st[NS + c1], lerp(rzk, q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * lerp(rzk, q1[2 * NX_P], q1[5 * NX_P])));
@@ -406,7 +409,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             sw_new = sg * w;
         }
         if (w1) {  // ring-1 edge column: only the flux toward the tile
-            const int e1 = lds_v(sI1 + tid), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff;
+            const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff;
             const Real* rg = sr + c1 - SX;
             const Real sj = sh1[1 - P];
             const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
