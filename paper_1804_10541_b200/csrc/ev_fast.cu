@@ -24,6 +24,9 @@
 
 #include "ptc.cuh"
 
+#ifndef MFREG_EV2_EXP
+#define MFREG_EV2_EXP 0  // timing experiment only (wrong Hv state): 1 = no rho-hat stores
+#endif
 #ifndef MFREG_REVMAP
 #define MFREG_REVMAP 1
 #endif
@@ -130,7 +133,8 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
 
     // ---- shared memory: ring | barriers | reduction (fp64) | fluxes, P^T buffers (Real) | ints
     Real* const stg = reinterpret_cast<Real*>(smem_raw);
-    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(stg + RING * SLOT);  // [RING] (48 B)
+    Real* const sOut = stg + RING * SLOT;       // [2][6][TY][TX] rho-hat of the tile plane (TMA store)
+    unsigned long long* const bars = reinterpret_cast<unsigned long long*>(sOut + 2 * 6 * NT);  // [RING] (48 B)
     double* const sred = reinterpret_cast<double*>(bars + 6);  // [NT / 32]
     Real* const sF = reinterpret_cast<Real*>(sred + NT / 32);  // [2][2][NT] consumer-indexed y fluxes
     Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
@@ -218,6 +222,9 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
             ycollapse(ypend);
             ypend = -1;
         }
+        // rho-hat of plane k-2 (staged last step, published by the barrier) -> global by TMA
+        if (a.frh_tma && tid == 0 && k - 2 >= z0 && k - 2 < z1)
+            tma_store_4d(&maps.d, sOut + (1 - P) * 6 * NT, x0, y0, k - 2, 0);
         mbar_wait_at(bar0 + 8 * slot, phase);
         const Real* st = stg + slot * SLOT;       // plane k (R, T_w), dT of plane k-2
         const Real* sp = stg + slot_prev * SLOT;  // plane k-1 (R, T_w)
@@ -237,12 +244,18 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
                                      in0 && jin);
             Rm0 = Rj;
             Tm0 = Tj;
-            if (in0 && j >= z0 && j < z1) {  // Hv state of the tile voxel (none when value-only lazy)
-                const long long gi = col0 + static_cast<long long>(j) * plane;
-                if (frh_out)
+            if (j >= z0 && j < z1) {  // Hv state of the tile plane (none when value-only lazy)
+                if (a.frh_tma) {  // staged for the TMA store next step (it clips columns past the volume)
+                    Real* o = sOut + P * 6 * NT + tid;
+#pragma unroll
+                    for (int d = 0; d < 6; ++d) o[d * NT] = cf.e[d];
+                    tma_store_fence();
+                } else if (frh_out && in0) {
+                    const long long gi = col0 + static_cast<long long>(j) * plane;
 #pragma unroll
                     for (int d = 0; d < 6; ++d) frh_out[d * n + gi] = cf.e[d];
-                if (j >= ilo && j < ihi) dsum += fma(-static_cast<double>(cf.r), static_cast<double>(cf.r), 1.0);
+                }
+                if (in0 && j >= ilo && j < ihi) dsum += fma(-static_cast<double>(cf.r), static_cast<double>(cf.r), 1.0);
             }
             const Real r = cf.r;
             const Real fpx = __shfl_up_sync(0xffffffffu, cf.e[1] * r, 1);
@@ -305,6 +318,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         fzp[P] = fzp_new;
         sw = sw_new;
         gx = gx_new;
+        if (a.frh_tma && tid == 0) tma_store_wait_read();  // the staging buffer is rewritten next step
         slot_prev = slot;
         if (++slot == RING) {
             slot = 0;
@@ -321,6 +335,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     }
     if (k <= klast) step(Par<0>{}, k);
 #undef EV2_ISSUE
+    if (a.frh_tma && tid == 0) tma_store_wait_all();  // rho-hat complete before the grid ends
     pdl_trigger();  // the finalize may be scheduled while the tiles flush
     if (grad) {  // flush: pending y collapse, then the last two nodal planes
         if (ypend >= 0) ycollapse(ypend);
@@ -479,7 +494,8 @@ namespace {
 template <typename Real>
 std::size_t smem_bytes(int nlx, int nly, int segw) {
     using G = Geo<Real>;
-    return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 48 + (NT / 32) * sizeof(double) +
+    return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 2 * 6 * NT * sizeof(Real) + 48 +
+           (NT / 32) * sizeof(double) +
            (2 * 2 * NT + 2 * 2 * TY + static_cast<std::size_t>(ptc_reals(TY, nlx, nly, segw))) * sizeof(Real) +
            (NX_A + ptc_ints(nlx)) * sizeof(int);
 }

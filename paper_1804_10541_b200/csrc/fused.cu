@@ -1052,6 +1052,7 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     const bool aligned = (g.m[0] % 2 == 0) && (reinterpret_cast<std::uintptr_t>(R) % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(Tw) % 16 == 0) &&
                          (reinterpret_cast<std::uintptr_t>(dT) % 16 == 0) && (reinterpret_cast<std::uintptr_t>(frh) % 16 == 0);
+    frh_base_ = frh;
     const char* off = std::getenv("MFREG_NO_TMA");
     tma_ = aligned && (fp32 || !(off && off[0] == '1')) && make_tma_maps(g, R, Tw, dT, frh);
     // two-CTA/SM Hv kernel (hv_fast.cu): TMA only; the nodal z cells must span >= 2 image
@@ -1268,7 +1269,7 @@ bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, cons
         TmaMaps hv2{}, ev2{};
         const bool ok = encw(&hv2.a, dT, 4, 3, SXf, CY, 3, 4) && encw(&hv2.b, frh, 4, 6, SXf, C1Y, 6, 4) &&
                         encw(&ev2.a, R, 3, 1, SXf, CY, 1, 4) && encw(&ev2.b, Tw, 3, 1, SXf, CY, 1, 4) &&
-                        encw(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3, 4);
+                        encw(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3, 4) && encw(&ev2.d, frh, 4, 6, FT_X, FT_Y, 6, 4);
         if (!ok) return false;
         std::memcpy(maps_hv2_, &hv2, sizeof(TmaMaps));
         std::memcpy(maps_ev2_, &ev2, sizeof(TmaMaps));
@@ -1281,7 +1282,8 @@ bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, cons
               enc(&ev.b, Tw, 3, 1, CX, CY, 1) && enc(&ev.c, dT, 4, 3, CX, CY, 3);
     TmaMaps hv2{}, ev2{};
     ok = ok && enc(&hv2.a, dT, 4, 3, CX, CY, 3) && enc(&hv2.b, frh, 4, 6, CX, C1Y, 6);
-    ok = ok && enc(&ev2.a, R, 3, 1, CX, CY, 1) && enc(&ev2.b, Tw, 3, 1, CX, CY, 1) && enc(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3);
+    ok = ok && enc(&ev2.a, R, 3, 1, CX, CY, 1) && enc(&ev2.b, Tw, 3, 1, CX, CY, 1) && enc(&ev2.c, dT, 4, 3, FT_X, FT_Y, 3) &&
+         enc(&ev2.d, frh, 4, 6, FT_X, FT_Y, 6);
     if (!ok) return false;
     std::memcpy(maps_hv2_, &hv2, sizeof(TmaMaps));
     std::memcpy(maps_ev2_, &ev2, sizeof(TmaMaps));
@@ -1356,6 +1358,8 @@ bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
                 return true;
             }
         }
+        // rho-hat by TMA store when the output is the state array the plan's map addresses
+        a.frh_tma = (frh != nullptr && frh == fp.frh_base() && !(std::getenv("MFREG_NO_FRH_TMA"))) ? 1 : 0;
         ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s,
                    fp.fp32());
         return a.vticket != nullptr;

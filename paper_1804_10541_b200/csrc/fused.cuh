@@ -63,6 +63,7 @@ public:
     bool ev2() const { return ev2_; }  // two-CTA/SM eval kernel (ev_fast.cu)
     std::size_t ev2_smem() const { return ev2_smem_; }
     const void* maps_ev2() const { return maps_ev2_; }
+    const void* frh_base() const { return frh_base_; }  // the rho-hat array the eval TMA store addresses
     const void* maps_hv2() const { return maps_hv2_; }
     const void* maps_hv() const { return maps_hv_; }
     const void* maps_ev() const { return maps_ev_; }
@@ -111,11 +112,12 @@ private:
     int gmax_ = 0;
     DevArray<unsigned int> vticket_;
     bool ev2_ = false;
+    const void* frh_base_ = nullptr;
     std::size_t ev2_smem_ = 0;
-    alignas(64) unsigned char maps_ev2_[3 * 128];
-    alignas(64) unsigned char maps_hv2_[3 * 128];
-    alignas(64) unsigned char maps_hv_[3 * 128];  // TmaMaps (3 CUtensorMap)
-    alignas(64) unsigned char maps_ev_[3 * 128];
+    alignas(64) unsigned char maps_ev2_[4 * 128];
+    alignas(64) unsigned char maps_hv2_[4 * 128];
+    alignas(64) unsigned char maps_hv_[4 * 128];  // TmaMaps (4 CUtensorMap)
+    alignas(64) unsigned char maps_ev_[4 * 128];
     bool hv3_ = false;
     bool hv3_stored_ = false;
     bool hv16_ = false;
@@ -126,7 +128,7 @@ private:
     int slab3_[2] = {0, 0};
     int gmax3_ = 0;
     std::size_t hv3_smem_ = 0;
-    alignas(64) unsigned char maps_hv3_[3 * 128];
+    alignas(64) unsigned char maps_hv3_[4 * 128];
     void setup_hv3(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh, bool zok,
                    int max_optin);
     bool fp32_ = false;

@@ -31,6 +31,7 @@ struct FArgs {
     int nxf, nyf;       // nodal slab footprint (max over tiles) per plane, x and y
     int dbg;            // profiling switches (0 in production)
     int segw;           // max image columns per nodal x cell (segmented-scan length)
+    int frh_tma;        // eval: frh_out is the array TmaMaps::d addresses (rho-hat stored by TMA)
     const int* skip;    // device flag: return immediately when set (CG already converged)
     // eval (two-CTA kernel): when set, the last CTA to finish sums the per-tile (1 - r^2) in tile
     // order and writes D = dscale * sum to dsc[0] and the mapped host scalar dsc_host[0]
@@ -42,6 +43,7 @@ struct FArgs {
 
 struct TmaMaps {
     CUtensorMap a, b, c;  // Hv: dT, rho-hat; eval: R, T_w, dT
+    CUtensorMap d;        // eval (two-CTA kernel): rho-hat output, one tile x 6 components (TMA store)
 };
 
 __device__ __forceinline__ double lerp(double t, double a, double b) { return fma(t, b - a, a); }
@@ -111,6 +113,19 @@ __device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, i
         "l"(map), "r"(x), "r"(y), "r"(z), "r"(w), "r"(smem_u32(bar))
         : "memory");
 }
+
+// TMA store of a shared-memory box (bulk group of the issuing thread); the writers of the box
+// execute tma_store_fence() before the barrier that precedes the issue
+__device__ __forceinline__ void tma_store_fence() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int x, int y, int z, int w) {
+    asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(map),
+                 "r"(smem_u32(src)), "r"(x), "r"(y), "r"(z), "r"(w)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// the issuing thread's stores have finished reading shared memory / are complete
+__device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void tma_store_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 }  // namespace fdev
 }  // namespace mfreg_b200
