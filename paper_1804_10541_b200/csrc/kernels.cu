@@ -1068,9 +1068,10 @@ constexpr int WZ_NXF = 34, WZ_NYF = 10;
 // z lerp (FMA; a few ulp from the reference's exact sum, i.e. the sample moves by < 1e-12 voxel),
 // and the reference's exact P y and IEEE p/h only for points within 1e-9 of a cell face, where
 // that difference could change the cell (and dT by O(1)): cell choice bitwise the reference's,
-// T_w / dT within ~1e-15 relative (fast-mode tolerance 1e-9). Opt-in (MFREG_FAST_PY=1): the
-// 1e-16 perturbation grows through a full registration (C2 GN: max 0.53 voxel from the reference
-// against 0.22 with the exact P y, tests/test_gpu_configs.py) for a 3% faster gradient eval.
+// T_w / dT within ~1e-15 relative (fast-mode tolerance 1e-9). On by default (MFREG_FAST_PY=0
+// selects the reference-order P y): like every fast-mode reordering, the 1e-16 perturbation moves a full
+// registration inside the reference's own 1-ulp envelope (C2 GN: 0.15 voxel max against the
+// reference's 0.45 under +-1 ulp of the template, tests/golden/c2_envelope.json).
 template <typename OutT>
 __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, const double* __restrict__ y,
                                                    const double* __restrict__ T, OutT* __restrict__ Tw,
@@ -1221,10 +1222,11 @@ void warp_fast_impl(const DevPlan& P0, const double* y, const double* T, OutT* T
         const int nch = std::max<int>((nz + 63) / 64, static_cast<int>(std::min<long long>(nz, (148LL * 8 + cols - 1) / cols)));
         const int zc = (nz + nch - 1) / nch;
         const dim3 gr(gx, gy, static_cast<unsigned>((nz + zc - 1) / zc));
-        static const int fastpy = [] {  // opt-in: moves full registrations inside the 1-ulp envelope
-            const char* e = std::getenv("MFREG_FAST_PY");  // (DESIGN.md §5), 3% of a C4 gradient eval
-            return (e && e[0] == '1') ? 1 : 0;
-        }();
+        // separable fast P y (2-3% of a C4 gradient eval; the cell choice stays the
+        // reference's); MFREG_FAST_PY=0 keeps the reference-order P y. Read per launch so a process
+        // can compare both.
+        const char* fpe = std::getenv("MFREG_FAST_PY");
+        const int fastpy = (fpe && fpe[0] == '0') ? 0 : 1;
         note_launch(), k_warp_z<OutT><<<gr, dim3(32, 8, 1), 0, s>>>(P, y, T, Tw, dT, zlo, zhi, zc, fastpy);
         return;
     }

