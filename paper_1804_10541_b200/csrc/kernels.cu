@@ -1389,11 +1389,11 @@ static bool lap_geo(const Grid& g, LapGeo& o) {
     return p2;
 }
 
-void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo, int zhi) {
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo, int zhi, bool exact) {
     LapGeo lg;
     dim3 gr;
     if (!zwin(g, gr, zlo, zhi)) return;
-    if (lap_geo(g, lg)) note_launch(), k_lap3<true><<<gr, block3(), 0, s>>>(lg, u, out, zlo);
+    if (lap_geo(g, lg) || !exact) note_launch(), k_lap3<true><<<gr, block3(), 0, s>>>(lg, u, out, zlo);
     else note_launch(), k_lap3<false><<<gr, block3(), 0, s>>>(lg, u, out, zlo);
 }
 
@@ -1406,12 +1406,12 @@ static void launch_bilap_t(dim3 gr, int zlo, const LapGeo& lg, const double* lap
 }
 
 void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
-                  const double* p, double* out, cudaStream_t s, int zlo, int zhi) {
+                  const double* p, double* out, cudaStream_t s, int zlo, int zhi, bool exact) {
     LapGeo lg;
     dim3 gr;
     if (!zwin(g, gr, zlo, zhi)) return;
     note_launch();
-    if (lap_geo(g, lg)) launch_bilap_t<true>(gr, zlo, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
+    if (lap_geo(g, lg) || !exact) launch_bilap_t<true>(gr, zlo, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
     else launch_bilap_t<false>(gr, zlo, lg, lap_u, scale, mode, alpha, gamma, p, out, s);
 }
 void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,

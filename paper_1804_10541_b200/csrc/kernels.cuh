@@ -81,10 +81,12 @@ idx_t tree_blocks(idx_t n);
 void launch_inf_norm(idx_t n, const double* a, double scale, double* out, cudaStream_t s);
 
 // ---- curvature (curvature.cpp:9-98), nodal grid, 3 components
-void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
+// exact = false (fast modes): the quotient by h*h is the product with its reciprocal (within 1 ulp)
+void launch_lap3(const Grid& g, const double* u, double* out, cudaStream_t s, int zlo = 0, int zhi = -1,
+                 bool exact = true);
 // mode 0: out = scale*Lap(in); 1: out += alpha*(scale*Lap(in)); 2: out = scale*Lap(in) + gamma*p
 void launch_bilap(const Grid& g, const double* lap_u, double scale, int mode, double alpha, double gamma,
-                  const double* p, double* out, cudaStream_t s, int zlo = 0, int zhi = -1);
+                  const double* p, double* out, cudaStream_t s, int zlo = 0, int zhi = -1, bool exact = true);
 // curvature value finalize: out = alpha * (cellvol * ((S0 + S1) + S2))
 void launch_curv_finalize(const double* S3, double cellvol, double alpha, double* out, cudaStream_t s);
 void launch_curv_value(const double* S, double cellvol, double alpha, double* out_dev, double* out_host,

@@ -447,7 +447,7 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     MFREG_CUDA(cudaEventRecord(ev_fork_, s));
     MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
     launch_sub(3 * ny, y, xid_.get(), u_.get(), s2_);
-    launch_lap3(dg_, u_.get(), lapu_.get(), s2_);
+    launch_lap3(dg_, u_.get(), lapu_.get(), s2_, 0, -1, false);  // (fast: reciprocal multiplies)
     const idx_t pn = dg_.m[0] * dg_.m[1];
     if (sliced_)  // owned nodal planes only, per component
         for (int d = 0; d < 3; ++d)
@@ -460,7 +460,8 @@ void DeviceObjective::enqueue_eval_fast(const double* y, double* grad, cudaStrea
     const bool scalars_direct = !sliced_ && fused_->ev2();
     if (scalars_direct) launch_curv_value(sc2_.get(), dg_.cell_volume(), alpha_, sc_.dev(1), sc_.host_dev() + 1, s2_);
     if (grad && alpha_ != 0.0)
-        launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+        launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_, 0,
+                     -1, false);
     MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
     warp_state(y, s, wlo, whi, state);
     launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_,
@@ -497,8 +498,9 @@ void DeviceObjective::enqueue_hv_fast(const double* p, double* q, const double* 
     if (alpha_ != 0.0) {
         MFREG_CUDA(cudaEventRecord(ev_fork_, s));
         MFREG_CUDA(cudaStreamWaitEvent(s2_, ev_fork_, 0));
-        launch_lap3(dg_, p, lapp_.get(), s2_);
-        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_);
+        launch_lap3(dg_, p, lapp_.get(), s2_, 0, -1, false);
+        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), s2_, 0, -1,
+                     false);
         MFREG_CUDA(cudaEventRecord(ev_join_, s2_));
     }
     launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s, skip);
