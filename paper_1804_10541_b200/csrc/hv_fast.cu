@@ -282,7 +282,12 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     auto zbase = [&](int k) { return sZb[k - kfirst]; };  // k in [kfirst, klast + 3]
     auto zrem = [&](int k) { return sZr[k - kfirst]; };
 
-    auto xstage = [&](Real v0, Real v1, Real v2) { ptc.xstage(row, lane, v0, v1, v2); };
+    // (FAST32: the shuffle scan, whose lane geometry fits its registers)
+    const auto plane_geom = ptc.lane_geom(a, x0, nxA, lane);
+    auto xstage = [&](Real v0, Real v1, Real v2) {
+        if constexpr (sizeof(Real) == 4) ptc.xstage_shfl(row, lane, plane_geom, segw, v0, v1, v2);
+        else ptc.xstage(row, lane, v0, v1, v2);
+    };
     auto ystage = [&](int nzp) { ptc.ystage(row, lane, part + static_cast<std::size_t>(nzp - nzA) * pstride); };
 
     pdl_wait();       // p (the CG update before this launch) from here on

@@ -119,6 +119,56 @@ struct Ptc {
             if (u < npx && L < nxi) ar[L] = o[u];
         }
     }
+    // FAST32 alternative of the x stage: a segmented shuffle scan over the lanes of one nodal cell
+    // (fp32 shuffles are single instructions and FAST32 has registers for the lane geometry);
+    // writes the same in-place row layout as xstage
+    struct Lane {
+        Real rx;
+        int bx;        // local nodal cell of the column (1024 + lane past the volume)
+        int sst;       // first lane of the column's segment
+        bool send, xin, xlast;
+    };
+    __device__ Lane lane_geom(const FArgs& a, int x0, int nxA, int lane) const {
+        const int mx = static_cast<int>(a.g.m[0]);
+        const int gx = x0 + lane, gxc = min(gx, mx - 1), xe = min(mx, x0 + kPtcTX);
+        Lane L;
+        L.xin = gx < mx;
+        L.xlast = gx == xe - 1;
+        L.bx = L.xin ? __ldg(&a.P.base[0][gxc]) - nxA : 1024 + lane;
+        L.rx = static_cast<Real>(__ldg(&a.P.rem[0][gxc]));
+        const int bx_prev = __shfl_up_sync(0xffffffffu, L.bx, 1);
+        const unsigned starts = __ballot_sync(0xffffffffu, lane == 0 || bx_prev != L.bx);
+        L.sst = 31 - __clz(starts & (0xffffffffu >> (31 - lane)));
+        L.send = lane == 31 || ((starts >> (lane + 1)) & 1u);
+        return L;
+    }
+    __device__ void xstage_shfl(int row, int lane, const Lane& g, int segw, Real v0, Real v1, Real v2) const {
+        Real* dst = sA + row * XR;
+        const int nlx_t = nxi / 3;
+        Real A[3] = {(Real(1) - g.rx) * v0, (Real(1) - g.rx) * v1, (Real(1) - g.rx) * v2};
+        Real B[3] = {g.rx * v0, g.rx * v1, g.rx * v2};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            if (o >= segw) break;  // uniform
+            const bool in = lane - o >= g.sst;
+#pragma unroll
+            for (int d = 0; d < 3; ++d) {
+                const Real ua = __shfl_up_sync(0xffffffffu, A[d], o);
+                const Real ub = __shfl_up_sync(0xffffffffu, B[d], o);
+                A[d] = in ? A[d] + ua : A[d];
+                B[d] = in ? B[d] + ub : B[d];
+            }
+        }
+        __syncwarp();  // (the y stage of the previous completion read this row two steps ago)
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+            const Real bp = __shfl_sync(0xffffffffu, B[d], max(g.sst - 1, 0));
+            if (g.send && g.xin) {
+                dst[d * nlx_t + g.bx] = g.sst > 0 ? A[d] + bp : A[d];
+                if (g.xlast) dst[d * nlx_t + g.bx + 1] = B[d];
+            }
+        }
+    }
     // y stage into the tile partial of one nodal plane (node row lyn on warp TY-1-lyn: the halo
     // items sit on the lowest warps)
     __device__ void ystage(int row, int lane, Real* pz) const {
