@@ -261,6 +261,48 @@ def cpu_reference_sample(wl: str, steps: int, threads: int):
                       f"is size-independent (the reference kernels are linear in the voxel count)"}
 
 
+def measured_registration_64(P, threads: int):
+    """A full registration timed on both sides (no extrapolation): the 64^3 phantom pair (h = 1,
+    phantom x1000, sinusoid amp 3 seed 42, the reference's own generators), 3-level Gauss-Newton
+    with the reference's defaults (multilevel.cpp:117-145) - the unmodified reference library
+    (oracle/_ref) on the host's threads against this library in fast and parity mode on the GPU,
+    with the parity field compared bitwise to the reference's."""
+    import torch
+    from oracle.oracle import Oracle, available
+    if not available("ref"):
+        return None
+    o = Oracle("ref")
+    o.set_threads(threads)
+    m, h = (64, 64, 64), (1.0, 1.0, 1.0)
+    R = o.make_phantom(m, h) * 1000.0
+    T = o.warp_sinusoid(R, m, h, 3.0, 42)
+    t0 = time.perf_counter()
+    y_ref, _, tr, _ = o.register_multilevel(R, T, m, h, levels=3, method="gn")
+    t_ref = time.perf_counter() - t0
+    img = P.make_image_grid(m, h)
+    out = {"workload": "64^3 h=1 phantom pair, 3-level GN, reference defaults", "reference_cpu_s": t_ref,
+           "cores": threads, "reference_outer_iters": [len(t) for t in tr],
+           "reference_cg_iters": int(sum(r[1] for t in tr for r in t))}
+    for name, md in (("fast", P.Mode.FAST), ("parity", P.Mode.PARITY)):
+        cfg = P.MultilevelConfig(levels=3, method=P.Method.GAUSS_NEWTON, mode=md)
+        walls = []
+        for _ in range(2 if name == "fast" else 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            y, _, lv = P.register_multilevel(R, T, img, cfg)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        y = np.asarray(y)
+        out[f"ours_{name}_s"] = min(walls)
+        if name == "parity":
+            out["parity_y_bitwise_equal"] = bool(np.array_equal(y.view(np.uint64), y_ref.view(np.uint64)))
+        else:
+            d = np.abs(y - y_ref).reshape(3, -1) / np.array(h)[:, None]
+            out["fast_vs_reference_max_voxel"] = float(d.max())
+    out["speedup_fast"] = t_ref / out["ours_fast_s"]
+    return out
+
+
 def cpu_gn_model(cpu: dict, levels_gpu, img_counts):
     """CPU reference wall time of the same multilevel GN run, extrapolated from the measured
     per-voxel costs: per level, (outer iterations) gradient evals + (CG iterations) GN Hv +
@@ -455,6 +497,8 @@ def run_ours(args, rank, world, local):
                                              f"({cpu['cores']} threads)")
         ckg.__exit__(None, None, None)
         gn["clocks"] = ckg.summary()
+        if rank == 0 and not args.no_cpu:
+            gn["measured_registration_64"] = measured_registration_64(P, os.cpu_count() or 1)
 
     if rank == 0:
         cpu_line = None
