@@ -79,6 +79,28 @@ struct Coef {
     Real r;     // residual
 };
 
+// the normalisation of one column: inv1, inv2 (ngf.cpp:204-209) and the residual
+template <typename Real>
+struct Norm {
+    Real in1, in2, r;
+};
+template <typename Real>
+__device__ __forceinline__ Norm<Real> ngf_norm(const FArgs& a, Real dR0, Real dR1, Real dR2, Real dR3, Real dR4,
+                                               Real dR5, Real dT0, Real dT1, Real dT2, Real dT3, Real dT4, Real dT5) {
+    const Real i0 = static_cast<Real>(a.ih2[0]), i1 = static_cast<Real>(a.ih2[1]), i2 = static_cast<Real>(a.ih2[2]);
+    const Real stt = fma(fma(dT0, dT0, dT1 * dT1), i0, fma(fma(dT2, dT2, dT3 * dT3), i1, fma(dT4, dT4, dT5 * dT5) * i2));
+    const Real srr = fma(fma(dR0, dR0, dR1 * dR1), i0, fma(fma(dR2, dR2, dR3 * dR3), i1, fma(dR4, dR4, dR5 * dR5) * i2));
+    const Real num = fma(Real(0.5), fma(fma(dT0, dR0, dT1 * dR1), i0, fma(fma(dT2, dR2, dT3 * dR3), i1, fma(dT4, dR4, dT5 * dR5) * i2)),
+                         static_cast<Real>(a.tau * a.rho));
+    const Real nt2 = fma(Real(0.5), stt, static_cast<Real>(a.tau * a.tau));
+    const Real nr2 = fma(Real(0.5), srr, static_cast<Real>(a.rho * a.rho));
+    Norm<Real> o;
+    o.in1 = rsq(nt2 * nr2);
+    o.in2 = num * ((o.in1 * o.in1) * (o.in1 * nr2));
+    o.r = num * o.in1;
+    return o;
+}
+
 template <typename Real>
 __device__ __forceinline__ Coef<Real> ngf_coef(const FArgs& a, Real dR0, Real dR1, Real dR2, Real dR3, Real dR4,
                                                Real dR5, Real dT0, Real dT1, Real dT2, Real dT3, Real dT4, Real dT5,
@@ -164,10 +186,11 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
                    (gx1 + 1 < mx ? 1 << 24 : 0) | (gy1 > 0 ? 1 << 25 : 0) | (gy1 + 1 < my ? 1 << 26 : 0) |
                    (gx1 >= 0 && gx1 < mx && gy1 >= 0 && gy1 < my ? 1 << 27 : 0);
     }
-    // boundary masks of the in-plane differences (reference clamped neighbours) and
-    // "inside the volume" flag of the tile column
-    const Real m0xm = gx0 > 0 ? Real(1) : Real(0), m0xp = gx0 + 1 < mx ? Real(1) : Real(0);
-    const Real m0ym = gy0 > 0 ? Real(1) : Real(0), m0yp = gy0 + 1 < my ? Real(1) : Real(0);
+    // in-plane neighbours of the tile column, clamped at the volume boundary like the reference's
+    // neighbours (the difference with itself is an exact zero: no mask multiplies), and its
+    // "inside the volume" flag
+    const int cxm0 = c0 - (gx0 > 0 ? 1 : 0), cxp0 = c0 + (gx0 + 1 < mx ? 1 : 0);
+    const int cym0 = c0 - (gy0 > 0 ? SX : 0), cyp0 = c0 + (gy0 + 1 < my ? SX : 0);
     const bool in0 = gx0 < mx && gy0 < my;
     const long long col0 = in0 ? static_cast<long long>(gx0) + static_cast<long long>(gy0) * mx : 0;
 
@@ -236,12 +259,10 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         {
             const Real Rj = sp[SLOT_R + c0], Tj = sp[SLOT_T + c0];
             const Real Rp = st[SLOT_R + c0], Tp = st[SLOT_T + c0];
-            const Coef cf = ngf_coef(a, m0xm * (sp[SLOT_R + c0 - 1] - Rj), m0xp * (sp[SLOT_R + c0 + 1] - Rj),
-                                     m0ym * (sp[SLOT_R + c0 - SX] - Rj), m0yp * (sp[SLOT_R + c0 + SX] - Rj),
-                                     mzm * (Rm0 - Rj), mzp * (Rp - Rj), m0xm * (sp[SLOT_T + c0 - 1] - Tj),
-                                     m0xp * (sp[SLOT_T + c0 + 1] - Tj), m0ym * (sp[SLOT_T + c0 - SX] - Tj),
-                                     m0yp * (sp[SLOT_T + c0 + SX] - Tj), mzm * (Tm0 - Tj), mzp * (Tp - Tj),
-                                     in0 && jin);
+            const Coef cf = ngf_coef(a, sp[SLOT_R + cxm0] - Rj, sp[SLOT_R + cxp0] - Rj, sp[SLOT_R + cym0] - Rj,
+                                     sp[SLOT_R + cyp0] - Rj, mzm * (Rm0 - Rj), mzp * (Rp - Rj), sp[SLOT_T + cxm0] - Tj,
+                                     sp[SLOT_T + cxp0] - Tj, sp[SLOT_T + cym0] - Tj, sp[SLOT_T + cyp0] - Tj,
+                                     mzm * (Tm0 - Tj), mzp * (Tp - Tj), in0 && jin);
             Rm0 = Rj;
             Tm0 = Tj;
             if (j >= z0 && j < z1) {  // Hv state of the tile plane (none when value-only lazy)
@@ -270,22 +291,29 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         }
         if (w1) {  // ring-1 edge column: the flux toward the tile
             const int e1 = lds_v(sI1 + tid), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff, dir1 = (e1 >> 20) & 3;
-            const Real m1xm = (e1 >> 23) & 1 ? Real(1) : Real(0), m1xp = (e1 >> 24) & 1 ? Real(1) : Real(0);
-            const Real m1ym = (e1 >> 25) & 1 ? Real(1) : Real(0), m1yp = (e1 >> 26) & 1 ? Real(1) : Real(0);
+            // clamped in-plane neighbours (exact-zero differences at the volume boundary)
+            const int cxm = c1 - ((e1 >> 23) & 1), cxp = c1 + ((e1 >> 24) & 1);
+            const int cym = c1 - ((e1 >> 25) & 1) * SX, cyp = c1 + ((e1 >> 26) & 1) * SX;
             const bool in1c = (e1 >> 27) & 1;
             const Real Rj = sp[SLOT_R + c1], Tj = sp[SLOT_T + c1];
             const Real Rp = st[SLOT_R + c1], Tp = st[SLOT_T + c1];
-            const Coef cf = ngf_coef(a, m1xm * (sp[SLOT_R + c1 - 1] - Rj), m1xp * (sp[SLOT_R + c1 + 1] - Rj),
-                                     m1ym * (sp[SLOT_R + c1 - SX] - Rj), m1yp * (sp[SLOT_R + c1 + SX] - Rj),
-                                     mzm * (Rm1 - Rj), mzp * (Rp - Rj), m1xm * (sp[SLOT_T + c1 - 1] - Tj),
-                                     m1xp * (sp[SLOT_T + c1 + 1] - Tj), m1ym * (sp[SLOT_T + c1 - SX] - Tj),
-                                     m1yp * (sp[SLOT_T + c1 + SX] - Tj), mzm * (Tm1 - Tj), mzp * (Tp - Tj),
-                                     in1c && jin);
+            const Real dR0 = sp[SLOT_R + cxm] - Rj, dR1 = sp[SLOT_R + cxp] - Rj, dR2 = sp[SLOT_R + cym] - Rj,
+                       dR3 = sp[SLOT_R + cyp] - Rj;
+            const Real dT0 = sp[SLOT_T + cxm] - Tj, dT1 = sp[SLOT_T + cxp] - Tj, dT2 = sp[SLOT_T + cym] - Tj,
+                       dT3 = sp[SLOT_T + cyp] - Tj;
+            const Norm<Real> nm = ngf_norm(a, dR0, dR1, dR2, dR3, mzm * (Rm1 - Rj), mzp * (Rp - Rj), dT0, dT1, dT2, dT3,
+                                           mzm * (Tm1 - Tj), mzp * (Tp - Tj));
             Rm1 = Rj;
             Tm1 = Tj;
-            const Real e = dir1 == 0 ? cf.e[1] : (dir1 == 1 ? cf.e[0] : (dir1 == 2 ? cf.e[3] : cf.e[2]));
-            if ((e1 >> 22) & 1) sE[(1 - P) * 2 * TY + f1] = e * cf.r;
-            else sF[(1 - P) * 2 * NT + f1] = e * cf.r;
+            // only the coefficient toward the tile: the +x flux comes from e[1] (x = -1 column), -x
+            // from e[0], +y from e[3], -y from e[2]
+            const Real dRs = dir1 == 0 ? dR1 : (dir1 == 1 ? dR0 : (dir1 == 2 ? dR3 : dR2));
+            const Real dTs = dir1 == 0 ? dT1 : (dir1 == 1 ? dT0 : (dir1 == 2 ? dT3 : dT2));
+            const Real hs = static_cast<Real>(dir1 < 2 ? a.hh[0] : a.hh[1]);
+            const bool ok = in1c && jin;
+            const Real e = ok ? hs * fma(dRs, nm.in1, -dTs * nm.in2) : Real(0), r1 = ok ? nm.r : Real(0);
+            if ((e1 >> 22) & 1) sE[(1 - P) * 2 * TY + f1] = e * r1;
+            else sF[(1 - P) * 2 * NT + f1] = e * r1;
         }
         // ---- Z: plane i = k-2 (tile columns): gradient -2h dT (dr^T r) -> P^T
         const int i = k - 2;
