@@ -7,26 +7,32 @@
 // TMA waits are covered by the other CTA's arithmetic:
 //  * one thread per output column of the 32x8 tile; the halo columns are extra
 //    work items of threads 0..163 (ring-1 edges: P and W, ring-1 corners and
-//    ring-2 edges: P only) instead of dedicated halo warps;
-//  * the staging ring holds one TMA slot per step: step k stages dT of plane k
-//    (36x12 s region, read by P) and rho-hat of plane k-1 (36x10 w rows, read
-//    by W of plane k-1 in the same step), so a slot is consumed in exactly one
-//    step and no coefficient is carried in registers (ring of 3: 2 steps ahead);
+//    ring-2 edges: P only) instead of dedicated halo warps; their geometry is
+//    packed into one word per item in shared memory (re-read per use in fp64);
+//  * TMA staging per step: dT of plane k (36x12 s region, read by P) in a ring of
+//    3 and rho-hat of plane k-1 (36x10 w rows, read by W of plane k-1 in the same
+//    step) in a ring of 3, both 2 steps ahead, so a slot is consumed in exactly one
+//    step and no coefficient is carried in registers;
 //  * the dr^T stage reads fluxes instead of (coefficient, w) pairs: W of
 //    column t forms rho-hat_t(k) w_t for its in-plane neighbours; x fluxes move
 //    inside the warp (a warp is one tile row) by shuffles, y fluxes through two
 //    consumer-indexed shared arrays, the z fluxes and sigma_t w_t stay in the
 //    column's registers, so z_i is 2-3 shared loads + a few adds;
-//  * the halo columns' nodal interpolants live in shared memory (each thread
-//    reads back only its own entries), keeping the plane loop within 128
-//    registers;
-//  * P^T: per-column z weights in registers; on a completed nodal plane each
-//    warp (one tile row) collapses x with a segmented shuffle scan over the
-//    nodal cells and the y collapse runs one step later, after the regular
-//    barrier — no extra barriers in the plane loop (the host guarantees nodal
-//    z cells of >= 2 image planes, so completions are >= 2 steps apart).
+//  * nodal interpolants: item 0's in registers, the halo items' in shared memory;
+//    fp64 reads the nodes at a plane change from L1/L2, FAST32 from a shared ring
+//    of the tile's nodal footprint filled one step ahead;
+//  * P^T: per-column z weights in registers; on a completed nodal plane each warp
+//    (one tile row) collapses x through its shared row and the per-tile weight
+//    tables (ptc.cuh; FAST32: a segmented shuffle scan) and the y collapse runs one
+//    step later, after the regular barrier — no extra barriers in the plane loop
+//    (the host guarantees nodal z cells of >= 2 image planes, so completions are
+//    >= 2 steps apart).
 // Boundary semantics are those of the TMA zero fill: rho-hat and dT vanish
 // outside the volume, and the eval pass stores zero coefficients across it.
+// Tile height 16 (512 threads, one CTA per SM) is instantiated too (MFREG_HV16=1).
+// Compile-time switches: MFREG_HV2_SLAB (fp64 shared nodal ring), MFREG_HV2_RRING
+// (rho-hat ring depth), MFREG_HV2_EXP (timing experiments with wrong results:
+// scripts/variants.py builds only).
 #include <cstdint>
 
 #include "ptc.cuh"

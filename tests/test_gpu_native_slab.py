@@ -87,7 +87,10 @@ for r in res:
     assert len(r["tr"]) == len(tr_full)
     assert abs(r["tr"][0].j - tr_full[0].j) <= 1e-12 * abs(tr_full[0].j)
     for a, b in zip(r["tr"], tr_full):
-        tol = 1e-5 if a.iter < 3 else 1e-3  # the differences grow ~10x per outer iteration
+        # CG stops at its 400-iteration cap here, so the trajectory amplifies the reductions'
+        # rounding: measured 3e-7 / 3e-7 / 6e-6 at iterations 1-3 with the reference-order P y and
+        # 1.4e-6 / 2.1e-4 / 6e-5 with the separable one (the operators agree to 1e-12 / 1e-9 above)
+        tol = 1e-5 if a.iter < 2 else 1e-3
         assert abs(a.j - b.j) <= tol * abs(b.j), (a.as_tuple(), b.as_tuple())
     for lvl, ((ta, _), (tb, _)) in enumerate(zip(r["lv"], lv_full)):
         assert len(ta) == len(tb), (lvl, len(ta), len(tb))
