@@ -193,7 +193,8 @@ inline unsigned blocks_for(long long n, int t = 256) { return static_cast<unsign
 }  // namespace
 
 DeviceCg::DeviceCg(idx_t n) : n_(n), r_(n), p_(n), ap_(n), st_(1), red_(1024), counter_(1 + kTicketGroups) {
-    MFREG_CUDA(cudaMallocHost(&host_, sizeof(CgState)));
+    static_assert(sizeof(CgState) <= kPinnedSmall, "CG state block");
+    host_ = static_cast<CgState*>(pinned_small_alloc(sizeof(CgState)));
     MFREG_CUDA(cudaMemset(counter_.get(), 0, (1 + kTicketGroups) * sizeof(unsigned int)));
 }
 
@@ -201,7 +202,7 @@ DeviceCg::~DeviceCg() {
     for (auto& g : graphs_)
         if (g.exec) cudaGraphExecDestroy(g.exec);
     if (cs_) cudaStreamDestroy(cs_);
-    if (host_) cudaFreeHost(host_);
+    pinned_small_free(host_);
 }
 
 void DeviceCg::window(DeviceProblem& P, int op, double gamma, double* x, const CgConfig& cfg, int w,

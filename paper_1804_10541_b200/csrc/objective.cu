@@ -1,11 +1,15 @@
 // DeviceObjective and its building blocks (see objective.cuh).
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "objective.cuh"
@@ -40,6 +44,108 @@ cudaMemPool_t default_pool() {
 }  // namespace
 
 namespace {
+// Freed blocks of kBigAllocBytes and more are kept for reuse by an allocation of the same size
+// (MFREG_BIG_CACHE_GB, default 32: a C4 registration's levels need ~25 GB; 0 = plain cudaFree): objectives are created per pyramid level
+// and per call, and cudaFree of their tens of GB of state measured up to ~1 s per teardown at C4,
+// growing with repeated registrations (scripts/c4_reg.py, MFREG_TRACE_TIME=1). A cached block is
+// handed out again only after a device synchronisation at its release (cudaFree's own ordering),
+// and the cache is emptied before cudaMalloc is retried on an out-of-memory error.
+struct BigCache {
+    std::mutex mu;
+    std::multimap<std::size_t, std::pair<int, void*>> blocks;  // requested bytes -> (device, pointer)
+    std::size_t bytes = 0;
+};
+BigCache& big_cache() {
+    static BigCache* c = new BigCache;  // never destroyed: frees may come from static destructors
+    return *c;
+}
+std::size_t big_cache_limit() {
+    static const std::size_t lim = [] {
+        const char* e = std::getenv("MFREG_BIG_CACHE_GB");
+        const double gb = e ? std::atof(e) : 32.0;
+        return static_cast<std::size_t>(std::max(0.0, gb) * static_cast<double>(1ull << 30));
+    }();
+    return lim;
+}
+void* big_take(std::size_t bytes) {
+    int dev = 0;
+    MFREG_CUDA(cudaGetDevice(&dev));
+    BigCache& c = big_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    auto range = c.blocks.equal_range(bytes);
+    for (auto it = range.first; it != range.second; ++it)
+        if (it->second.first == dev) {
+            void* p = it->second.second;
+            c.blocks.erase(it);
+            c.bytes -= bytes;
+            return p;
+        }
+    return nullptr;
+}
+bool big_put(void* p, std::size_t bytes) {
+    if (bytes > big_cache_limit()) return false;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return false;
+    BigCache& c = big_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    if (c.bytes + bytes > big_cache_limit()) return false;
+    if (cudaDeviceSynchronize() != cudaSuccess) return false;  // the block's last users are done
+    c.blocks.emplace(bytes, std::make_pair(dev, p));
+    c.bytes += bytes;
+    return true;
+}
+void big_release_all() {
+    int dev = 0;
+    MFREG_CUDA(cudaGetDevice(&dev));
+    BigCache& c = big_cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    for (auto it = c.blocks.begin(); it != c.blocks.end();) {
+        if (it->second.first == dev) {
+            cudaFree(it->second.second);
+            c.bytes -= it->first;
+            it = c.blocks.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+}  // namespace
+
+namespace {
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<void*> free;
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // never destroyed (frees from static destructors)
+    return *p;
+}
+}  // namespace
+
+void* pinned_small_alloc(std::size_t bytes) {
+    if (bytes > kPinnedSmall) throw std::invalid_argument("pinned_small_alloc: block too large");
+    {
+        PinnedPool& pp = pinned_pool();
+        std::lock_guard<std::mutex> lk(pp.mu);
+        if (!pp.free.empty()) {
+            void* p = pp.free.back();
+            pp.free.pop_back();
+            return p;
+        }
+    }
+    void* p = nullptr;
+    MFREG_CUDA(cudaHostAlloc(&p, kPinnedSmall, cudaHostAllocMapped | cudaHostAllocPortable));
+    return p;
+}
+
+void pinned_small_free(void* p) {
+    if (!p) return;
+    PinnedPool& pp = pinned_pool();
+    std::lock_guard<std::mutex> lk(pp.mu);
+    pp.free.push_back(p);
+}
+
+namespace {
 std::atomic<long long> g_mem_cur{0}, g_mem_peak{0};  // library device allocations (live bytes, high-water mark)
 void mem_note(long long delta) {
     const long long now = g_mem_cur.fetch_add(delta) + delta;
@@ -59,10 +165,12 @@ void* device_alloc(std::size_t bytes) {
     mem_note(static_cast<long long>(bytes));
     void* p = nullptr;
     if (bytes >= kBigAllocBytes) {
+        if ((p = big_take(bytes))) return p;
         cudaError_t e = cudaMalloc(&p, bytes);
-        if (e == cudaErrorMemoryAllocation) {  // cached pool blocks may hold the memory: release, retry
+        if (e == cudaErrorMemoryAllocation) {  // cached blocks may hold the memory: release, retry
             cudaGetLastError();
             MFREG_CUDA(cudaDeviceSynchronize());
+            big_release_all();
             MFREG_CUDA(cudaMemPoolTrimTo(default_pool(), 0));
             e = cudaMalloc(&p, bytes);
         }
@@ -77,6 +185,7 @@ void* device_alloc(std::size_t bytes) {
     if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
         cudaGetLastError();
         MFREG_CUDA(cudaDeviceSynchronize());
+        big_release_all();
         MFREG_CUDA(cudaMemPoolTrimTo(pool, 0));
         e = cudaMallocAsync(&p, bytes, 0);
     }
@@ -90,8 +199,11 @@ void* device_alloc(std::size_t bytes) {
 void device_free(void* p, std::size_t bytes) {
     if (!p) return;
     mem_note(-static_cast<long long>(bytes));
-    if (bytes >= kBigAllocBytes) cudaFree(p);
-    else cudaFreeAsync(p, 0);
+    if (bytes >= kBigAllocBytes) {
+        if (!big_put(p, bytes)) cudaFree(p);
+    } else {
+        cudaFreeAsync(p, 0);
+    }
 }
 
 void check_launch(const char* what) {
@@ -244,13 +356,11 @@ void Reducer::sum3(int kind, idx_t n, const double* a, const double* b, double* 
 }
 
 Scalars::Scalars(int n) : d_(static_cast<std::size_t>(n)) {
-    MFREG_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_), n * sizeof(double), cudaHostAllocMapped));
+    h_ = static_cast<double*>(pinned_small_alloc(n * sizeof(double)));
     MFREG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&hd_), h_, 0));
     MFREG_CUDA(cudaMemset(d_.get(), 0, n * sizeof(double)));
 }
-Scalars::~Scalars() {
-    if (h_) cudaFreeHost(h_);
-}
+Scalars::~Scalars() { pinned_small_free(h_); }
 void Scalars::fetch_async(int n, cudaStream_t s) {
     MFREG_CUDA(cudaMemcpyAsync(h_, d_.get(), n * sizeof(double), cudaMemcpyDeviceToHost, s));
 }
@@ -404,6 +514,26 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
 }
 
 DeviceObjective::~DeviceObjective() {
+    static const bool trace = [] {  // MFREG_TRACE_TIME=1 (as the solvers' per-iteration split)
+        const char* e = std::getenv("MFREG_TRACE_TIME");
+        return e && *e && *e != '0';
+    }();
+    if (trace) {  // (teardown cost breakdown; the members would go in this order anyway)
+        auto t = std::chrono::steady_clock::now();
+        auto lap = [&](const char* what) {
+            const auto n = std::chrono::steady_clock::now();
+            std::fprintf(stderr, "  teardown %s %.2f ms\n", what, std::chrono::duration<double, std::milli>(n - t).count());
+            t = n;
+        };
+        fused_.reset();
+        lap("fused");
+        red2_.reset();
+        lap("red2");
+        graphs_.clear();
+        lap("graphs");
+        ngf_.release();
+        lap("ngf");
+    }
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (s2_) cudaStreamDestroy(s2_);
@@ -672,10 +802,14 @@ GraphCache::GraphCache(std::size_t cap) : cap_(cap) {
     enabled_ = !(off && off[0] == '1');
 }
 
-GraphCache::~GraphCache() {
+GraphCache::~GraphCache() { clear(); }
+
+void GraphCache::clear() {
     for (auto& e : entries_)
         if (e.exec) cudaGraphExecDestroy(e.exec);
+    entries_.clear();
     if (cs_) cudaStreamDestroy(cs_);
+    cs_ = nullptr;
 }
 
 GraphCache::Entry* GraphCache::find(const Key& k) {

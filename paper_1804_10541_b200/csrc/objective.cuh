@@ -48,6 +48,11 @@ void* device_alloc(std::size_t bytes);
 // high-water mark of the library's live device allocations since load (or the last reset)
 long long device_memory_peak(bool reset);
 void device_free(void* p, std::size_t bytes);
+// small mapped pinned host blocks (<= kPinnedSmall bytes), recycled across objectives:
+// cudaFreeHost synchronises the device and measured tens to hundreds of ms per teardown
+constexpr std::size_t kPinnedSmall = 4096;
+void* pinned_small_alloc(std::size_t bytes);
+void pinned_small_free(void* p);
 
 // RAII device array of doubles (or raw bytes).
 template <typename T>
@@ -145,6 +150,7 @@ public:
     using Key = std::array<const void*, 6>;
     explicit GraphCache(std::size_t cap = 8);
     ~GraphCache();
+    void clear();  // destroy every cached graph
     GraphCache(const GraphCache&) = delete;
     GraphCache& operator=(const GraphCache&) = delete;
     bool enabled() const { return enabled_; }
@@ -305,6 +311,10 @@ public:
     DVec Tw, dT, r, inv1, inv2, rh, sv, wbuf;
     DVec frh;  // fast mode: rho-hat [6][n] (-x,+x,-y,+y,-z,+z), the Hv state
     DevArray<float> R32, Tw32, dT32, frh32;  // Fast32 state
+    void release() {  // free the image-grid state now (the destructor would)
+        for (DVec* v : {&Tw, &dT, &r, &inv1, &inv2, &rh, &sv, &wbuf, &frh}) v->release();
+        for (DevArray<float>* v : {&R32, &Tw32, &dT32, &frh32}) v->release();
+    }
     bool fp32() const { return mode_ == Mode::Fast32; }
     const void* state_R() const { return fp32() ? static_cast<const void*>(R32.get()) : R_; }
     void* state_Tw() { return fp32() ? static_cast<void*>(Tw32.get()) : Tw.get(); }

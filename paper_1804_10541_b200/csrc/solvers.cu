@@ -238,6 +238,11 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
         launch_downsample(G[l - 1], G[l], tp, T[l].get(), s);
     }
     check_launch("build_pyramid");
+    const auto t_start = std::chrono::steady_clock::now();
+    if (trace_time()) {
+        MFREG_CUDA(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "pyramid built\n");
+    }
 
     MultilevelResult out;
     DVec y, y0;
@@ -246,7 +251,10 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
     auto ms_since = [](std::chrono::steady_clock::time_point t) {
         return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
     };
+    auto t_prev_end = t_start;  // the previous level's objective is destroyed between its total and here
     for (int l = cfg.levels - 1; l >= 0; --l) {
+        if (trace_time() && l != cfg.levels - 1)
+            std::fprintf(stderr, "level %d: objective teardown %.2f ms\n", l + 1, ms_since(t_prev_end));
         const auto t_level = std::chrono::steady_clock::now();
         const Grid dg = deformation_grid_for(G[l], cfg.deform_ratio);
         const double* rp = l == 0 ? R_dev : R[l].get();
@@ -266,6 +274,7 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
                                                          : gauss_newton_minimize(obj, y0.get(), yl.get(), cfg.opt);
         MFREG_CUDA(cudaStreamSynchronize(s));
         if (trace_time()) std::fprintf(stderr, "level %d: total %.2f ms\n", l, ms_since(t_level));
+        t_prev_end = std::chrono::steady_clock::now();
         LevelResult lr{G[l], dg, std::move(res), DVec()};
         if (cfg.keep_level_y) {
             lr.y.resize(static_cast<std::size_t>(obj.dof()));
@@ -276,6 +285,7 @@ MultilevelResult register_multilevel(const double* R_dev, const double* T_dev, c
         prev = dg;
         have_prev = true;
     }
+    if (trace_time()) std::fprintf(stderr, "level 0: objective teardown %.2f ms\n", ms_since(t_prev_end));
     out.y = std::move(y);
     out.deform_grid = prev;
     return out;
