@@ -43,6 +43,18 @@
 #ifndef MFREG_HV2_EXP
 #define MFREG_HV2_EXP 0  // timing experiments only (wrong results): 1 no P^T collapse, 2 no halo items
 #endif
+#ifndef MFREG_HV2_PAD
+#define MFREG_HV2_PAD 1  // conflict-free P^T x stage (ptc.cuh): +1.7 KB of shared memory
+#endif
+#ifndef MFREG_HV2_BF
+#define MFREG_HV2_BF 1  // branch-free y flux stores (padded flux arrays: the last / first tile row writes a junk row)
+#endif
+#ifndef MFREG_HV2_PD
+#define MFREG_HV2_PD 0  // nodal interpolants kept as (P p at bz, difference to bz+1): the per-plane z lerp is one FMA
+#endif
+#ifndef MFREG_HV2_WF
+#define MFREG_HV2_WF 1  // w = sum_k rho_k s_{t+k} - sigma s_t (FMA chains) instead of sum_k rho_k (s_{t+k} - s_t)
+#endif
 
 namespace mfreg_b200 {
 
@@ -53,7 +65,7 @@ using namespace fdev;
 constexpr int TX = FT_X;                               // 32-column output tiles
 constexpr int DRING = 3;                               // dT staging slots (2 planes ahead)
 #ifndef MFREG_HV2_RRING
-#define MFREG_HV2_RRING 3  // measured: 2 (one plane ahead) is 3% slower at C4 even with the smem freed
+#define MFREG_HV2_RRING 2  // one plane ahead (3: 17 KB more shared memory, which the padded P^T rows need)
 #endif
 #ifndef MFREG_HV2_SLAB
 #define MFREG_HV2_SLAB 0   // nodal footprint in shared memory (1) or the interpolants read from L1/L2 (0)
@@ -72,6 +84,10 @@ struct Tl {
     static constexpr int NX_W = 2 * TX + 2 * TY;            // extra items [0, NX_W): ring-1 edges (P + W)
     static constexpr int NX_P = NX_W + 4 + 2 * TX + 2 * TY;  // then ring-1 corners, ring-2 edges (P only)
     static constexpr int MINB = TY == 8 ? 2 : 1;            // CTAs per SM
+    // consumer-indexed y flux arrays of one plane parity: +y at 0, -y at FM; branch-free stores pad
+    // each with a junk row (+y: after, written by the last tile row; -y: before, by the first)
+    static constexpr int FM = MFREG_HV2_BF ? NT + 2 * TX : NT;
+    static constexpr int FPAR = MFREG_HV2_BF ? 2 * NT + 2 * TX : 2 * NT;
 };
 
 // Box geometry per state precision: a TMA box must start 16-byte aligned in x, so the
@@ -153,15 +169,16 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     const int nxf = a.nxf, nyf = a.nyf, pl = nxf * nyf, nsl = 3 * pl;
     Real* const slab = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [NSL][3][nyf][nxf] nodal p footprint
     Real* const sS = slab + (SLAB ? NSL * nsl : 0);  // [2][NS] by plane parity
-    Real* const sF = sS + 2 * NS;               // [2][2][NT] consumer-indexed y fluxes by plane parity
-    Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
+    constexpr int FM = Tl<TY_>::FM, FPAR = Tl<TY_>::FPAR;
+    Real* const sF = sS + 2 * NS;               // [2][FPAR] consumer-indexed y fluxes by plane parity
+    Real* const sE = sF + 2 * FPAR;             // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
                                                 // then 2 zero entries (the edge-flux slot of inner lanes)
     Real* const sQ1 = sE + 2 * 2 * TY + 2;      // [6][NX_P] item-1 P p at nodal planes bz, bz+1
     // P^T collapse buffers and tables (ptc.cuh)
     Real* const sPt = sQ1 + 6 * NX_P;
-    int* const sZb = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw));  // [zc + 8] base_z of planes kfirst ..
+    int* const sZb = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw, MFREG_HV2_PAD));  // [zc + 8] base_z of planes kfirst ..
     int* const sI1 = sZb + tm.zc + 8;           // [NX_P] packed item-1 geometry
-    Ptc<Real, TY> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
+    Ptc<Real, TY, MFREG_HV2_PAD> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned barD = smem_u32(bars), barR = barD + 8 * DRING;
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
@@ -171,17 +188,17 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     const bool has1 = (MFREG_HV2_EXP & 2) ? false : tid < NX_P, w1 = (MFREG_HV2_EXP & 2) ? false : tid < NX_W;  // warp-aligned except warp 2 (split P+W / P) and warp 5
     // item-1 geometry, packed once into shared memory and re-read where it is used (keeping it
     // live in registers across the plane loop costs more than the loads): bits 0-9 the s-frame
-    // index c1, 10-19 the flux slot f1, 20-21 the coefficient toward the tile, 22 x edge
+    // index c1, 10-20 the flux slot f1, 21-22 the coefficient toward the tile, 23 x edge
     if (has1) {
         int lx1 = 0, ly1 = 0, dir1 = -1;
         extra_item<XO, TY>(tid, lx1, ly1, dir1);
         // where the ring-1 edge flux goes: y edges -> consumer-indexed sF (+y: 0, -y: 1), x edges -> sE
         const bool xedge = dir1 == 0 || dir1 == 1;
         const int f1 = xedge ? dir1 * TY + min(max(ly1 - 2, 0), TY - 1)
-                             : (dir1 - 2) * NT + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
+                             : (dir1 - 2) * FM + min(max(lx1 - XO, 0), TX - 1) + (dir1 == 2 ? 0 : TY - 1) * TX;
         const int ci = dir1 == 0 ? 1 : (dir1 == 1 ? 0 : (dir1 == 2 ? 3 : 2));
-        static_assert(G::NS <= 1024 && 2 * NT <= 1024, "item-1 packing");
-        sI1[tid] = (lx1 + ly1 * SX) | (max(f1, 0) << 10) | (ci << 20) | (xedge ? 1 << 22 : 0);
+        static_assert(G::NS <= 1024 && FPAR <= 2048, "item-1 packing");
+        sI1[tid] = (lx1 + ly1 * SX) | (max(f1, 0) << 10) | (ci << 21) | (xedge ? 1 << 23 : 0);
     }
     // (FAST32 has registers to spare: it keeps the packed word in one instead of reloading it)
     const int e1r = has1 ? sI1[tid] : 0;
@@ -364,6 +381,32 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             }
             const Real rxq = static_cast<Real>(rx0d), ry0 = static_cast<Real>(ry0d);
             const Real rx1r = static_cast<Real>(rx1), ry1r = static_cast<Real>(ry1);
+#if MFREG_HV2_PD
+            // (Pa, Pb) = (P p at bz, at bz+1 minus at bz); the shift to the next cell takes Pa + Pb
+            if (bzk == pz + 1) {
+                Pa0 += Pb0; Pa1 += Pb1; Pa2 += Pb2;
+                if (has1) {
+                    q1[0] += q1[3 * NX_P];
+                    q1[NX_P] += q1[4 * NX_P];
+                    q1[2 * NX_P] += q1[5 * NX_P];
+                }
+            } else {
+                bilerp(bzk, off0, rxq, ry0, Pa0, Pa1, Pa2);
+                if (has1) bilerp(bzk, off1, rx1r, ry1r, q1[0], q1[NX_P], q1[2 * NX_P]);
+            }
+            const int bz1 = min(bzk + 1, msz - 1);
+            {
+                Real b0, b1, b2;
+                bilerp(bz1, off0, rxq, ry0, b0, b1, b2);
+                Pb0 = b0 - Pa0; Pb1 = b1 - Pa1; Pb2 = b2 - Pa2;
+                if (has1) {
+                    bilerp(bz1, off1, rx1r, ry1r, b0, b1, b2);
+                    q1[3 * NX_P] = b0 - q1[0];
+                    q1[4 * NX_P] = b1 - q1[NX_P];
+                    q1[5 * NX_P] = b2 - q1[2 * NX_P];
+                }
+            }
+#else
             if (bzk == pz + 1) {
                 Pa0 = Pb0; Pa1 = Pb1; Pa2 = Pb2;
                 if (has1) {
@@ -378,6 +421,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             const int bz1 = min(bzk + 1, msz - 1);
             bilerp(bz1, off0, rxq, ry0, Pb0, Pb1, Pb2);
             if (has1) bilerp(bz1, off1, rx1r, ry1r, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
+#endif
             pz = bzk;
         }
         mbar_wait_at(barD + 8 * dslot, dphase);
@@ -385,7 +429,13 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         const Real* st = stgD + dslot * SLOT_DT;
         const Real* sr = stgR + rslot * SLOT_RH;
         // ---- P: plane k
+#if MFREG_HV2_PD
+        const Real pp0 = fma(rzk, Pb0, Pa0), pp1 = fma(rzk, Pb1, Pa1), pp2 = fma(rzk, Pb2, Pa2);
+        auto zl = [&](Real a0, Real d0) { return fma(rzk, d0, a0); };
+#else
         const Real pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
+        auto zl = [&](Real a0, Real b0) { return lerp(rzk, a0, b0); };
+#endif
         const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
         const Real s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
         sS[P * NS + c0] = s0;
@@ -393,50 +443,62 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         if (has1) {
             const int c1 = item1() & 0x3ff;
             const Real* q1 = sQ1 + tid;
-            s1 = fma(st[c1], lerp(rzk, q1[0], q1[3 * NX_P]),
-                     fma(st[NS + c1], lerp(rzk, q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * lerp(rzk, q1[2 * NX_P], q1[5 * NX_P])));
+            s1 = fma(st[c1], zl(q1[0], q1[3 * NX_P]),
+                     fma(st[NS + c1], zl(q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * zl(q1[2 * NX_P], q1[5 * NX_P])));
             sS[P * NS + c1] = s1;
         }
         // ---- W: plane j = k-1 (in-plane neighbours' s from the other parity buffer)
         const Real* sn = sS + (1 - P) * NS;
         const Real* rh = sr + w0;  // rho-hat of plane j, [6][NW]
-        Real* const Fj = sF + (1 - P) * 2 * NT;
+        Real* const Fj = sF + (1 - P) * FPAR;
         Real fzm, fzp_new, sw_new, gx_new;
         {
             const Real sj = sh0[1 - P];
+            const Real sg = ((rh[0] + rh[1 * NW]) + (rh[2 * NW] + rh[3 * NW])) + (rh[4 * NW] + rh[5 * NW]);
+#if MFREG_HV2_WF
+            const Real wa = fma(rh[1 * NW], sn[c0 + 1], rh[0] * sn[c0 - 1]);
+            const Real wb = fma(rh[3 * NW], sn[c0 + SX], rh[2 * NW] * sn[c0 - SX]);
+            const Real wc = fma(rh[5 * NW], s0, rh[4 * NW] * sh0[P]);
+            const Real w = fma(-sg, sj, (wa + wb) + wc);
+#else
             const Real wa = fma(rh[1 * NW], sn[c0 + 1] - sj, rh[0] * (sn[c0 - 1] - sj));
             const Real wb = fma(rh[3 * NW], sn[c0 + SX] - sj, rh[2 * NW] * (sn[c0 - SX] - sj));
             const Real wc = fma(rh[5 * NW], s0 - sj, rh[4 * NW] * (sh0[P] - sj));
             const Real w = (wa + wb) + wc;
-            const Real sg = ((rh[0] + rh[1 * NW]) + (rh[2 * NW] + rh[3 * NW])) + (rh[4 * NW] + rh[5 * NW]);
+#endif
             // x fluxes stay in the warp (one tile row): from lane-1 (+x) and lane+1 (-x)
             const Real fpx = __shfl_up_sync(0xffffffffu, rh[1 * NW] * w, 1);
             const Real fmx = __shfl_down_sync(0xffffffffu, rh[0] * w, 1);
             gx_new = fma(mpx, fpx, mmx * fmx);
-            if (ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;       // +y flux -> (tx, ty+1)
-            if (ty > 0) Fj[NT + tid - TX] = rh[2 * NW] * w;       // -y flux -> (tx, ty-1)
+            if (MFREG_HV2_BF || ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;  // +y flux -> (tx, ty+1)
+            if (MFREG_HV2_BF || ty > 0) Fj[FM + tid - TX] = rh[2 * NW] * w;  // -y flux -> (tx, ty-1)
             fzm = rh[4 * NW] * w;
             fzp_new = rh[5 * NW] * w;
             sw_new = sg * w;
         }
         if (w1) {  // ring-1 edge column: only the flux toward the tile
-            const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x3ff;
+            const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x7ff;
             const Real* rg = sr + c1 - SX;
             const Real sj = sh1[1 - P];
             const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
             const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
             const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
             const Real w = (wa + wb) + wc;
-            const Real cf = rg[((e1 >> 20) & 3) * NW];
-            if (e1 & (1 << 22)) sE[(1 - P) * 2 * TY + f1] = cf * w;
-            else Fj[f1] = cf * w;
+            const Real cf = rg[((e1 >> 21) & 3) * NW];
+            if constexpr (MFREG_HV2_BF) {
+                Real* const dst = (e1 & (1 << 23)) ? sE + (1 - P) * 2 * TY : Fj;
+                dst[f1] = cf * w;
+            } else {
+                if (e1 & (1 << 23)) sE[(1 - P) * 2 * TY + f1] = cf * w;
+                else Fj[f1] = cf * w;
+            }
         }
         // ---- Z: plane i = k-2 (tile columns)
         const int i = k - 2;
         if (i >= ilo && i < ihi) {  // uniform
-            const Real* Fi = sF + P * 2 * NT;
+            const Real* Fi = sF + P * FPAR;
             const Real ex = sE[eoff >= 0 ? P * 2 * TY + eoff : 4 * TY];  // ring-1 x edge flux (or zero)
-            const Real z = ((gx + ex) + (Fi[tid] + Fi[NT + tid])) + ((fzm + fzp[P]) - sw);
+            const Real z = ((gx + ex) + (Fi[tid] + Fi[FM + tid])) + ((fzm + fzp[P]) - sw);
             const Real sz = scale * z;  // dT (TMA zero fill) makes q vanish outside the volume
             const Real q0 = sz * dq[P][0], q1 = sz * dq[P][1], q2 = sz * dq[P][2];
             const int bz = zbase(i);
@@ -511,8 +573,8 @@ std::size_t smem_bytes(int nlx, int nly, int segw, int zc, int nsl) {
     const std::size_t ring = (static_cast<std::size_t>(DRING) * G::SLOT_DT + RRING * G::SLOT_RH) * sizeof(Real) + 64;
     const std::size_t dbl = (zc + 8) * sizeof(double);
     constexpr bool SLAB = MFREG_HV2_SLAB || sizeof(Real) == 4;
-    const std::size_t real = (static_cast<std::size_t>(SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * 2 * T::NT + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
-                              ptc_reals(T::TY, nlx, nly, segw)) *
+    const std::size_t real = (static_cast<std::size_t>(SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * T::FPAR + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
+                              ptc_reals(T::TY, nlx, nly, segw, MFREG_HV2_PAD)) *
                              sizeof(Real);
     return ring + dbl + real + (zc + 8 + ptc_ints(nlx) + T::NX_P) * sizeof(int);
 }

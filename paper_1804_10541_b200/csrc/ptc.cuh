@@ -9,37 +9,54 @@
 //    with a per-tile weight table and writes the tile partial of that nodal plane.
 // Replaces the segmented shuffle scan (fp64 shuffles are two SHFL + moves + selects per level and
 // value). Tables are built once per CTA; completions are >= 2 steps apart (host guarantee).
+// Bank layout (MFREG_PTC_PAD, default on): the lanes of the x stage read windows that start 4
+// columns apart (ratio 4), i.e. 32 bytes apart — 8-way bank conflicts on every fp64 load (ncu:
+// ~80% of both passes' excess shared wavefronts, a quarter of all their shared wavefronts). The row
+// buffer therefore stores logical column c at c + c/4 (one pad word per 4 columns) and the weight
+// table rows are WX + 1 long, which makes the window and weight loads of a warp conflict-free for
+// ratio-4 grids; windows that start 4-aligned (every tile of a ratio-4 grid) read with immediate
+// offsets, others compute the padded index per load.
 #pragma once
 
 #include "fused_dev.cuh"
+
+#ifndef MFREG_PTC_PAD
+#define MFREG_PTC_PAD 1
+#endif
 
 namespace mfreg_b200 {
 namespace fdev {
 
 constexpr int kPtcTX = FT_X;
 
-__host__ __device__ constexpr int ptc_row_len(int nlx) { return 3 * nlx > 3 * kPtcTX ? 3 * nlx : 3 * kPtcTX; }
+// physical index of logical row column c (pad: one pad word per 4 columns)
+__host__ __device__ constexpr int ptc_phys(int c, bool pad) { return pad ? c + (c >> 2) : c; }
+__host__ __device__ constexpr int ptc_row_len(int nlx, bool pad) {
+    return ptc_phys(3 * nlx > 3 * kPtcTX ? 3 * nlx : 3 * kPtcTX, pad) + (pad ? 1 : 0);
+}
 __host__ __device__ constexpr int ptc_win(int segw) { return 2 * segw < kPtcTX ? 2 * segw : kPtcTX; }
+__host__ __device__ constexpr int ptc_wstride(int segw, bool pad) { return ptc_win(segw) + (pad ? 1 : 0); }
 // shared-memory footprint: Reals (row buffers, weights) and ints (window starts, items)
-__host__ __device__ constexpr int ptc_reals(int ty, int nlx, int nly, int segw) {
-    return ty * ptc_row_len(nlx) + nlx * ptc_win(segw) + nly * ty;
+__host__ __device__ constexpr int ptc_reals(int ty, int nlx, int nly, int segw, bool pad = MFREG_PTC_PAD) {
+    return ty * ptc_row_len(nlx, pad) + nlx * ptc_wstride(segw, pad) + nly * ty;
 }
 __host__ __device__ constexpr int ptc_ints(int nlx) { return 4 * nlx; }
 
-template <typename Real, int TY>
+template <typename Real, int TY, bool PAD = MFREG_PTC_PAD>
 struct Ptc {
+    static __device__ __forceinline__ constexpr int ptc_phys(int c) { return fdev::ptc_phys(c, PAD); }
     Real* sA;   // [TY][XR] row buffers
-    Real* sWx;  // [nlx][WX] x weights of node j over columns xs[j] ..
+    Real* sWx;  // [nlx][WXS] x weights of node j over columns xs[j] ..
     Real* sWy;  // [nly][TY] y weights of node row lyn over the tile rows
     int* sXs;   // [nlx] first column of node j's window
-    int* sXi;   // [3 nlx] item L = d * nlx_t + j: window offset | weight offset << 8 | j << 20 | d << 26
-    int XR, WX, nxi, nlx, nly_t;
+    int* sXi;   // [3 nlx] item L = d * nlx_t + j: window offset (logical) | weight offset << 8 | j << 20 | d << 26
+    int XR, WX, WXS, nxi, nlx, nly_t;
 
     __device__ Ptc(Real* reals, int* ints, int nlx_, int nly_, int segw, int nlx_t, int nly_t_)
-        : XR(ptc_row_len(nlx_)), WX(ptc_win(segw)), nxi(3 * nlx_t), nlx(nlx_), nly_t(nly_t_) {
+        : XR(ptc_row_len(nlx_, PAD)), WX(ptc_win(segw)), WXS(ptc_wstride(segw, PAD)), nxi(3 * nlx_t), nlx(nlx_), nly_t(nly_t_) {
         sA = reals;
         sWx = sA + TY * XR;
-        sWy = sWx + nlx_ * WX;
+        sWy = sWx + nlx_ * WXS;
         sXs = ints;
         sXi = sXs + nlx_;
         (void)nly_;
@@ -64,7 +81,7 @@ struct Ptc {
                     const Real r = static_cast<Real>(__ldg(&a.P.rem[0][gx]));
                     w = b == j ? Real(1) - r : (b == j - 1 ? r : Real(0));
                 }
-                sWx[j * WX + t] = w;
+                sWx[j * WXS + t] = w;
             }
         }
         for (int t = tid; t < nly * TY; t += nthreads) {
@@ -83,15 +100,15 @@ struct Ptc {
         const int nlx_t = nxi / 3;
         for (int L = tid; L < nxi; L += nthreads) {
             const int d = L / nlx_t, j = L - d * nlx_t;
-            sXi[L] = (d * kPtcTX + sXs[j]) | ((j * WX) << 8) | (j << 20) | (d << 26);
+            sXi[L] = (d * kPtcTX + sXs[j]) | ((j * WXS) << 8) | (j << 20) | (d << 26);
         }
     }
     // x stage of tile row `row` (whole warp)
     __device__ void xstage(int row, int lane, Real v0, Real v1, Real v2) const {
         Real* ar = sA + row * XR;
-        ar[lane] = v0;
-        ar[kPtcTX + lane] = v1;
-        ar[2 * kPtcTX + lane] = v2;
+        ar[ptc_phys(lane)] = v0;
+        ar[ptc_phys(kPtcTX + lane)] = v1;
+        ar[ptc_phys(2 * kPtcTX + lane)] = v2;
         __syncwarp();
         const int npx = (nxi + 31) >> 5;  // host: nlx <= 42
         Real o[4];
@@ -101,13 +118,23 @@ struct Ptc {
             o[u] = Real(0);
             if (u < npx && L < nxi) {
                 const int e = sXi[L];
-                const Real* v = ar + (e & 0xff);
+                const int c0 = e & 0xff;  // logical first column of the window
                 const Real* w = sWx + ((e >> 8) & 0xfff);
                 Real acc0 = Real(0), acc1 = Real(0);  // WX is even: two chains
+                if (!PAD || (c0 & 3) == 0) {
+                    // 4-aligned window: the padded offsets t + t/4 are immediates
+                    const Real* v = ar + ptc_phys(c0);
+#pragma unroll 4
+                    for (int t = 0; t < WX; t += 2) {
+                        acc0 = fma(w[t], v[ptc_phys(t)], acc0);
+                        acc1 = fma(w[t + 1], v[ptc_phys(t + 1)], acc1);
+                    }
+                } else {
 #pragma unroll 2
-                for (int t = 0; t < WX; t += 2) {
-                    acc0 = fma(w[t], v[t], acc0);
-                    acc1 = fma(w[t + 1], v[t + 1], acc1);
+                    for (int t = 0; t < WX; t += 2) {
+                        acc0 = fma(w[t], ar[ptc_phys(c0 + t)], acc0);
+                        acc1 = fma(w[t + 1], ar[ptc_phys(c0 + t + 1)], acc1);
+                    }
                 }
                 o[u] = acc0 + acc1;
             }
@@ -116,7 +143,7 @@ struct Ptc {
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int L = lane + 32 * u;
-            if (u < npx && L < nxi) ar[L] = o[u];
+            if (u < npx && L < nxi) ar[ptc_phys(L)] = o[u];
         }
     }
     // FAST32 alternative of the x stage: a segmented shuffle scan over the lanes of one nodal cell
@@ -164,8 +191,8 @@ struct Ptc {
         for (int d = 0; d < 3; ++d) {
             const Real bp = __shfl_sync(0xffffffffu, B[d], max(g.sst - 1, 0));
             if (g.send && g.xin) {
-                dst[d * nlx_t + g.bx] = g.sst > 0 ? A[d] + bp : A[d];
-                if (g.xlast) dst[d * nlx_t + g.bx + 1] = B[d];
+                dst[ptc_phys(d * nlx_t + g.bx)] = g.sst > 0 ? A[d] + bp : A[d];
+                if (g.xlast) dst[ptc_phys(d * nlx_t + g.bx + 1)] = B[d];
             }
         }
     }
@@ -179,7 +206,9 @@ struct Ptc {
                 const int j = (e >> 20) & 0x3f, d = e >> 26;
                 Real v = Real(0);
 #pragma unroll
-                for (int r = 0; r < TY; ++r) v = fma(w[r], sA[r * XR + L], v);
+                const Real* col = sA + ptc_phys(L);
+#pragma unroll
+                for (int r = 0; r < TY; ++r) v = fma(w[r], col[r * XR], v);
                 pz[(lyn * nlx + j) * 3 + d] = v;
             }
         }
