@@ -352,6 +352,8 @@ int mfreg_cu_objective_eval(mfreg_cu_objective* obj, const double* y, double* gr
     return guard([&] {
         const idx_t nd = obj->obj->dof();
         if (!y) throw std::invalid_argument("Objective::eval: y length mismatch");
+        check_where(where);
+        if (where == MFREG_CU_HOST && grad && obj->obj->eval_host(y, grad, j)) return;  // copies pipelined
         In yi(y, nd, where, kStream, &obj->stage[0]);
         Out g(grad, nd, where, &obj->stage[1]);
         // one synchronisation: the gradient copy-out rides behind the scalar copy-out
@@ -372,6 +374,8 @@ int mfreg_cu_objective_last(mfreg_cu_objective* obj, double* distance, double* r
 int mfreg_cu_objective_gn_hessian_vec(mfreg_cu_objective* obj, const double* p, double* q, int where) {
     return guard([&] {
         const idx_t nd = obj->obj->dof();
+        check_where(where);
+        if (where == MFREG_CU_HOST && p && q && obj->obj->hv_host(p, q)) return;  // copies pipelined
         In pi(p, nd, where, kStream, &obj->stage[2]);
         Out o(q, nd, where, &obj->stage[3]);
         obj->obj->gn_hessian_vec(pi.ptr, o.ptr);

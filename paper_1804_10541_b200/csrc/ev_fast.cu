@@ -140,13 +140,14 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
     const long long n = a.g.count(), plane = static_cast<long long>(mx) * my;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int bzc = static_cast<int>(blockIdx.z) + a.zch0;  // z tile chunk (z-group launches)
+    const int z0 = tm.zlo + bzc * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
     const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);
     const int xe = min(mx, x0 + TX), ye = min(my, y0 + TY);
     const int nxA = __ldg(&a.P.base[0][x0]), nyA = __ldg(&a.P.base[1][y0]), nzA = __ldg(&a.P.base[2][z0]);
     const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
     const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
-    const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
+    const long long tile_id = (static_cast<long long>(bzc) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
     Real* const part = reinterpret_cast<Real*>(a.part) + tile_id * tm.part_stride;
     Real* const frh_out = reinterpret_cast<Real*>(a.frh_out);
     const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
@@ -390,7 +391,8 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
         a.vpart[tile_id] = s;
         if (a.vticket) {  // two-level completion ticket over the CTAs (32 group counters, then one)
             __threadfence();
-            const unsigned nct = gridDim.x * gridDim.y * gridDim.z, id = static_cast<unsigned>(tile_id);
+            // (over all tiles: a pass launched in z groups counts every group's CTAs)
+            const unsigned nct = static_cast<unsigned>(tm.ntx * tm.nty * tm.ntz), id = static_cast<unsigned>(tile_id);
             const unsigned g = id % 32u, ng = min(nct, 32u), gsize = (nct - g + 31u) / 32u;
             unsigned lst = 0;
             if (atomicAdd(a.vticket + 1 + g, 1u) == gsize - 1) {
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     if (!*s_last) return;
     // last CTA: D = h_bar * sum over tiles in tile order per thread, then a fixed tree
     __threadfence();
-    const unsigned nct = gridDim.x * gridDim.y * gridDim.z;
+    const unsigned nct = static_cast<unsigned>(tm.ntx * tm.nty * tm.ntz);
     double v = 0.0;
     for (unsigned t = tid; t < nct; t += NT) v += a.vpart[t];
 #pragma unroll
@@ -441,9 +443,10 @@ __global__ void __launch_bounds__(NT) k_ev_value(const __grid_constant__ FArgs a
     const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
     const long long plane = static_cast<long long>(mx) * my;
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int bzc = static_cast<int>(blockIdx.z) + a.zch0;  // z tile chunk (z-group launches)
+    const int z0 = tm.zlo + bzc * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
     const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);
-    const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
+    const long long tile_id = (static_cast<long long>(bzc) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
     const int gx0 = x0 + lane, gy0 = y0 + row;
     const bool in0 = gx0 < mx && gy0 < my;
     const Real m0xm = gx0 > 0 ? Real(1) : Real(0), m0xp = gx0 + 1 < mx ? Real(1) : Real(0);

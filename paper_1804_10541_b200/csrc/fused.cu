@@ -1294,8 +1294,12 @@ bool FusedPlan::make_tma_maps(const Grid& g, const void* R, const void* Tw, cons
 }
 
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     double tau, double rho, cudaStream_t s, const int* skip) {
+                     double tau, double rho, cudaStream_t s, const int* skip, int c0, int c1) {
     FArgs a = make_args(plan, fp);
+    const bool group = c0 != 0 || (c1 >= 0 && c1 != fp.meta().ntz);
+    if (group && (!fp.hv2() || fp.hv3())) throw std::logic_error("Hv pass z groups need the two-CTA kernel");
+    if (c1 < 0) c1 = fp.meta().ntz;
+    a.zch0 = c0;
     a.tau = tau;
     a.rho = rho;
     a.skip = skip;
@@ -1324,7 +1328,7 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
     note_launch();
     const std::size_t smem = fused_smem_bytes(t, a.nxf, a.nyf, false);
     if (fp.hv2()) {
-        hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, t.ntz), fp.hv2_smem(), s,
+        hv2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_hv2()), dim3(t.ntx, t.nty, c1 - c0), fp.hv2_smem(), s,
                    fp.fp32(), 8);
         return;
     }
@@ -1334,8 +1338,13 @@ void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* f
 }
 
 bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
-                       double tau, double rho, double* frh, bool grad, cudaStream_t s, double* d_dev, double* d_host) {
+                       double tau, double rho, double* frh, bool grad, cudaStream_t s, double* d_dev, double* d_host,
+                       int c0, int c1) {
     FArgs a = make_args(plan, fp);
+    const bool group = c0 != 0 || (c1 >= 0 && c1 != fp.meta().ntz);
+    if (group && !fp.ev2()) throw std::logic_error("eval pass z groups need the two-CTA kernel");
+    if (c1 < 0) c1 = fp.meta().ntz;
+    a.zch0 = c0;
     a.scale = -2.0 * a.g.cell_volume();
     a.tau = tau;
     a.rho = rho;
@@ -1353,14 +1362,14 @@ bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double*
             a.dsc = d_dev;
             a.dsc_host = d_host;
             a.dscale = plan.view().tgt.cell_volume();  // h_bar (ngf.cpp:227)
-            if (!grad && !frh && value_pass_enabled()) {  // Armijo trial: D only, bitwise k_ev2's D
+            if (!grad && !frh && value_pass_enabled() && !group) {  // Armijo trial: D only, bitwise k_ev2's D
                 ev_value_launch(a, fp.state_R(), fp.state_Tw(), dim3(t.ntx, t.nty, t.ntz), s, fp.fp32());
                 return true;
             }
         }
         // rho-hat by TMA store when the output is the state array the plan's map addresses
         a.frh_tma = (frh != nullptr && frh == fp.frh_base() && !(std::getenv("MFREG_NO_FRH_TMA"))) ? 1 : 0;
-        ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, t.ntz), fp.ev2_smem(), s,
+        ev2_launch(a, *reinterpret_cast<const TmaMaps*>(fp.maps_ev2()), dim3(t.ntx, t.nty, c1 - c0), fp.ev2_smem(), s,
                    fp.fp32());
         return a.vticket != nullptr;
     }
@@ -1377,6 +1386,11 @@ bool value_pass_enabled() {
         return !(e && e[0] == '1');
     }();
     return on;
+}
+
+bool& pdl_suspended() {
+    thread_local bool off = false;
+    return off;
 }
 
 bool pdl_enabled() {
@@ -1413,6 +1427,12 @@ void launch_nodal_finalize(const DevicePlanOwner& plan, FusedPlan& fp, const Fin
     const long long pn = a.gy.m[0] * a.gy.m[1];
     a.fin_lo = fp.fin_lo() * pn;
     a.nwin = (fp.fin_hi() - fp.fin_lo()) * pn;
+    if (spec.nlo >= 0) {  // a z range of the window (pure gather)
+        if (spec.sc || spec.dot_a || spec.value || spec.nlo < fp.fin_lo() || spec.nhi > fp.fin_hi() || spec.nhi <= spec.nlo)
+            throw std::logic_error("finalize: nodal z range only for pure gathers inside the window");
+        a.fin_lo = spec.nlo * pn;
+        a.nwin = (spec.nhi - spec.nlo) * pn;
+    }
     a.add_lo = fp.own_lo() * pn;
     a.add_hi = fp.own_hi() * pn;
     note_launch();

@@ -142,17 +142,19 @@ constexpr int kRhoDirs = 6;
 
 // Gauss-Newton Hv image pass: s = dT . P p -> w -> z -> q^ = 2h z dT -> P^T partials.
 // (tau, rho: the NGF parameters, used when the pass recomputes the coefficients, hv3)
+// [c0, c1): the z tile chunks of this launch (a z group of the two-CTA kernel; c1 < 0: all)
 void launch_hv_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* frh, const double* dT, const double* p,
-                     double tau, double rho, cudaStream_t s, const int* skip = nullptr);
+                     double tau, double rho, cudaStream_t s, const int* skip = nullptr, int c0 = 0, int c1 = -1);
 
 // Eval image pass on the warped state (T_w, dT from launch_warp): rho-hat (6 per
 // voxel, stored as Hv state), per-tile sums of (1 - r^2) and, when `grad`, the
 // NGF gradient -2h dT (dr^T r) spread by P^T into per-tile partials.
 // d_dev / d_host (optional): with the two-CTA kernel, its last CTA writes D there (returns
 // true); otherwise (legacy kernel) D is left to the finalize (returns false)
+// [c0, c1): z tile chunks of this launch (two-CTA kernel; the D ticket counts every group's CTAs)
 bool launch_eval_fused(const DevicePlanOwner& plan, FusedPlan& fp, const double* R, const double* Tw, const double* dT,
                        double tau, double rho, double* frh, bool grad, cudaStream_t s, double* d_dev = nullptr,
-                       double* d_host = nullptr);
+                       double* d_host = nullptr, int c0 = 0, int c1 = -1);
 
 // Nodal finalize (one launch):
 //   out != null: out = gather(P^T partials) [+ add];
@@ -171,9 +173,13 @@ struct FinalizeSpec {
     double* sc_host = nullptr;    // device view of mapped host scalars: value mode also writes D, alpha S there
     const int* skip = nullptr;    // device flag: skip the launch when set
     bool hv_pass = false;         // the partials come from the Hv pass (hv3 tiling when on)
+    int nlo = -1, nhi = -1;       // nodal z planes [nlo, nhi) only (pure gathers: out without sc); -1: the plan's window
 };
 // cudaLaunchKernelEx with programmatic stream serialisation (MFREG_NO_PDL=1: plain launch)
 bool pdl_enabled();
+// (host pipeline: the z groups launch without PDL, so a group's CTAs are not placed on the SMs
+// ahead of the previous group's finalize; per host thread)
+bool& pdl_suspended();
 bool value_pass_enabled();
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t smem, cudaStream_t s, Args&&... args) {
@@ -186,7 +192,7 @@ void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, std::size_t sme
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = pdl_enabled() && !pdl_suspended() ? 1 : 0;
     MFREG_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 

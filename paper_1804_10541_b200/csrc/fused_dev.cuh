@@ -39,6 +39,7 @@ struct FArgs {
     double* dsc;
     double* dsc_host;
     double dscale;
+    int zch0;  // first z tile chunk of this launch (a pass launched in z groups; blockIdx.z + zch0)
 };
 
 struct TmaMaps {

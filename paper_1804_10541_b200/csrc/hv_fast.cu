@@ -147,13 +147,14 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     const int tid = threadIdx.x, lane = tid & 31, row = tid >> 5;
     const int mx = static_cast<int>(a.g.m[0]), my = static_cast<int>(a.g.m[1]), mz = static_cast<int>(a.g.m[2]);
     const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-    const int z0 = tm.zlo + static_cast<int>(blockIdx.z) * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
+    const int bzc = static_cast<int>(blockIdx.z) + a.zch0;  // z tile chunk
+    const int z0 = tm.zlo + bzc * tm.zc, z1 = min(tm.zhi, z0 + tm.zc);
     const int ilo = max(z0, a.olo), ihi = min(z1, a.ohi);
     const int xe = min(mx, x0 + TX), ye = min(my, y0 + TY);
     const int nxA = __ldg(&a.P.base[0][x0]), nyA = __ldg(&a.P.base[1][y0]), nzA = __ldg(&a.P.base[2][z0]);
     const int nlx_t = __ldg(&a.P.base[0][xe - 1]) - nxA + 2;
     const int nly_t = __ldg(&a.P.base[1][ye - 1]) - nyA + 2;
-    const long long tile_id = (static_cast<long long>(blockIdx.z) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
+    const long long tile_id = (static_cast<long long>(bzc) * tm.nty + blockIdx.y) * tm.ntx + blockIdx.x;
     Real* const part = reinterpret_cast<Real*>(a.part) + tile_id * tm.part_stride;
     const std::size_t pstride = static_cast<std::size_t>(tm.nly) * nlx * 3;
     const int msx = static_cast<int>(a.P.src.m[0]), msy = static_cast<int>(a.P.src.m[1]);

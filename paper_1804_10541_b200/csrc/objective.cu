@@ -537,6 +537,12 @@ DeviceObjective::~DeviceObjective() {
     if (ev_fork_) cudaEventDestroy(ev_fork_);
     if (ev_join_) cudaEventDestroy(ev_join_);
     if (s2_) cudaStreamDestroy(s2_);
+    for (auto* v : {&pipe_.evh, &pipe_.eve, &pipe_.evf})
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
+    if (pipe_.ev0) cudaEventDestroy(pipe_.ev0);
+    if (pipe_.evd) cudaEventDestroy(pipe_.evd);
+    for (cudaStream_t q : {pipe_.h2d, pipe_.d2h, pipe_.fin})
+        if (q) cudaStreamDestroy(q);
 }
 
 double DeviceObjective::min_spacing() const { return std::min({dg_.h[0], dg_.h[1], dg_.h[2]}); }
@@ -674,6 +680,232 @@ double DeviceObjective::profile_kernel(int which, const double* p, int reps, std
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return total / std::max(1, reps);
+}
+
+// ---- host-buffer pipeline (eval_host / hv_host)
+// Plan, once per objective: G <= 4 z groups of the two-CTA passes' z tile chunks; per group the
+// image planes it covers, the nodal planes its warp / Hv pass reads (H2D chunk bounds: nodal
+// planes up to base_z + 1 of the group's last plane read, the Hv tiles two steps past it) and the
+// nodes complete after it (P^T of plane i touches base_z(i), base_z(i) + 1, so once the groups up
+// to g ran, the nodes below base_z of the next group's first plane are final).
+namespace {
+// MFREG_PIPE_TRACE=1: timing events along the host pipeline, printed per call (stderr)
+struct PipeTrace {
+    bool on = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> ev;
+    PipeTrace() {
+        const char* e = std::getenv("MFREG_PIPE_TRACE");
+        on = e && e[0] == '1';
+    }
+    void mark(const std::string& what, cudaStream_t s) {
+        if (!on) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, s);
+        ev.emplace_back(what, e);
+    }
+    void dump(const char* call) {
+        if (!on || ev.empty()) return;
+        cudaDeviceSynchronize();
+        std::fprintf(stderr, "%s:", call);
+        for (auto& [w, e] : ev) {
+            float ms = 0.0f;
+            cudaEventElapsedTime(&ms, ev[0].second, e);
+            std::fprintf(stderr, " %s %.3f", w.c_str(), ms);
+        }
+        std::fprintf(stderr, "\n");
+        for (auto& [w, e] : ev) cudaEventDestroy(e);
+        ev.clear();
+    }
+};
+PipeTrace& ptrace() {
+    static PipeTrace t;
+    return t;
+}
+}  // namespace
+
+bool DeviceObjective::pipe_ready() {
+    if (pipe_.state) return pipe_.state == 1;
+    pipe_.state = 2;
+    const char* off = std::getenv("MFREG_NO_PIPE");
+    if ((off && off[0] == '1') || !fused_ || sliced_ || !fused_->hv2() || !fused_->ev2() || fused_->hv3()) return false;
+    const TileMeta& t = fused_->meta();
+    const idx_t ny = dg_.count();
+    const char* mb = std::getenv("MFREG_PIPE_MIN_MB");  // (tests force it on small grids)
+    const long long min_bytes = (mb && *mb ? std::atoll(mb) : 16LL) << 20;
+    if (t.ntz < 2 || 3 * ny * static_cast<idx_t>(sizeof(double)) < min_bytes) return false;  // copies too small to hide
+    const int G = t.ntz >= 4 ? 2 + std::min(3, t.ntz - 2) : t.ntz, mz = static_cast<int>(img_.m[2]), msz = static_cast<int>(dg_.m[2]);
+    const auto& bz = plan_.host_base[2];
+    Pipe& q = pipe_;
+    q.G = G;
+    q.cb.resize(G + 1);
+    // one z tile chunk in the first group (the first H2D chunk is all the pipeline waits for) and
+    // in the last (its finalize and D2H are what remains exposed), the rest in up to three groups
+    // whose D2H each fits under the next group's pass; sizes 1, 2, 2, 2, 1 at C4 (8 chunks)
+    if (t.ntz >= 4) {
+        const int mid = G - 2;
+        q.cb[0] = 0;
+        for (int k = 0; k <= mid; ++k) q.cb[1 + k] = 1 + static_cast<int>((static_cast<long long>(k) * (t.ntz - 2)) / mid);
+        q.cb[G] = t.ntz;
+    } else
+        for (int g = 0; g <= G; ++g) q.cb[g] = static_cast<int>((static_cast<long long>(g) * t.ntz) / G);
+    q.za.resize(G);
+    q.zb.resize(G);
+    q.hb_warp.assign(G + 1, 0);
+    q.hb_hv.assign(G + 1, 0);
+    q.fb.assign(G + 1, 0);
+    for (int g = 0; g < G; ++g) {
+        q.za[g] = t.zlo + q.cb[g] * t.zc;
+        q.zb[g] = std::min(t.zhi, t.zlo + q.cb[g + 1] * t.zc);
+        const int lw = q.zb[g] - 1, lh = std::min(mz - 1, q.zb[g] + 1);
+        q.hb_warp[g + 1] = std::max(q.hb_warp[g], std::min(msz, bz[lw] + 2));
+        q.hb_hv[g + 1] = std::max(q.hb_hv[g], std::min(msz, bz[lh] + 2));
+        q.fb[g + 1] = g + 1 < G ? std::max(q.fb[g], bz[t.zlo + q.cb[g + 1] * t.zc]) : msz;
+    }
+    q.hb_warp[G] = q.hb_hv[G] = msz;
+    q.din.resize(3 * static_cast<std::size_t>(ny));
+    q.dout.resize(3 * static_cast<std::size_t>(ny));
+    for (cudaStream_t* st : {&q.h2d, &q.d2h}) MFREG_CUDA(cudaStreamCreateWithFlags(st, cudaStreamNonBlocking));
+    // the per-group finalize at the highest priority: otherwise the block scheduler keeps handing
+    // the SMs to the next group's image-pass CTAs and the gathers (and their D2H) slip to the end
+    int lo_prio = 0, hi_prio = 0;
+    MFREG_CUDA(cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio));
+    MFREG_CUDA(cudaStreamCreateWithPriority(&q.fin, cudaStreamNonBlocking, hi_prio));
+    auto mk = [](std::vector<cudaEvent_t>& v, int n) {
+        v.resize(n);
+        for (auto& e : v) MFREG_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    };
+    mk(q.evh, G);
+    mk(q.eve, G);
+    mk(q.evf, G);
+    MFREG_CUDA(cudaEventCreateWithFlags(&q.ev0, cudaEventDisableTiming));
+    MFREG_CUDA(cudaEventCreateWithFlags(&q.evd, cudaEventDisableTiming));
+    pipe_.state = 1;
+    return true;
+}
+
+void DeviceObjective::pipe_in(const double* host, const std::vector<int>& hb) {
+    Pipe& q = pipe_;
+    const idx_t ny = dg_.count(), pn = dg_.m[0] * dg_.m[1];
+    MFREG_CUDA(cudaEventRecord(q.ev0, s_));  // pin_in_ is free once the work before this call ran
+    MFREG_CUDA(cudaStreamWaitEvent(q.h2d, q.ev0, 0));
+    ptrace().mark("t0", q.h2d);
+    for (int g = 0; g < q.G; ++g) {
+        if (hb[g + 1] > hb[g])
+            for (int d = 0; d < 3; ++d) {
+                const idx_t off = d * ny + hb[g] * pn;
+                MFREG_CUDA(cudaMemcpyAsync(q.din.get() + off, host + off, (hb[g + 1] - hb[g]) * pn * sizeof(double),
+                                           cudaMemcpyHostToDevice, q.h2d));
+            }
+        MFREG_CUDA(cudaEventRecord(q.evh[g], q.h2d));
+        ptrace().mark("h2d" + std::to_string(g), q.h2d);
+    }
+}
+
+// group g's pass was just enqueued on s_: its nodes are gathered on the finalize stream and copied
+// out on the D2H stream while the next group runs
+void DeviceObjective::pipe_out(int g, double* host, bool hv) {
+    Pipe& q = pipe_;
+    const idx_t ny = dg_.count(), pn = dg_.m[0] * dg_.m[1];
+    MFREG_CUDA(cudaEventRecord(q.eve[g], s_));
+    ptrace().mark("pass" + std::to_string(g), s_);
+    MFREG_CUDA(cudaStreamWaitEvent(q.fin, q.eve[g], 0));
+    if (q.fb[g + 1] > q.fb[g]) {
+        FinalizeSpec f;
+        f.add = alpha_ != 0.0 ? curv_.get() : nullptr;
+        f.out = q.dout.get();
+        f.hv_pass = hv;
+        f.nlo = q.fb[g];
+        f.nhi = q.fb[g + 1];
+        launch_nodal_finalize(plan_, *fused_, f, q.fin);
+    }
+    MFREG_CUDA(cudaEventRecord(q.evf[g], q.fin));
+    ptrace().mark("fin" + std::to_string(g), q.fin);
+    MFREG_CUDA(cudaStreamWaitEvent(q.d2h, q.evf[g], 0));
+    if (q.fb[g + 1] > q.fb[g])
+        for (int d = 0; d < 3; ++d) {
+            const idx_t off = d * ny + q.fb[g] * pn;
+            MFREG_CUDA(cudaMemcpyAsync(host + off, q.dout.get() + off, (q.fb[g + 1] - q.fb[g]) * pn * sizeof(double),
+                                       cudaMemcpyDeviceToHost, q.d2h));
+        }
+    ptrace().mark("d2h" + std::to_string(g), q.d2h);
+}
+
+void DeviceObjective::pipe_sync() {
+    MFREG_CUDA(cudaEventRecord(pipe_.evd, pipe_.d2h));
+    MFREG_CUDA(cudaStreamWaitEvent(s_, pipe_.evd, 0));
+    MFREG_CUDA(cudaStreamSynchronize(s_));
+}
+
+bool DeviceObjective::eval_host(const double* y_host, double* grad_host, double* j) {
+    if (!y_host || !grad_host || !pipe_ready()) return false;
+    if (!(ngf_.tau_ > 0.0) || !(ngf_.rho_ > 0.0)) throw std::invalid_argument("NGF: tau and rho must be > 0");
+    Pipe& q = pipe_;
+    const idx_t ny = dg_.count();
+    const double* y = q.din.get();
+    pipe_in(y_host, q.hb_warp);
+    // curvature value / gradient once the whole operand is in, on the high-priority finalize
+    // stream (ahead of the group finalizes that add it): at normal priority its kernels queue
+    // behind the next image-pass group's CTAs and hold every finalize back to the last group
+    const cudaStream_t cs = q.fin;
+    MFREG_CUDA(cudaStreamWaitEvent(cs, q.evh[q.G - 1], 0));
+    launch_sub(3 * ny, y, xid_.get(), u_.get(), cs);
+    launch_lap3(dg_, u_.get(), lapu_.get(), cs, 0, -1, false);
+    red2_->sum(SUM_SQ, 3 * ny, lapu_.get(), nullptr, sc2_.get(), 1.0, cs);
+    launch_curv_value(sc2_.get(), dg_.cell_volume(), alpha_, sc_.dev(1), sc_.host_dev() + 1, cs);
+    if (alpha_ != 0.0)
+        launch_bilap(dg_, lapu_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), cs, 0,
+                     -1, false);
+    // warp per z group as its nodal planes arrive, then the eval pass per group
+    for (int g = 0; g < q.G; ++g) {
+        MFREG_CUDA(cudaStreamWaitEvent(s_, q.evh[g], 0));  // chunk g completes the group's nodal planes
+        warp_state(y, s_, q.za[g], q.zb[g], true);
+        ptrace().mark("warp" + std::to_string(g), s_);
+    }
+    struct NoPdl {
+        NoPdl() { pdl_suspended() = true; }
+        ~NoPdl() { pdl_suspended() = false; }
+    } nopdl;
+    for (int g = 0; g < q.G; ++g) {
+        launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, frh_out(), true,
+                          s_, sc_.dev(0), sc_.host_dev(), q.cb[g], q.cb[g + 1]);
+        pipe_out(g, grad_host, false);
+    }
+    check_launch("Objective::eval (host pipeline)");
+    pipe_sync();
+    ptrace().dump("eval_host");
+    stale_ = false;
+    const double v = eval_end();
+    if (j) *j = v;
+    return true;
+}
+
+bool DeviceObjective::hv_host(const double* p_host, double* q_host) {
+    if (!p_host || !q_host || !pipe_ready()) return false;
+    Pipe& q = pipe_;
+    refresh_state();
+    const double* p = q.din.get();
+    pipe_in(p_host, q.hb_hv);
+    if (alpha_ != 0.0) {  // (on the finalize stream, as in eval_host)
+        MFREG_CUDA(cudaStreamWaitEvent(q.fin, q.evh[q.G - 1], 0));
+        launch_lap3(dg_, p, lapp_.get(), q.fin, 0, -1, false);
+        launch_bilap(dg_, lapp_.get(), alpha_ * (2.0 * dg_.cell_volume()), 0, 0.0, 0.0, nullptr, curv_.get(), q.fin, 0,
+                     -1, false);
+    }
+    struct NoPdl {
+        NoPdl() { pdl_suspended() = true; }
+        ~NoPdl() { pdl_suspended() = false; }
+    } nopdl;
+    for (int g = 0; g < q.G; ++g) {
+        MFREG_CUDA(cudaStreamWaitEvent(s_, q.evh[g], 0));  // chunk g completes group g's planes
+        launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s_, nullptr, q.cb[g],
+                        q.cb[g + 1]);
+        pipe_out(g, q_host, true);
+    }
+    check_launch("Objective::gn_hessian_vec (host pipeline)");
+    pipe_sync();
+    ptrace().dump("hv_host");
+    return true;
 }
 
 // optimizer.cpp:64-92

@@ -338,6 +338,13 @@ public:
     // let the caller enqueue its own copies, synchronise once, then read J
     void eval_begin(const double* y, double* grad);
     double eval_end();
+    // host-buffer calls with the copies pipelined against the passes: the H2D of
+    // the operand in nodal z chunks ahead of the warp / Hv pass launched in z groups, each group's
+    // nodes finalized and copied out while the next group runs. Returns false (nothing done) when
+    // the pipeline does not apply (parity mode, z slabs, legacy kernels, small grids,
+    // MFREG_NO_PIPE=1); the caller then stages the buffers whole.
+    bool eval_host(const double* y_host, double* grad_host, double* j);
+    bool hv_host(const double* p_host, double* q_host);
     void gn_hessian_vec(const double* p, double* q) override;
     void seed_hessian_vec(const double* p, double gamma, double* q) override;
     double min_spacing() const override;
@@ -379,6 +386,22 @@ private:
     // where the eval pass stores rho-hat: nowhere when the Hv pass recomputes it (hv3)
     double* frh_out();
     void enqueue_hv_fast(const double* p, double* q, const double* dot_a, double* sc, const int* skip, cudaStream_t s);
+    bool pipe_ready();
+    void pipe_in(const double* host, const std::vector<int>& hb);  // H2D by nodal z chunks -> pin_in_
+    void pipe_out(int g, double* host, bool hv);                   // finalize group g's nodes -> D2H
+    void pipe_sync();
+    struct Pipe {
+        int state = 0;                        // 0 unset, 1 on, 2 off
+        int G = 0;                            // z groups
+        std::vector<int> cb;                  // [G + 1] z tile chunk bounds of the groups
+        std::vector<int> za, zb;              // image planes of group g
+        std::vector<int> hb_warp, hb_hv;      // [G + 1] nodal z bounds of the H2D chunks (eval / Hv)
+        std::vector<int> fb;                  // [G + 1] nodal z bounds of the per-group finalize
+        cudaStream_t h2d = nullptr, d2h = nullptr, fin = nullptr;
+        std::vector<cudaEvent_t> evh, eve, evf;
+        cudaEvent_t ev0 = nullptr, evd = nullptr;
+        DVec din, dout;
+    } pipe_;
     Grid img_, dg_;
     SlabSpec slab_;
     bool sliced_ = false;
