@@ -228,6 +228,73 @@ __device__ __forceinline__ void warp_sample_store(const DevPlan& P, const double
     dT[2 * n + i] = static_cast<OutT>(gzv * P.tgt.ih[2]);
 }
 
+// Fast-P-y sample (k_warp_z, points not within 1e-9 of a cell face): the caller has the sample
+// coordinate sa = p/h - 0.5 (FMA with the reciprocal), c = ceil(sa) and f = sa - (c - 1) (exactly
+// the fraction warp_sample_store forms through an integer round trip). Interior cells (every tap
+// inside the volume: all but a boundary shell) take 8 unpredicated loads from one base index;
+// boundary cells the per-tap zero fill. Same arithmetic as warp_sample_store, bitwise.
+template <typename OutT>
+__device__ __forceinline__ void warp_sample_store_c(const DevPlan& P, const double* __restrict__ T, const double c[3],
+                                                    const double f[3], int mx, int my, int mz, long long i, long long n,
+                                                    OutT* __restrict__ Tw, OutT* __restrict__ dT) {
+    const int m3[3] = {mx, my, mz};
+    int b[3];
+    bool inner = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        // (saturating conversion, then the clamp of warp_sample_store: far outside is all zero)
+        b[a] = min(max(__double2int_rz(c[a]), -4), m3[a] + 4) - 1;
+        inner = inner && static_cast<unsigned>(b[a]) < static_cast<unsigned>(m3[a] - 1);
+    }
+    const int plane = mx * my;
+    double t[2][2][2];
+    if (inner) {
+        const double* t0 = T + (b[0] + b[1] * mx + b[2] * plane);
+        const double* t1 = t0 + plane;
+        t[0][0][0] = __ldg(t0);
+        t[0][0][1] = __ldg(t0 + 1);
+        t[0][1][0] = __ldg(t0 + mx);
+        t[0][1][1] = __ldg(t0 + mx + 1);
+        t[1][0][0] = __ldg(t1);
+        t[1][0][1] = __ldg(t1 + 1);
+        t[1][1][0] = __ldg(t1 + mx);
+        t[1][1][1] = __ldg(t1 + mx + 1);
+    } else {
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+            for (int bb = 0; bb < 2; ++bb)
+#pragma unroll
+                for (int a = 0; a < 2; ++a) {
+                    const int ix = b[0] + a, iy = b[1] + bb, iz = b[2] + g;
+                    const bool ok = ix >= 0 && ix < mx && iy >= 0 && iy < my && iz >= 0 && iz < mz;
+                    t[g][bb][a] = ok ? __ldg(T + (ix + iy * mx + static_cast<long long>(iz) * plane)) : 0.0;
+                }
+    }
+    const double fx = f[0], fy = f[1], fz = f[2];
+    double cx[2][2], dx[2][2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+        for (int bb = 0; bb < 2; ++bb) {
+            dx[g][bb] = t[g][bb][1] - t[g][bb][0];
+            cx[g][bb] = fma(fx, dx[g][bb], t[g][bb][0]);
+        }
+    double cy[2], dyv[2], dxv[2];
+#pragma unroll
+    for (int g = 0; g < 2; ++g) {
+        dyv[g] = cx[g][1] - cx[g][0];
+        cy[g] = fma(fy, dyv[g], cx[g][0]);
+        dxv[g] = fma(fy, dx[g][1] - dx[g][0], dx[g][0]);
+    }
+    const double gzv = cy[1] - cy[0];
+    Tw[i] = static_cast<OutT>(fma(fz, gzv, cy[0]));
+    if (dT == nullptr) return;
+    dT[i] = static_cast<OutT>(fma(fz, dxv[1] - dxv[0], dxv[0]) * P.tgt.ih[0]);
+    dT[n + i] = static_cast<OutT>(fma(fz, dyv[1] - dyv[0], dyv[0]) * P.tgt.ih[1]);
+    dT[2 * n + i] = static_cast<OutT>(gzv * P.tgt.ih[2]);
+}
+
 __global__ void k_sample(Grid g, const double* __restrict__ T, const double* __restrict__ pts, idx_t n,
                          double* __restrict__ vals, double* __restrict__ dT) {
     const idx_t i = static_cast<idx_t>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -1150,7 +1217,7 @@ __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, con
         }
         if (in) {
             const double rz = __ldg(&P.rem[2][z]);
-            double pt[3];
+            double pt[3], c[3], f[3];
             bool near = true;
             if (fastpy) {
                 near = false;
@@ -1158,14 +1225,18 @@ __global__ void __launch_bounds__(256, MFREG_WARPZ_MINB) k_warp_z(DevPlan P, con
                 for (int d = 0; d < 3; ++d) {
                     pt[d] = fma(rz, Pd[d], Pa[d]);
                     const double sa = fma(pt[d], P.tgt.ih[d], -0.5);
-                    near = near || fabs(sa - rint(sa)) < 1e-9;
+                    c[d] = ceil(sa);
+                    f[d] = sa - (c[d] - 1.0);  // in (0, 1]: 1 at a tie
+                    near = near || f[d] < 1e-9 || f[d] > 1.0 - 1e-9;
                 }
             }
             if (near) {
                 ptof(rz, pt);
                 warp_sample_store(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
             } else {
-                warp_sample_store<OutT, false>(P, T, pt, x, yy, z, mx, my, mz, Tw, dT);
+                const long long n = static_cast<long long>(mx) * my * mz;
+                warp_sample_store_c(P, T, c, f, mx, my, mz, x + static_cast<long long>(yy) * mx + static_cast<long long>(z) * mx * my,
+                                    n, Tw, dT);
             }
         }
         ++z;
