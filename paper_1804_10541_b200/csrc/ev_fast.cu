@@ -162,8 +162,10 @@ __global__ void __launch_bounds__(NT, sizeof(Real) == 4 ? 3 : 2) k_ev2(const __g
     Real* const sF = reinterpret_cast<Real*>(sred + NT / 32);  // [2][2][NT] consumer-indexed y fluxes
     Real* const sE = sF + 2 * 2 * NT;           // [2][2][TY] x fluxes from the ring-1 x edges by plane parity
     Real* const sPt = sE + 2 * 2 * TY;          // P^T collapse buffers and tables (ptc.cuh)
-    int* const sI1 = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw));  // [NX_A] packed item 1
-    Ptc<Real, TY> ptc(sPt, sI1 + NX_A, nlx, tm.nly, segw, nlx_t, nly_t);
+    // (conflict-free padded P^T rows for fp64; FAST32 measured faster without them)
+    constexpr bool PAD = MFREG_PTC_PAD && sizeof(Real) == 8;
+    int* const sI1 = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw, PAD));  // [NX_A] packed item 1
+    Ptc<Real, TY, PAD> ptc(sPt, sI1 + NX_A, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned bar0 = smem_u32(bars);
 
     // ---- columns: item 0 = tile column (lane, row); item 1 (threads < 80) = ring-1 edge column
@@ -527,7 +529,7 @@ std::size_t smem_bytes(int nlx, int nly, int segw) {
     using G = Geo<Real>;
     return static_cast<std::size_t>(RING) * G::SLOT * sizeof(Real) + 2 * 6 * NT * sizeof(Real) + 48 +
            (NT / 32) * sizeof(double) +
-           (2 * 2 * NT + 2 * 2 * TY + static_cast<std::size_t>(ptc_reals(TY, nlx, nly, segw))) * sizeof(Real) +
+           (2 * 2 * NT + 2 * 2 * TY + static_cast<std::size_t>(ptc_reals(TY, nlx, nly, segw, MFREG_PTC_PAD && sizeof(Real) == 8))) * sizeof(Real) +
            (NX_A + ptc_ints(nlx)) * sizeof(int);
 }
 }  // namespace

@@ -70,7 +70,14 @@ constexpr int DRING = 3;                               // dT staging slots (2 pl
 #ifndef MFREG_HV2_SLAB
 #define MFREG_HV2_SLAB 0   // nodal footprint in shared memory (1) or the interpolants read from L1/L2 (0)
 #endif
-constexpr int RRING = MFREG_HV2_RRING;                 // rho-hat staging slots (RRING - 1 planes ahead)
+// per precision: the shared-memory-bound switches apply to fp64 (FAST32 measured 1.3% slower with
+// them: its 4-byte rows conflict less and its rho-hat ring of 3 fits anyway)
+template <typename Real>
+struct Cfg {
+    static constexpr bool F64 = sizeof(Real) == 8;
+    static constexpr int RRING = F64 ? MFREG_HV2_RRING : 3;  // rho-hat staging slots (RRING - 1 planes ahead)
+    static constexpr bool PAD = F64 && MFREG_HV2_PAD, BF = F64 && MFREG_HV2_BF, WF = F64 && MFREG_HV2_WF;
+};
 constexpr int NSL = 4;                                 // nodal plane ring (power of 2)
 
 // Tile height variants: 32 x 8 (256 threads, two CTAs per SM; shares the eval pass's tiling) and
@@ -86,8 +93,10 @@ struct Tl {
     static constexpr int MINB = TY == 8 ? 2 : 1;            // CTAs per SM
     // consumer-indexed y flux arrays of one plane parity: +y at 0, -y at FM; branch-free stores pad
     // each with a junk row (+y: after, written by the last tile row; -y: before, by the first)
-    static constexpr int FM = MFREG_HV2_BF ? NT + 2 * TX : NT;
-    static constexpr int FPAR = MFREG_HV2_BF ? 2 * NT + 2 * TX : 2 * NT;
+    template <bool BF>
+    static constexpr int FM = BF ? NT + 2 * TX : NT;
+    template <bool BF>
+    static constexpr int FPAR = BF ? 2 * NT + 2 * TX : 2 * NT;
 };
 
 // Box geometry per state precision: a TMA box must start 16-byte aligned in x, so the
@@ -134,6 +143,8 @@ struct Par {
 template <typename Real, int TY_>
 __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid_constant__ FArgs a, const __grid_constant__ TmaMaps maps) {
     using G = Geo<Real, TY_>;
+    using C = Cfg<Real>;
+    constexpr int RRING = C::RRING;
     // FAST32 keeps the nodal footprint in shared memory (its smem has room; the L1/L2 reads of the
     // interpolants at a plane change stall it); fp64 reads them from L1/L2 (no room for the ring)
     constexpr bool SLAB = MFREG_HV2_SLAB || sizeof(Real) == 4;
@@ -170,16 +181,16 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     const int nxf = a.nxf, nyf = a.nyf, pl = nxf * nyf, nsl = 3 * pl;
     Real* const slab = reinterpret_cast<Real*>(sZr + tm.zc + 8);  // [NSL][3][nyf][nxf] nodal p footprint
     Real* const sS = slab + (SLAB ? NSL * nsl : 0);  // [2][NS] by plane parity
-    constexpr int FM = Tl<TY_>::FM, FPAR = Tl<TY_>::FPAR;
+    constexpr int FM = Tl<TY_>::template FM<C::BF>, FPAR = Tl<TY_>::template FPAR<C::BF>;
     Real* const sF = sS + 2 * NS;               // [2][FPAR] consumer-indexed y fluxes by plane parity
     Real* const sE = sF + 2 * FPAR;             // [2][2][TY] x fluxes from the ring-1 x edges by plane parity,
                                                 // then 2 zero entries (the edge-flux slot of inner lanes)
     Real* const sQ1 = sE + 2 * 2 * TY + 2;      // [6][NX_P] item-1 P p at nodal planes bz, bz+1
     // P^T collapse buffers and tables (ptc.cuh)
     Real* const sPt = sQ1 + 6 * NX_P;
-    int* const sZb = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw, MFREG_HV2_PAD));  // [zc + 8] base_z of planes kfirst ..
+    int* const sZb = reinterpret_cast<int*>(sPt + ptc_reals(TY, nlx, tm.nly, segw, C::PAD));  // [zc + 8] base_z of planes kfirst ..
     int* const sI1 = sZb + tm.zc + 8;           // [NX_P] packed item-1 geometry
-    Ptc<Real, TY, MFREG_HV2_PAD> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
+    Ptc<Real, TY, C::PAD> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned barD = smem_u32(bars), barR = barD + 8 * DRING;
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
@@ -456,23 +467,24 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         {
             const Real sj = sh0[1 - P];
             const Real sg = ((rh[0] + rh[1 * NW]) + (rh[2 * NW] + rh[3 * NW])) + (rh[4 * NW] + rh[5 * NW]);
-#if MFREG_HV2_WF
-            const Real wa = fma(rh[1 * NW], sn[c0 + 1], rh[0] * sn[c0 - 1]);
-            const Real wb = fma(rh[3 * NW], sn[c0 + SX], rh[2 * NW] * sn[c0 - SX]);
-            const Real wc = fma(rh[5 * NW], s0, rh[4 * NW] * sh0[P]);
-            const Real w = fma(-sg, sj, (wa + wb) + wc);
-#else
-            const Real wa = fma(rh[1 * NW], sn[c0 + 1] - sj, rh[0] * (sn[c0 - 1] - sj));
-            const Real wb = fma(rh[3 * NW], sn[c0 + SX] - sj, rh[2 * NW] * (sn[c0 - SX] - sj));
-            const Real wc = fma(rh[5 * NW], s0 - sj, rh[4 * NW] * (sh0[P] - sj));
-            const Real w = (wa + wb) + wc;
-#endif
+            Real w;
+            if constexpr (C::WF) {
+                const Real wa = fma(rh[1 * NW], sn[c0 + 1], rh[0] * sn[c0 - 1]);
+                const Real wb = fma(rh[3 * NW], sn[c0 + SX], rh[2 * NW] * sn[c0 - SX]);
+                const Real wc = fma(rh[5 * NW], s0, rh[4 * NW] * sh0[P]);
+                w = fma(-sg, sj, (wa + wb) + wc);
+            } else {
+                const Real wa = fma(rh[1 * NW], sn[c0 + 1] - sj, rh[0] * (sn[c0 - 1] - sj));
+                const Real wb = fma(rh[3 * NW], sn[c0 + SX] - sj, rh[2 * NW] * (sn[c0 - SX] - sj));
+                const Real wc = fma(rh[5 * NW], s0 - sj, rh[4 * NW] * (sh0[P] - sj));
+                w = (wa + wb) + wc;
+            }
             // x fluxes stay in the warp (one tile row): from lane-1 (+x) and lane+1 (-x)
             const Real fpx = __shfl_up_sync(0xffffffffu, rh[1 * NW] * w, 1);
             const Real fmx = __shfl_down_sync(0xffffffffu, rh[0] * w, 1);
             gx_new = fma(mpx, fpx, mmx * fmx);
-            if (MFREG_HV2_BF || ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;  // +y flux -> (tx, ty+1)
-            if (MFREG_HV2_BF || ty > 0) Fj[FM + tid - TX] = rh[2 * NW] * w;  // -y flux -> (tx, ty-1)
+            if (C::BF || ty + 1 < TY) Fj[tid + TX] = rh[3 * NW] * w;  // +y flux -> (tx, ty+1)
+            if (C::BF || ty > 0) Fj[FM + tid - TX] = rh[2 * NW] * w;  // -y flux -> (tx, ty-1)
             fzm = rh[4 * NW] * w;
             fzp_new = rh[5 * NW] * w;
             sw_new = sg * w;
@@ -486,7 +498,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
             const Real w = (wa + wb) + wc;
             const Real cf = rg[((e1 >> 21) & 3) * NW];
-            if constexpr (MFREG_HV2_BF) {
+            if constexpr (C::BF) {
                 Real* const dst = (e1 & (1 << 23)) ? sE + (1 - P) * 2 * TY : Fj;
                 dst[f1] = cf * w;
             } else {
@@ -571,11 +583,12 @@ template <typename Real, int TY_>
 std::size_t smem_bytes(int nlx, int nly, int segw, int zc, int nsl) {
     using G = Geo<Real, TY_>;
     using T = Tl<TY_>;
-    const std::size_t ring = (static_cast<std::size_t>(DRING) * G::SLOT_DT + RRING * G::SLOT_RH) * sizeof(Real) + 64;
+    using C = Cfg<Real>;
+    const std::size_t ring = (static_cast<std::size_t>(DRING) * G::SLOT_DT + C::RRING * G::SLOT_RH) * sizeof(Real) + 64;
     const std::size_t dbl = (zc + 8) * sizeof(double);
     constexpr bool SLAB = MFREG_HV2_SLAB || sizeof(Real) == 4;
-    const std::size_t real = (static_cast<std::size_t>(SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * T::FPAR + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
-                              ptc_reals(T::TY, nlx, nly, segw, MFREG_HV2_PAD)) *
+    const std::size_t real = (static_cast<std::size_t>(SLAB ? NSL * nsl : 0) + 2 * static_cast<std::size_t>(G::NS) + 2 * T::template FPAR<C::BF> + 2 * 2 * T::TY + 2 + 6 * T::NX_P +
+                              ptc_reals(T::TY, nlx, nly, segw, C::PAD)) *
                              sizeof(Real);
     return ring + dbl + real + (zc + 8 + ptc_ints(nlx) + T::NX_P) * sizeof(int);
 }
