@@ -451,14 +451,6 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
         const Real s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
         sS[P * NS + c0] = s0;
-        Real s1 = 0.0;
-        if (has1) {
-            const int c1 = item1() & 0x3ff;
-            const Real* q1 = sQ1 + tid;
-            s1 = fma(st[c1], zl(q1[0], q1[3 * NX_P]),
-                     fma(st[NS + c1], zl(q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * zl(q1[2 * NX_P], q1[5 * NX_P])));
-            sS[P * NS + c1] = s1;
-        }
         // ---- W: plane j = k-1 (in-plane neighbours' s from the other parity buffer)
         const Real* sn = sS + (1 - P) * NS;
         const Real* rh = sr + w0;  // rho-hat of plane j, [6][NW]
@@ -489,23 +481,6 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             fzp_new = rh[5 * NW] * w;
             sw_new = sg * w;
         }
-        if (w1) {  // ring-1 edge column: only the flux toward the tile
-            const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x7ff;
-            const Real* rg = sr + c1 - SX;
-            const Real sj = sh1[1 - P];
-            const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
-            const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
-            const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
-            const Real w = (wa + wb) + wc;
-            const Real cf = rg[((e1 >> 21) & 3) * NW];
-            if constexpr (C::BF) {
-                Real* const dst = (e1 & (1 << 23)) ? sE + (1 - P) * 2 * TY : Fj;
-                dst[f1] = cf * w;
-            } else {
-                if (e1 & (1 << 23)) sE[(1 - P) * 2 * TY + f1] = cf * w;
-                else Fj[f1] = cf * w;
-            }
-        }
         // ---- Z: plane i = k-2 (tile columns)
         const int i = k - 2;
         if (i >= ilo && i < ihi) {  // uniform
@@ -531,6 +506,33 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             acc11 = fma(rz, q1, acc11);
             acc02 = fma(Real(1) - rz, q2, acc02);
             acc12 = fma(rz, q2, acc12);
+        }
+        // ---- halo items (after the tile column's P, W and Z: one basic block the compiler can
+        // interleave; their s and fluxes are read in the next step)
+        Real s1 = 0.0;
+        if (has1) {
+            const int c1 = item1() & 0x3ff;
+            const Real* q1 = sQ1 + tid;
+            s1 = fma(st[c1], zl(q1[0], q1[3 * NX_P]),
+                     fma(st[NS + c1], zl(q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * zl(q1[2 * NX_P], q1[5 * NX_P])));
+            sS[P * NS + c1] = s1;
+        }
+        if (w1) {  // ring-1 edge column: only the flux toward the tile
+            const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x7ff;
+            const Real* rg = sr + c1 - SX;
+            const Real sj = sh1[1 - P];
+            const Real wa = fma(rg[1 * NW], sn[c1 + 1] - sj, rg[0] * (sn[c1 - 1] - sj));
+            const Real wb = fma(rg[3 * NW], sn[c1 + SX] - sj, rg[2 * NW] * (sn[c1 - SX] - sj));
+            const Real wc = fma(rg[5 * NW], s1 - sj, rg[4 * NW] * (sh1[P] - sj));
+            const Real w = (wa + wb) + wc;
+            const Real cf = rg[((e1 >> 21) & 3) * NW];
+            if constexpr (C::BF) {
+                Real* const dst = (e1 & (1 << 23)) ? sE + (1 - P) * 2 * TY : Fj;
+                dst[f1] = cf * w;
+            } else {
+                if (e1 & (1 << 23)) sE[(1 - P) * 2 * TY + f1] = cf * w;
+                else Fj[f1] = cf * w;
+            }
         }
         // ---- histories
         dq[P][0] = D0;
