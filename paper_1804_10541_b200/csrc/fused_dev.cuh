@@ -81,6 +81,9 @@ __device__ __forceinline__ void mbar_wait_at(unsigned bar, unsigned parity) {
         "r"(parity)
         : "memory");
 }
+__device__ __forceinline__ void mbar_arrive_at(unsigned bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
     asm volatile(
         "{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"

@@ -46,6 +46,9 @@
 #ifndef MFREG_HV2_PAD
 #define MFREG_HV2_PAD 1  // conflict-free P^T x stage (ptc.cuh): +1.7 KB of shared memory
 #endif
+#ifndef MFREG_HV2_SPLIT
+#define MFREG_HV2_SPLIT 0  // split (arrive / wait) step barrier on an mbarrier
+#endif
 #ifndef MFREG_HV2_BF
 #define MFREG_HV2_BF 1  // branch-free y flux stores (padded flux arrays: the last / first tile row writes a junk row)
 #endif
@@ -192,6 +195,11 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     int* const sI1 = sZb + tm.zc + 8;           // [NX_P] packed item-1 geometry
     Ptc<Real, TY, C::PAD> ptc(sPt, sI1 + NX_P, nlx, tm.nly, segw, nlx_t, nly_t);
     const unsigned barD = smem_u32(bars), barR = barD + 8 * DRING;
+    // split step barrier (fp64, MFREG_HV2_SPLIT): threads arrive on an mbarrier at the end of a
+    // step and wait for it only after the next step's TMA wait, nodal interpolants and P values,
+    // which touch nothing another thread writes (FAST32's shared nodal ring would)
+    constexpr bool SPLIT = MFREG_HV2_SPLIT && sizeof(Real) == 8 && !SLAB;
+    const unsigned barS = barD + 8 * 7;
 
     // ---- per-thread columns: item 0 = tile column (tx, ty) = (lane, row); item 1 = extra halo column
     const int tx = lane, ty = row;
@@ -289,6 +297,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     }
     if (tid == 0) {
         for (int b = 0; b < DRING + RRING; ++b) mbar_init(&bars[b], 1);
+        if (SPLIT) mbar_init(&bars[7], NT);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
 
@@ -360,11 +369,18 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     int cur = nzA, ypend = -1;
     const Real scale = a.scale;
 
+#define STEP_END()                                               \
+    do {                                                         \
+        if constexpr (SPLIT) mbar_arrive_at(barS);               \
+        else __syncthreads();                                    \
+    } while (0)
     auto step = [&](auto parc, int k) {
         constexpr int P = decltype(parc)::P;
+        if constexpr (!SPLIT) {
         // refill the slots step k-1 read (free since the barrier)
         if (k + 2 <= klast) HV2_ISSUE_D(k + 2, dslot == 0 ? DRING - 1 : dslot - 1);
         if (k + RRING - 1 <= klast) HV2_ISSUE_R(k + RRING - 2, rslot == 0 ? RRING - 1 : rslot - 1);
+        }
         bool slab_pending = false;
         int slab_nz = 0;
         {
@@ -376,9 +392,11 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
                 slab_hi = nzq;
             }
         }
+        if constexpr (!SPLIT) {
         if (ypend >= 0) {  // y collapse of the plane completed last step (sA published by the barrier)
             ystage(ypend);
             ypend = -1;
+        }
         }
         const int bzk = zbase(k);
         const Real rzk = zrem(k);
@@ -450,7 +468,30 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
 #endif
         const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
         const Real s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
+        Real s1 = 0.0;
+        auto halo_s = [&]() {  // s of the halo item (stored by the caller)
+            if (has1) {
+                const int c1 = item1() & 0x3ff;
+                const Real* q1 = sQ1 + tid;
+                s1 = fma(st[c1], zl(q1[0], q1[3 * NX_P]),
+                         fma(st[NS + c1], zl(q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * zl(q1[2 * NX_P], q1[5 * NX_P])));
+            }
+        };
+        if constexpr (SPLIT) {
+        halo_s();
+        // the previous step's barrier: everything above only read this step's TMA slots and
+        // own registers / sQ1 entries; from here on the shared buffers of the previous step
+        if (k != kfirst) mbar_wait_at(barS, (k - kfirst - 1) & 1);
+        // refill the slots step k-1 read (free since the barrier)
+        if (k + 2 <= klast) HV2_ISSUE_D(k + 2, dslot == 0 ? DRING - 1 : dslot - 1);
+        if (k + RRING - 1 <= klast) HV2_ISSUE_R(k + RRING - 2, rslot == 0 ? RRING - 1 : rslot - 1);
+        if (ypend >= 0) {  // y collapse of the plane completed last step (sA published by the barrier)
+            ystage(ypend);
+            ypend = -1;
+        }
+        }
         sS[P * NS + c0] = s0;
+        if (SPLIT && has1) sS[P * NS + (item1() & 0x3ff)] = s1;
         // ---- W: plane j = k-1 (in-plane neighbours' s from the other parity buffer)
         const Real* sn = sS + (1 - P) * NS;
         const Real* rh = sr + w0;  // rho-hat of plane j, [6][NW]
@@ -509,13 +550,9 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         }
         // ---- halo items (after the tile column's P, W and Z: one basic block the compiler can
         // interleave; their s and fluxes are read in the next step)
-        Real s1 = 0.0;
-        if (has1) {
-            const int c1 = item1() & 0x3ff;
-            const Real* q1 = sQ1 + tid;
-            s1 = fma(st[c1], zl(q1[0], q1[3 * NX_P]),
-                     fma(st[NS + c1], zl(q1[NX_P], q1[4 * NX_P]), st[2 * NS + c1] * zl(q1[2 * NX_P], q1[5 * NX_P])));
-            sS[P * NS + c1] = s1;
+        if constexpr (!SPLIT) {  // (halo items after the tile column's P, W and Z: one basic block)
+            halo_s();
+            if (has1) sS[P * NS + (item1() & 0x3ff)] = s1;
         }
         if (w1) {  // ring-1 edge column: only the flux toward the tile
             const int e1 = item1(), c1 = e1 & 0x3ff, f1 = (e1 >> 10) & 0x7ff;
@@ -552,7 +589,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             rphase ^= 1u;
         }
         if (slab_pending) slab_store(slab_nz);
-        __syncthreads();
+        STEP_END();
     };
     // pairs of steps without a conditional second step (no register moves on the back edge),
     // then the odd last step
@@ -564,6 +601,7 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
     }
     if (k <= klast) step(Par<0>{}, k);
     pdl_trigger();  // the finalize may be scheduled while the tiles flush
+    if constexpr (SPLIT) __syncthreads();  // (the last step only arrived)
     // ---- flush: pending y collapse, then the last two nodal planes
     if (ypend >= 0) ystage(ypend);
     __syncthreads();
