@@ -510,6 +510,10 @@ DeviceObjective::DeviceObjective(const double* R_dev, const double* T_dev, const
         red2_ = std::make_unique<Reducer>(Mode::Fast, 3 * dg_.count());
         curv_.resize(3 * ny);
         sc2_.resize(4);
+        // the lazy value-only state's y copy, allocated here rather than inside the first Armijo
+        // trial: allocated there (stream-ordered pool, behind the CG's queued work) it measured
+        // 0.3-0.8 s stalls on the first trial of each C4 level-0 solve after the first registration
+        if (!sliced_ && !no_lazy_state()) ylazy_.resize(3 * ny);
     }
 }
 
