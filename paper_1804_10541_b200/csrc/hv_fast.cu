@@ -52,9 +52,6 @@
 #ifndef MFREG_HV2_BF
 #define MFREG_HV2_BF 1  // branch-free y flux stores (padded flux arrays: the last / first tile row writes a junk row)
 #endif
-#ifndef MFREG_HV2_PD
-#define MFREG_HV2_PD 0  // nodal interpolants kept as (P p at bz, difference to bz+1): the per-plane z lerp is one FMA
-#endif
 #ifndef MFREG_HV2_WF
 #define MFREG_HV2_WF 1  // w = sum_k rho_k s_{t+k} - sigma s_t (FMA chains) instead of sum_k rho_k (s_{t+k} - s_t)
 #endif
@@ -411,32 +408,6 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             }
             const Real rxq = static_cast<Real>(rx0d), ry0 = static_cast<Real>(ry0d);
             const Real rx1r = static_cast<Real>(rx1), ry1r = static_cast<Real>(ry1);
-#if MFREG_HV2_PD
-            // (Pa, Pb) = (P p at bz, at bz+1 minus at bz); the shift to the next cell takes Pa + Pb
-            if (bzk == pz + 1) {
-                Pa0 += Pb0; Pa1 += Pb1; Pa2 += Pb2;
-                if (has1) {
-                    q1[0] += q1[3 * NX_P];
-                    q1[NX_P] += q1[4 * NX_P];
-                    q1[2 * NX_P] += q1[5 * NX_P];
-                }
-            } else {
-                bilerp(bzk, off0, rxq, ry0, Pa0, Pa1, Pa2);
-                if (has1) bilerp(bzk, off1, rx1r, ry1r, q1[0], q1[NX_P], q1[2 * NX_P]);
-            }
-            const int bz1 = min(bzk + 1, msz - 1);
-            {
-                Real b0, b1, b2;
-                bilerp(bz1, off0, rxq, ry0, b0, b1, b2);
-                Pb0 = b0 - Pa0; Pb1 = b1 - Pa1; Pb2 = b2 - Pa2;
-                if (has1) {
-                    bilerp(bz1, off1, rx1r, ry1r, b0, b1, b2);
-                    q1[3 * NX_P] = b0 - q1[0];
-                    q1[4 * NX_P] = b1 - q1[NX_P];
-                    q1[5 * NX_P] = b2 - q1[2 * NX_P];
-                }
-            }
-#else
             if (bzk == pz + 1) {
                 Pa0 = Pb0; Pa1 = Pb1; Pa2 = Pb2;
                 if (has1) {
@@ -451,7 +422,6 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
             const int bz1 = min(bzk + 1, msz - 1);
             bilerp(bz1, off0, rxq, ry0, Pb0, Pb1, Pb2);
             if (has1) bilerp(bz1, off1, rx1r, ry1r, q1[3 * NX_P], q1[4 * NX_P], q1[5 * NX_P]);
-#endif
             pz = bzk;
         }
         mbar_wait_at(barD + 8 * dslot, dphase);
@@ -459,13 +429,8 @@ __global__ void __launch_bounds__(Tl<TY_>::NT, Tl<TY_>::MINB) k_hv2(const __grid
         const Real* st = stgD + dslot * SLOT_DT;
         const Real* sr = stgR + rslot * SLOT_RH;
         // ---- P: plane k
-#if MFREG_HV2_PD
-        const Real pp0 = fma(rzk, Pb0, Pa0), pp1 = fma(rzk, Pb1, Pa1), pp2 = fma(rzk, Pb2, Pa2);
-        auto zl = [&](Real a0, Real d0) { return fma(rzk, d0, a0); };
-#else
         const Real pp0 = lerp(rzk, Pa0, Pb0), pp1 = lerp(rzk, Pa1, Pb1), pp2 = lerp(rzk, Pa2, Pb2);
         auto zl = [&](Real a0, Real b0) { return lerp(rzk, a0, b0); };
-#endif
         const Real D0 = st[c0], D1 = st[NS + c0], D2 = st[2 * NS + c0];
         const Real s0 = fma(D0, pp0, fma(D1, pp1, D2 * pp2));
         Real s1 = 0.0;
