@@ -11,17 +11,19 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [((128, 96, 120), (0.7, 0.7, 0.7), 4), ((96, 64, 80), (0.97, 0.97, 2.5), 3), ((160, 128, 64), (1.0, 1.0, 1.0), 4)]
+SHAPES = [((128, 96, 120), (0.7, 0.7, 0.7), 4, 1.0), ((96, 64, 80), (0.97, 0.97, 2.5), 3, 1.0),
+          ((160, 128, 64), (1.0, 1.0, 1.0), 4, 0.0), ((160, 160, 64), (1.0, 1.0, 1.0), 4, 1.0),
+          ((64, 64, 260), (1.0, 1.0, 1.0), 4, 0.5)]
 
 
-def _run(P, torch, R, T, m, h, ratio, mode, y, p, host, pipe):
+def _run(P, torch, R, T, m, h, ratio, alpha, mode, y, p, host, pipe):
     env = {"MFREG_PIPE_MIN_MB": "0", "MFREG_NO_PIPE": "0" if pipe else "1"}
     old = {k: os.environ.get(k) for k in env}
     os.environ.update(env)
     try:
         img = P.make_image_grid(m, h)
         dg = P.deformation_grid_for(img, ratio)
-        obj = P.Objective(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda(), img, dg, P.NgfParams(), 1.0, mode)
+        obj = P.Objective(torch.from_numpy(R).cuda(), torch.from_numpy(T).cuda(), img, dg, P.NgfParams(), alpha, mode)
         n0 = P.launch_count()
         if host:
             g = np.empty_like(y)
@@ -45,11 +47,11 @@ def _run(P, torch, R, T, m, h, ratio, mode, y, p, host, pipe):
 
 
 @pytest.mark.parametrize("mode", ["fast", "fast32"])
-@pytest.mark.parametrize("case", SHAPES, ids=lambda c: "x".join(map(str, c[0])) + f"_r{c[2]}")
+@pytest.mark.parametrize("case", SHAPES, ids=lambda c: "x".join(map(str, c[0])) + f"_r{c[2]}_a{c[3]}")
 def test_host_pipeline_bitwise(P, oracle, case, mode):
     import torch
 
-    m, h, ratio = case
+    m, h, ratio, alpha = case
     md = P.Mode.FAST if mode == "fast" else P.Mode.FAST32
     if md == P.Mode.FAST32 and m[0] % 4:
         pytest.skip("FAST32 needs mx % 4 == 0")
@@ -60,9 +62,9 @@ def test_host_pipeline_bitwise(P, oracle, case, mode):
     rng = np.random.default_rng(5)
     y = dg.point_coords() + rng.uniform(-0.4, 0.4, 3 * dg.count())
     p = rng.uniform(-1.0, 1.0, 3 * dg.count())
-    jd, gd, qd, _ = _run(P, torch, R, T, m, h, ratio, md, y, p, host=False, pipe=False)
-    jh, gh, qh, n_pipe = _run(P, torch, R, T, m, h, ratio, md, y, p, host=True, pipe=True)
-    js, gs, qs, n_staged = _run(P, torch, R, T, m, h, ratio, md, y, p, host=True, pipe=False)
+    jd, gd, qd, _ = _run(P, torch, R, T, m, h, ratio, alpha, md, y, p, host=False, pipe=False)
+    jh, gh, qh, n_pipe = _run(P, torch, R, T, m, h, ratio, alpha, md, y, p, host=True, pipe=True)
+    js, gs, qs, n_staged = _run(P, torch, R, T, m, h, ratio, alpha, md, y, p, host=True, pipe=False)
     assert n_pipe > n_staged, "the pipelined host path did not run (no z groups)"
     for a, b in ((gh, gd), (qh, qd), (gs, gd), (qs, qd)):
         assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
