@@ -43,6 +43,10 @@ WORKLOADS = {
            "name": "C4 finest level: 512x512x900 image (h=0.7) / 129x129x226 nodal, eval(grad) + gn_hessian_vec"},
     "c2": {"m": (128, 128, 128), "h": (1.0, 1.0, 1.0), "sample_m": (128, 128, 128),
            "name": "C2 finest level: 128^3 image / 33^3 nodal, eval(grad) + gn_hessian_vec"},
+    # BASELINE configs[4]: the derivative-only sweep (no registration; fp64 state ~103 GB on one
+    # GPU, so the FAST32 line, which would need a second objective, is left out)
+    "c5": {"m": (1024, 1024, 1024), "h": (1.0, 1.0, 1.0), "sample_m": (1024, 1024, 8), "derivative_only": True,
+           "name": "C5 derivative sweep: 1024^3 image / 257^3 nodal, eval(grad) + gn_hessian_vec"},
 }
 B_CANON_GRAD = 48.0  # R, T read; T_w, dT written (fp64)
 B_CANON_HV = 40.0    # R, T_w, dT read (fp64)
@@ -438,7 +442,7 @@ def run_ours(args, rank, world, local):
 
     # the optional fp32 mode (FAST32) on the same workload: operator rate and Hv kernel time
     fast32 = None
-    if mode == P.Mode.FAST and world == 1 and not args.no_fast32:
+    if mode == P.Mode.FAST and world == 1 and not args.no_fast32 and not wl.get("derivative_only"):
         o32 = P.Objective(R, T, img, dg, P.NgfParams(10.0, 10.0), 1.0, P.Mode.FAST32)
         for _ in range(3):
             o32.eval(y, grad)
@@ -467,7 +471,7 @@ def run_ours(args, rank, world, local):
     # same run in FAST32; the CPU reference's wall time for the same iteration counts,
     # extrapolated from its measured per-voxel costs
     gn = None
-    if not args.no_gn and world == 1 and mode == P.Mode.FAST:
+    if not args.no_gn and world == 1 and mode == P.Mode.FAST and not wl.get("derivative_only"):
         gn = {"workload": f"{wl['m'][0]}x{wl['m'][1]}x{wl['m'][2]} h={wl['h'][0]}, {LEVELS} levels, ratio {RATIO}",
               "method": "gauss-newton"}
         sizes, mm = [], list(wl["m"])
@@ -595,7 +599,7 @@ def run_slabs(args, rank, world, local):
                 "traffic": None, "kernel": "gn_hessian_vec per rank (slab incl. NCCL halo exchange)",
                 "algorithmic_bytes_per_voxel": B_CANON_HV, "units_per_launch": n_loc, "peak_source": peak_kind}
     gn = None
-    if not args.no_gn:
+    if not args.no_gn and not wl.get("derivative_only"):
         cfg = P.MultilevelConfig(levels=LEVELS, deform_ratio=RATIO, method=P.Method.GAUSS_NEWTON, mode=md)
         walls = []
         for _ in range(2):  # cold, then warm
