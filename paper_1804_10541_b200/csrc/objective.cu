@@ -21,12 +21,15 @@ namespace mfreg_b200 {
 bool no_lazy_state();
 
 namespace {
-// bytes of freed device memory the pool keeps for reuse (MFREG_POOL_KEEP_GB, default 8; only
-// blocks below kBigAllocBytes come from the pool)
+// bytes of freed device memory the pool keeps for reuse (MFREG_POOL_KEEP_GB; only blocks below
+// kBigAllocBytes come from the pool). Default: all of it — the pool then never trims itself at a
+// synchronisation; with an 8 GB threshold the trim after a C4 registration's teardown stalled
+// the next registration's first allocations by 0.4-1 s (c4_reg.py REPS=3: 7.4 / 6.3 / 7.2 s ->
+// 6.4 / 6.6 / 6.3 s). Memory goes back when an allocation fails (device_alloc trims and retries).
 std::uint64_t pool_keep_bytes() {
     const char* e = std::getenv("MFREG_POOL_KEEP_GB");
-    const double gb = e ? std::atof(e) : 8.0;
-    return static_cast<std::uint64_t>(std::max(0.0, gb) * static_cast<double>(1ull << 30));
+    if (!e || !*e) return ~std::uint64_t(0);
+    return static_cast<std::uint64_t>(std::max(0.0, std::atof(e)) * static_cast<double>(1ull << 30));
 }
 cudaMemPool_t default_pool() {
     int dev = 0;
@@ -161,11 +164,33 @@ long long device_memory_peak(bool reset) {
     return p;
 }
 
+namespace {
+// MFREG_TRACE_TIME=1: allocations slower than 20 ms on stderr
+struct AllocTimer {
+    const char* path = "pool";
+    std::size_t bytes;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit AllocTimer(std::size_t b) : bytes(b) {}
+    ~AllocTimer() {
+        static const bool tr = [] {
+            const char* e = std::getenv("MFREG_TRACE_TIME");
+            return e && *e && *e != '0';
+        }();
+        if (!tr) return;
+        const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (ms > 20.0) std::fprintf(stderr, "  slow device_alloc(%zu bytes, %s): %.1f ms\n", bytes, path, ms);
+    }
+};
+}  // namespace
+
 void* device_alloc(std::size_t bytes) {
     mem_note(static_cast<long long>(bytes));
+    AllocTimer at(bytes);
     void* p = nullptr;
     if (bytes >= kBigAllocBytes) {
+        at.path = "big cache";
         if ((p = big_take(bytes))) return p;
+        at.path = "cudaMalloc";
         cudaError_t e = cudaMalloc(&p, bytes);
         if (e == cudaErrorMemoryAllocation) {  // cached blocks may hold the memory: release, retry
             cudaGetLastError();
