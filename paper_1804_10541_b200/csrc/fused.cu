@@ -934,7 +934,7 @@ FArgs make_args(const DevicePlanOwner& plan, FusedPlan& fp) {
 }  // namespace
 
 FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
-                     const SlabSpec& slab, bool fp32)
+                     const SlabSpec& slab, bool fp32, int zc_cap)
     : fp32_(fp32), state_R_(R), state_Tw_(Tw) {
     const DevPlan& P = plan.view();
     const Grid& g = P.tgt;
@@ -959,9 +959,34 @@ FusedPlan::FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw,
     // two-CTA Hv kernel (the eval kernel runs 2 CTAs/SM in fp64, 3 in FAST32)
     const long long nxy = static_cast<long long>(t.ntx) * t.nty;
     const int mz = t.zhi - t.zlo;
-    // (chunks of <= zmax planes: the two-CTA kernels keep per-chunk z tables in shared memory)
-    const char* zenv = std::getenv("MFREG_ZC_MAX");
-    const int zmax = zenv ? std::max(4, std::atoi(zenv)) : 128;  // measured: longer chunks stream slower
+    // (chunks of <= zmax planes: the two-CTA Hv kernel keeps per-chunk z tables in shared memory,
+    // 12 B per plane, so zmax is what its shared-memory budget leaves; the round-1 cap of 128 planes
+    // — then measured faster — measured 3% slower than 450-plane chunks at C4 with the current
+    // kernels, which stream L2-friendlier with fewer halo steps; MFREG_ZC_MAX overrides)
+    int zmax = 1 << 20;
+    {
+        int nlxy[2];
+        const int tsz2[2] = {FT_X, FT_Y}, ntl2[2] = {t.ntx, t.nty};
+        for (int a = 0; a < 2; ++a) {
+            const auto& base = plan.host_base[a];
+            nlxy[a] = 0;
+            for (int k = 0; k < ntl2[a]; ++k) {
+                const int x0 = k * tsz2[a], x1 = std::min(static_cast<int>(g.m[a]), x0 + tsz2[a]);
+                nlxy[a] = std::max(nlxy[a], base[x1 - 1] + 1 - base[x0] + 1);
+            }
+        }
+        int sw = 1, run = 1;  // longest run of image columns sharing a nodal x cell (segw_ below)
+        for (std::size_t k = 1; k < plan.host_base[0].size(); ++k) {
+            run = plan.host_base[0][k] == plan.host_base[0][k - 1] ? run + 1 : 1;
+            sw = std::max(sw, run);
+        }
+        const std::size_t s0 = hv2_smem_bytes(nlxy[0], nlxy[1], sw, 0, hv2_nsl_max(8), fp32, 8);
+        const std::size_t s1 = hv2_smem_bytes(nlxy[0], nlxy[1], sw, 1, hv2_nsl_max(8), fp32, 8);
+        if (s0 < static_cast<std::size_t>(kSmem2Cta) && s1 > s0)
+            zmax = std::max(16, static_cast<int>((static_cast<std::size_t>(kSmem2Cta) - s0) / (s1 - s0)) - 8);
+    }
+    if (const char* zenv = std::getenv("MFREG_ZC_MAX")) zmax = std::max(4, std::atoi(zenv));
+    if (zc_cap > 0) zmax = std::min(zmax, zc_cap);
     int best = (mz + zmax - 1) / zmax;
     double best_cost = 1e300;
     for (int ntz = (mz + zmax - 1) / zmax; ntz <= std::max((mz + zmax - 1) / zmax, mz / 4); ++ntz) {

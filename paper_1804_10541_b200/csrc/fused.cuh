@@ -49,8 +49,10 @@ public:
     // built over them when TMA can address the grid)
     // `slab`: z window; the full domain when slab.full()
     // fp32: the state arrays are single precision (FAST32 mode; two-CTA kernels only)
+    // zc_cap > 0: z tile chunks of at most that many planes (the host-buffer pipeline's plan);
+    // 0: as the shared-memory budget of the z tables allows (MFREG_ZC_MAX overrides)
     FusedPlan(const DevicePlanOwner& plan, const void* R, const void* Tw, const void* dT, const void* frh,
-              const SlabSpec& slab, bool fp32 = false);
+              const SlabSpec& slab, bool fp32 = false, int zc_cap = 0);
     bool fp32() const { return fp32_; }
     const void* state_R() const { return state_R_; }    // the arrays the passes read (fp64 or FAST32)
     const void* state_Tw() const { return state_Tw_; }

@@ -758,7 +758,18 @@ bool DeviceObjective::pipe_ready() {
     pipe_.state = 2;
     const char* off = std::getenv("MFREG_NO_PIPE");
     if ((off && off[0] == '1') || !fused_ || sliced_ || !fused_->hv2() || !fused_->ev2() || fused_->hv3()) return false;
-    const TileMeta& t = fused_->meta();
+    // A plan of its own, on z chunks of <= 128 planes: the pipeline's granularity is the z tile
+    // chunk, and the device-call plan's long chunks (2 x 450 planes at C4, 3% faster passes) would
+    // leave it half of the operand to copy before the first group and half to copy back after the
+    // last (e2e 33.4 -> 28.5 Gvoxel/s). Same kernels and state arrays; the results differ from the
+    // device calls' in the last bits (per-tile sums over other plane ranges).
+    pipe_.fp = std::make_unique<FusedPlan>(plan_, ngf_.state_R(), ngf_.state_Tw(), ngf_.state_dT(), ngf_.state_frh(),
+                                           slab_, ngf_.fp32(), 128);
+    if (!pipe_.fp->hv2() || !pipe_.fp->ev2() || pipe_.fp->hv3()) {
+        pipe_.fp.reset();
+        return false;
+    }
+    const TileMeta& t = pipe_.fp->meta();
     const idx_t ny = dg_.count();
     const char* mb = std::getenv("MFREG_PIPE_MIN_MB");  // (tests force it on small grids)
     const long long min_bytes = (mb && *mb ? std::atoll(mb) : 16LL) << 20;
@@ -846,7 +857,7 @@ void DeviceObjective::pipe_out(int g, double* host, bool hv) {
         f.hv_pass = hv;
         f.nlo = q.fb[g];
         f.nhi = q.fb[g + 1];
-        launch_nodal_finalize(plan_, *fused_, f, q.fin);
+        launch_nodal_finalize(plan_, *q.fp, f, q.fin);
     }
     MFREG_CUDA(cudaEventRecord(q.evf[g], q.fin));
     ptrace().mark("fin" + std::to_string(g), q.fin);
@@ -896,7 +907,7 @@ bool DeviceObjective::eval_host(const double* y_host, double* grad_host, double*
         ~NoPdl() { pdl_suspended() = false; }
     } nopdl;
     for (int g = 0; g < q.G; ++g) {
-        launch_eval_fused(plan_, *fused_, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, frh_out(), true,
+        launch_eval_fused(plan_, *q.fp, ngf_.R_, ngf_.Tw.get(), ngf_.dT.get(), ngf_.tau_, ngf_.rho_, frh_out(), true,
                           s_, sc_.dev(0), sc_.host_dev(), q.cb[g], q.cb[g + 1]);
         pipe_out(g, grad_host, false);
     }
@@ -927,7 +938,7 @@ bool DeviceObjective::hv_host(const double* p_host, double* q_host) {
     } nopdl;
     for (int g = 0; g < q.G; ++g) {
         MFREG_CUDA(cudaStreamWaitEvent(s_, q.evh[g], 0));  // chunk g completes group g's planes
-        launch_hv_fused(plan_, *fused_, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s_, nullptr, q.cb[g],
+        launch_hv_fused(plan_, *q.fp, ngf_.frh.get(), ngf_.dT.get(), p, ngf_.tau_, ngf_.rho_, s_, nullptr, q.cb[g],
                         q.cb[g + 1]);
         pipe_out(g, q_host, true);
     }

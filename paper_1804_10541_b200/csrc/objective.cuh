@@ -401,6 +401,7 @@ private:
         std::vector<cudaEvent_t> evh, eve, evf;
         cudaEvent_t ev0 = nullptr, evd = nullptr;
         DVec din, dout;
+        std::unique_ptr<class FusedPlan> fp;  // the same passes on z chunks of <= 128 planes
     } pipe_;
     Grid img_, dg_;
     SlabSpec slab_;
