@@ -48,7 +48,7 @@ cudaMemPool_t default_pool() {
 
 namespace {
 // Freed blocks of kBigAllocBytes and more are kept for reuse by an allocation of the same size
-// (MFREG_BIG_CACHE_GB, default 32: a C4 registration's levels need ~25 GB; 0 = plain cudaFree): objectives are created per pyramid level
+// (MFREG_BIG_CACHE_GB, default 64: a C4 registration's levels need ~30 GB; 0 = plain cudaFree): objectives are created per pyramid level
 // and per call, and cudaFree of their tens of GB of state measured up to ~1 s per teardown at C4,
 // growing with repeated registrations (scripts/c4_reg.py, MFREG_TRACE_TIME=1). A cached block is
 // handed out again only after a device synchronisation at its release (cudaFree's own ordering),
@@ -65,7 +65,7 @@ BigCache& big_cache() {
 std::size_t big_cache_limit() {
     static const std::size_t lim = [] {
         const char* e = std::getenv("MFREG_BIG_CACHE_GB");
-        const double gb = e ? std::atof(e) : 32.0;
+        const double gb = e ? std::atof(e) : 64.0;
         return static_cast<std::size_t>(std::max(0.0, gb) * static_cast<double>(1ull << 30));
     }();
     return lim;

@@ -39,11 +39,14 @@ enum class Mode : int { Parity = 0, Fast = 1, Fast32 = 2 };
 
 // Device allocations come from the device's default stream-ordered pool (allocated and
 // freed on the legacy stream, which all library work is ordered with) with up to
-// MFREG_POOL_KEEP_GB (default 8) kept cached: objectives are created per pyramid level and per call, and
+// MFREG_POOL_KEEP_GB kept cached: objectives are created per pyramid level and per call, and
 // cudaMalloc/cudaFree of their state cost tens of milliseconds with a wide spread.
-// (blocks of kBigAllocBytes and more use plain cudaMalloc / cudaFree: growing the pool by tens of
-// GB on first use measured 0.6-4 s against 0.05 s for cudaMalloc)
-constexpr std::size_t kBigAllocBytes = std::size_t(256) << 20;
+// (blocks of kBigAllocBytes and more use cudaMalloc and an exact-size cache of freed blocks:
+// growing the pool by tens of GB on first use measured 0.6-4 s against 0.05 s for cudaMalloc, and
+// pool allocations of 90-180 MB measured 0.1-0.5 s stalls when a registration's level objectives
+// were rebuilt — the 256 MB threshold of earlier let the per-level nodal and partial arrays
+// through the pool)
+constexpr std::size_t kBigAllocBytes = std::size_t(32) << 20;
 void* device_alloc(std::size_t bytes);
 // high-water mark of the library's live device allocations since load (or the last reset)
 long long device_memory_peak(bool reset);
