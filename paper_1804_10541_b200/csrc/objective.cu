@@ -758,6 +758,10 @@ bool DeviceObjective::pipe_ready() {
     pipe_.state = 2;
     const char* off = std::getenv("MFREG_NO_PIPE");
     if ((off && off[0] == '1') || !fused_ || sliced_ || !fused_->hv2() || !fused_->ev2() || fused_->hv3()) return false;
+    const idx_t ny = dg_.count();
+    const char* mb = std::getenv("MFREG_PIPE_MIN_MB");  // (tests force it on small grids)
+    const long long min_bytes = (mb && *mb ? std::atoll(mb) : 16LL) << 20;
+    if (3 * ny * static_cast<idx_t>(sizeof(double)) < min_bytes) return false;  // copies too small to hide
     // A plan of its own, on z chunks of <= 128 planes: the pipeline's granularity is the z tile
     // chunk, and the device-call plan's long chunks (2 x 450 planes at C4, 3% faster passes) would
     // leave it half of the operand to copy before the first group and half to copy back after the
@@ -770,10 +774,10 @@ bool DeviceObjective::pipe_ready() {
         return false;
     }
     const TileMeta& t = pipe_.fp->meta();
-    const idx_t ny = dg_.count();
-    const char* mb = std::getenv("MFREG_PIPE_MIN_MB");  // (tests force it on small grids)
-    const long long min_bytes = (mb && *mb ? std::atoll(mb) : 16LL) << 20;
-    if (t.ntz < 2 || 3 * ny * static_cast<idx_t>(sizeof(double)) < min_bytes) return false;  // copies too small to hide
+    if (t.ntz < 2) {  // one z chunk: nothing to pipeline
+        pipe_.fp.reset();
+        return false;
+    }
     const int G = t.ntz >= 4 ? 2 + std::min(3, t.ntz - 2) : t.ntz, mz = static_cast<int>(img_.m[2]), msz = static_cast<int>(dg_.m[2]);
     const auto& bz = plan_.host_base[2];
     Pipe& q = pipe_;
