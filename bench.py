@@ -224,7 +224,7 @@ def make_inputs_gpu(P, torch, wl: str):
     return img, dg, R, T, y, p
 
 
-def cpu_reference_sample(wl: str, steps: int, threads: int):
+def cpu_reference_sample(wl: str, steps: int, threads: int, warmup: int = 1):
     """The reference CPU implementation (oracle/_ref = the unmodified reference library, else
     the C port) on a bounded sample of the workload: the same spacing, ratio and inputs
     generated by the reference's own synthetic.cpp, on a z sub-slab (C4: 512x512x24). Only
@@ -241,7 +241,9 @@ def cpu_reference_sample(wl: str, steps: int, threads: int):
     rng = np.random.default_rng(8)
     y = obj.identity() + rng.uniform(-0.3, 0.3, obj.dof)
     p = rng.uniform(-1.0, 1.0, obj.dof)
-    obj.eval(y)  # warm
+    for _ in range(max(1, warmup)):  # untimed warm-up steps
+        obj.eval(y)
+        obj.gn_hessian_vec(p)
     te, th, tv = [], [], []
     for _ in range(steps):
         t0 = time.perf_counter()
@@ -319,19 +321,31 @@ def cpu_gn_model(cpu: dict, levels_gpu, img_counts):
     return t
 
 
+def bench_config(wl: dict, mode: str, world: int, slabs: bool) -> dict:
+    """The workload description both arms print (the reference arm runs it on a bounded sample,
+    described in its cpu_baseline); nodal points as deformation_grid_for (multilevel.cpp:39-49)."""
+    nodal = [max(2, (m + RATIO - 1) // RATIO + 1) for m in wl["m"]]
+    par = f"z slabs x{world} (C++ SlabProblem; NCCL plane exchanges)" if (world > 1 or slabs) else "single GPU"
+    return {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]), "nodal": nodal, "mode": mode,
+            "l2": "inputs larger than L2 (per-step state > 20 GB at C4) and L2 flushed between steps (256 MB write)",
+            "parallelism": par}
+
+
 def run_reference_arm(args, rank, world):
     """--impl reference: the reference's CPU implementation of the path on the host cores, on a
     bounded sample of the same workload (rank 0 only). Loads oracle/_ref only."""
     if rank != 0:
         return
     threads = os.cpu_count() or 1
-    steps = max(1, min(args.steps, 5))
-    cpu = cpu_reference_sample(args.workload, steps, threads)
+    # the driver's K and W (one step ~0.5 s on the sub-slab), capped so that a large K still
+    # finishes within a few minutes
+    steps, warmup = max(1, min(args.steps, 100)), max(1, min(args.warmup, 10))
+    cpu = cpu_reference_sample(args.workload, steps, threads, warmup)
     wl = WORKLOADS[args.workload]
     line = {"metric": METRIC, "value": cpu["value"], "unit": "Gvoxel/s", "n_gpus": world, "steps": steps,
-            "warmup": 1, "ms_per_step": cpu["s_per_step"] * 1e3, "higher_is_better": True,
+            "warmup": warmup, "ms_per_step": cpu["s_per_step"] * 1e3, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": DATA,
-            "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]), "threads": threads},
+            "config": bench_config(wl, args.mode, world, args.slabs),
             "impl": "reference",
             "cpu_baseline": {"value": cpu["value"], "unit": "Gvoxel/s", "cores": cpu["cores"], "kind": cpu["kind"],
                              "sample": cpu["sample"]},
@@ -512,11 +526,7 @@ def run_ours(args, rank, world, local):
         line = {"metric": METRIC, "value": value, "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": DATA,
-                "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]),
-                           "nodal": list(dg.m), "mode": args.mode,
-                           "l2": "inputs larger than L2 (per-step state > 20 GB at C4) and L2 flushed between steps "
-                                 "(256 MB write)",
-                           "parallelism": "single GPU"},
+                "config": bench_config(wl, args.mode, world, args.slabs),
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv,
                 "gvox_s_grad_eval": n / (ms_eval * 1e-3) / 1e9, "gvox_s_gn_hv": n / (ms_hv * 1e-3) / 1e9,
                 "roofline": roofline, "cpu_baseline": cpu_line, "e2e": e2e, "gpu_launches": launches,
@@ -619,9 +629,7 @@ def run_slabs(args, rank, world, local):
         line = {"metric": METRIC, "value": value, "unit": "Gvoxel/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
                 "vs_baseline": None, "dtype": "f64", "data": DATA,
-                "config": {"workload": wl["name"], "image": list(wl["m"]), "spacing": list(wl["h"]),
-                           "nodal": list(dg.m), "mode": args.mode, "l2": "inputs larger than L2; flushed between steps",
-                           "parallelism": f"z slabs x{world} (C++ SlabProblem; NCCL plane exchanges)"},
+                "config": bench_config(wl, args.mode, world, True),
                 "ms_grad_eval": ms_eval, "ms_gn_hv": ms_hv, "roofline": roofline, "cpu_baseline": None,
                 "e2e": e2e, "gpu_launches": launches, "clocks": clocks, "gn_registration": gn}
         print(json.dumps(line), flush=True)
